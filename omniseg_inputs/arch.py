@@ -1,0 +1,241 @@
+"""Architecture strings, workload configs and the seeded weight generator.
+
+This module is an INPUT GENERATOR shared by the oracle side (tests, bench's
+cpu_baseline leg) and the CUDA side (bench, smoke). It holds none of the
+method's arithmetic: only configuration records, the blob *layout* (names and
+shapes, in the documented order of DESIGN.md §3 / SURVEY §8(c) O7) and a
+seeded He-normal random draw. The oracle and the C library each parse the
+blob on their own.
+
+Sources: BASELINE.json ``configs[0..4]`` (called BJ:configs[i] below),
+SURVEY.md §8(c) O7 (blob order, He-normal from the seed, BN folded as
+identity, bf16-exact rounding) and §0 D12 (class / scale codes).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# Class and scale codes (§3.1 class list; PAPER.md:24 scales).
+CLASSES = ("TUFT", "CAP", "PT", "DT", "PTC", "VES")
+SCALE_CODES_4 = (5, 10, 20, 40)
+HEAD_WIDTH = 8                      # "Dynamic head: 8-ch, 3 layers" (BJ:configs[0])
+THETA_LEN = 8 * 8 + 8 + 8 * 8 + 8 + 1 * 8 + 1   # W1 b1 W2 b2 W3 b3 = 153
+
+
+def arch_dict(levels=5, base=32, ncls=6, scale_codes=SCALE_CODES_4, slide_mag=40,
+              dtype="fp16", batch=64):
+    return dict(levels=int(levels), base=int(base), head=HEAD_WIDTH, ncls=int(ncls),
+                scale_codes=tuple(int(s) for s in scale_codes), slide_mag=int(slide_mag),
+                dtype=str(dtype), batch=int(batch))
+
+
+def arch_string(a: dict) -> str:
+    """Format an arch dict as the key=value string omniseg_create() takes."""
+    return ("levels={levels};base={base};head={head};ncls={ncls};scale_codes={sc};"
+            "slide_mag={slide_mag};dtype={dtype};batch={batch}").format(
+                sc=",".join(str(s) for s in a["scale_codes"]), **a)
+
+
+def channels(a: dict):
+    return [a["base"] << l for l in range(a["levels"])]
+
+
+def blob_layout(a: dict):
+    """(name, shape) list in blob order. Conv weights are [C_out][kh][kw][C_in]."""
+    C = channels(a)
+    L = a["levels"]
+    out = []
+
+    def conv(name, cout, k, cin):
+        out.append((name + ".w", (cout, k, k, cin)))
+        out.append((name + ".b", (cout,)))
+
+    conv("stem", C[0], 3, 3)
+    for l in range(L):
+        conv(f"enc{l}.a", C[l], 3, C[l])
+        conv(f"enc{l}.b", C[l], 3, C[l])
+        if l < L - 1:
+            conv(f"down{l}", C[l + 1], 3, C[l])
+    for l in range(L - 2, -1, -1):
+        conv(f"up{l}", C[l], 1, C[l + 1])
+        conv(f"dec{l}.a", C[l], 3, C[l])
+        conv(f"dec{l}.b", C[l], 3, C[l])
+    conv("precls", HEAD_WIDTH, 1, C[0])
+    nin = C[L - 1] + a["ncls"] + len(a["scale_codes"])
+    out.append(("ctrl.w", (THETA_LEN, nin)))
+    out.append(("ctrl.b", (THETA_LEN,)))
+    return out
+
+
+def param_count(a: dict) -> int:
+    return sum(int(np.prod(s)) for _, s in blob_layout(a))
+
+
+def _round_bf16_exact(w: np.ndarray) -> np.ndarray:
+    """Round fp32 -> bf16 (round-to-nearest-even) and flush |w| < 2^-14 to 0, so
+    every value is exactly representable in BOTH bf16 and fp16."""
+    u = w.astype(np.float32).view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    u = ((u + 0x7FFF + lsb) >> 16) << 16
+    r = u.astype(np.uint32).view(np.float32)
+    r = np.where(np.abs(r) < 2.0 ** -14, np.float32(0), r)
+    return r.astype(np.float32)
+
+
+def make_weights(a: dict, seed: int, stem_scale: float = 4.0 / 255.0,
+                 head_alpha: float = 1.0, head_beta: float = 0.0) -> np.ndarray:
+    """Seeded weight blob (flat little-endian fp32) for arch ``a``.
+
+    * conv weights: standard normal x sqrt(2 / fan_in) (He-normal, BJ:configs[0]
+      "He-normal random weights from seed 1"), drawn in blob order from
+      ``numpy.random.default_rng(seed)``; the stem additionally x ``stem_scale``
+      (the u8 input scale folded into the stem); all rounded to
+      bf16-and-fp16-exact values.
+    * conv biases: 0 ("BN folded" with no statistics = identity).
+    * controller: N(0, 1/fan_in) weights, zero bias; the logit rows (W3, b3 =
+      theta[144:153]) are multiplied by ``head_alpha`` and ``head_beta`` is added
+      to bc[152] (the output-logit calibration knob of SURVEY O7; the values used
+      by the configs are the constants in CONFIGS).
+    """
+    rng = np.random.default_rng(seed)
+    parts = []
+    for name, shape in blob_layout(a):
+        n = int(np.prod(shape))
+        if name.startswith("ctrl."):
+            if name == "ctrl.w":
+                w = rng.standard_normal(shape) * math.sqrt(1.0 / shape[1])
+                w[THETA_LEN - 9:THETA_LEN] *= head_alpha
+                parts.append(w.astype(np.float32).ravel())
+            else:
+                b = np.zeros(shape, np.float32)
+                b[THETA_LEN - 1] = head_beta
+                parts.append(b)
+            continue
+        if name.endswith(".b"):
+            parts.append(np.zeros(n, np.float32))
+            continue
+        cout, kh, kw, cin = shape
+        w = rng.standard_normal(shape) * math.sqrt(2.0 / (kh * kw * cin))
+        if name == "stem.w":
+            w = w * stem_scale
+        parts.append(_round_bf16_exact(w.astype(np.float32)).ravel())
+    blob = np.concatenate(parts).astype("<f4")
+    assert blob.size == param_count(a)
+    return blob
+
+
+def split_blob(a: dict, blob: np.ndarray) -> dict:
+    """Convenience view for generators/tests (NOT used by the oracle or the C lib)."""
+    out, o = {}, 0
+    for name, shape in blob_layout(a):
+        n = int(np.prod(shape))
+        out[name] = blob[o:o + n].reshape(shape)
+        o += n
+    return out
+
+
+@dataclass
+class Workload:
+    """One BJ:configs entry as concrete parameters."""
+    name: str
+    slide: dict                    # synth.make_slide spec
+    pad: int
+    patch: int
+    stride: int
+    scales: tuple                  # per task: magnification code
+    classes: tuple                 # per task: class index
+    arch: dict
+    weight_seed: int
+    head_alpha: float = 1.0
+    head_beta: float = 0.0
+    notes: str = ""
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def H(self):
+        return self.slide["H"]
+
+    @property
+    def W(self):
+        return self.slide["W"]
+
+    def weights(self) -> np.ndarray:
+        return make_weights(self.arch, self.weight_seed, head_alpha=self.head_alpha,
+                            head_beta=self.head_beta)
+
+
+# Default task map: TUFT, CAP @5x; PT, DT, VES @10x; PTC @40x.
+TASKS_6 = ((5, 0), (5, 1), (10, 2), (10, 3), (10, 5), (40, 4))
+
+
+def _net(**kw):
+    return arch_dict(**kw)
+
+
+# Output-logit calibration constants, written by the committed script
+# scripts/calibrate_head.py, which calls only oracle/ and these generators:
+# alpha = 2 / std(z) on calibration tiles, beta = -4 - alpha * z(pad-colour tile).
+CALIBRATION = {
+    ("levels=3,base=8", 1): (0.7307895023087443, -0.7857670206643332),
+    ("levels=5,base=32", 1): (7.028853572246453e-07, 2.8050914515179706),
+}
+
+
+def _calibrated(w: "Workload") -> "Workload":
+    key = (f"levels={w.arch['levels']},base={w.arch['base']}", w.weight_seed)
+    if key in CALIBRATION:
+        w.head_alpha, w.head_beta = CALIBRATION[key]
+    return w
+
+
+def workload(cfg: int, **over) -> Workload:
+    """BJ:configs[cfg-1] (1-based like SURVEY §8(d))."""
+    if cfg == 1:
+        w = Workload(
+            name="cfg1_tiny", slide=dict(kind="blobs", seed=0, W=1024, H=1024, n_blobs=6,
+                                         axes=(60, 200), rings=False, nuclei=False),
+            pad=128, patch=256, stride=128, scales=(1,), classes=(0,),
+            arch=_net(levels=3, base=8, ncls=1, scale_codes=(1,), slide_mag=1, batch=16),
+            weight_seed=1)
+    elif cfg == 2:
+        w = Workload(
+            name="cfg2_single_scale", slide=dict(kind="blobs", seed=2, W=4096, H=4096, n_blobs=40,
+                                                 axes=(60, 300), rings=True, nuclei=False),
+            pad=512, patch=512, stride=256, scales=(10, 10, 10), classes=(2, 3, 5),
+            arch=_net(levels=5, base=32, ncls=6, scale_codes=SCALE_CODES_4, slide_mag=10, batch=64),
+            weight_seed=1)
+    elif cfg == 3:
+        w = Workload(
+            name="cfg3_multiscale", slide=dict(kind="blobs", seed=3, W=8192, H=16384, n_blobs=0,
+                                               coverage=0.35, axes=(150, 900), rings=True, nuclei=True),
+            pad=2048, patch=512, stride=256, scales=tuple(s for s, _ in TASKS_6),
+            classes=tuple(c for _, c in TASKS_6),
+            arch=_net(levels=5, base=32, ncls=6, scale_codes=SCALE_CODES_4, slide_mag=40, batch=64),
+            weight_seed=1)
+    elif cfg == 4:
+        w = Workload(
+            name="cfg4_needle_biopsy", slide=dict(kind="cores", seed=4, W=20000, H=60000, n_cores=3,
+                                                  rings=True, nuclei=True),
+            pad=2048, patch=512, stride=256, scales=tuple(s for s, _ in TASKS_6),
+            classes=tuple(c for _, c in TASKS_6),
+            arch=_net(levels=5, base=32, ncls=6, scale_codes=SCALE_CODES_4, slide_mag=40, batch=64),
+            weight_seed=1)
+    elif cfg == 5:
+        frac = over.pop("fg_fraction", 0.95)
+        seed = {0.05: 5, 0.25: 6, 0.60: 7, 0.95: 8}[frac]
+        w = Workload(
+            name=f"cfg5_sweep_fg{int(frac * 100)}",
+            slide=dict(kind="field", seed=seed, W=40000, H=40000, fraction=frac, rings=True, nuclei=True),
+            pad=2048, patch=512, stride=over.pop("stride", 256), scales=tuple(s for s, _ in TASKS_6),
+            classes=tuple(c for _, c in TASKS_6),
+            arch=_net(levels=5, base=32, ncls=6, scale_codes=SCALE_CODES_4, slide_mag=40, batch=64),
+            weight_seed=1)
+    else:
+        raise ValueError(cfg)
+    _calibrated(w)
+    for k, v in over.items():
+        setattr(w, k, v)
+    return w
