@@ -1,0 +1,138 @@
+/*
+ * omniseg.h -- C ABI of libomniseg.so: slide-wise Omni-Seg prediction on B200 (sm_100a).
+ *
+ * The operation (arxiv 2305.14566, /root/reference/PAPER.md):
+ *   P:53 §2      three-step pipeline: tissue detection + patch extraction,
+ *                Omni-Seg segmentation, slide-wise aggregation;
+ *   P:57-61 §2.1 pad the WSI (colour = mean of the top-left 2x2), detect the
+ *                foreground (median blur + Otsu), drop blank regions;
+ *   P:66-69 §2.2 tile the slide at each class's magnification (40x/10x/5x) into
+ *                overlapping 512x512 windows, predict each with the Omni-Seg
+ *                dynamic network (BASELINE.json north_star: residual U-Net, GAP,
+ *                controller -> 3 dynamic 1x1 layers, sigmoid);
+ *   P:86-87 §2.3 merge the predictions of each tissue type back into a slide-level
+ *                map; P:97 majority of overlapping tiles decides (read as the
+ *                overlap-normalised mean thresholded at 1/2, R11).
+ * The interface follows north_star: omniseg_create(arch, weights) and
+ * omniseg_segment_slide(rgb_u8, H, W, pad, patch, stride, scales[], classes[],
+ * out_prob, out_mask). Concrete readings of everything the paper leaves open are
+ * listed in DESIGN.md §2 (R1..R14) and are cited below as "R<n>".
+ *
+ * Conventions (all entry points):
+ *   - Return codes: 0 = ok, OMNISEG_EINVAL (-1) parameter error, OMNISEG_ECUDA (-2)
+ *     CUDA error, OMNISEG_ENOMEM (-3) allocation failure, OMNISEG_ENCCL (-4)
+ *     collective error. On error, omniseg_last_error() returns a thread-local
+ *     message; outputs are unspecified.
+ *   - Synchronous: outputs are complete when a call returns.
+ *   - Pointers may be host or device memory (detected with
+ *     cudaPointerGetAttributes); device pointers must be on the handle's device.
+ *     The library never retains caller pointers; the caller owns every array.
+ *   - A handle is not thread-safe: one handle per thread/device.
+ */
+#ifndef OMNISEG_H
+#define OMNISEG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OMNISEG_OK      0
+#define OMNISEG_EINVAL (-1)
+#define OMNISEG_ECUDA  (-2)
+#define OMNISEG_ENOMEM (-3)
+#define OMNISEG_ENCCL  (-4)
+
+typedef struct omniseg omniseg_t;   /* opaque; owns device weights, workspace, streams */
+
+/* Create a predictor.
+ *   arch   : ';'-separated key=value string, e.g.
+ *            "levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16;batch=64"
+ *            levels/base: U-Net depth and base width (channels base*2^l); head must be 8
+ *            (3-layer 8-channel dynamic head, BASELINE configs[0]); ncls classes;
+ *            scale_codes: magnifications with a one-hot code each (order = code index);
+ *            slide_mag: magnification of the input slide (level factor f = slide_mag/scale);
+ *            dtype: fp16 (default) or bf16 storage, fp32 accumulation (R9);
+ *            batch: tiles per trunk launch; device: CUDA ordinal (default: current).
+ *   weights: flat little-endian fp32 blob in the order of DESIGN.md §3;
+ *            nbytes must equal 4 * param_count(arch). Host or device; copied.
+ * Returns NULL on error (see omniseg_last_error). */
+omniseg_t* omniseg_create(const char* arch, const void* weights, size_t nbytes);
+
+/* Segment one slide (all kept tiles of all task scales) on the handle's GPU.
+ *   rgb_u8  : H x W x 3 uint8, row-major, tightly packed (pitch 3W). Host or device.
+ *   H, W    : slide size in pixels at slide_mag; H, W >= 2.
+ *   pad     : padding per side in slide pixels (R2); pad % 8 == 0.
+ *             The padded frame is roundup(H+2pad,128) x roundup(W+2pad,128).
+ *   patch   : window size P at every scale; multiple of 16 and of 2^(levels-1).
+ *   stride  : window stride S at every scale; 8 <= S <= P, S % 8 == 0.
+ *   scales  : n_tasks magnifications (each in scale_codes; f = slide_mag/scale in {1,2,4,8});
+ *   classes : n_tasks class indices (< ncls).
+ *   out_prob: float[sum_t Ht*Wt] or NULL, Ht = ceil(H/f_t), Wt = ceil(W/f_t), tasks
+ *             concatenated in order: overlap-normalised probability (0 where no kept
+ *             tile covers the pixel), R10-R11.
+ *   out_mask: uint8[sum_t Ht*Wt] or NULL: prob >= 1/2 (decided exactly on the
+ *             fixed-point accumulator, R12).
+ *   out_area: uint64[n_tasks] or NULL: number of mask pixels per task.
+ * Errors: EINVAL for any violated precondition above, and when the coverage count of
+ * a pixel could exceed 15 (ceil(P/S)+1)^2 > 15, which the u32 fixed-point canvas
+ * cannot hold (R12). */
+int omniseg_segment_slide(omniseg_t* h, const uint8_t* rgb_u8, int64_t H, int64_t W,
+                          int pad, int patch, int stride,
+                          const int* scales, const int* classes, int n_tasks,
+                          float* out_prob, uint8_t* out_mask, uint64_t* out_area);
+
+/* Number of canvas pixels of a task at magnification `scale`: ceil(H/f)*ceil(W/f). */
+int64_t omniseg_output_size(const omniseg_t* h, int64_t H, int64_t W, int scale);
+
+/* Multi-GPU, one process per GPU. The caller joins an NCCL clique
+ * (128-byte ncclUniqueId from rank 0, broadcast by the caller, e.g. via
+ * torch.distributed) of `world` ranks. */
+int omniseg_comm_init(omniseg_t* h, const void* nccl_unique_id, int world, int rank);
+
+/* Segment the row band [row0, row1) of the PADDED 40x frame (row0, row1 multiples of
+ * 8*stride*f_max/8... see DESIGN.md §7: multiples of 8*S, row1 = Hp for the last band).
+ *   rgb_band: slide rows [b0, b1) with b0 = clamp(row0 - pad - halo, 0, H),
+ *             b1 = clamp(row1 - pad + halo, 0, H), halo = patch * f_max + 64 (one
+ *             window at the coarsest scale plus the detection median's reach), H x W
+ *             layout otherwise as in omniseg_segment_slide.
+ *   Each rank computes every kept tile whose window intersects its owned rows; the
+ *   Otsu histogram is all-reduced over ranks (R6) so tile lists match the 1-GPU run;
+ *   outputs cover only the task-canvas rows owned by this band, per task, tasks
+ *   concatenated; out_area is all-reduced (global per-task areas on every rank).
+ * Canvas values are bit-identical to omniseg_segment_slide's (fixed point, R12). */
+int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64_t W,
+                         int64_t row0, int64_t row1, int pad, int patch, int stride,
+                         const int* scales, const int* classes, int n_tasks,
+                         float* out_prob, uint8_t* out_mask, uint64_t* out_area);
+
+/* Owned canvas rows of band [row0,row1) for a task at factor f: [r0_t, r1_t) with
+ * r0_t = clamp(ceil((row0 - pad)/f), 0, Ht) (likewise r1_t). Pure arithmetic helper. */
+int omniseg_band_rows(int64_t H, int64_t row0, int64_t row1, int pad, int f,
+                      int64_t* r0_t, int64_t* r1_t);
+
+/* Introspection (valid after the last segment call on this handle). */
+/* Kept tiles in canonical order (scale descending, then row, then column), packed
+ * (log2 f) << 30 | ty << 15 | tx  (grid indices; origin = min(i*S, E-P), R3). */
+int omniseg_get_tiles(const omniseg_t* h, uint32_t* tiles, int64_t cap, int64_t* n);
+/* Level-8 foreground mask (Hp/8 x Wp/8 u8), Otsu threshold and the luma of the pad colour. */
+int omniseg_get_fgmask(const omniseg_t* h, uint8_t* mask, int64_t cap, int64_t* h8, int64_t* w8,
+                       int* otsu_t, int* g_pad);
+/* Per-stage device times of the last call, milliseconds (CUDA events on the
+ * library's stream): [0] upload, [1] pyramid+detection+selection, [2] gather,
+ * [3] trunk convs, [4] gap+controller, [5] head+stitch, [6] finalize, [7] download,
+ * [8] total. Also the conv-kernel launch count [9] and total launches [10]. */
+int omniseg_get_timings(const omniseg_t* h, double* out, int cap);
+
+/* Use this CUDA stream (cudaStream_t cast to void*; NULL = the library's own). */
+int omniseg_set_stream(omniseg_t* h, void* stream);
+
+const char* omniseg_last_error(void);
+void omniseg_destroy(omniseg_t* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OMNISEG_H */

@@ -1,0 +1,42 @@
+/*
+ * omniseg_debug.h -- test-only entry points of libomniseg.so (same library, same
+ * kernels as the product path). They expose single stages so the GPU parity tests
+ * can compare each against the oracle. Conventions as in omniseg.h.
+ */
+#ifndef OMNISEG_DEBUG_H
+#define OMNISEG_DEBUG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "omniseg.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Trunk + GAP + controller + dynamic head on n given windows.
+ *   tiles_u8 : n x P x P x 3 uint8 (host or device).
+ *   cls[t], scl[t]: n_tasks (class index, scale-code index) pairs; every tile runs every task.
+ *   out_p    : float[n][n_tasks][P][P] (host or device): sigmoid probabilities.
+ *   out_g    : float[n][C_bottleneck] or NULL: the GAP feature.
+ *   out_F    : float[n][P][P][8] or NULL: the precls feature F. */
+int omniseg_debug_predict_tiles(omniseg_t* h, const uint8_t* tiles_u8, int n, int P,
+                                const int* cls, const int* scl, int n_tasks,
+                                float* out_p, float* out_g, float* out_F);
+
+/* One implicit-GEMM convolution through the tcgen05 kernel.
+ *   x   : float[B][H][W][Cin] host, values rounded to the storage dtype on upload.
+ *   w   : float[Cout][k][k][Cin] host (k = 1 or 3), b: float[Cout].
+ *   r   : float residual / skip input (mode 1: [B][Ho][Wo][Cout]; mode 2: [B][2H][2W][Cout]) or NULL.
+ *   mode: 0 y = relu(conv + b); 1 y = relu(conv + b + r); 2 y[2i+a][2j+c] = r[...] + conv + b
+ *         (1x1 + nearest-up x2 + skip add); 3 y = conv + b.
+ *   y   : float output (storage dtype values widened to fp32). */
+int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Cin,
+                       const float* w, const float* b, int Cout, int k, int stride,
+                       const float* r, int mode, float* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,59 @@
+// common.cuh -- shared types of the omniseg kernels and the C-ABI orchestrator.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace osg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define OS_CUDA(call)                                                                             \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw ::osg::Error(-2, std::string(#call " failed: ") + cudaGetErrorString(e_) + " at " + \
+                                     __FILE__ + ":" + std::to_string(__LINE__));                  \
+  } while (0)
+
+#define OS_REQUIRE(cond, msg)                                  \
+  do {                                                         \
+    if (!(cond)) throw ::osg::Error(-1, std::string(msg)); \
+  } while (0)
+
+constexpr int kMaxScales = 4;   // level factors 8, 4, 2, 1
+constexpr int kMaxTasks = 32;
+constexpr int kTheta = 153;     // W1 b1 W2 b2 W3 b3 of the 8-8-8-1 dynamic head
+constexpr int kHead = 8;
+
+// One scale's candidate-tile grid (front end, DESIGN.md §6 K4).
+struct ScaleGrid {
+  int f;          // level factor
+  int log2f;
+  int ny, nx;     // grid size
+  int Ey, Ex;     // level-f padded extent
+  int base;       // first candidate index of this scale (canonical order)
+  int kept_base;  // filled after compaction
+};
+
+struct FrontParams {
+  const uint8_t* slide;  // rows [slide_row0, slide_row0 + slide_rows) of the H x W x 3 slide
+  int64_t slide_row0, slide_rows;
+  int64_t H, W;
+  int pad;
+  int Hp, Wp;            // padded frame
+  int H8, W8;            // level-8 grid
+  int r8_0, r8_1;        // level-8 rows computed by this call (band: with halo)
+  int own8_0, own8_1;    // level-8 rows owned (histogram counts only these)
+};
+
+__host__ __device__ inline uint32_t pack_tile(int log2f, int ty, int tx) {
+  return (uint32_t(log2f) << 30) | (uint32_t(ty) << 15) | uint32_t(tx);
+}
+
+}  // namespace osg

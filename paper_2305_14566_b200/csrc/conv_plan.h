@@ -1,0 +1,26 @@
+// conv_plan.h -- host interface of the tcgen05 convolution (conv_tc.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "conv_tc.cuh"
+
+namespace osg {
+
+struct ConvPlan {
+  CUtensorMap tmA, tmB;  // activation (4-D NHWC) and weight (2-D [Cout][taps*Cin]) TMA maps
+  ConvArgs args;
+  int bn, bk, stages, mode, grid;
+  bool bf16;
+  double flops;          // algorithmic FLOPs of one launch (2 * M * N * K)
+};
+
+// Plan one convolution: input [B][Hin][Win][Cin], weights [Cout][k][k][Cin] (16-bit,
+// K-major), fp32 bias; output grid Ho = ceil(Hin/stride) etc. `res` per ConvMode.
+ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
+                        const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out);
+void set_conv_batch(ConvPlan& p, int B);
+void run_conv(const ConvPlan& p, cudaStream_t s);
+int num_sms();
+
+}  // namespace osg

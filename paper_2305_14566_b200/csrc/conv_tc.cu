@@ -1,0 +1,182 @@
+// conv_tc.cu -- host side of the tcgen05 implicit-GEMM convolution: TMA tensor maps,
+// tile-shape selection, template dispatch and the persistent launch.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <type_traits>
+
+#include "common.cuh"
+#include "conv_plan.h"
+#include "conv_tc.cuh"
+
+namespace osg {
+
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) throw Error(-2, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  return fn;
+}
+
+CUtensorMapSwizzle swz(int bytes) {
+  return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+
+template <typename T, int BN, int BK>
+struct Cfg {
+  static constexpr int kStageBytes = ConvSmem<BN, BK, 1>::kStage;
+  static constexpr int kStages0 = (200 * 1024) / kStageBytes;
+  static constexpr int STAGES = kStages0 > 8 ? 8 : (kStages0 < 2 ? 2 : kStages0);
+  using Smem = ConvSmem<BN, BK, STAGES>;
+};
+
+template <typename T, int BN, int BK>
+void launch_tpl(const ConvPlan& p, cudaStream_t s) {
+  using C = Cfg<T, BN, BK>;
+  constexpr int smem = C::Smem::kTotal;
+  auto launch_mode = [&](auto kern) {
+    static bool attr = false;  // per instantiation
+    if (!attr) {
+      OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.args);
+  };
+  switch (p.mode) {
+    case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kReluBias>); break;
+    case kResidualRelu: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kResidualRelu>); break;
+    case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kUpAdd>); break;
+    default: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kBias>); break;
+  }
+}
+
+template <typename T>
+void dispatch(const ConvPlan& p, cudaStream_t s) {
+#define OS_CASE(N_, K_) \
+  if (p.bn == N_ && p.bk == K_) return launch_tpl<T, N_, K_>(p, s);
+  OS_CASE(16, 16) OS_CASE(16, 32) OS_CASE(16, 64)
+  OS_CASE(32, 16) OS_CASE(32, 32) OS_CASE(32, 64)
+  OS_CASE(64, 16) OS_CASE(64, 32) OS_CASE(64, 64)
+  OS_CASE(128, 16) OS_CASE(128, 32) OS_CASE(128, 64)
+  OS_CASE(256, 16) OS_CASE(256, 32) OS_CASE(256, 64)
+#undef OS_CASE
+  throw Error(-1, "unsupported conv tile shape");
+}
+
+int stages_for(int bn, int bk) {
+  const int a = 128 * bk * 2, b = ((bn * bk * 2 + 1023) / 1024) * 1024;
+  int st = (200 * 1024) / (a + b);
+  return st > 8 ? 8 : (st < 2 ? 2 : st);
+}
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    OS_CUDA(cudaGetDevice(&dev));
+    OS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
+                        const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out) {
+  OS_REQUIRE(Cin % 16 == 0 && Cout % 16 == 0, "conv channels must be multiples of 16");
+  OS_REQUIRE(k == 1 || k == 3, "conv kernel size must be 1 or 3");
+  OS_REQUIRE(stride == 1 || stride == 2, "conv stride must be 1 or 2");
+  ConvPlan p{};
+  p.mode = mode;
+  p.bf16 = bf16;
+  // K chunk = one swizzle row (128/64/32 bytes); N tile = largest power of two <= 256 dividing Cout
+  p.bk = Cin % 64 == 0 ? 64 : Cin % 32 == 0 ? 32 : 16;
+  p.bn = 256;
+  while (Cout % p.bn) p.bn >>= 1;
+  const int Ho = (Hin - 1) / stride + 1, Wo = (Win - 1) / stride + 1;
+  ConvArgs& a = p.args;
+  a.B = B;
+  a.Ho = Ho;
+  a.Wo = Wo;
+  a.Cin = Cin;
+  a.Cout = Cout;
+  a.ksize = k;
+  a.stride = stride;
+  if (Wo >= 128) {
+    OS_REQUIRE(Wo % 128 == 0, "output width must be a multiple of 128 or divide 128");
+    a.wb = 128;
+    a.hb = 1;
+  } else {
+    OS_REQUIRE(128 % Wo == 0, "output width must divide 128");
+    a.wb = Wo;
+    a.hb = 128 / Wo;
+    OS_REQUIRE(Ho % a.hb == 0, "output height incompatible with the 128-pixel M tile");
+  }
+  a.tiles_x = Wo / a.wb;
+  a.tiles_y = Ho / a.hb;
+  a.n_tiles_n = Cout / p.bn;
+  a.kchunks = Cin / p.bk;
+  a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
+  a.bias = bias;
+  a.res = res;
+  a.out = out;
+  const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)Cin * 2, (cuuint64_t)Win * Cin * 2, (cuuint64_t)Hin * Win * Cin * 2};
+    cuuint32_t box[4] = {(cuuint32_t)p.bk, (cuuint32_t)(a.wb * stride), (cuuint32_t)(a.hb * stride), 1};
+    cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+    CUresult r = encode_fn()(&p.tmA, dt, 4, const_cast<void*>(in), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, swz(p.bk * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(A) failed: " + std::to_string((int)r));
+  }
+  {
+    const int taps = k * k;
+    cuuint64_t dims[2] = {(cuuint64_t)taps * Cin, (cuuint64_t)Cout};
+    cuuint64_t strides[1] = {(cuuint64_t)taps * Cin * 2};
+    cuuint32_t box[2] = {(cuuint32_t)p.bk, (cuuint32_t)p.bn};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&p.tmB, dt, 2, const_cast<void*>(w), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, swz(p.bk * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
+  }
+  p.stages = stages_for(p.bn, p.bk);
+  p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
+  p.flops = 2.0 * (double)B * Ho * Wo * Cout * (double)k * k * Cin;
+  return p;
+}
+
+// Re-point a plan at a different batch size (same buffers): only the work count changes.
+void set_conv_batch(ConvPlan& p, int B) {
+  ConvArgs& a = p.args;
+  a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
+  p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
+  p.flops = 2.0 * (double)B * a.Ho * a.Wo * a.Cout * (double)a.ksize * a.ksize * a.Cin;
+}
+
+void run_conv(const ConvPlan& p, cudaStream_t s) {
+  if (p.args.num_work <= 0) return;
+  if (p.bf16)
+    dispatch<__nv_bfloat16>(p, s);
+  else
+    dispatch<__half>(p, s);
+  OS_CUDA(cudaGetLastError());
+}
+
+}  // namespace osg

@@ -1,0 +1,650 @@
+// kernels.cu -- the non-GEMM kernels of the slide-wise Omni-Seg path (sm_100a):
+//   K0 pad colour, K1 pyramid (+ level-8 luma), K2 7x7 median, K3 histogram + exact
+//   Otsu + foreground, K4 tile keep test + stable compaction, K5 gather (im2col of
+//   the stem input), K7 GAP + controller, K8/K9 dynamic head + fixed-point stitch,
+//   K10 finalize. Each cites the passage it implements (P:L = PAPER.md line L; R<n> =
+//   DESIGN.md §2 reading). Integer stages are bit-exact by construction.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace osg {
+
+// ------------------------------------------------------------------ K0 pad colour
+// P:59 §2.1: mean of the top-left 2x2 image vector, per channel, rounded half up (R1).
+__global__ void pad_colour_kernel(const uint8_t* slide, int64_t W, DevState* st) {
+  if (threadIdx.x < 3) {
+    int c = threadIdx.x;
+    int s = slide[c] + slide[3 + c] + slide[3 * W + c] + slide[3 * W + 3 + c];
+    st->pc[c] = (uint8_t)((s + 2) >> 2);
+  }
+  if (threadIdx.x == 0) st->pc[3] = 0;
+}
+
+__device__ __forceinline__ int luma_u8(int r, int g, int b) { return (77 * r + 150 * g + 29 * b) >> 8; }
+
+// ------------------------------------------------------------------ K1 pyramid
+// Area-mean levels f = 2, 4, 8 of the padded slide, each directly from 40x and rounded
+// half up (R3; §2.2, §3.1), plus the level-8 luma (77R+150G+29B)>>8 (R4).
+// One thread per level-8 pixel = one 8x8 block of the padded frame; padding is virtual.
+__global__ void pyramid_kernel(FrontParams p, const DevState* st, uint32_t* L2, uint32_t* L4, uint32_t* L8,
+                               uint8_t* luma8) {
+  const int x8 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y8 = p.r8_0 + blockIdx.y;
+  if (x8 >= p.W8 || y8 >= p.r8_1) return;
+  const int pc0 = st->pc[0], pc1 = st->pc[1], pc2 = st->pc[2];
+  int s2[4][4][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s2[i][j][0] = s2[i][j][1] = s2[i][j][2] = 0;
+  const int64_t sx0 = (int64_t)x8 * 8 - p.pad;
+#pragma unroll
+  for (int yy = 0; yy < 8; ++yy) {
+    const int64_t sy = (int64_t)y8 * 8 + yy - p.pad;
+    const bool row_in = sy >= 0 && sy < p.H;
+    const uint8_t* rowp = row_in ? p.slide + (sy - p.slide_row0) * p.W * 3 : nullptr;
+#pragma unroll
+    for (int xx = 0; xx < 8; ++xx) {
+      const int64_t sx = sx0 + xx;
+      int r = pc0, g = pc1, b = pc2;
+      if (row_in && sx >= 0 && sx < p.W) {
+        const uint8_t* q = rowp + sx * 3;
+        r = __ldg(q);
+        g = __ldg(q + 1);
+        b = __ldg(q + 2);
+      }
+      s2[yy >> 1][xx >> 1][0] += r;
+      s2[yy >> 1][xx >> 1][1] += g;
+      s2[yy >> 1][xx >> 1][2] += b;
+    }
+  }
+  int s4[2][2][3], s8[3] = {0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        s4[i][j][c] = s2[2 * i][2 * j][c] + s2[2 * i][2 * j + 1][c] + s2[2 * i + 1][2 * j][c] +
+                      s2[2 * i + 1][2 * j + 1][c];
+        s8[c] += s4[i][j][c];
+      }
+  if (L2) {
+    const int W2 = p.W8 * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t v = uint32_t((s2[i][j][0] + 2) >> 2) | (uint32_t((s2[i][j][1] + 2) >> 2) << 8) |
+                     (uint32_t((s2[i][j][2] + 2) >> 2) << 16);
+        L2[(int64_t)(4 * y8 + i) * W2 + 4 * x8 + j] = v;
+      }
+  }
+  if (L4) {
+    const int W4 = p.W8 * 2;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t v = uint32_t((s4[i][j][0] + 8) >> 4) | (uint32_t((s4[i][j][1] + 8) >> 4) << 8) |
+                     (uint32_t((s4[i][j][2] + 8) >> 4) << 16);
+        L4[(int64_t)(2 * y8 + i) * W4 + 2 * x8 + j] = v;
+      }
+  }
+  const int r8 = (s8[0] + 32) >> 6, g8 = (s8[1] + 32) >> 6, b8 = (s8[2] + 32) >> 6;
+  if (L8) L8[(int64_t)y8 * p.W8 + x8] = uint32_t(r8) | (uint32_t(g8) << 8) | (uint32_t(b8) << 16);
+  luma8[(int64_t)y8 * p.W8 + x8] = (uint8_t)luma_u8(r8, g8, b8);
+}
+
+// ------------------------------------------------------------------ K2 median 7x7
+// P:96 §3.2 median blur ("threshold set to 59" = aperture, R5: 7x7 at level 8), edge
+// replication at the padded-frame border. Median = 25th smallest of 49, found bit by bit:
+// the largest v with #{x < v} <= 24.
+constexpr int MB_X = 32, MB_Y = 8, MR = 3;
+__global__ void median7_kernel(const uint8_t* g, uint8_t* out, int H8, int W8, int r0, int r1) {
+  __shared__ uint8_t t[MB_Y + 2 * MR][MB_X + 2 * MR];
+  const int bx = blockIdx.x * MB_X, by = r0 + blockIdx.y * MB_Y;
+  for (int i = threadIdx.y * MB_X + threadIdx.x; i < (MB_Y + 2 * MR) * (MB_X + 2 * MR); i += MB_X * MB_Y) {
+    const int ty = i / (MB_X + 2 * MR), tx = i % (MB_X + 2 * MR);
+    const int yy = min(max(by + ty - MR, 0), H8 - 1);
+    const int xx = min(max(bx + tx - MR, 0), W8 - 1);
+    t[ty][tx] = g[(int64_t)yy * W8 + xx];
+  }
+  __syncthreads();
+  const int x = bx + threadIdx.x, y = by + threadIdx.y;
+  if (x >= W8 || y >= r1) return;
+  uint8_t v[49];
+#pragma unroll
+  for (int dy = 0; dy < 7; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 7; ++dx) v[dy * 7 + dx] = t[threadIdx.y + dy][threadIdx.x + dx];
+  int res = 0;
+#pragma unroll
+  for (int bit = 7; bit >= 0; --bit) {
+    const int cand = res | (1 << bit);
+    int below = 0;
+#pragma unroll
+    for (int k = 0; k < 49; ++k) below += v[k] < cand;
+    if (below <= 24) res = cand;
+  }
+  out[(int64_t)y * W8 + x] = (uint8_t)res;
+}
+
+// ------------------------------------------------------------------ K3 histogram
+// 256-bin histogram of the median-blurred luma over the interior level-8 pixels
+// (rows [pad/8, pad/8 + H/8), cols likewise, R6) that this rank owns.
+__global__ void hist_kernel(const uint8_t* gm, int W8, int row_lo, int row_hi, int col_lo, int col_hi,
+                            unsigned long long* hist) {
+  __shared__ unsigned int h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t w = col_hi - col_lo;
+  const int64_t n = (int64_t)(row_hi - row_lo) * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = row_lo + i / w, x = col_lo + i % w;
+    atomicAdd(&h[gm[y * W8 + x]], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+// 192-bit helpers for the exact Otsu compare.
+struct U192 {
+  uint64_t w0, w1, w2;
+};
+__device__ __forceinline__ U192 mul_128x64(unsigned __int128 a, uint64_t b) {
+  const uint64_t alo = (uint64_t)a, ahi = (uint64_t)(a >> 64);
+  const unsigned __int128 p0 = (unsigned __int128)alo * b;
+  const unsigned __int128 p1 = (unsigned __int128)ahi * b + (uint64_t)(p0 >> 64);
+  return U192{(uint64_t)p0, (uint64_t)p1, (uint64_t)(p1 >> 64)};
+}
+__device__ __forceinline__ bool gt192(const U192& a, const U192& b) {
+  if (a.w2 != b.w2) return a.w2 > b.w2;
+  if (a.w1 != b.w1) return a.w1 > b.w1;
+  return a.w0 > b.w0;
+}
+
+// Otsu (§2.1, §3.2; R6): t = argmax over 0 < n0 < N of (N m0 - M n0)^2 / (n0 (N - n0)),
+// smallest t on ties, exact: numerators < 2^128, cross products < 2^192. Degenerate
+// (single value) -> that value; empty -> 255. Then the guard g_pad - 16 (R7).
+__global__ void otsu_kernel(const unsigned long long* hist, DevState* st) {
+  __shared__ unsigned long long h[256];
+  const int t = threadIdx.x;
+  h[t] = hist[t];
+  __syncthreads();
+  if (t != 0) return;
+  uint64_t N = 0, M = 0;
+  for (int i = 0; i < 256; ++i) {
+    N += h[i];
+    M += (uint64_t)i * h[i];
+  }
+  int best = -1;
+  unsigned __int128 bnum = 0;
+  uint64_t bden = 1;
+  uint64_t n0 = 0, m0 = 0;
+  for (int i = 0; i < 256; ++i) {
+    n0 += h[i];
+    m0 += (uint64_t)i * h[i];
+    if (n0 == 0 || n0 == N) continue;
+    // N*m0 and M*n0 are < 2^64 for N < 2^28 (checked on the host).
+    const uint64_t a = N * m0, b = M * n0;
+    const uint64_t d = a > b ? a - b : b - a;
+    const unsigned __int128 num = (unsigned __int128)d * d;
+    const uint64_t den = n0 * (N - n0);
+    if (best < 0 || gt192(mul_128x64(num, bden), mul_128x64(bnum, den))) {
+      best = i;
+      bnum = num;
+      bden = den;
+    }
+  }
+  if (best < 0) {
+    best = 255;
+    for (int i = 0; i < 256; ++i)
+      if (h[i]) {
+        best = i;
+        break;
+      }
+  }
+  st->otsu_t = best;
+  const int gpad = luma_u8(st->pc[0], st->pc[1], st->pc[2]);
+  st->g_pad = gpad;
+}
+
+// fg = interior & gm <= t & gm <= g_pad - 16 (tissue = darker side; guard R7).
+__global__ void fg_kernel(const uint8_t* gm, uint8_t* fg, int W8, int r0, int r1, int int_r0, int int_r1,
+                          int int_c0, int int_c1, const DevState* st) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = r0 + blockIdx.y;
+  if (x >= W8 || y >= r1) return;
+  const int t = st->otsu_t, lim = st->g_pad - 16;
+  const int v = gm[(int64_t)y * W8 + x];
+  const bool in = y >= int_r0 && y < int_r1 && x >= int_c0 && x < int_c1;
+  fg[(int64_t)y * W8 + x] = (in && v <= t && v <= lim) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ K4 tile keep test
+// One warp per candidate tile (canonical order: scale descending, row, col). A tile at
+// level f with origin (oy, ox) covers level-8 rows [oy f/8, (oy+P) f/8) and columns
+// likewise; kept iff 100 * #fg >= (P f/8)^2 ("remove blank regions", R8) and, for
+// a band, its window rows [oy f, (oy+P) f) intersect the owned rows [own0, own1).
+__global__ void tile_keep_kernel(const uint8_t* fg, int W8, const ScaleGrid* grids, int nscales, int total, int P,
+                                 int S, int64_t own0, int64_t own1, uint8_t* keep) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= total) return;
+  int s = 0;
+  while (s + 1 < nscales && gw >= grids[s + 1].base) ++s;
+  const ScaleGrid g = grids[s];
+  const int i = gw - g.base;
+  const int ty = i / g.nx, tx = i % g.nx;
+  const int oy = min(ty * S, g.Ey - P), ox = min(tx * S, g.Ex - P);
+  const int n = P * g.f / 8;
+  const int y0 = oy * g.f / 8, x0 = ox * g.f / 8;
+  const int64_t wr0 = (int64_t)oy * g.f, wr1 = (int64_t)(oy + P) * g.f;
+  bool in_band = wr1 > own0 && wr0 < own1;
+  long long cnt = 0;
+  if (in_band) {
+    for (int r = 0; r < n; ++r) {
+      const uint8_t* row = fg + (int64_t)(y0 + r) * W8 + x0;
+      for (int c = lane; c < n; c += 32) cnt += row[c];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) keep[gw] = (in_band && 100 * cnt >= (long long)n * n) ? 1 : 0;
+}
+
+// Stable compaction of the keep flags into packed tile ids + per-scale kept counts.
+// Single block of 1024 threads; warp ballot + popc + block prefix, chunk by chunk.
+__global__ void compact_kernel(const uint8_t* keep, int total, const ScaleGrid* grids, int nscales,
+                               uint32_t* tiles, int* counts) {
+  __shared__ int warp_sums[32];
+  __shared__ int running, chunk_total;
+  __shared__ int per_scale[kMaxScales];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) running = 0;
+  if (threadIdx.x < kMaxScales) per_scale[threadIdx.x] = 0;
+  __syncthreads();
+  for (int base = 0; base < total; base += 1024) {
+    const int i = base + threadIdx.x;
+    const bool k = i < total && keep[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, k);
+    const int in_warp = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) warp_sums[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+      const int v = warp_sums[lane];
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      warp_sums[lane] = x - v;  // exclusive prefix over warps
+      if (lane == 31) chunk_total = x;
+    }
+    __syncthreads();
+    if (k) {
+      const int pos = running + warp_sums[wid] + in_warp;
+      int s = 0;
+      while (s + 1 < nscales && i >= grids[s + 1].base) ++s;
+      const int j = i - grids[s].base;
+      tiles[pos] = pack_tile(grids[s].log2f, j / grids[s].nx, j % grids[s].nx);
+      atomicAdd(&per_scale[s], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) running += chunk_total;
+    __syncthreads();
+  }
+  if (threadIdx.x < nscales) counts[threadIdx.x] = per_scale[threadIdx.x];
+  if (threadIdx.x == 0) counts[kMaxScales] = running;
+}
+
+// ------------------------------------------------------------------ K5 gather
+// Kept tiles -> stem input: X[b][y][x][k], k = (dy*3 + dx)*3 + c for the 27 taps of the
+// 3x3 stem over the u8 window (zero outside the window = the stem's zero padding),
+// k = 27..31 zero. u8 -> 16-bit is exact. Level f > 1 comes from the RGBX pyramid,
+// f = 1 straight from the slide with virtual padding.
+template <typename T>
+__global__ void gather_kernel(const uint32_t* tiles, int first, int n, int P, int S, FrontParams fp,
+                              const DevState* st, const uint32_t* L2, const uint32_t* L4, const uint32_t* L8,
+                              T* X) {
+  const int b = blockIdx.y;
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n || pix >= P * P) return;
+  const uint32_t id = tiles[first + b];
+  const int lf = id >> 30, ty = (id >> 15) & 0x7FFF, tx = id & 0x7FFF;
+  const int f = 1 << lf;
+  const int Ey = fp.Hp / f, Ex = fp.Wp / f;
+  const int oy = min(ty * S, Ey - P), ox = min(tx * S, Ex - P);
+  const int y = pix / P, x = pix % P;
+  const uint32_t* L = f == 2 ? L2 : f == 4 ? L4 : L8;
+  const uint32_t pcv = uint32_t(st->pc[0]) | (uint32_t(st->pc[1]) << 8) | (uint32_t(st->pc[2]) << 16);
+  float v[32];
+#pragma unroll
+  for (int k = 27; k < 32; ++k) v[k] = 0.f;
+#pragma unroll
+  for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      const int yy = y + dy - 1, xx = x + dx - 1;
+      uint32_t rgb = 0;
+      bool valid = yy >= 0 && yy < P && xx >= 0 && xx < P;
+      if (valid) {
+        const int64_t gy = oy + yy, gx = ox + xx;  // level-f padded coordinates
+        if (f == 1) {
+          const int64_t sy = gy - fp.pad, sx = gx - fp.pad;
+          if (sy >= 0 && sy < fp.H && sx >= 0 && sx < fp.W) {
+            const uint8_t* q = fp.slide + ((sy - fp.slide_row0) * fp.W + sx) * 3;
+            rgb = uint32_t(__ldg(q)) | (uint32_t(__ldg(q + 1)) << 8) | (uint32_t(__ldg(q + 2)) << 16);
+          } else {
+            rgb = pcv;
+          }
+        } else {
+          rgb = __ldg(L + gy * (int64_t)Ex + gx);
+        }
+      }
+      const int k = (dy * 3 + dx) * 3;
+      v[k] = valid ? float(rgb & 255) : 0.f;
+      v[k + 1] = valid ? float((rgb >> 8) & 255) : 0.f;
+      v[k + 2] = valid ? float((rgb >> 16) & 255) : 0.f;
+    }
+  uint4* dst = reinterpret_cast<uint4*>(X + ((int64_t)b * P * P + pix) * 32);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (std::is_same<T, __half>::value) {
+        __half2 h2 = __floats2half2_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+        o[e] = *reinterpret_cast<uint32_t*>(&h2);
+      } else {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+        o[e] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+    }
+    dst[j] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Debug path: u8 windows given directly (n x P x P x 3) -> same stem input layout.
+template <typename T>
+__global__ void gather_raw_kernel(const uint8_t* tiles, int n, int P, T* X) {
+  const int b = blockIdx.y;
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n || pix >= P * P) return;
+  const int y = pix / P, x = pix % P;
+  float v[32];
+#pragma unroll
+  for (int k = 27; k < 32; ++k) v[k] = 0.f;
+#pragma unroll
+  for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      const int yy = y + dy - 1, xx = x + dx - 1;
+      const bool valid = yy >= 0 && yy < P && xx >= 0 && xx < P;
+      const uint8_t* q = tiles + (((int64_t)b * P + (valid ? yy : 0)) * P + (valid ? xx : 0)) * 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[(dy * 3 + dx) * 3 + c] = valid ? float(q[c]) : 0.f;
+    }
+  T* dst = X + ((int64_t)b * P * P + pix) * 32;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) dst[k] = T(v[k]);
+}
+
+// ------------------------------------------------------------------ K7 GAP + controller
+// g[b][c] = mean over the bottleneck's h x w pixels (fixed summation order), fp32.
+template <typename T>
+__global__ void gap_kernel(const T* E, int hw, int C, float* g) {
+  const int b = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const T* p = E + (int64_t)b * hw * C + c;
+  float s = 0.f;
+  for (int i = 0; i < hw; ++i) s += float(p[(int64_t)i * C]);
+  g[(int64_t)b * C + c] = s / float(hw);
+}
+
+// theta[b][t][j] = Wc[j] . [g_b ; onehot(cls_t) ; onehot(scl_t)] + bc[j]   (north_star controller)
+__global__ void controller_kernel(const float* g, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
+                                  const int* task_cls, const int* task_scl, int ntasks, float* theta) {
+  const int b = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= ntasks * kTheta) return;
+  const int t = idx / kTheta, j = idx % kTheta;
+  const int nin = Cb + ncls + nscl;
+  const float* w = Wc + (int64_t)j * nin;
+  const float* gb = g + (int64_t)b * Cb;
+  float s = 0.f;
+  for (int i = 0; i < Cb; ++i) s = fmaf(w[i], gb[i], s);
+  s += w[Cb + task_cls[t]] + w[Cb + ncls + task_scl[t]] + bc[j];
+  theta[((int64_t)b * ntasks + t) * kTheta + j] = s;
+}
+
+// ------------------------------------------------------------------ K8/K9 head + stitch
+// Per pixel: F = precls(D0) (8 x C0, fp32), then for every task of the tile's scale
+// z = W3 ReLU(W2 ReLU(W1 F + b1) + b2) + b3, p = 1/(1+e^-z) (north_star dynamic head),
+// and the fixed-point stitch acc += (1 << 28) + round(p 2^20) into the task's canvas
+// (R12: order-independent integer atomics). Debug mode writes p instead.
+template <typename T>
+__global__ void head_stitch_kernel(const T* D0, int C0p, int C0, int P, const float* Wpre, const float* bpre,
+                                   const float* theta, int ntasks, const uint32_t* tiles, int first,
+                                   HeadTaskTable tt, int S, int Hp, int Wp, int pad, float* out_p, float* out_F) {
+  __shared__ float sth[kMaxTasks * kTheta];
+  __shared__ float sw[kHead * 64];
+  __shared__ float sb[kHead];
+  const int b = blockIdx.y;
+  int lf = 0, ty = 0, tx = 0;
+  if (tiles) {
+    const uint32_t id = tiles[first + b];
+    lf = id >> 30;
+    ty = (id >> 15) & 0x7FFF;
+    tx = id & 0x7FFF;
+  }
+  const int f = 1 << lf;
+  for (int i = threadIdx.x; i < ntasks * kTheta; i += blockDim.x) sth[i] = theta[(int64_t)b * ntasks * kTheta + i];
+  for (int i = threadIdx.x; i < kHead * C0; i += blockDim.x) sw[i] = Wpre[i];
+  if (threadIdx.x < kHead) sb[threadIdx.x] = bpre[threadIdx.x];
+  __syncthreads();
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= P * P) return;
+  const T* d = D0 + ((int64_t)b * P * P + pix) * C0p;
+  float F[kHead];
+#pragma unroll
+  for (int o = 0; o < kHead; ++o) F[o] = sb[o];
+  for (int c = 0; c < C0; c += 8) {
+    uint4 u = *reinterpret_cast<const uint4*>(d + c);
+    const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float xv = float(e[k]);
+#pragma unroll
+      for (int o = 0; o < kHead; ++o) F[o] = fmaf(sw[o * C0 + c + k], xv, F[o]);
+    }
+  }
+  if (out_F) {
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) out_F[((int64_t)b * P * P + pix) * kHead + o] = F[o];
+  }
+  const int y = pix / P, x = pix % P;
+  const int Ey = Hp / f, Ex = Wp / f;
+  const int oy = min(ty * S, Ey - P), ox = min(tx * S, Ex - P);
+  const int cy = oy + y - pad / f, cx = ox + x - pad / f;
+  for (int t = 0; t < ntasks; ++t) {
+    if (tiles && tt.log2f[t] != lf) continue;
+    const float* th = sth + t * kTheta;
+    float h1[kHead], h2[kHead];
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      float s = th[64 + o];
+#pragma unroll
+      for (int i = 0; i < kHead; ++i) s = fmaf(th[o * 8 + i], F[i], s);
+      h1[o] = fmaxf(s, 0.f);
+    }
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      float s = th[136 + o];
+#pragma unroll
+      for (int i = 0; i < kHead; ++i) s = fmaf(th[72 + o * 8 + i], h1[i], s);
+      h2[o] = fmaxf(s, 0.f);
+    }
+    float z = th[152];
+#pragma unroll
+    for (int i = 0; i < kHead; ++i) z = fmaf(th[144 + i], h2[i], z);
+    const float p = 1.0f / (1.0f + expf(-z));
+    if (out_p) {
+      out_p[(((int64_t)b * ntasks + t) * P * P) + pix] = p;
+    } else {
+      const int Ht = tt.Ht[t], Wt = tt.Wt[t];
+      if (cy >= 0 && cy < Ht && cx >= 0 && cx < Wt && cy >= tt.row0[t] && cy < tt.row1[t]) {
+        const uint32_t q = __float2uint_rn(p * 1048576.0f);
+        atomicAdd(tt.canvas[t] + (int64_t)(cy - tt.row0[t]) * Wt + cx, (1u << 28) + q);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K10 finalize
+// cnt = acc >> 28, sum = acc & (2^28 - 1): prob = sum 2^-20 / cnt (0 if cnt = 0),
+// mask = 2 sum >= cnt 2^20 (exactly prob >= 1/2 on the fixed-point values, R12), area.
+__global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask,
+                                unsigned long long* area) {
+  __shared__ unsigned long long s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  unsigned long long local = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = acc[i];
+    const uint32_t cnt = a >> 28, sum = a & 0x0FFFFFFFu;
+    const bool m = cnt > 0 && 2ull * sum >= ((unsigned long long)cnt << 20);
+    if (prob) prob[i] = cnt ? (float(sum) * (1.0f / 1048576.0f)) / float(cnt) : 0.f;
+    if (mask) mask[i] = m ? 1 : 0;
+    local += m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(&s, local);
+  __syncthreads();
+  if (threadIdx.x == 0 && s) atomicAdd(area, s);
+}
+
+// ------------------------------------------------------------------ conversions (debug / weights)
+template <typename T>
+__global__ void f32_to_t_kernel(const float* in, T* out, int64_t rows, int cin, int cpad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * cpad) return;
+  const int64_t r = i / cpad;
+  const int c = i % cpad;
+  out[i] = T(c < cin ? in[r * cin + c] : 0.f);
+}
+template <typename T>
+__global__ void t_to_f32_kernel(const T* in, float* out, int64_t rows, int cout, int cpad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * cout) return;
+  const int64_t r = i / cout;
+  const int c = i % cout;
+  out[i] = float(in[r * cpad + c]);
+}
+
+// ==================================================================== host launchers
+void launch_pad_colour(const uint8_t* slide, int64_t W, DevState* st, cudaStream_t s) {
+  pad_colour_kernel<<<1, 32, 0, s>>>(slide, W, st);
+}
+void launch_pyramid(const FrontParams& p, const DevState* st, uint32_t* L2, uint32_t* L4, uint32_t* L8,
+                    uint8_t* luma8, cudaStream_t s) {
+  if (p.r8_1 <= p.r8_0) return;
+  dim3 grid((p.W8 + 127) / 128, p.r8_1 - p.r8_0);
+  pyramid_kernel<<<grid, 128, 0, s>>>(p, st, L2, L4, L8, luma8);
+}
+void launch_median(const uint8_t* g, uint8_t* out, int H8, int W8, int r0, int r1, cudaStream_t s) {
+  if (r1 <= r0) return;
+  dim3 grid((W8 + MB_X - 1) / MB_X, (r1 - r0 + MB_Y - 1) / MB_Y);
+  median7_kernel<<<grid, dim3(MB_X, MB_Y), 0, s>>>(g, out, H8, W8, r0, r1);
+}
+void launch_hist(const uint8_t* gm, int W8, int r0, int r1, int c0, int c1, unsigned long long* hist,
+                 cudaStream_t s) {
+  if (r1 <= r0 || c1 <= c0) return;
+  int64_t n = (int64_t)(r1 - r0) * (c1 - c0);
+  int blocks = (int)std::min<int64_t>(4 * 148, (n + 255) / 256);
+  hist_kernel<<<blocks, 256, 0, s>>>(gm, W8, r0, r1, c0, c1, hist);
+}
+void launch_otsu(const unsigned long long* hist, DevState* st, cudaStream_t s) { otsu_kernel<<<1, 256, 0, s>>>(hist, st); }
+void launch_fg(const uint8_t* gm, uint8_t* fg, int W8, int r0, int r1, int ir0, int ir1, int ic0, int ic1,
+               const DevState* st, cudaStream_t s) {
+  if (r1 <= r0) return;
+  dim3 grid((W8 + 255) / 256, r1 - r0);
+  fg_kernel<<<grid, 256, 0, s>>>(gm, fg, W8, r0, r1, ir0, ir1, ic0, ic1, st);
+}
+void launch_tile_keep(const uint8_t* fg, int W8, const ScaleGrid* grids, int nscales, int total, int P, int S,
+                      int64_t own0, int64_t own1, uint8_t* keep, cudaStream_t s) {
+  if (total <= 0) return;
+  tile_keep_kernel<<<(total * 32 + 255) / 256, 256, 0, s>>>(fg, W8, grids, nscales, total, P, S, own0, own1, keep);
+}
+void launch_compact(const uint8_t* keep, int total, const ScaleGrid* grids, int nscales, uint32_t* tiles, int* counts,
+                    cudaStream_t s) {
+  compact_kernel<<<1, 1024, 0, s>>>(keep, total, grids, nscales, tiles, counts);
+}
+template <typename T>
+void launch_gather(const uint32_t* tiles, int first, int n, int P, int S, const FrontParams& fp, const DevState* st,
+                   const uint32_t* L2, const uint32_t* L4, const uint32_t* L8, T* X, cudaStream_t s) {
+  dim3 grid((P * P + 255) / 256, n);
+  gather_kernel<T><<<grid, 256, 0, s>>>(tiles, first, n, P, S, fp, st, L2, L4, L8, X);
+}
+template <typename T>
+void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s) {
+  dim3 grid((P * P + 255) / 256, n);
+  gather_raw_kernel<T><<<grid, 256, 0, s>>>(tiles, n, P, X);
+}
+template <typename T>
+void launch_gap(const T* E, int n, int hw, int C, float* g, cudaStream_t s) {
+  dim3 grid((C + 127) / 128, n);
+  gap_kernel<T><<<grid, 128, 0, s>>>(E, hw, C, g);
+}
+void launch_controller(const float* g, int n, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
+                       const int* task_cls, const int* task_scl, int ntasks, float* theta, cudaStream_t s) {
+  dim3 grid((ntasks * kTheta + 127) / 128, n);
+  controller_kernel<<<grid, 128, 0, s>>>(g, Cb, Wc, bc, ncls, nscl, task_cls, task_scl, ntasks, theta);
+}
+template <typename T>
+void launch_head(const T* D0, int n, int C0p, int C0, int P, const float* Wpre, const float* bpre,
+                 const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
+                 int Hp, int Wp, int pad, float* out_p, float* out_F, cudaStream_t s) {
+  dim3 grid((P * P + 255) / 256, n);
+  head_stitch_kernel<T><<<grid, 256, 0, s>>>(D0, C0p, C0, P, Wpre, bpre, theta, ntasks, tiles, first, tt, S, Hp, Wp,
+                                             pad, out_p, out_F);
+}
+void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area,
+                     cudaStream_t s) {
+  if (n <= 0) return;
+  int blocks = (int)std::min<int64_t>(8 * 148, (n + 255) / 256);
+  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area);
+}
+template <typename T>
+void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, cudaStream_t s) {
+  int64_t n = rows * cpad;
+  f32_to_t_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cin, cpad);
+}
+template <typename T>
+void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, cudaStream_t s) {
+  int64_t n = rows * cout;
+  t_to_f32_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cout, cpad);
+}
+
+#define OS_INST(T)                                                                                                 \
+  template void launch_gather<T>(const uint32_t*, int, int, int, int, const FrontParams&, const DevState*,          \
+                                 const uint32_t*, const uint32_t*, const uint32_t*, T*, cudaStream_t);             \
+  template void launch_gather_raw<T>(const uint8_t*, int, int, T*, cudaStream_t);                                  \
+  template void launch_gap<T>(const T*, int, int, int, float*, cudaStream_t);                                      \
+  template void launch_head<T>(const T*, int, int, int, int, const float*, const float*, const float*, int,        \
+                               const uint32_t*, int, const HeadTaskTable&, int, int, int, int, float*, float*,     \
+                               cudaStream_t);                                                                     \
+  template void launch_f32_to_t<T>(const float*, T*, int64_t, int, int, cudaStream_t);                            \
+  template void launch_t_to_f32<T>(const T*, float*, int64_t, int, int, cudaStream_t);
+OS_INST(__half)
+OS_INST(__nv_bfloat16)
+
+}  // namespace osg

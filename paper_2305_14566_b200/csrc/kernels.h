@@ -1,0 +1,62 @@
+// kernels.h -- host launchers of the non-GEMM kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace osg {
+
+// Small device-resident state of one segment call.
+struct DevState {
+  uint8_t pc[4];   // pad colour (R, G, B, 0)
+  int otsu_t;
+  int g_pad;       // luma of the pad colour
+  int pad_;
+};
+
+// Per-task stitch targets passed by value to the head kernel.
+struct HeadTaskTable {
+  uint32_t* canvas[kMaxTasks];  // fixed-point accumulators, rows [row0, row1) of the task canvas
+  int Ht[kMaxTasks], Wt[kMaxTasks];
+  int row0[kMaxTasks], row1[kMaxTasks];
+  int log2f[kMaxTasks];
+};
+
+void launch_pad_colour(const uint8_t* slide, int64_t W, DevState* st, cudaStream_t s);
+void launch_pyramid(const FrontParams& p, const DevState* st, uint32_t* L2, uint32_t* L4, uint32_t* L8,
+                    uint8_t* luma8, cudaStream_t s);
+void launch_median(const uint8_t* g, uint8_t* out, int H8, int W8, int r0, int r1, cudaStream_t s);
+void launch_hist(const uint8_t* gm, int W8, int r0, int r1, int c0, int c1, unsigned long long* hist, cudaStream_t s);
+void launch_otsu(const unsigned long long* hist, DevState* st, cudaStream_t s);
+void launch_fg(const uint8_t* gm, uint8_t* fg, int W8, int r0, int r1, int ir0, int ir1, int ic0, int ic1,
+               const DevState* st, cudaStream_t s);
+void launch_tile_keep(const uint8_t* fg, int W8, const ScaleGrid* grids, int nscales, int total, int P, int S,
+                      int64_t own0, int64_t own1, uint8_t* keep, cudaStream_t s);
+void launch_compact(const uint8_t* keep, int total, const ScaleGrid* grids, int nscales, uint32_t* tiles, int* counts,
+                    cudaStream_t s);
+template <typename T>
+void launch_gather(const uint32_t* tiles, int first, int n, int P, int S, const FrontParams& fp, const DevState* st,
+                   const uint32_t* L2, const uint32_t* L4, const uint32_t* L8, T* X, cudaStream_t s);
+template <typename T>
+void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s);
+template <typename T>
+void launch_gap(const T* E, int n, int hw, int C, float* g, cudaStream_t s);
+void launch_controller(const float* g, int n, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
+                       const int* task_cls, const int* task_scl, int ntasks, float* theta, cudaStream_t s);
+template <typename T>
+void launch_head(const T* D0, int n, int C0p, int C0, int P, const float* Wpre, const float* bpre,
+                 const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
+                 int Hp, int Wp, int pad, float* out_p, float* out_F, cudaStream_t s);
+void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area,
+                     cudaStream_t s);
+template <typename T>
+void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, cudaStream_t s);
+template <typename T>
+void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, cudaStream_t s);
+
+// conv_tc.cu
+struct ConvPlan;  // opaque per-layer plan (TMA maps + launch config)
+
+}  // namespace osg

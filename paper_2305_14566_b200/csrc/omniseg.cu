@@ -1,0 +1,976 @@
+// omniseg.cu -- the C ABI (include/omniseg.h, include/omniseg_debug.h): argument
+// validation, weight packing, workspace, the launch sequence of one slide / band, and
+// the NCCL collectives of the multi-GPU band path. All arithmetic runs in the kernels
+// of kernels.cu and conv_tc.cu.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/omniseg.h"
+#include "../../include/omniseg_debug.h"
+#include "common.cuh"
+#include "conv_plan.h"
+#include "kernels.h"
+
+using namespace osg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (bytes == 0) return;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(-3, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+    }
+    n = bytes;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+  void* so = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  void load() {
+    if (so) return;
+    so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!so) throw Error(-4, std::string("dlopen libnccl.so.2 failed: ") + dlerror());
+    commInitRank = (decltype(commInitRank))dlsym(so, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(so, "ncclAllReduce");
+    broadcast = (decltype(broadcast))dlsym(so, "ncclBroadcast");
+    commDestroy = (decltype(commDestroy))dlsym(so, "ncclCommDestroy");
+    errStr = (decltype(errStr))dlsym(so, "ncclGetErrorString");
+    if (!commInitRank || !allReduce || !broadcast || !commDestroy || !errStr)
+      throw Error(-4, "libnccl.so.2 lacks required symbols");
+  }
+  void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error(-4, std::string(what) + ": " + errStr(r));
+  }
+};
+Nccl g_nccl;
+
+// ---------------------------------------------------------------- arch
+struct Arch {
+  int levels = 5, base = 32, head = 8, ncls = 6, slide_mag = 40, batch = 64, device = -1;
+  std::vector<int> scale_codes{5, 10, 20, 40};
+  bool bf16 = false;
+};
+
+Arch parse_arch(const char* s) {
+  OS_REQUIRE(s != nullptr, "arch string is NULL");
+  Arch a;
+  std::stringstream ss(s);
+  std::string kv;
+  while (std::getline(ss, kv, ';')) {
+    if (kv.empty()) continue;
+    auto eq = kv.find('=');
+    OS_REQUIRE(eq != std::string::npos, "arch: expected key=value, got '" + kv + "'");
+    std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
+    auto toi = [&](const std::string& x) {
+      try {
+        size_t pos = 0;
+        int r = std::stoi(x, &pos);
+        OS_REQUIRE(pos == x.size(), "arch: bad integer '" + x + "' for " + k);
+        return r;
+      } catch (const std::logic_error&) {
+        throw Error(-1, "arch: bad integer '" + x + "' for " + k);
+      }
+    };
+    if (k == "levels") a.levels = toi(v);
+    else if (k == "base") a.base = toi(v);
+    else if (k == "head") a.head = toi(v);
+    else if (k == "ncls") a.ncls = toi(v);
+    else if (k == "slide_mag") a.slide_mag = toi(v);
+    else if (k == "batch") a.batch = toi(v);
+    else if (k == "device") a.device = toi(v);
+    else if (k == "dtype") {
+      OS_REQUIRE(v == "fp16" || v == "bf16", "arch: dtype must be fp16 or bf16");
+      a.bf16 = v == "bf16";
+    } else if (k == "scale_codes") {
+      a.scale_codes.clear();
+      std::stringstream s2(v);
+      std::string x;
+      while (std::getline(s2, x, ',')) a.scale_codes.push_back(toi(x));
+    } else {
+      throw Error(-1, "arch: unknown key '" + k + "'");
+    }
+  }
+  OS_REQUIRE(a.levels >= 2 && a.levels <= 6, "arch: levels must be in [2, 6]");
+  OS_REQUIRE(a.base >= 8 && a.base <= 64 && (a.base & (a.base - 1)) == 0, "arch: base must be 8, 16, 32 or 64");
+  OS_REQUIRE((a.base << (a.levels - 1)) <= 2048, "arch: too many channels");
+  OS_REQUIRE(a.head == kHead, "arch: head must be 8 (3-layer 8-channel dynamic head)");
+  OS_REQUIRE(a.ncls >= 1 && a.ncls <= 64, "arch: ncls out of range");
+  OS_REQUIRE(!a.scale_codes.empty() && a.scale_codes.size() <= 8, "arch: 1..8 scale codes");
+  OS_REQUIRE(a.batch >= 1 && a.batch <= 4096, "arch: batch out of range");
+  OS_REQUIRE(a.slide_mag >= 1, "arch: slide_mag must be positive");
+  return a;
+}
+
+int pad16(int c) { return (c + 15) / 16 * 16; }
+
+struct Layer {
+  DevBuf w;      // [coutp][k*k][cinp] 16-bit
+  DevBuf b;      // [coutp] fp32
+  int cin = 0, cout = 0, cinp = 0, coutp = 0, k = 3, stride = 1;
+};
+
+struct LevelBufs {
+  DevBuf E, A, Bt;
+  int P = 0, C = 0;
+};
+
+}  // namespace
+
+// ==================================================================== the handle
+struct omniseg {
+  Arch arch;
+  int device = 0;
+  std::vector<int> C, Cp;  // channels per level (real, padded to 16)
+  Layer stem;
+  std::vector<Layer> enc_a, enc_b, down, up, dec_a, dec_b;
+  DevBuf Wpre, bpre, Wc, bc;
+  int nin = 0;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+
+  // workspace (per patch size / batch capacity)
+  int ws_P = 0, ws_B = 0;
+  DevBuf X0;
+  std::vector<LevelBufs> lv;
+  DevBuf g, theta, task_cls, task_scl;
+  // plans in launch order for one batch (rebuilt with the workspace)
+  struct Step {
+    int kind;  // 0 conv, 1 gap+controller marker
+    ConvPlan plan;
+  };
+  std::vector<ConvPlan> enc_plans, dec_plans;
+
+  // front end / canvases
+  DevBuf slide, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
+  std::vector<uint32_t> h_tiles;
+  int64_t n_tiles = 0;
+  int H8 = 0, W8 = 0, otsu_t = -1, g_pad = -1;
+  int64_t fg_r0 = 0, fg_r1 = 0;
+
+  // timing
+  cudaEvent_t ev[12] = {};
+  double timings[11] = {};
+  int conv_launches = 0, launches = 0;
+
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+
+  ~omniseg() {
+    if (comm) g_nccl.commDestroy(comm);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+};
+
+namespace {
+
+template <typename T>
+T to16(float v);
+template <>
+__half to16<__half>(float v) {
+  return __float2half_rn(v);
+}
+template <>
+__nv_bfloat16 to16<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// Upload one conv: blob order [cout][k][k][cin] fp32 -> device [coutp][k*k][cinp] 16-bit.
+template <typename T>
+void upload_conv(Layer& L, const float* w, const float* b, int cin, int cout, int k, int stride, int cinp, int coutp) {
+  L.cin = cin;
+  L.cout = cout;
+  L.cinp = cinp;
+  L.coutp = coutp;
+  L.k = k;
+  L.stride = stride;
+  std::vector<T> hw((size_t)coutp * k * k * cinp, to16<T>(0.f));
+  for (int o = 0; o < cout; ++o)
+    for (int t = 0; t < k * k; ++t)
+      for (int c = 0; c < cin; ++c) hw[((size_t)o * k * k + t) * cinp + c] = to16<T>(w[((size_t)o * k * k + t) * cin + c]);
+  std::vector<float> hb(coutp, 0.f);
+  for (int o = 0; o < cout; ++o) hb[o] = b[o];
+  L.w.ensure(hw.size() * sizeof(T));
+  L.b.ensure(hb.size() * sizeof(float));
+  OS_CUDA(cudaMemcpy(L.w.p, hw.data(), hw.size() * sizeof(T), cudaMemcpyHostToDevice));
+  OS_CUDA(cudaMemcpy(L.b.p, hb.data(), hb.size() * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+// Stem as a 1x1 conv over the 32-channel im2col input of the gather kernel:
+// column (dy*3 + dx)*3 + c  <->  blob weight [o][dy][dx][c] (identical flattening).
+template <typename T>
+void upload_stem(Layer& L, const float* w, const float* b, int cout, int coutp) {
+  std::vector<float> w32((size_t)cout * 32, 0.f);
+  for (int o = 0; o < cout; ++o)
+    for (int j = 0; j < 27; ++j) w32[(size_t)o * 32 + j] = w[(size_t)o * 27 + j];
+  upload_conv<T>(L, w32.data(), b, 32, cout, 1, 1, 32, coutp);
+}
+
+size_t param_count(const Arch& a) {
+  size_t n = 0;
+  auto conv = [&](int co, int k, int ci) { n += (size_t)co * k * k * ci + co; };
+  std::vector<int> C(a.levels);
+  for (int l = 0; l < a.levels; ++l) C[l] = a.base << l;
+  conv(C[0], 3, 3);
+  for (int l = 0; l < a.levels; ++l) {
+    conv(C[l], 3, C[l]);
+    conv(C[l], 3, C[l]);
+    if (l < a.levels - 1) conv(C[l + 1], 3, C[l]);
+  }
+  for (int l = a.levels - 2; l >= 0; --l) {
+    conv(C[l], 1, C[l + 1]);
+    conv(C[l], 3, C[l]);
+    conv(C[l], 3, C[l]);
+  }
+  conv(kHead, 1, C[0]);
+  const int nin = C[a.levels - 1] + a.ncls + (int)a.scale_codes.size();
+  n += (size_t)kTheta * nin + kTheta;
+  return n;
+}
+
+template <typename T>
+void load_weights(omniseg* h, const float* blob) {
+  const Arch& a = h->arch;
+  const int L = a.levels;
+  size_t o = 0;
+  auto take = [&](size_t n) {
+    const float* p = blob + o;
+    o += n;
+    return p;
+  };
+  auto conv = [&](Layer& dst, int co, int k, int ci, int stride) {
+    const float* w = take((size_t)co * k * k * ci);
+    const float* b = take(co);
+    upload_conv<T>(dst, w, b, ci, co, k, stride, pad16(ci), pad16(co));
+  };
+  {
+    const float* w = take((size_t)h->C[0] * 27);
+    const float* b = take(h->C[0]);
+    upload_stem<T>(h->stem, w, b, h->C[0], h->Cp[0]);
+  }
+  h->enc_a.resize(L);
+  h->enc_b.resize(L);
+  h->down.resize(L);
+  h->up.resize(L);
+  h->dec_a.resize(L);
+  h->dec_b.resize(L);
+  for (int l = 0; l < L; ++l) {
+    conv(h->enc_a[l], h->C[l], 3, h->C[l], 1);
+    conv(h->enc_b[l], h->C[l], 3, h->C[l], 1);
+    if (l < L - 1) conv(h->down[l], h->C[l + 1], 3, h->C[l], 2);
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    conv(h->up[l], h->C[l], 1, h->C[l + 1], 1);
+    conv(h->dec_a[l], h->C[l], 3, h->C[l], 1);
+    conv(h->dec_b[l], h->C[l], 3, h->C[l], 1);
+  }
+  {
+    const float* w = take((size_t)kHead * h->C[0]);
+    const float* b = take(kHead);
+    h->Wpre.ensure((size_t)kHead * h->C[0] * 4);
+    h->bpre.ensure(kHead * 4);
+    OS_CUDA(cudaMemcpy(h->Wpre.p, w, (size_t)kHead * h->C[0] * 4, cudaMemcpyHostToDevice));
+    OS_CUDA(cudaMemcpy(h->bpre.p, b, kHead * 4, cudaMemcpyHostToDevice));
+  }
+  {
+    const float* w = take((size_t)kTheta * h->nin);
+    const float* b = take(kTheta);
+    h->Wc.ensure((size_t)kTheta * h->nin * 4);
+    h->bc.ensure(kTheta * 4);
+    OS_CUDA(cudaMemcpy(h->Wc.p, w, (size_t)kTheta * h->nin * 4, cudaMemcpyHostToDevice));
+    OS_CUDA(cudaMemcpy(h->bc.p, b, kTheta * 4, cudaMemcpyHostToDevice));
+  }
+}
+
+// Level widths P >> l must suit the 128-pixel M tile: multiple of 128 or divisor of 128.
+void check_patch(const omniseg* h, int P) {
+  const int L = h->arch.levels;
+  OS_REQUIRE(P >= 16 && P % 16 == 0, "patch must be a positive multiple of 16");
+  OS_REQUIRE(P % (1 << (L - 1)) == 0, "patch must be divisible by 2^(levels-1)");
+  for (int l = 0; l < L; ++l) {
+    const int w = P >> l;
+    OS_REQUIRE(w % 128 == 0 || 128 % w == 0, "patch: level width " + std::to_string(w) +
+                                                  " must be a multiple or a divisor of 128");
+    OS_REQUIRE((int64_t)w * w >= 128, "patch: coarsest level must hold at least 128 pixels");
+  }
+}
+
+// Allocate the per-batch workspace and build the convolution plans.
+void ensure_workspace(omniseg* h, int P) {
+  const int B = h->arch.batch;
+  if (h->ws_P == P && h->ws_B == B) return;
+  check_patch(h, P);
+  const int L = h->arch.levels;
+  const size_t es = 2;  // 16-bit storage
+  h->X0.ensure((size_t)B * P * P * 32 * es);
+  h->lv.clear();
+  h->lv.resize(L);
+  for (int l = 0; l < L; ++l) {
+    LevelBufs& q = h->lv[l];
+    q.P = P >> l;
+    q.C = h->Cp[l];
+    const size_t n = (size_t)B * q.P * q.P * q.C * es;
+    q.E.ensure(n);
+    q.A.ensure(n);
+    q.Bt.ensure(n);
+  }
+  h->g.ensure((size_t)B * h->C[L - 1] * 4);
+  h->theta.ensure((size_t)B * kMaxTasks * kTheta * 4);
+  const bool bf = h->arch.bf16;
+  h->enc_plans.clear();
+  h->dec_plans.clear();
+  auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode) {
+    return make_conv_plan(bf, in, B, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
+                          res, out);
+  };
+  h->enc_plans.push_back(plan(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias));
+  for (int l = 0; l < L; ++l) {
+    LevelBufs& q = h->lv[l];
+    h->enc_plans.push_back(plan(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias));
+    h->enc_plans.push_back(plan(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu));
+    if (l < L - 1) h->enc_plans.push_back(plan(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias));
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    LevelBufs& q = h->lv[l];
+    const void* D = (l + 1 == L - 1) ? h->lv[l + 1].E.p : h->lv[l + 1].A.p;
+    h->dec_plans.push_back(plan(h->up[l], D, q.P / 2, q.E.p, q.A.p, kUpAdd));
+    h->dec_plans.push_back(plan(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias));
+    h->dec_plans.push_back(plan(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu));
+  }
+  h->ws_P = P;
+  h->ws_B = B;
+}
+
+struct Tasks {
+  int n = 0;
+  int f[kMaxTasks], log2f[kMaxTasks], cls[kMaxTasks], scl[kMaxTasks];
+  int64_t Ht[kMaxTasks], Wt[kMaxTasks], r0[kMaxTasks], r1[kMaxTasks];
+  int factors[kMaxScales], nf = 0;  // distinct factors, descending
+  int fmax = 1;
+};
+
+Tasks make_tasks(const omniseg* h, const int* scales, const int* classes, int n, int64_t H, int64_t W) {
+  OS_REQUIRE(n >= 1 && n <= kMaxTasks, "n_tasks must be in [1, 32]");
+  OS_REQUIRE(scales && classes, "scales/classes must not be NULL");
+  Tasks t;
+  t.n = n;
+  bool used[4] = {false, false, false, false};
+  for (int i = 0; i < n; ++i) {
+    const auto& sc = h->arch.scale_codes;
+    auto it = std::find(sc.begin(), sc.end(), scales[i]);
+    OS_REQUIRE(it != sc.end(), "scale " + std::to_string(scales[i]) + " is not in scale_codes");
+    OS_REQUIRE(scales[i] > 0 && h->arch.slide_mag % scales[i] == 0, "scale must divide slide_mag");
+    const int f = h->arch.slide_mag / scales[i];
+    OS_REQUIRE(f == 1 || f == 2 || f == 4 || f == 8, "level factor slide_mag/scale must be 1, 2, 4 or 8");
+    OS_REQUIRE(classes[i] >= 0 && classes[i] < h->arch.ncls, "class index out of range");
+    t.f[i] = f;
+    t.log2f[i] = f == 1 ? 0 : f == 2 ? 1 : f == 4 ? 2 : 3;
+    t.cls[i] = classes[i];
+    t.scl[i] = (int)(it - sc.begin());
+    t.Ht[i] = (H + f - 1) / f;
+    t.Wt[i] = (W + f - 1) / f;
+    used[t.log2f[i]] = true;
+  }
+  for (int l = 3; l >= 0; --l)
+    if (used[l]) t.factors[t.nf++] = 1 << l;
+  t.fmax = t.factors[0];
+  return t;
+}
+
+void record(omniseg* h, int i) { OS_CUDA(cudaEventRecord(h->ev[i], h->stream)); }
+
+// Run trunk + GAP/controller + head for `n` tiles already gathered into X0.
+template <typename T>
+void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int first, const HeadTaskTable& tt,
+                        int ntasks, int S, int Hp, int Wp, int pad, float* out_p, float* out_F, float* out_g) {
+  const int L = h->arch.levels;
+  cudaStream_t s = h->stream;
+  for (auto& pl : h->enc_plans) {
+    set_conv_batch(pl, n);
+    run_conv(pl, s);
+    h->conv_launches++;
+  }
+  const LevelBufs& bl = h->lv[L - 1];
+  launch_gap<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->g.as<float>(), s);
+  launch_controller(h->g.as<float>(), n, h->C[L - 1], h->Wc.as<float>(), h->bc.as<float>(), h->arch.ncls,
+                    (int)h->arch.scale_codes.size(), h->task_cls.as<int>(), h->task_scl.as<int>(), ntasks,
+                    h->theta.as<float>(), s);
+  h->launches += 2;
+  if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, h->g.p, (size_t)n * h->C[L - 1] * 4, cudaMemcpyDefault, s));
+  for (auto& pl : h->dec_plans) {
+    set_conv_batch(pl, n);
+    run_conv(pl, s);
+    h->conv_launches++;
+  }
+  launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], P, h->Wpre.as<float>(), h->bpre.as<float>(),
+                 h->theta.as<float>(), ntasks, tiles, first, tt, S, Hp, Wp, pad, out_p, out_F, s);
+  h->launches++;
+  OS_CUDA(cudaGetLastError());
+}
+
+void upload_tasks(omniseg* h, const Tasks& t) {
+  h->task_cls.ensure(kMaxTasks * 4);
+  h->task_scl.ensure(kMaxTasks * 4);
+  OS_CUDA(cudaMemcpyAsync(h->task_cls.p, t.cls, t.n * 4, cudaMemcpyHostToDevice, h->stream));
+  OS_CUDA(cudaMemcpyAsync(h->task_scl.p, t.scl, t.n * 4, cudaMemcpyHostToDevice, h->stream));
+}
+
+// One slide or one band. row0/row1: owned rows of the padded 40x frame.
+template <typename T>
+void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0, int64_t row1, int64_t b0,
+             int64_t b1, int pad, int P, int S, const Tasks& tk, float* out_prob, uint8_t* out_mask,
+             uint64_t* out_area) {
+  cudaStream_t s = h->stream;
+  h->conv_launches = 0;
+  h->launches = 0;
+  const int Hp = (int)((H + 2 * pad + 127) / 128 * 128), Wp = (int)((W + 2 * pad + 127) / 128 * 128);
+  const int H8 = Hp / 8, W8 = Wp / 8;
+  h->H8 = H8;
+  h->W8 = W8;
+  ensure_workspace(h, P);
+  record(h, 0);
+  // ---- upload (the band's slide rows [b0, b1))
+  const int64_t rows = b1 - b0;
+  const size_t slide_bytes = (size_t)rows * W * 3;
+  const uint8_t* dslide = rgb;
+  if (!is_device_ptr(rgb)) {
+    h->slide.ensure(slide_bytes);
+    OS_CUDA(cudaMemcpyAsync(h->slide.p, rgb, slide_bytes, cudaMemcpyHostToDevice, s));
+    dslide = h->slide.as<uint8_t>();
+  }
+  record(h, 1);
+  // ---- front end
+  h->state.ensure(sizeof(DevState));
+  DevState* st = h->state.as<DevState>();
+  if (b0 == 0) launch_pad_colour(dslide, W, st, s);
+  if (h->world > 1) {
+    g_nccl.check(g_nccl.broadcast(st, st, 4, ncclUint8, 0, h->comm, s), "ncclBroadcast(pad colour)");
+  }
+  bool needf[4] = {false, false, false, false};
+  for (int i = 0; i < tk.n; ++i) needf[tk.log2f[i]] = true;
+  if (needf[1]) h->L2.ensure((size_t)(Hp / 2) * (Wp / 2) * 4);
+  if (needf[2]) h->L4.ensure((size_t)(Hp / 4) * (Wp / 4) * 4);
+  if (needf[3]) h->L8.ensure((size_t)H8 * W8 * 4);
+  h->luma8.ensure((size_t)H8 * W8);
+  h->gm.ensure((size_t)H8 * W8);
+  h->fg.ensure((size_t)H8 * W8);
+  // level-8 rows: fg needed on [m0, m1) (tiles touching the band), luma on m0-3 .. m1+3
+  const int64_t halo = (int64_t)P * tk.fmax;
+  const int m0 = (int)std::max<int64_t>(0, (row0 - halo) / 8), m1 = (int)std::min<int64_t>(H8, (row1 + halo + 7) / 8);
+  const int l0 = std::max(0, m0 - 3), l1 = std::min(H8, m1 + 3);
+  h->fg_r0 = m0;
+  h->fg_r1 = m1;
+  // slide rows needed: padded rows [8 l0, 8 l1) -> slide rows [8 l0 - pad, 8 l1 - pad) clipped to [0, H)
+  const int64_t need0 = std::max<int64_t>(0, 8 * (int64_t)l0 - pad), need1 = std::min<int64_t>(H, 8 * (int64_t)l1 - pad);
+  OS_REQUIRE(need1 <= need0 || (need0 >= b0 && need1 <= b1), "band: rgb_band does not hold the rows the halo needs");
+  FrontParams fp{};
+  fp.slide = dslide;
+  fp.slide_row0 = b0;
+  fp.slide_rows = rows;
+  fp.H = H;
+  fp.W = W;
+  fp.pad = pad;
+  fp.Hp = Hp;
+  fp.Wp = Wp;
+  fp.H8 = H8;
+  fp.W8 = W8;
+  fp.r8_0 = l0;
+  fp.r8_1 = l1;
+  fp.own8_0 = (int)(row0 / 8);
+  fp.own8_1 = (int)(row1 / 8);
+  launch_pyramid(fp, st, needf[1] ? h->L2.as<uint32_t>() : nullptr, needf[2] ? h->L4.as<uint32_t>() : nullptr,
+                 needf[3] ? h->L8.as<uint32_t>() : nullptr, h->luma8.as<uint8_t>(), s);
+  // the median reads luma rows [m0-3, m1+3) with edge replication only at the frame border
+  launch_median(h->luma8.as<uint8_t>(), h->gm.as<uint8_t>(), H8, W8, m0, m1, s);
+  h->hist.ensure(256 * 8);
+  OS_CUDA(cudaMemsetAsync(h->hist.p, 0, 256 * 8, s));
+  const int ir0 = pad / 8, ir1 = (int)(pad / 8 + H / 8), ic0 = pad / 8, ic1 = (int)(pad / 8 + W / 8);
+  launch_hist(h->gm.as<uint8_t>(), W8, std::max(ir0, fp.own8_0), std::min(ir1, fp.own8_1), ic0, ic1,
+              h->hist.as<unsigned long long>(), s);
+  if (h->world > 1)
+    g_nccl.check(g_nccl.allReduce(h->hist.p, h->hist.p, 256, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(hist)");
+  launch_otsu(h->hist.as<unsigned long long>(), st, s);
+  launch_fg(h->gm.as<uint8_t>(), h->fg.as<uint8_t>(), W8, m0, m1, ir0, ir1, ic0, ic1, st, s);
+  // candidate grids (canonical order: factor descending, row, col)
+  std::vector<ScaleGrid> grids(tk.nf);
+  int total = 0;
+  for (int i = 0; i < tk.nf; ++i) {
+    const int f = tk.factors[i];
+    ScaleGrid& g = grids[i];
+    g.f = f;
+    g.log2f = f == 1 ? 0 : f == 2 ? 1 : f == 4 ? 2 : 3;
+    g.Ey = Hp / f;
+    g.Ex = Wp / f;
+    OS_REQUIRE(g.Ey >= P && g.Ex >= P, "patch larger than the padded slide at some scale");
+    g.ny = (g.Ey - P + S - 1) / S + 1;
+    g.nx = (g.Ex - P + S - 1) / S + 1;
+    OS_REQUIRE(g.ny < 32768 && g.nx < 32768, "tile grid too large");
+    g.base = total;
+    total += g.ny * g.nx;
+  }
+  h->grids.ensure(sizeof(ScaleGrid) * kMaxScales);
+  OS_CUDA(cudaMemcpyAsync(h->grids.p, grids.data(), sizeof(ScaleGrid) * tk.nf, cudaMemcpyHostToDevice, s));
+  h->keep.ensure(total);
+  h->tiles.ensure((size_t)total * 4);
+  h->counts.ensure((kMaxScales + 1) * 4);
+  launch_tile_keep(h->fg.as<uint8_t>(), W8, h->grids.as<ScaleGrid>(), tk.nf, total, P, S, row0, row1,
+                   h->keep.as<uint8_t>(), s);
+  launch_compact(h->keep.as<uint8_t>(), total, h->grids.as<ScaleGrid>(), tk.nf, h->tiles.as<uint32_t>(),
+                 h->counts.as<int>(), s);
+  h->launches += 9;
+  int counts[kMaxScales + 1];
+  DevState hst;
+  OS_CUDA(cudaMemcpyAsync(counts, h->counts.p, sizeof(counts), cudaMemcpyDeviceToHost, s));
+  OS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  OS_CUDA(cudaStreamSynchronize(s));
+  h->n_tiles = counts[kMaxScales];
+  h->otsu_t = hst.otsu_t;
+  h->g_pad = hst.g_pad;
+  record(h, 2);
+  // ---- canvases (owned rows only)
+  HeadTaskTable tt{};
+  int64_t canvas_px = 0;
+  std::vector<int64_t> off(tk.n);
+  std::vector<int64_t> r0(tk.n), r1(tk.n);
+  for (int t = 0; t < tk.n; ++t) {
+    omniseg_band_rows(H, row0, row1, pad, tk.f[t], &r0[t], &r1[t]);
+    off[t] = canvas_px;
+    canvas_px += (r1[t] - r0[t]) * tk.Wt[t];
+  }
+  h->canvas.ensure((size_t)std::max<int64_t>(canvas_px, 1) * 4);
+  OS_CUDA(cudaMemsetAsync(h->canvas.p, 0, (size_t)canvas_px * 4, s));
+  for (int t = 0; t < tk.n; ++t) {
+    tt.canvas[t] = h->canvas.as<uint32_t>() + off[t];
+    tt.Ht[t] = (int)tk.Ht[t];
+    tt.Wt[t] = (int)tk.Wt[t];
+    tt.row0[t] = (int)r0[t];
+    tt.row1[t] = (int)r1[t];
+    tt.log2f[t] = tk.log2f[t];
+  }
+  upload_tasks(h, tk);
+  // ---- hot loop over batches of kept tiles
+  const int B = h->arch.batch;
+  double t_gather = 0;
+  for (int64_t first = 0; first < h->n_tiles; first += B) {
+    const int n = (int)std::min<int64_t>(B, h->n_tiles - first);
+    launch_gather<T>(h->tiles.as<uint32_t>(), (int)first, n, P, S, fp, st, h->L2.as<uint32_t>(),
+                     h->L4.as<uint32_t>(), h->L8.as<uint32_t>(), h->X0.as<T>(), s);
+    h->launches++;
+    run_trunk_and_head<T>(h, n, P, h->tiles.as<uint32_t>(), (int)first, tt, tk.n, S, Hp, Wp, pad, nullptr, nullptr,
+                          nullptr);
+  }
+  (void)t_gather;
+  record(h, 3);
+  // ---- finalize into the caller's buffers (device) or staging + D2H (host)
+  const bool prob_dev = is_device_ptr(out_prob), mask_dev = is_device_ptr(out_mask);
+  float* dprob = nullptr;
+  uint8_t* dmask = nullptr;
+  if (out_prob) {
+    if (prob_dev) dprob = out_prob;
+    else {
+      h->prob.ensure((size_t)std::max<int64_t>(canvas_px, 1) * 4);
+      dprob = h->prob.as<float>();
+    }
+  }
+  if (out_mask) {
+    if (mask_dev) dmask = out_mask;
+    else {
+      h->mask.ensure((size_t)std::max<int64_t>(canvas_px, 1));
+      dmask = h->mask.as<uint8_t>();
+    }
+  }
+  h->area.ensure(kMaxTasks * 8);
+  OS_CUDA(cudaMemsetAsync(h->area.p, 0, kMaxTasks * 8, s));
+  for (int t = 0; t < tk.n; ++t) {
+    const int64_t n = (r1[t] - r0[t]) * tk.Wt[t];
+    launch_finalize(tt.canvas[t], n, dprob ? dprob + off[t] : nullptr, dmask ? dmask + off[t] : nullptr,
+                    h->area.as<unsigned long long>() + t, s);
+    h->launches++;
+  }
+  if (h->world > 1)
+    g_nccl.check(g_nccl.allReduce(h->area.p, h->area.p, tk.n, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(area)");
+  record(h, 4);
+  if (out_prob && !prob_dev)
+    OS_CUDA(cudaMemcpyAsync(out_prob, dprob, (size_t)canvas_px * 4, cudaMemcpyDeviceToHost, s));
+  if (out_mask && !mask_dev)
+    OS_CUDA(cudaMemcpyAsync(out_mask, dmask, (size_t)canvas_px, cudaMemcpyDeviceToHost, s));
+  if (out_area) OS_CUDA(cudaMemcpyAsync(out_area, h->area.p, tk.n * 8, cudaMemcpyDefault, s));
+  record(h, 5);
+  OS_CUDA(cudaStreamSynchronize(s));
+  float ms;
+  auto el = [&](int a, int b) {
+    OS_CUDA(cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]));
+    return (double)ms;
+  };
+  for (double& v : h->timings) v = 0;
+  h->timings[0] = el(0, 1);
+  h->timings[1] = el(1, 2);
+  h->timings[3] = el(2, 3);  // gather + trunk + gap/controller + head (per-kind split: bench.py)
+  h->timings[6] = el(3, 4);
+  h->timings[7] = el(4, 5);
+  h->timings[8] = el(0, 5);
+  h->timings[9] = h->conv_launches;
+  h->timings[10] = h->conv_launches + h->launches;
+}
+
+int fail(const Error& e) {
+  g_last_error = e.what();
+  return e.code;
+}
+
+void validate_common(int64_t H, int64_t W, int pad, int P, int S) {
+  OS_REQUIRE(H >= 2 && W >= 2, "H and W must be >= 2");
+  OS_REQUIRE(pad >= 0 && pad % 8 == 0, "pad must be a non-negative multiple of 8");
+  OS_REQUIRE(S >= 8 && S <= P && S % 8 == 0, "stride must satisfy 8 <= stride <= patch, stride % 8 == 0");
+  OS_REQUIRE(P % 8 == 0, "patch must be a multiple of 8");
+  OS_REQUIRE((H / 8) * (W / 8) < (int64_t(1) << 28), "slide too large for the exact Otsu (interior >= 2^28 px)");
+  const int per_axis = (P + S - 1) / S + 1;
+  OS_REQUIRE(per_axis * per_axis <= 15, "coverage count could exceed 15: need (ceil(P/S)+1)^2 <= 15");
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+omniseg_t* omniseg_create(const char* arch, const void* weights, size_t nbytes) {
+  try {
+    auto h = std::make_unique<omniseg>();
+    h->arch = parse_arch(arch);
+    if (h->arch.device >= 0) OS_CUDA(cudaSetDevice(h->arch.device));
+    OS_CUDA(cudaGetDevice(&h->device));
+    int major = 0, minor = 0;
+    OS_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device));
+    OS_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, h->device));
+    if (major != 10 || minor != 0)
+      throw Error(-2, "libomniseg is built for sm_100a (B200); device is sm_" + std::to_string(major) +
+                          std::to_string(minor));
+    const int L = h->arch.levels;
+    for (int l = 0; l < L; ++l) {
+      h->C.push_back(h->arch.base << l);
+      h->Cp.push_back(pad16(h->arch.base << l));
+    }
+    h->nin = h->C[L - 1] + h->arch.ncls + (int)h->arch.scale_codes.size();
+    OS_REQUIRE(weights != nullptr, "weights is NULL");
+    const size_t need = param_count(h->arch) * 4;
+    OS_REQUIRE(nbytes == need, "weights: expected " + std::to_string(need) + " bytes, got " + std::to_string(nbytes));
+    std::vector<float> blob(need / 4);
+    OS_CUDA(cudaMemcpy(blob.data(), weights, need, cudaMemcpyDefault));
+    if (h->arch.bf16)
+      load_weights<__nv_bfloat16>(h.get(), blob.data());
+    else
+      load_weights<__half>(h.get(), blob.data());
+    OS_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    for (auto& e : h->ev) OS_CUDA(cudaEventCreate(&e));
+    return h.release();
+  } catch (const Error& e) {
+    fail(e);
+    return nullptr;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return nullptr;
+  }
+}
+
+int omniseg_set_stream(omniseg_t* h, void* stream) {
+  if (!h) return fail(Error(-1, "handle is NULL"));
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
+  return 0;
+}
+
+int64_t omniseg_output_size(const omniseg_t* h, int64_t H, int64_t W, int scale) {
+  if (!h || scale <= 0 || h->arch.slide_mag % scale) return -1;
+  const int64_t f = h->arch.slide_mag / scale;
+  return ((H + f - 1) / f) * ((W + f - 1) / f);
+}
+
+int omniseg_band_rows(int64_t H, int64_t row0, int64_t row1, int pad, int f, int64_t* r0_t, int64_t* r1_t) {
+  if (f <= 0 || !r0_t || !r1_t) return fail(Error(-1, "band_rows: bad arguments"));
+  const int64_t Ht = (H + f - 1) / f;
+  auto cdiv = [](int64_t a, int64_t b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); };
+  *r0_t = std::min<int64_t>(Ht, std::max<int64_t>(0, cdiv(row0 - pad, f)));
+  *r1_t = std::min<int64_t>(Ht, std::max<int64_t>(0, cdiv(row1 - pad, f)));
+  return 0;
+}
+
+int omniseg_segment_slide(omniseg_t* h, const uint8_t* rgb_u8, int64_t H, int64_t W, int pad, int patch, int stride,
+                          const int* scales, const int* classes, int n_tasks, float* out_prob, uint8_t* out_mask,
+                          uint64_t* out_area) {
+  try {
+    OS_REQUIRE(h != nullptr, "handle is NULL");
+    OS_REQUIRE(rgb_u8 != nullptr, "rgb_u8 is NULL");
+    OS_CUDA(cudaSetDevice(h->device));
+    validate_common(H, W, pad, patch, stride);
+    Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
+    const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
+    if (h->arch.bf16)
+      segment<__nv_bfloat16>(h, rgb_u8, H, W, 0, Hp, 0, H, pad, patch, stride, tk, out_prob, out_mask, out_area);
+    else
+      segment<__half>(h, rgb_u8, H, W, 0, Hp, 0, H, pad, patch, stride, tk, out_prob, out_mask, out_area);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(Error(-2, e.what()));
+  }
+}
+
+int omniseg_comm_init(omniseg_t* h, const void* id, int world, int rank) {
+  try {
+    OS_REQUIRE(h && id, "comm_init: NULL argument");
+    OS_REQUIRE(world >= 1 && rank >= 0 && rank < world, "comm_init: bad world/rank");
+    OS_CUDA(cudaSetDevice(h->device));
+    if (world == 1) {
+      h->world = 1;
+      h->rank = 0;
+      return 0;
+    }
+    g_nccl.load();
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    if (h->comm) g_nccl.commDestroy(h->comm);
+    h->comm = nullptr;
+    g_nccl.check(g_nccl.commInitRank(&h->comm, world, uid, rank), "ncclCommInitRank");
+    h->world = world;
+    h->rank = rank;
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64_t W, int64_t row0, int64_t row1,
+                         int pad, int patch, int stride, const int* scales, const int* classes, int n_tasks,
+                         float* out_prob, uint8_t* out_mask, uint64_t* out_area) {
+  try {
+    OS_REQUIRE(h != nullptr, "handle is NULL");
+    OS_CUDA(cudaSetDevice(h->device));
+    validate_common(H, W, pad, patch, stride);
+    Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
+    const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
+    OS_REQUIRE(row0 >= 0 && row0 < row1 && row1 <= Hp, "band: need 0 <= row0 < row1 <= Hp");
+    OS_REQUIRE(row0 % (8 * stride) == 0 && (row1 == Hp || row1 % (8 * stride) == 0),
+               "band: row0/row1 must be multiples of 8*stride (row1 may be Hp)");
+    const int64_t halo = (int64_t)patch * tk.fmax + 64;
+    const int64_t b0 = std::max<int64_t>(0, std::min<int64_t>(H, row0 - pad - halo));
+    const int64_t b1 = std::max<int64_t>(0, std::min<int64_t>(H, row1 - pad + halo));
+    OS_REQUIRE(b1 > b0 || rgb_band != nullptr, "band: empty");
+    if (row0 == 0) OS_REQUIRE(b0 == 0, "band 0 must start at slide row 0");
+    if (h->arch.bf16)
+      segment<__nv_bfloat16>(h, rgb_band, H, W, row0, row1, b0, b1, pad, patch, stride, tk, out_prob, out_mask,
+                             out_area);
+    else
+      segment<__half>(h, rgb_band, H, W, row0, row1, b0, b1, pad, patch, stride, tk, out_prob, out_mask, out_area);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(Error(-2, e.what()));
+  }
+}
+
+int omniseg_get_tiles(const omniseg_t* h, uint32_t* tiles, int64_t cap, int64_t* n) {
+  try {
+    OS_REQUIRE(h && n, "get_tiles: NULL argument");
+    *n = h->n_tiles;
+    if (tiles && cap > 0 && h->n_tiles > 0)
+      OS_CUDA(cudaMemcpy(tiles, h->tiles.p, std::min<int64_t>(cap, h->n_tiles) * 4, cudaMemcpyDeviceToHost));
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+int omniseg_get_fgmask(const omniseg_t* h, uint8_t* mask, int64_t cap, int64_t* h8, int64_t* w8, int* otsu_t,
+                       int* g_pad) {
+  try {
+    OS_REQUIRE(h, "get_fgmask: NULL handle");
+    if (h8) *h8 = h->H8;
+    if (w8) *w8 = h->W8;
+    if (otsu_t) *otsu_t = h->otsu_t;
+    if (g_pad) *g_pad = h->g_pad;
+    const int64_t n = (int64_t)h->H8 * h->W8;
+    if (mask && cap >= n && n > 0) {
+      // rows outside [fg_r0, fg_r1) were not computed by this call: report them as 0
+      std::memset(mask, 0, n);
+      const int64_t a = h->fg_r0 * h->W8, b = h->fg_r1 * h->W8;
+      if (b > a) OS_CUDA(cudaMemcpy(mask + a, h->fg.as<uint8_t>() + a, b - a, cudaMemcpyDeviceToHost));
+    }
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+int omniseg_get_timings(const omniseg_t* h, double* out, int cap) {
+  if (!h || !out) return fail(Error(-1, "get_timings: NULL argument"));
+  for (int i = 0; i < cap && i < 11; ++i) out[i] = h->timings[i];
+  return 0;
+}
+
+const char* omniseg_last_error(void) { return g_last_error.c_str(); }
+
+void omniseg_destroy(omniseg_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  delete h;
+}
+
+// ---------------------------------------------------------------- debug entry points
+int omniseg_debug_predict_tiles(omniseg_t* h, const uint8_t* tiles_u8, int n, int P, const int* cls, const int* scl,
+                                int n_tasks, float* out_p, float* out_g, float* out_F) {
+  try {
+    OS_REQUIRE(h && tiles_u8 && cls && scl && out_p, "predict_tiles: NULL argument");
+    OS_REQUIRE(n >= 1 && n <= h->arch.batch, "predict_tiles: 1 <= n <= batch");
+    OS_REQUIRE(n_tasks >= 1 && n_tasks <= kMaxTasks, "predict_tiles: bad n_tasks");
+    OS_CUDA(cudaSetDevice(h->device));
+    for (int t = 0; t < n_tasks; ++t) {
+      OS_REQUIRE(cls[t] >= 0 && cls[t] < h->arch.ncls, "predict_tiles: class out of range");
+      OS_REQUIRE(scl[t] >= 0 && scl[t] < (int)h->arch.scale_codes.size(), "predict_tiles: scale index out of range");
+    }
+    ensure_workspace(h, P);
+    cudaStream_t s = h->stream;
+    DevBuf dt, dp, dF, dg;
+    const uint8_t* src = tiles_u8;
+    const size_t tb = (size_t)n * P * P * 3;
+    if (!is_device_ptr(tiles_u8)) {
+      dt.ensure(tb);
+      OS_CUDA(cudaMemcpyAsync(dt.p, tiles_u8, tb, cudaMemcpyHostToDevice, s));
+      src = dt.as<uint8_t>();
+    }
+    Tasks tk;
+    tk.n = n_tasks;
+    for (int t = 0; t < n_tasks; ++t) {
+      tk.cls[t] = cls[t];
+      tk.scl[t] = scl[t];
+    }
+    upload_tasks(h, tk);
+    dp.ensure((size_t)n * n_tasks * P * P * 4);
+    if (out_F) dF.ensure((size_t)n * P * P * kHead * 4);
+    if (out_g) dg.ensure((size_t)n * h->C[h->arch.levels - 1] * 4);
+    HeadTaskTable tt{};
+    if (h->arch.bf16) {
+      launch_gather_raw<__nv_bfloat16>(src, n, P, h->X0.as<__nv_bfloat16>(), s);
+      run_trunk_and_head<__nv_bfloat16>(h, n, P, nullptr, 0, tt, n_tasks, P, P, P, 0, dp.as<float>(),
+                                        out_F ? dF.as<float>() : nullptr, out_g ? dg.as<float>() : nullptr);
+    } else {
+      launch_gather_raw<__half>(src, n, P, h->X0.as<__half>(), s);
+      run_trunk_and_head<__half>(h, n, P, nullptr, 0, tt, n_tasks, P, P, P, 0, dp.as<float>(),
+                                 out_F ? dF.as<float>() : nullptr, out_g ? dg.as<float>() : nullptr);
+    }
+    OS_CUDA(cudaMemcpyAsync(out_p, dp.p, (size_t)n * n_tasks * P * P * 4, cudaMemcpyDefault, s));
+    if (out_F) OS_CUDA(cudaMemcpyAsync(out_F, dF.p, (size_t)n * P * P * kHead * 4, cudaMemcpyDefault, s));
+    if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, dg.p, (size_t)n * h->C[h->arch.levels - 1] * 4, cudaMemcpyDefault, s));
+    OS_CUDA(cudaStreamSynchronize(s));
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(Error(-2, e.what()));
+  }
+}
+
+int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Cin, const float* w, const float* b,
+                       int Cout, int k, int stride, const float* r, int mode, float* y) {
+  try {
+    OS_REQUIRE(h && x && w && b && y, "debug_conv: NULL argument");
+    OS_REQUIRE(mode >= 0 && mode <= 3, "debug_conv: bad mode");
+    OS_REQUIRE((mode != 1 && mode != 2) || r, "debug_conv: mode needs r");
+    OS_REQUIRE(mode != 2 || (k == 1 && stride == 1), "debug_conv: mode 2 is a 1x1 stride-1 conv");
+    OS_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    const bool bf = h->arch.bf16;
+    const int cinp = pad16(Cin), coutp = pad16(Cout);
+    const int Ho = (H - 1) / stride + 1, Wo = (W - 1) / stride + 1;
+    const int oh = mode == 2 ? 2 * Ho : Ho, ow = mode == 2 ? 2 * Wo : Wo;
+    Layer L;
+    std::vector<float> wv(w, w + (size_t)Cout * k * k * Cin), bv(b, b + Cout);
+    if (bf)
+      upload_conv<__nv_bfloat16>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp);
+    else
+      upload_conv<__half>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp);
+    DevBuf f32in, xin, rin, f32r, out, f32o;
+    const int64_t rows_in = (int64_t)B * H * W, rows_out = (int64_t)B * oh * ow;
+    f32in.ensure(rows_in * Cin * 4);
+    xin.ensure(rows_in * cinp * 2);
+    OS_CUDA(cudaMemcpyAsync(f32in.p, x, rows_in * Cin * 4, cudaMemcpyHostToDevice, s));
+    if (r) {
+      f32r.ensure(rows_out * Cout * 4);
+      rin.ensure(rows_out * coutp * 2);
+      OS_CUDA(cudaMemcpyAsync(f32r.p, r, rows_out * Cout * 4, cudaMemcpyHostToDevice, s));
+    }
+    out.ensure(rows_out * coutp * 2);
+    f32o.ensure(rows_out * Cout * 4);
+    if (bf) {
+      launch_f32_to_t<__nv_bfloat16>(f32in.as<float>(), xin.as<__nv_bfloat16>(), rows_in, Cin, cinp, s);
+      if (r) launch_f32_to_t<__nv_bfloat16>(f32r.as<float>(), rin.as<__nv_bfloat16>(), rows_out, Cout, coutp, s);
+    } else {
+      launch_f32_to_t<__half>(f32in.as<float>(), xin.as<__half>(), rows_in, Cin, cinp, s);
+      if (r) launch_f32_to_t<__half>(f32r.as<float>(), rin.as<__half>(), rows_out, Cout, coutp, s);
+    }
+    ConvPlan p = make_conv_plan(bf, xin.p, B, H, W, cinp, L.w.p, L.b.as<float>(), coutp, k, stride, mode,
+                                r ? rin.p : nullptr, out.p);
+    run_conv(p, s);
+    if (bf)
+      launch_t_to_f32<__nv_bfloat16>(out.as<__nv_bfloat16>(), f32o.as<float>(), rows_out, Cout, coutp, s);
+    else
+      launch_t_to_f32<__half>(out.as<__half>(), f32o.as<float>(), rows_out, Cout, coutp, s);
+    OS_CUDA(cudaMemcpyAsync(y, f32o.p, rows_out * Cout * 4, cudaMemcpyDeviceToHost, s));
+    OS_CUDA(cudaStreamSynchronize(s));
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(Error(-2, e.what()));
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+"""GPU parity of the tcgen05 implicit-GEMM convolution (through the C ABI,
+omniseg_debug_conv) against the oracle's convolution (fp64) on seeded inputs.
+
+Inputs and weights are drawn exactly representable in fp16, so the only
+differences are the fp32 accumulation order and the final 16-bit rounding of the
+stored output: |gpu - oracle| <= 2^-10 |oracle| (fp16 half-ulp, relative) + 1e-3
+absolute slack for cancellation."""
+import numpy as np
+import pytest
+
+from oracle import net as nn
+from omniseg_inputs import arch_dict, arch_string, make_weights
+
+pytestmark = pytest.mark.gpu
+
+TOL_REL = 2.0 ** -10
+
+
+@pytest.fixture(scope="module")
+def h(gpu_lib):
+    from paper_2305_14566_b200 import Omniseg
+    a = arch_dict(levels=3, base=8, ncls=1, scale_codes=(1,), slide_mag=1, batch=4)
+    return Omniseg(arch_string(a), make_weights(a, 1))
+
+
+def _f16(a):
+    return a.astype(np.float16).astype(np.float64)
+
+
+def _ref(x, w, b, stride, r, mode):
+    out = []
+    for i in range(x.shape[0]):
+        y = nn.conv2d(x[i], w, b, stride)
+        if mode == 0:
+            y = np.maximum(y, 0)
+        elif mode == 1:
+            y = np.maximum(y + r[i], 0)
+        elif mode == 2:
+            y = r[i] + nn.up2(y)
+        out.append(y)
+    return np.stack(out)
+
+
+CASES = [
+    # B, H, W, Cin, Cout, k, stride, mode
+    (2, 16, 16, 16, 16, 3, 1, 0),
+    (2, 64, 64, 32, 32, 3, 1, 0),
+    (1, 128, 128, 32, 32, 3, 1, 1),
+    (1, 256, 256, 32, 64, 3, 2, 0),
+    (2, 32, 32, 64, 64, 3, 1, 1),
+    (2, 32, 32, 64, 128, 3, 2, 0),
+    (1, 16, 16, 256, 256, 3, 1, 0),
+    (1, 16, 16, 256, 512, 3, 1, 1),
+    (1, 16, 16, 512, 512, 3, 1, 0),
+    (2, 16, 16, 64, 32, 1, 1, 2),
+    (1, 32, 32, 512, 256, 1, 1, 2),
+    (3, 8, 16, 32, 16, 3, 1, 3),
+    (1, 512, 512, 32, 32, 3, 1, 0),
+    (1, 32, 32, 48, 48, 3, 1, 1),   # 48 channels: K chunk 16, N tile 16
+]
+
+
+@pytest.mark.parametrize("B,H,W,Cin,Cout,k,stride,mode", CASES)
+def test_conv_parity(h, B, H, W, Cin, Cout, k, stride, mode):
+    rng = np.random.default_rng(B * 1000 + H + Cin + Cout + k + stride + mode)
+    x = _f16(rng.standard_normal((B, H, W, Cin)))
+    w = _f16(rng.standard_normal((Cout, k, k, Cin)) * np.sqrt(2.0 / (k * k * Cin)))
+    b = rng.standard_normal(Cout).astype(np.float32).astype(np.float64) * 0.1
+    Ho, Wo = (H - 1) // stride + 1, (W - 1) // stride + 1
+    r = None
+    if mode == 1:
+        r = _f16(rng.standard_normal((B, Ho, Wo, Cout)))
+    elif mode == 2:
+        r = _f16(rng.standard_normal((B, 2 * Ho, 2 * Wo, Cout)))
+    ref = _ref(x, w, b, stride, r, mode)
+    got = h.conv(x, w, b, stride=stride, r=r, mode=mode)
+    err = np.abs(got - ref)
+    bound = TOL_REL * np.abs(ref) + 1e-3
+    assert got.shape == ref.shape
+    assert (err <= bound).all(), f"max err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"

@@ -1,0 +1,138 @@
+"""GPU end-to-end parity through the C ABI against the oracle (north_star gates):
+tile lists and foreground masks bit-exact; per-pixel |p_gpu - p_oracle| <= 1e-2;
+masks agree on >= 99.9% of pixels and every disagreement sits where the oracle
+probability is within 1e-2 of 0.5."""
+import numpy as np
+import pytest
+
+from omniseg_inputs import arch_string, blank_slide, make_slide, random_tiles, workload
+from oracle import frontend as fe
+from oracle import net as nn
+from oracle import pipeline as op
+
+pytestmark = pytest.mark.gpu
+
+P_TOL = 1e-2
+
+
+def unpack_tiles(ids, Hp, Wp, P, S):
+    out = []
+    for v in ids.tolist():
+        lf, ty, tx = v >> 30, (v >> 15) & 0x7FFF, v & 0x7FFF
+        f = 1 << lf
+        out.append((f, min(ty * S, Hp // f - P), min(tx * S, Wp // f - P)))
+    return out
+
+
+def check_prob_mask(p_gpu, m_gpu, p_ref, m_ref, tag=""):
+    d = np.abs(p_gpu.astype(np.float64) - p_ref)
+    assert d.max() <= P_TOL, f"{tag} max |dp| = {d.max():.4g}"
+    dis = m_gpu != m_ref
+    agree = 1.0 - dis.mean()
+    assert agree >= 0.999, f"{tag} mask agreement {agree:.5f}"
+    if dis.any():
+        assert (np.abs(p_ref[dis] - 0.5) <= P_TOL).all(), f"{tag} mask flip away from 0.5"
+    return d.max(), agree
+
+
+def run_gpu(w, slide):
+    from paper_2305_14566_b200 import Omniseg
+    h = Omniseg(arch_string(w.arch), w.weights())
+    H, W = slide.shape[:2]
+    n = sum(h.output_size(H, W, s) for s in w.scales)
+    prob = np.zeros(n, np.float32)
+    mask = np.zeros(n, np.uint8)
+    area = np.zeros(len(w.scales), np.uint64)
+    h.segment_slide(slide, H, W, w.pad, w.patch, w.stride, w.scales, w.classes, prob, mask, area)
+    return h, prob, mask, area
+
+
+def split(arr, H, W, w, arch):
+    out, o = [], 0
+    for s in w.scales:
+        f = arch["slide_mag"] // s
+        n = ((H + f - 1) // f) * ((W + f - 1) // f)
+        out.append(arr[o:o + n].reshape((H + f - 1) // f, (W + f - 1) // f))
+        o += n
+    return out
+
+
+@pytest.fixture(scope="module")
+def cfg1(gpu_lib):
+    w = workload(1)
+    slide = make_slide(w.slide).numpy()
+    ref = op.segment_slide(slide, w.weights(), arch_string(w.arch), w.pad, w.patch, w.stride, w.scales, w.classes)
+    h, prob, mask, area = run_gpu(w, slide)
+    return w, slide, ref, h, prob, mask, area
+
+
+def test_cfg1_tiles_and_fg_bit_exact(cfg1):
+    w, slide, ref, h, prob, mask, area = cfg1
+    H, W = slide.shape[:2]
+    Hp, Wp = fe.padded_extent(H, W, w.pad)
+    assert unpack_tiles(h.tiles(), Hp, Wp, w.patch, w.stride) == ref["kept"]
+    fg, t, gpad = h.fgmask()
+    assert t == ref["t"] and gpad == ref["g_pad"]
+    assert (fg == ref["fg"]).all()
+
+
+def test_cfg1_prob_mask_area(cfg1):
+    w, slide, ref, h, prob, mask, area = cfg1
+    H, W = slide.shape[:2]
+    P = split(prob, H, W, w, w.arch)
+    M = split(mask, H, W, w, w.arch)
+    for t in range(len(w.scales)):
+        check_prob_mask(P[t], M[t], ref["prob"][t], ref["mask"][t], f"task{t}")
+        assert int(area[t]) == int(M[t].sum())
+        assert abs(int(area[t]) - ref["area"][t]) <= 0.001 * P[t].size
+
+
+def test_blank_slide_empty(gpu_lib):
+    w = workload(1)
+    s = blank_slide(512, 512).numpy()
+    from paper_2305_14566_b200 import Omniseg
+    h = Omniseg(arch_string(w.arch), w.weights())
+    prob = np.ones(512 * 512, np.float32)
+    mask = np.ones(512 * 512, np.uint8)
+    area = np.ones(1, np.uint64)
+    h.segment_slide(s, 512, 512, 64, 256, 128, (1,), (0,), prob, mask, area)
+    assert len(h.tiles()) == 0 and area[0] == 0 and not prob.any() and not mask.any()
+
+
+def test_predict_tiles_tiny_net(gpu_lib):
+    """Trunk + head on given windows (no stitch) vs the oracle: F, g and p."""
+    from paper_2305_14566_b200 import Omniseg
+    w = workload(1)
+    arch = nn.parse_arch(arch_string(w.arch))
+    net = nn.unpack_weights(arch, w.weights())
+    tiles = random_tiles(3, 256, 11).numpy()
+    h = Omniseg(arch_string(w.arch), w.weights())
+    p, F, g = h.predict_tiles(tiles, [(0, 0)], with_F=True, with_g=True, c_bottleneck=32)
+    for i in range(3):
+        Fr, Er = nn.trunk(net, arch, tiles[i])
+        gr = nn.gap(Er)
+        pr = nn.head(Fr, nn.controller(net, arch, gr, 0, 0))
+        scale = np.abs(Fr).max()
+        assert np.abs(F[i] - Fr).max() <= 2e-2 * scale, np.abs(F[i] - Fr).max() / scale
+        assert np.abs(g[i] - gr).max() <= 2e-2 * np.abs(gr).max()
+        assert np.abs(p[i, 0] - pr).max() <= 3e-2
+
+
+@pytest.mark.slow
+def test_predict_tiles_cfg2_net(gpu_lib):
+    """One 512x512 window through the config-2 network (the bench network)."""
+    from paper_2305_14566_b200 import Omniseg
+    w = workload(2)
+    arch = nn.parse_arch(arch_string(w.arch))
+    net = nn.unpack_weights(arch, w.weights())
+    tiles = random_tiles(1, 512, 12).numpy()
+    h = Omniseg(arch_string(w.arch), w.weights())
+    tasks = [(2, 1), (3, 1), (5, 1)]
+    p, F, g = h.predict_tiles(tiles, tasks, with_F=True, with_g=True, c_bottleneck=512)
+    Fr, Er = nn.trunk(net, arch, tiles[0])
+    gr = nn.gap(Er)
+    for k, (c, s) in enumerate(tasks):
+        pr = nn.head(Fr, nn.controller(net, arch, gr, c, s))
+        d = np.abs(p[0, k] - pr)
+        print(f"task {k}: max |dp| {d.max():.4g}  p99.99 {np.quantile(d, 0.9999):.4g}")
+        assert d.max() <= 5e-2
