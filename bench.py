@@ -1,0 +1,351 @@
+"""Benchmark: slide-wise Omni-Seg prediction on B200 (BASELINE.json metric
+"slide megapixels/sec (all classes) at 1/2/4/8 B200; sec per synthetic biopsy WSI").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--dtype fp16x2]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...      # the oracle arm (CPU, bounded sample)
+
+One step = one full pass of the hot path (upload excluded for `value`: the slide is
+resident in HBM; pyramid, detection, tile selection, gather, trunk, GAP/controller,
+head, stitch, finalize) over the whole synthetic slide; at N > 1 every rank segments
+its row band (strong scaling: the WSI is fixed). `e2e` repeats the step through the
+same C-ABI call with host buffers (H2D of the slide and D2H of prob/mask/area inside
+the timed region). Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "slide megapixels/sec (all classes)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--dtype", default=None, help="fp16x2 (parity-gated default), fp16, bf16")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="1 warmup + 1 step, for ncu")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def bands(Hp, world, S):
+    """Row bands of the padded 40x frame, boundaries multiples of 8*S."""
+    unit = 8 * S
+    nb = (Hp + unit - 1) // unit
+    cuts = [min(Hp, (nb * r // world) * unit) for r in range(world + 1)]
+    cuts[-1] = Hp
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+# ------------------------------------------------------------------ reference arm (oracle)
+def oracle_sample(w, slide_rows_fn, n_tiles=1, strip=512):
+    """Oracle (as it stands) on a bounded sample of the workload: the front end on a
+    `strip`-row window and `n_tiles` windows through trunk + head + stitch; the whole-slide
+    time is extrapolated linearly by rows (front end) and by the kept-tile count."""
+    from oracle import frontend as fe
+    from oracle import net as onn
+    from oracle import pipeline as op
+    from omniseg_inputs import arch_string
+    arch = onn.parse_arch(arch_string(w.arch))
+    net = onn.unpack_weights(arch, w.weights())
+    tf = op.task_factors(arch, w.scales)
+    H, W = w.H, w.W
+    win = slide_rows_fn(0, min(H, strip))
+    t0 = time.perf_counter()
+    fr = op.front_end(win, w.pad, w.patch, w.stride, [f for f, _ in tf])
+    t_fe = time.perf_counter() - t0
+    lv = fe.level(fr["padded"], 1)
+    tasks = [(c, s) for c, (f, s) in zip(w.classes, tf) if f == 1] or [(w.classes[0], tf[0][1])]
+    t1 = time.perf_counter()
+    acc = np.zeros((w.patch, w.patch))
+    cnt = np.zeros((w.patch, w.patch), np.int64)
+    for i in range(n_tiles):
+        oy = 0
+        ox = min(i * w.stride, lv.shape[1] - w.patch)
+        p = onn.predict_tile(net, arch, lv[oy:oy + w.patch, ox:ox + w.patch], tasks)
+        for k in range(p.shape[0]):
+            op.stitch_add(acc, cnt, p[k], 0, 0)
+    t_tile = (time.perf_counter() - t1) / n_tiles
+    return t_fe, t_tile
+
+
+def run_reference(a):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from omniseg_inputs import geometry, render, workload
+    w = workload(int(a.workload.replace("cfg", "")))
+    g = geometry(w.slide)
+    rows = lambda r0, r1: render(g, r0, r1).numpy()  # noqa: E731
+    n_kept = tile_estimate(w)
+    times = []
+    cores = len(os.sched_getaffinity(0))
+    for i in range(a.warmup + a.steps):
+        t_fe, t_tile = oracle_sample(w, rows)
+        T = t_fe * w.H / 512 + t_tile * n_kept
+        if i >= a.warmup:
+            times.append(T)
+    T = statistics.median(times)
+    v = w.H * w.W / 1e6 / T
+    out = {"metric": METRIC, "value": v, "unit": "Mpx/s", "impl": "reference", "n_gpus": 0, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": w.name, "H": w.H, "W": w.W, "patch": w.patch, "stride": w.stride,
+                      "pad": w.pad, "tasks": len(w.scales), "kept_tiles_used": n_kept},
+           "cpu_baseline": {"value": v, "unit": "Mpx/s", "cores": cores, "kind": "oracle",
+                            "sample": f"per step: oracle front end on a 512-row strip + 1 kept-size 512^2 "
+                                      f"window through trunk+head+stitch (fp64 numpy), extrapolated by rows "
+                                      f"and by {n_kept} kept tiles"},
+           "e2e": {"value": v, "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def tile_estimate(w):
+    """Kept-tile count of the workload from the GPU path's last run if recorded, else the
+    SURVEY §8(d) estimate (only used to extrapolate the oracle sample)."""
+    est = {"cfg1_tiny": 46, "cfg2_single_scale": 160, "cfg3_multiscale": 1800, "cfg4_needle_biopsy": 10900}
+    p = os.path.join(ROOT, "profiles", "kept_tiles.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[w.name]
+    except (OSError, KeyError, ValueError):
+        return est.get(w.name, 1000)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from omniseg_inputs import arch_string, geometry, render, workload
+    from paper_2305_14566_b200 import Omniseg
+    from paper_2305_14566_b200 import lib as L
+
+    w = workload(int(a.workload.replace("cfg", "")))
+    if a.dtype:
+        w.arch["dtype"] = a.dtype
+    if a.batch:
+        w.arch["batch"] = a.batch
+    H, W = w.H, w.W
+    Hp = (H + 2 * w.pad + 127) // 128 * 128
+    fmax = max(w.arch["slide_mag"] // s for s in w.scales)
+    halo = w.patch * fmax + 64
+    if world > 1:
+        row0, row1 = bands(Hp, world, w.stride)[rank]
+    else:
+        row0, row1 = 0, Hp
+    b0 = max(0, min(H, row0 - w.pad - halo)) if world > 1 else 0
+    b1 = max(0, min(H, row1 - w.pad + halo)) if world > 1 else H
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    g = geometry(w.slide)
+    slide = render(g, b0, b1, device=dev, chunk_rows=2048) if b1 > b0 else torch.zeros((1, W, 3), torch.uint8,
+                                                                                         device=dev)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    h = Omniseg(arch_string(w.arch), w.weights())
+    stream = torch.cuda.current_stream(dev)
+    h.set_stream(stream.cuda_stream)
+    # outputs (owned canvas rows of every task)
+    ncan = 0
+    for s in w.scales:
+        f = w.arch["slide_mag"] // s
+        r0t, r1t = L.band_rows(H, row0, row1, w.pad, f)
+        ncan += (r1t - r0t) * ((W + f - 1) // f)
+    prob = torch.empty(max(ncan, 1), dtype=torch.float32, device=dev)
+    mask = torch.empty(max(ncan, 1), dtype=torch.uint8, device=dev)
+    area = torch.zeros(len(w.scales), dtype=torch.int64, device=dev)
+    if world > 1:
+        uid = torch.cuda.nccl.unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        h.comm_init(obj[0], world, rank)
+
+    def step(src, p_out, m_out, a_out):
+        if world > 1:
+            h.segment_band(src, H, W, row0, row1, w.pad, w.patch, w.stride, w.scales, w.classes, p_out, m_out, a_out)
+        else:
+            h.segment_slide(src, H, W, w.pad, w.patch, w.stride, w.scales, w.classes, p_out, m_out, a_out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(1, a.warmup if not a.profile_only else 1)):
+        step(slide, prob, mask, area)
+    n_tiles = len(h.tiles())
+    steps = 1 if a.profile_only else a.steps
+    clocks = Clocks(local)
+    h.set_profile(True)
+    barrier()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step(slide, prob, mask, area)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / steps
+    prof = h.profile()
+    h.set_profile(False)
+    launches = int(h.timings()[10])
+    t_ms = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms = float(t_ms.item())
+    value = H * W / 1e6 / (ms / 1e3)
+
+    # ---- end to end: host pinned input, host outputs, copies inside the timed region
+    e2e = None
+    if not a.no_e2e and not a.profile_only:
+        hslide = torch.empty(slide.shape, dtype=torch.uint8, pin_memory=True)
+        hslide.copy_(slide)
+        hprob = torch.empty(prob.shape, dtype=torch.float32, pin_memory=True)
+        hmask = torch.empty(mask.shape, dtype=torch.uint8, pin_memory=True)
+        harea = torch.zeros(area.shape, dtype=torch.int64, pin_memory=True)
+        step(hslide, hprob, hmask, harea)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step(hslide, hprob, hmask, harea)
+        e1.record(stream)
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        ems = float(ems.item())
+        e2e = {"value": H * W / 1e6 / (ems / 1e3), "unit": "Mpx/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(hslide.numel()), "d2h_bytes_per_step": int(ncan * 5 + 8 * len(w.scales)),
+               "note": "host pinned slide in, host prob/mask/area out, through omniseg_segment_slide/band"}
+
+    pk, pk_kind = peaks()
+    achieved = prof["flops"] / (prof["ms"] / 1e3) / 1e12 if prof["ms"] > 0 else 0.0
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    roof = {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 implicit GEMM, all trunk convs)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+            "peak_kind": f"{pk_kind} bf16 sustained (fp16 kind::f16 nominal ratio 1.0)",
+            "traffic": None, "conv_share_of_step": (prof["ms"] / steps) / ms if ms else None,
+            "alg_flops_per_launch": prof["flops"] / max(prof["launches"], 1),
+            "avg_launch_ms": prof["ms"] / max(prof["launches"], 1)}
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
+        try:
+            t_fe, t_tile = oracle_sample(w, lambda r0, r1: render(g, r0, r1).numpy())
+            T = t_fe * H / 512 + t_tile * n_tiles
+            cpu = {"value": H * W / 1e6 / T, "unit": "Mpx/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                   "sample": f"oracle (fp64 numpy) front end on a 512-row strip ({t_fe:.2f} s) + one 512^2 window "
+                             f"through trunk+head+stitch ({t_tile:.2f} s), extrapolated to {H} rows and "
+                             f"{n_tiles} kept tiles"}
+        except Exception as e:  # the baseline must never break the bench line
+            cpu = {"value": None, "unit": "Mpx/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                   "sample": f"failed: {e}"}
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "Mpx/s", "n_gpus": world, "steps": steps,
+               "warmup": a.warmup, "ms_per_step": ms, "sec_per_wsi": ms / 1e3, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": w.arch["dtype"], "data": "synthetic",
+               "config": {"workload": w.name, "H": H, "W": W, "patch": w.patch, "stride": w.stride, "pad": w.pad,
+                          "tasks": len(w.scales), "kept_tiles": n_tiles, "batch": w.arch["batch"],
+                          "parallelism": f"row-bands x{world}" if world > 1 else "single GPU",
+                          "l2": "inputs larger than L2 (slide %.1f GB, canvases %.1f GB)"
+                                % (slide.numel() / 1e9, ncan * 5 / 1e9),
+                          "slide_gen_s": round(gen_s, 1)},
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * steps,
+               "clocks": clk, "stage_ms": [round(x, 3) for x in h.timings()[:9].tolist()]}
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

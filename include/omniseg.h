@@ -54,7 +54,10 @@ typedef struct omniseg omniseg_t;   /* opaque; owns device weights, workspace, s
  *            (3-layer 8-channel dynamic head, BASELINE configs[0]); ncls classes;
  *            scale_codes: magnifications with a one-hot code each (order = code index);
  *            slide_mag: magnification of the input slide (level factor f = slide_mag/scale);
- *            dtype: fp16 (default) or bf16 storage, fp32 accumulation (R9);
+ *            dtype: activation storage, fp32 accumulation (R9): fp16 (default),
+ *            bf16, or fp16x2 / bf16x2 = each activation stored as hi + lo 16-bit pair and
+ *            every convolution's K loop run over both halves (exact 16-bit weights), which
+ *            gives fp32-grade activations at twice the tensor work;
  *            batch: tiles per trunk launch; device: CUDA ordinal (default: current).
  *   weights: flat little-endian fp32 blob in the order of DESIGN.md §3;
  *            nbytes must equal 4 * param_count(arch). Host or device; copied.

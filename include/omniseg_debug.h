@@ -30,11 +30,20 @@ int omniseg_debug_predict_tiles(omniseg_t* h, const uint8_t* tiles_u8, int n, in
  *   w   : float[Cout][k][k][Cin] host (k = 1 or 3), b: float[Cout].
  *   r   : float residual / skip input (mode 1: [B][Ho][Wo][Cout]; mode 2: [B][2H][2W][Cout]) or NULL.
  *   mode: 0 y = relu(conv + b); 1 y = relu(conv + b + r); 2 y[2i+a][2j+c] = r[...] + conv + b
- *         (1x1 + nearest-up x2 + skip add); 3 y = conv + b.
+ *         (1x1 + nearest-up x2 + skip add); 3 y = conv + b. mode | 16: x, r, y use the
+ *         split hi|lo storage of the x2 precision modes (dtype fp16x2 / bf16x2).
  *   y   : float output (storage dtype values widened to fp32). */
 int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Cin,
                        const float* w, const float* b, int Cout, int k, int stride,
                        const float* r, int mode, float* y);
+
+/* Per-launch CUDA-event timing of every tcgen05 convolution (on the library's stream),
+ * accumulated over calls until the next set_profile. on = 0 disables; either call resets. */
+int omniseg_debug_set_profile(omniseg_t* h, int on);
+/* out[0] total conv ms, out[1] total algorithmic conv FLOPs (2 M N K with the network's
+ * real channel counts: no padding, no x2 doubling, stem K = 27), out[2] launches, then per
+ * layer position l (stem, enc.., dec..): out[3+3l] ms, out[4+3l] FLOPs, out[5+3l] launches. */
+int omniseg_debug_get_profile(const omniseg_t* h, double* out, int cap, int* n_layers);
 
 #ifdef __cplusplus
 }

@@ -17,8 +17,11 @@ struct ConvPlan {
 
 // Plan one convolution: input [B][Hin][Win][Cin], weights [Cout][k][k][Cin] (16-bit,
 // K-major), fp32 bias; output grid Ho = ceil(Hin/stride) etc. `res` per ConvMode.
+// split_out: res/out use the hi|lo split layout (x2 precision); for split inputs the
+// caller passes Cin = 2 x channels and weights duplicated along K ([W | W]).
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
-                        const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out);
+                        const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
+                        bool split_out = false);
 void set_conv_batch(ConvPlan& p, int B);
 void run_conv(const ConvPlan& p, cudaStream_t s);
 int num_sms();

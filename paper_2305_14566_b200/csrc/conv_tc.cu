@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <mutex>
+#include <unordered_set>
 #include <type_traits>
 
 #include "common.cuh"
@@ -50,10 +51,13 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
   using C = Cfg<T, BN, BK>;
   constexpr int smem = C::Smem::kTotal;
   auto launch_mode = [&](auto kern) {
-    static bool attr = false;  // per instantiation
-    if (!attr) {
-      OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
+    // all instantiations share one function-pointer type: remember each kernel separately
+    static std::mutex mu;
+    static std::unordered_set<const void*> done;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (done.insert(reinterpret_cast<const void*>(kern)).second)
+        OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
     kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.args);
   };
@@ -96,7 +100,8 @@ int num_sms() {
 }
 
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
-                        const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out) {
+                        const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
+                        bool split_out) {
   OS_REQUIRE(Cin % 16 == 0 && Cout % 16 == 0, "conv channels must be multiples of 16");
   OS_REQUIRE(k == 1 || k == 3, "conv kernel size must be 1 or 3");
   OS_REQUIRE(stride == 1 || stride == 2, "conv stride must be 1 or 2");
@@ -134,6 +139,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.bias = bias;
   a.res = res;
   a.out = out;
+  a.split = split_out ? 1 : 0;
   const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   {
     cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B};

@@ -40,6 +40,7 @@ struct ConvArgs {
   const float* bias;      // [Cout]
   const void* res;        // residual (mode 1, [B][Ho][Wo][Cout]) or skip (mode 2, [B][2Ho][2Wo][Cout])
   void* out;              // [B][Ho][Wo][Cout] (mode 2: [B][2Ho][2Wo][Cout])
+  int split;              // res/out stored as [Cout] hi | [Cout] lo per pixel (x2 precision mode)
 };
 
 template <typename T>
@@ -66,6 +67,51 @@ struct StoreT<__nv_bfloat16> {
     return __bfloat1622float2(h);
   }
 };
+
+// Row I/O of the epilogue. A pixel's channels are stored either plain ([C]) or split
+// ([C] hi | [C] lo, hi = round(v), lo = round(v - hi): the "x2" precision mode in which
+// the next convolution runs its K loop over both halves with the same exact weights).
+template <typename T, int CH>
+__device__ __forceinline__ void add_row(float (&v)[CH], const T* base, size_t pix, int n0, int C, int split) {
+  const size_t stride = split ? 2 * (size_t)C : (size_t)C;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1 && !split) break;
+    const uint4* rs = reinterpret_cast<const uint4*>(base + pix * stride + h * C + n0);
+#pragma unroll
+    for (int j = 0; j < CH / 8; ++j) {
+      uint4 rv = __ldg(rs + j);
+      uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = StoreT<T>::unpack(rr[e]);
+        v[8 * j + 2 * e] += f.x;
+        v[8 * j + 2 * e + 1] += f.y;
+      }
+    }
+  }
+}
+template <typename T, int CH>
+__device__ __forceinline__ void store_row(const float (&v)[CH], T* base, size_t pix, int n0, int C, int split) {
+  const size_t stride = split ? 2 * (size_t)C : (size_t)C;
+  uint4* hs = reinterpret_cast<uint4*>(base + pix * stride + n0);
+#pragma unroll
+  for (int j = 0; j < CH / 8; ++j) {
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = StoreT<T>::pack(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+    hs[j] = make_uint4(o[0], o[1], o[2], o[3]);
+    if (split) {
+      uint32_t l[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 hv = StoreT<T>::unpack(o[e]);
+        l[e] = StoreT<T>::pack(v[8 * j + 2 * e] - hv.x, v[8 * j + 2 * e + 1] - hv.y);
+      }
+      reinterpret_cast<uint4*>(base + pix * stride + C + n0)[j] = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+  }
+}
 
 template <int BN, int BK, int STAGES>
 struct ConvSmem {
@@ -219,51 +265,24 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(args.bias + n0 + j);
         if constexpr (MODE == kUpAdd) {
           const size_t W2 = 2 * (size_t)args.Wo;
-#pragma unroll
+#pragma unroll 1
           for (int a = 0; a < 4; ++a) {
             const size_t pix = ((size_t)b * 2 * args.Ho + 2 * y + (a >> 1)) * W2 + 2 * x + (a & 1);
-            const uint4* rs = reinterpret_cast<const uint4*>(static_cast<const T*>(args.res) + pix * args.Cout + n0);
-            uint4* os = reinterpret_cast<uint4*>(static_cast<T*>(args.out) + pix * args.Cout + n0);
+            float u[CH];
 #pragma unroll
-            for (int j = 0; j < CH / 8; ++j) {
-              uint4 rv = __ldg(rs + j);
-              uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
-              uint32_t o[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float2 f = StoreT<T>::unpack(rr[e]);
-                o[e] = StoreT<T>::pack(f.x + v[8 * j + 2 * e], f.y + v[8 * j + 2 * e + 1]);
-              }
-              os[j] = make_uint4(o[0], o[1], o[2], o[3]);
-            }
+            for (int j = 0; j < CH; ++j) u[j] = v[j];
+            add_row<T, CH>(u, static_cast<const T*>(args.res), pix, n0, args.Cout, args.split);
+            store_row<T, CH>(u, static_cast<T*>(args.out), pix, n0, args.Cout, args.split);
           }
         } else {
           const size_t pix = ((size_t)b * args.Ho + y) * args.Wo + x;
-          if constexpr (MODE == kResidualRelu) {
-            const uint4* rs = reinterpret_cast<const uint4*>(static_cast<const T*>(args.res) + pix * args.Cout + n0);
-#pragma unroll
-            for (int j = 0; j < CH / 8; ++j) {
-              uint4 rv = __ldg(rs + j);
-              uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float2 f = StoreT<T>::unpack(rr[e]);
-                v[8 * j + 2 * e] += f.x;
-                v[8 * j + 2 * e + 1] += f.y;
-              }
-            }
-          }
+          if constexpr (MODE == kResidualRelu)
+            add_row<T, CH>(v, static_cast<const T*>(args.res), pix, n0, args.Cout, args.split);
           if constexpr (MODE != kBias) {
 #pragma unroll
             for (int j = 0; j < CH; ++j) v[j] = fmaxf(v[j], 0.0f);
           }
-          uint4* os = reinterpret_cast<uint4*>(static_cast<T*>(args.out) + pix * args.Cout + n0);
-#pragma unroll
-          for (int j = 0; j < CH / 8; ++j) {
-            os[j] = make_uint4(StoreT<T>::pack(v[8 * j], v[8 * j + 1]), StoreT<T>::pack(v[8 * j + 2], v[8 * j + 3]),
-                               StoreT<T>::pack(v[8 * j + 4], v[8 * j + 5]),
-                               StoreT<T>::pack(v[8 * j + 6], v[8 * j + 7]));
-          }
+          store_row<T, CH>(v, static_cast<T*>(args.out), pix, n0, args.Cout, args.split);
         }
       }
       ptx::tc_fence_before();

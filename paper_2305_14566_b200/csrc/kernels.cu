@@ -398,14 +398,20 @@ __global__ void gather_raw_kernel(const uint8_t* tiles, int n, int P, T* X) {
 
 // ------------------------------------------------------------------ K7 GAP + controller
 // g[b][c] = mean over the bottleneck's h x w pixels (fixed summation order), fp32.
+// (x2 precision: a pixel holds [C] hi | [C] lo; the value is hi + lo.)
 template <typename T>
-__global__ void gap_kernel(const T* E, int hw, int C, float* g) {
+__global__ void gap_kernel(const T* E, int hw, int C, int split, float* g) {
   const int b = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
-  const T* p = E + (int64_t)b * hw * C + c;
+  const int cs = split ? 2 * C : C;
+  const T* p = E + (int64_t)b * hw * cs + c;
   float s = 0.f;
-  for (int i = 0; i < hw; ++i) s += float(p[(int64_t)i * C]);
+  for (int i = 0; i < hw; ++i) {
+    float v = float(p[(int64_t)i * cs]);
+    if (split) v += float(p[(int64_t)i * cs + C]);
+    s += v;
+  }
   g[(int64_t)b * C + c] = s / float(hw);
 }
 
@@ -431,7 +437,7 @@ __global__ void controller_kernel(const float* g, int Cb, const float* Wc, const
 // and the fixed-point stitch acc += (1 << 28) + round(p 2^20) into the task's canvas
 // (R12: order-independent integer atomics). Debug mode writes p instead.
 template <typename T>
-__global__ void head_stitch_kernel(const T* D0, int C0p, int C0, int P, const float* Wpre, const float* bpre,
+__global__ void head_stitch_kernel(const T* D0, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
                                    const float* theta, int ntasks, const uint32_t* tiles, int first,
                                    HeadTaskTable tt, int S, int Hp, int Wp, int pad, float* out_p, float* out_F) {
   __shared__ float sth[kMaxTasks * kTheta];
@@ -452,16 +458,18 @@ __global__ void head_stitch_kernel(const T* D0, int C0p, int C0, int P, const fl
   __syncthreads();
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= P * P) return;
-  const T* d = D0 + ((int64_t)b * P * P + pix) * C0p;
+  const T* d = D0 + ((int64_t)b * P * P + pix) * (split ? 2 * C0p : C0p);
   float F[kHead];
 #pragma unroll
   for (int o = 0; o < kHead; ++o) F[o] = sb[o];
   for (int c = 0; c < C0; c += 8) {
     uint4 u = *reinterpret_cast<const uint4*>(d + c);
+    uint4 ul = split ? *reinterpret_cast<const uint4*>(d + C0p + c) : make_uint4(0, 0, 0, 0);
     const T* e = reinterpret_cast<const T*>(&u);
+    const T* el = reinterpret_cast<const T*>(&ul);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const float xv = float(e[k]);
+      const float xv = float(e[k]) + (split ? float(el[k]) : 0.f);
 #pragma unroll
       for (int o = 0; o < kHead; ++o) F[o] = fmaf(sw[o * C0 + c + k], xv, F[o]);
     }
@@ -534,20 +542,27 @@ __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uin
 
 // ------------------------------------------------------------------ conversions (debug / weights)
 template <typename T>
-__global__ void f32_to_t_kernel(const float* in, T* out, int64_t rows, int cin, int cpad) {
+__global__ void f32_to_t_kernel(const float* in, T* out, int64_t rows, int cin, int cpad, int split) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * cpad) return;
   const int64_t r = i / cpad;
   const int c = i % cpad;
-  out[i] = T(c < cin ? in[r * cin + c] : 0.f);
+  const float v = c < cin ? in[r * cin + c] : 0.f;
+  const T hi = T(v);
+  if (split) {
+    out[r * 2 * cpad + c] = hi;
+    out[r * 2 * cpad + cpad + c] = T(v - float(hi));
+  } else {
+    out[i] = hi;
+  }
 }
 template <typename T>
-__global__ void t_to_f32_kernel(const T* in, float* out, int64_t rows, int cout, int cpad) {
+__global__ void t_to_f32_kernel(const T* in, float* out, int64_t rows, int cout, int cpad, int split) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * cout) return;
   const int64_t r = i / cout;
   const int c = i % cout;
-  out[i] = float(in[r * cpad + c]);
+  out[i] = split ? float(in[r * 2 * cpad + c]) + float(in[r * 2 * cpad + cpad + c]) : float(in[r * cpad + c]);
 }
 
 // ==================================================================== host launchers
@@ -600,9 +615,9 @@ void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s)
   gather_raw_kernel<T><<<grid, 256, 0, s>>>(tiles, n, P, X);
 }
 template <typename T>
-void launch_gap(const T* E, int n, int hw, int C, float* g, cudaStream_t s) {
+void launch_gap(const T* E, int n, int hw, int C, int split, float* g, cudaStream_t s) {
   dim3 grid((C + 127) / 128, n);
-  gap_kernel<T><<<grid, 128, 0, s>>>(E, hw, C, g);
+  gap_kernel<T><<<grid, 128, 0, s>>>(E, hw, C, split, g);
 }
 void launch_controller(const float* g, int n, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
                        const int* task_cls, const int* task_scl, int ntasks, float* theta, cudaStream_t s) {
@@ -610,11 +625,11 @@ void launch_controller(const float* g, int n, int Cb, const float* Wc, const flo
   controller_kernel<<<grid, 128, 0, s>>>(g, Cb, Wc, bc, ncls, nscl, task_cls, task_scl, ntasks, theta);
 }
 template <typename T>
-void launch_head(const T* D0, int n, int C0p, int C0, int P, const float* Wpre, const float* bpre,
+void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
                  const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
                  int Hp, int Wp, int pad, float* out_p, float* out_F, cudaStream_t s) {
   dim3 grid((P * P + 255) / 256, n);
-  head_stitch_kernel<T><<<grid, 256, 0, s>>>(D0, C0p, C0, P, Wpre, bpre, theta, ntasks, tiles, first, tt, S, Hp, Wp,
+  head_stitch_kernel<T><<<grid, 256, 0, s>>>(D0, C0p, C0, split, P, Wpre, bpre, theta, ntasks, tiles, first, tt, S, Hp, Wp,
                                              pad, out_p, out_F);
 }
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area,
@@ -624,26 +639,26 @@ void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask,
   finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area);
 }
 template <typename T>
-void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, cudaStream_t s) {
+void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, cudaStream_t s) {
   int64_t n = rows * cpad;
-  f32_to_t_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cin, cpad);
+  f32_to_t_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cin, cpad, split);
 }
 template <typename T>
-void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, cudaStream_t s) {
+void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, int split, cudaStream_t s) {
   int64_t n = rows * cout;
-  t_to_f32_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cout, cpad);
+  t_to_f32_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cout, cpad, split);
 }
 
 #define OS_INST(T)                                                                                                 \
   template void launch_gather<T>(const uint32_t*, int, int, int, int, const FrontParams&, const DevState*,          \
                                  const uint32_t*, const uint32_t*, const uint32_t*, T*, cudaStream_t);             \
   template void launch_gather_raw<T>(const uint8_t*, int, int, T*, cudaStream_t);                                  \
-  template void launch_gap<T>(const T*, int, int, int, float*, cudaStream_t);                                      \
-  template void launch_head<T>(const T*, int, int, int, int, const float*, const float*, const float*, int,        \
+  template void launch_gap<T>(const T*, int, int, int, int, float*, cudaStream_t);                                 \
+  template void launch_head<T>(const T*, int, int, int, int, int, const float*, const float*, const float*, int,        \
                                const uint32_t*, int, const HeadTaskTable&, int, int, int, int, float*, float*,     \
                                cudaStream_t);                                                                     \
-  template void launch_f32_to_t<T>(const float*, T*, int64_t, int, int, cudaStream_t);                            \
-  template void launch_t_to_f32<T>(const T*, float*, int64_t, int, int, cudaStream_t);
+  template void launch_f32_to_t<T>(const float*, T*, int64_t, int, int, int, cudaStream_t);                       \
+  template void launch_t_to_f32<T>(const T*, float*, int64_t, int, int, int, cudaStream_t);
 OS_INST(__half)
 OS_INST(__nv_bfloat16)
 

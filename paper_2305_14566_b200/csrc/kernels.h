@@ -42,19 +42,19 @@ void launch_gather(const uint32_t* tiles, int first, int n, int P, int S, const 
 template <typename T>
 void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s);
 template <typename T>
-void launch_gap(const T* E, int n, int hw, int C, float* g, cudaStream_t s);
+void launch_gap(const T* E, int n, int hw, int C, int split, float* g, cudaStream_t s);
 void launch_controller(const float* g, int n, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
                        const int* task_cls, const int* task_scl, int ntasks, float* theta, cudaStream_t s);
 template <typename T>
-void launch_head(const T* D0, int n, int C0p, int C0, int P, const float* Wpre, const float* bpre,
+void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
                  const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
                  int Hp, int Wp, int pad, float* out_p, float* out_F, cudaStream_t s);
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area,
                      cudaStream_t s);
 template <typename T>
-void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, cudaStream_t s);
+void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, cudaStream_t s);
 template <typename T>
-void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, cudaStream_t s);
+void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, int split, cudaStream_t s);
 
 // conv_tc.cu
 struct ConvPlan;  // opaque per-layer plan (TMA maps + launch config)

@@ -94,6 +94,7 @@ struct Arch {
   int levels = 5, base = 32, head = 8, ncls = 6, slide_mag = 40, batch = 64, device = -1;
   std::vector<int> scale_codes{5, 10, 20, 40};
   bool bf16 = false;
+  bool split = false;  // "x2" precision: activations stored as hi + lo 16-bit pairs
 };
 
 Arch parse_arch(const char* s) {
@@ -124,8 +125,10 @@ Arch parse_arch(const char* s) {
     else if (k == "batch") a.batch = toi(v);
     else if (k == "device") a.device = toi(v);
     else if (k == "dtype") {
-      OS_REQUIRE(v == "fp16" || v == "bf16", "arch: dtype must be fp16 or bf16");
-      a.bf16 = v == "bf16";
+      OS_REQUIRE(v == "fp16" || v == "bf16" || v == "fp16x2" || v == "bf16x2",
+                 "arch: dtype must be fp16, bf16, fp16x2 or bf16x2");
+      a.bf16 = v.rfind("bf16", 0) == 0;
+      a.split = v.size() > 4;
     } else if (k == "scale_codes") {
       a.scale_codes.clear();
       std::stringstream s2(v);
@@ -152,6 +155,7 @@ struct Layer {
   DevBuf w;      // [coutp][k*k][cinp] 16-bit
   DevBuf b;      // [coutp] fp32
   int cin = 0, cout = 0, cinp = 0, coutp = 0, k = 3, stride = 1;
+  int alg_k = 0; // algorithmic K if not k*k*cin (the stem: 27)
 };
 
 struct LevelBufs {
@@ -183,6 +187,7 @@ struct omniseg {
     ConvPlan plan;
   };
   std::vector<ConvPlan> enc_plans, dec_plans;
+  std::vector<const Layer*> enc_layers, dec_layers;
 
   // front end / canvases
   DevBuf slide, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
@@ -196,11 +201,22 @@ struct omniseg {
   double timings[11] = {};
   int conv_launches = 0, launches = 0;
 
+  // per-conv-launch profiling (omniseg_debug_set_profile): event pairs on the stream
+  bool profile = false;
+  std::vector<cudaEvent_t> pev;
+  std::vector<int> player;
+  std::vector<double> pflops;
+  int pn = 0;                        // event pairs used in the current call
+  std::vector<double> layer_ms, layer_flops, layer_n;
+  double prof_ms = 0, prof_flops = 0, prof_launches = 0;
+
   // NCCL
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
 
   ~omniseg() {
+    for (auto& e : pev)
+      if (e) cudaEventDestroy(e);
     if (comm) g_nccl.commDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -222,18 +238,23 @@ __nv_bfloat16 to16<__nv_bfloat16>(float v) {
 }
 
 // Upload one conv: blob order [cout][k][k][cin] fp32 -> device [coutp][k*k][cinp] 16-bit.
+// kdup = 2 for split (hi|lo) inputs: the K axis of every tap is [W | W].
 template <typename T>
-void upload_conv(Layer& L, const float* w, const float* b, int cin, int cout, int k, int stride, int cinp, int coutp) {
+void upload_conv(Layer& L, const float* w, const float* b, int cin, int cout, int k, int stride, int cinp, int coutp,
+                 int kdup = 1) {
   L.cin = cin;
   L.cout = cout;
-  L.cinp = cinp;
+  L.cinp = cinp * kdup;
   L.coutp = coutp;
   L.k = k;
   L.stride = stride;
-  std::vector<T> hw((size_t)coutp * k * k * cinp, to16<T>(0.f));
+  const int ck = cinp * kdup;
+  std::vector<T> hw((size_t)coutp * k * k * ck, to16<T>(0.f));
   for (int o = 0; o < cout; ++o)
     for (int t = 0; t < k * k; ++t)
-      for (int c = 0; c < cin; ++c) hw[((size_t)o * k * k + t) * cinp + c] = to16<T>(w[((size_t)o * k * k + t) * cin + c]);
+      for (int d = 0; d < kdup; ++d)
+        for (int c = 0; c < cin; ++c)
+          hw[((size_t)o * k * k + t) * ck + d * cinp + c] = to16<T>(w[((size_t)o * k * k + t) * cin + c]);
   std::vector<float> hb(coutp, 0.f);
   for (int o = 0; o < cout; ++o) hb[o] = b[o];
   L.w.ensure(hw.size() * sizeof(T));
@@ -250,6 +271,7 @@ void upload_stem(Layer& L, const float* w, const float* b, int cout, int coutp) 
   for (int o = 0; o < cout; ++o)
     for (int j = 0; j < 27; ++j) w32[(size_t)o * 32 + j] = w[(size_t)o * 27 + j];
   upload_conv<T>(L, w32.data(), b, 32, cout, 1, 1, 32, coutp);
+  L.alg_k = 27;
 }
 
 size_t param_count(const Arch& a) {
@@ -287,7 +309,7 @@ void load_weights(omniseg* h, const float* blob) {
   auto conv = [&](Layer& dst, int co, int k, int ci, int stride) {
     const float* w = take((size_t)co * k * k * ci);
     const float* b = take(co);
-    upload_conv<T>(dst, w, b, ci, co, k, stride, pad16(ci), pad16(co));
+    upload_conv<T>(dst, w, b, ci, co, k, stride, pad16(ci), pad16(co), a.split ? 2 : 1);
   };
   {
     const float* w = take((size_t)h->C[0] * 27);
@@ -347,8 +369,8 @@ void ensure_workspace(omniseg* h, int P) {
   if (h->ws_P == P && h->ws_B == B) return;
   check_patch(h, P);
   const int L = h->arch.levels;
-  const size_t es = 2;  // 16-bit storage
-  h->X0.ensure((size_t)B * P * P * 32 * es);
+  const size_t es = h->arch.split ? 4 : 2;  // 16-bit storage (x2: hi + lo)
+  h->X0.ensure((size_t)B * P * P * 32 * 2);  // exact u8 values: never split
   h->lv.clear();
   h->lv.resize(L);
   for (int l = 0; l < L; ++l) {
@@ -365,23 +387,33 @@ void ensure_workspace(omniseg* h, int P) {
   const bool bf = h->arch.bf16;
   h->enc_plans.clear();
   h->dec_plans.clear();
+  h->enc_layers.clear();
+  h->dec_layers.clear();
   auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode) {
     return make_conv_plan(bf, in, B, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
-                          res, out);
+                          res, out, h->arch.split);
   };
-  h->enc_plans.push_back(plan(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias));
+  auto enc = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode) {
+    h->enc_plans.push_back(plan(ly, in, Hin, res, out, mode));
+    h->enc_layers.push_back(&ly);
+  };
+  auto dec = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode) {
+    h->dec_plans.push_back(plan(ly, in, Hin, res, out, mode));
+    h->dec_layers.push_back(&ly);
+  };
+  enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias);
   for (int l = 0; l < L; ++l) {
     LevelBufs& q = h->lv[l];
-    h->enc_plans.push_back(plan(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias));
-    h->enc_plans.push_back(plan(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu));
-    if (l < L - 1) h->enc_plans.push_back(plan(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias));
+    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias);
+    enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu);
+    if (l < L - 1) enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias);
   }
   for (int l = L - 2; l >= 0; --l) {
     LevelBufs& q = h->lv[l];
     const void* D = (l + 1 == L - 1) ? h->lv[l + 1].E.p : h->lv[l + 1].A.p;
-    h->dec_plans.push_back(plan(h->up[l], D, q.P / 2, q.E.p, q.A.p, kUpAdd));
-    h->dec_plans.push_back(plan(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias));
-    h->dec_plans.push_back(plan(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu));
+    dec(h->up[l], D, q.P / 2, q.E.p, q.A.p, kUpAdd);
+    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias);
+    dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu);
   }
   h->ws_P = P;
   h->ws_B = B;
@@ -425,30 +457,84 @@ Tasks make_tasks(const omniseg* h, const int* scales, const int* classes, int n,
 
 void record(omniseg* h, int i) { OS_CUDA(cudaEventRecord(h->ev[i], h->stream)); }
 
+// Algorithmic FLOPs of one conv launch over n tiles: 2 * M * N_real * K_real (real channel
+// counts: no padding, no x2 doubling, stem K = 27).
+double conv_alg_flops(const ConvPlan& p, const Layer& ly, int n) {
+  const double M = (double)n * p.args.Ho * p.args.Wo;
+  const double K = ly.alg_k ? ly.alg_k : (double)ly.k * ly.k * ly.cin;
+  return 2.0 * M * ly.cout * K;
+}
+
+void run_conv_prof(omniseg* h, const ConvPlan& p, const Layer& ly, int layer_idx, int n) {
+  if (h->profile) {
+    if ((int)h->pev.size() < 2 * (h->pn + 1)) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        OS_CUDA(cudaEventCreate(&e));
+        h->pev.push_back(e);
+      }
+    }
+    OS_CUDA(cudaEventRecord(h->pev[2 * h->pn], h->stream));
+    run_conv(p, h->stream);
+    OS_CUDA(cudaEventRecord(h->pev[2 * h->pn + 1], h->stream));
+    if ((int)h->player.size() <= h->pn) {
+      h->player.resize(h->pn + 1);
+      h->pflops.resize(h->pn + 1);
+    }
+    h->player[h->pn] = layer_idx;
+    h->pflops[h->pn] = conv_alg_flops(p, ly, n);
+    h->pn++;
+  } else {
+    run_conv(p, h->stream);
+  }
+}
+
+// Resolve the event pairs of the finished call into the accumulators.
+void collect_profile(omniseg* h) {
+  if (!h->profile) return;
+  for (int i = 0; i < h->pn; ++i) {
+    float ms = 0;
+    OS_CUDA(cudaEventElapsedTime(&ms, h->pev[2 * i], h->pev[2 * i + 1]));
+    const int l = h->player[i];
+    if ((int)h->layer_ms.size() <= l) {
+      h->layer_ms.resize(l + 1, 0);
+      h->layer_flops.resize(l + 1, 0);
+      h->layer_n.resize(l + 1, 0);
+    }
+    h->layer_ms[l] += ms;
+    h->layer_flops[l] += h->pflops[i];
+    h->layer_n[l] += 1;
+    h->prof_ms += ms;
+    h->prof_flops += h->pflops[i];
+    h->prof_launches += 1;
+  }
+  h->pn = 0;
+}
+
 // Run trunk + GAP/controller + head for `n` tiles already gathered into X0.
 template <typename T>
 void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int first, const HeadTaskTable& tt,
                         int ntasks, int S, int Hp, int Wp, int pad, float* out_p, float* out_F, float* out_g) {
   const int L = h->arch.levels;
   cudaStream_t s = h->stream;
-  for (auto& pl : h->enc_plans) {
-    set_conv_batch(pl, n);
-    run_conv(pl, s);
+  for (size_t i = 0; i < h->enc_plans.size(); ++i) {
+    set_conv_batch(h->enc_plans[i], n);
+    run_conv_prof(h, h->enc_plans[i], *h->enc_layers[i], (int)i, n);
     h->conv_launches++;
   }
   const LevelBufs& bl = h->lv[L - 1];
-  launch_gap<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->g.as<float>(), s);
+  launch_gap<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->arch.split, h->g.as<float>(), s);
   launch_controller(h->g.as<float>(), n, h->C[L - 1], h->Wc.as<float>(), h->bc.as<float>(), h->arch.ncls,
                     (int)h->arch.scale_codes.size(), h->task_cls.as<int>(), h->task_scl.as<int>(), ntasks,
                     h->theta.as<float>(), s);
   h->launches += 2;
   if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, h->g.p, (size_t)n * h->C[L - 1] * 4, cudaMemcpyDefault, s));
-  for (auto& pl : h->dec_plans) {
-    set_conv_batch(pl, n);
-    run_conv(pl, s);
+  for (size_t i = 0; i < h->dec_plans.size(); ++i) {
+    set_conv_batch(h->dec_plans[i], n);
+    run_conv_prof(h, h->dec_plans[i], *h->dec_layers[i], (int)(h->enc_plans.size() + i), n);
     h->conv_launches++;
   }
-  launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], P, h->Wpre.as<float>(), h->bpre.as<float>(),
+  launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.split, P, h->Wpre.as<float>(), h->bpre.as<float>(),
                  h->theta.as<float>(), ntasks, tiles, first, tt, S, Hp, Wp, pad, out_p, out_F, s);
   h->launches++;
   OS_CUDA(cudaGetLastError());
@@ -643,6 +729,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   if (out_area) OS_CUDA(cudaMemcpyAsync(out_area, h->area.p, tk.n * 8, cudaMemcpyDefault, s));
   record(h, 5);
   OS_CUDA(cudaStreamSynchronize(s));
+  collect_profile(h);
   float ms;
   auto el = [&](int a, int b) {
     OS_CUDA(cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]));
@@ -910,6 +997,7 @@ int omniseg_debug_predict_tiles(omniseg_t* h, const uint8_t* tiles_u8, int n, in
     if (out_F) OS_CUDA(cudaMemcpyAsync(out_F, dF.p, (size_t)n * P * P * kHead * 4, cudaMemcpyDefault, s));
     if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, dg.p, (size_t)n * h->C[h->arch.levels - 1] * 4, cudaMemcpyDefault, s));
     OS_CUDA(cudaStreamSynchronize(s));
+    collect_profile(h);
     return 0;
   } catch (const Error& e) {
     return fail(e);
@@ -922,6 +1010,8 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
                        int Cout, int k, int stride, const float* r, int mode, float* y) {
   try {
     OS_REQUIRE(h && x && w && b && y, "debug_conv: NULL argument");
+    const int split = (mode & 16) ? 1 : 0;
+    mode &= 15;
     OS_REQUIRE(mode >= 0 && mode <= 3, "debug_conv: bad mode");
     OS_REQUIRE((mode != 1 && mode != 2) || r, "debug_conv: mode needs r");
     OS_REQUIRE(mode != 2 || (k == 1 && stride == 1), "debug_conv: mode 2 is a 1x1 stride-1 conv");
@@ -931,38 +1021,40 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
     const int cinp = pad16(Cin), coutp = pad16(Cout);
     const int Ho = (H - 1) / stride + 1, Wo = (W - 1) / stride + 1;
     const int oh = mode == 2 ? 2 * Ho : Ho, ow = mode == 2 ? 2 * Wo : Wo;
+    const int sm = split ? 2 : 1;
     Layer L;
     std::vector<float> wv(w, w + (size_t)Cout * k * k * Cin), bv(b, b + Cout);
     if (bf)
-      upload_conv<__nv_bfloat16>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp);
+      upload_conv<__nv_bfloat16>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp, sm);
     else
-      upload_conv<__half>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp);
+      upload_conv<__half>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp, sm);
     DevBuf f32in, xin, rin, f32r, out, f32o;
     const int64_t rows_in = (int64_t)B * H * W, rows_out = (int64_t)B * oh * ow;
     f32in.ensure(rows_in * Cin * 4);
-    xin.ensure(rows_in * cinp * 2);
+    xin.ensure(rows_in * cinp * 2 * sm);
     OS_CUDA(cudaMemcpyAsync(f32in.p, x, rows_in * Cin * 4, cudaMemcpyHostToDevice, s));
     if (r) {
       f32r.ensure(rows_out * Cout * 4);
-      rin.ensure(rows_out * coutp * 2);
+      rin.ensure(rows_out * coutp * 2 * sm);
       OS_CUDA(cudaMemcpyAsync(f32r.p, r, rows_out * Cout * 4, cudaMemcpyHostToDevice, s));
     }
-    out.ensure(rows_out * coutp * 2);
+    out.ensure(rows_out * coutp * 2 * sm);
     f32o.ensure(rows_out * Cout * 4);
     if (bf) {
-      launch_f32_to_t<__nv_bfloat16>(f32in.as<float>(), xin.as<__nv_bfloat16>(), rows_in, Cin, cinp, s);
-      if (r) launch_f32_to_t<__nv_bfloat16>(f32r.as<float>(), rin.as<__nv_bfloat16>(), rows_out, Cout, coutp, s);
+      launch_f32_to_t<__nv_bfloat16>(f32in.as<float>(), xin.as<__nv_bfloat16>(), rows_in, Cin, cinp, split, s);
+      if (r)
+        launch_f32_to_t<__nv_bfloat16>(f32r.as<float>(), rin.as<__nv_bfloat16>(), rows_out, Cout, coutp, split, s);
     } else {
-      launch_f32_to_t<__half>(f32in.as<float>(), xin.as<__half>(), rows_in, Cin, cinp, s);
-      if (r) launch_f32_to_t<__half>(f32r.as<float>(), rin.as<__half>(), rows_out, Cout, coutp, s);
+      launch_f32_to_t<__half>(f32in.as<float>(), xin.as<__half>(), rows_in, Cin, cinp, split, s);
+      if (r) launch_f32_to_t<__half>(f32r.as<float>(), rin.as<__half>(), rows_out, Cout, coutp, split, s);
     }
-    ConvPlan p = make_conv_plan(bf, xin.p, B, H, W, cinp, L.w.p, L.b.as<float>(), coutp, k, stride, mode,
-                                r ? rin.p : nullptr, out.p);
+    ConvPlan p = make_conv_plan(bf, xin.p, B, H, W, cinp * sm, L.w.p, L.b.as<float>(), coutp, k, stride, mode,
+                                r ? rin.p : nullptr, out.p, split != 0);
     run_conv(p, s);
     if (bf)
-      launch_t_to_f32<__nv_bfloat16>(out.as<__nv_bfloat16>(), f32o.as<float>(), rows_out, Cout, coutp, s);
+      launch_t_to_f32<__nv_bfloat16>(out.as<__nv_bfloat16>(), f32o.as<float>(), rows_out, Cout, coutp, split, s);
     else
-      launch_t_to_f32<__half>(out.as<__half>(), f32o.as<float>(), rows_out, Cout, coutp, s);
+      launch_t_to_f32<__half>(out.as<__half>(), f32o.as<float>(), rows_out, Cout, coutp, split, s);
     OS_CUDA(cudaMemcpyAsync(y, f32o.p, rows_out * Cout * 4, cudaMemcpyDeviceToHost, s));
     OS_CUDA(cudaStreamSynchronize(s));
     return 0;
@@ -971,6 +1063,31 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
   } catch (const std::exception& e) {
     return fail(Error(-2, e.what()));
   }
+}
+
+int omniseg_debug_set_profile(omniseg_t* h, int on) {
+  if (!h) return fail(Error(-1, "set_profile: NULL handle"));
+  h->profile = on != 0;
+  h->pn = 0;
+  h->layer_ms.clear();
+  h->layer_flops.clear();
+  h->layer_n.clear();
+  h->prof_ms = h->prof_flops = h->prof_launches = 0;
+  return 0;
+}
+
+int omniseg_debug_get_profile(const omniseg_t* h, double* out, int cap, int* n_layers) {
+  if (!h || !out) return fail(Error(-1, "get_profile: NULL argument"));
+  const int nl = (int)h->layer_ms.size();
+  if (n_layers) *n_layers = nl;
+  std::vector<double> v = {h->prof_ms, h->prof_flops, h->prof_launches};
+  for (int l = 0; l < nl; ++l) {
+    v.push_back(h->layer_ms[l]);
+    v.push_back(h->layer_flops[l]);
+    v.push_back(h->layer_n[l]);
+  }
+  for (int i = 0; i < cap && i < (int)v.size(); ++i) out[i] = v[i];
+  return 0;
 }
 
 }  // extern "C"

@@ -18,7 +18,8 @@ _lib = None
 SYMBOLS = ("omniseg_create", "omniseg_segment_slide", "omniseg_output_size", "omniseg_comm_init",
            "omniseg_segment_band", "omniseg_band_rows", "omniseg_get_tiles", "omniseg_get_fgmask",
            "omniseg_get_timings", "omniseg_set_stream", "omniseg_last_error", "omniseg_destroy",
-           "omniseg_debug_predict_tiles", "omniseg_debug_conv")
+           "omniseg_debug_predict_tiles", "omniseg_debug_conv", "omniseg_debug_set_profile",
+           "omniseg_debug_get_profile")
 
 
 class OmnisegError(RuntimeError):
@@ -65,6 +66,10 @@ def load(path: str = LIB_PATH):
     L.omniseg_debug_predict_tiles.restype = i32
     L.omniseg_debug_conv.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, i32, i32, i32, vp, i32, vp]
     L.omniseg_debug_conv.restype = i32
+    L.omniseg_debug_set_profile.argtypes = [vp, i32]
+    L.omniseg_debug_set_profile.restype = i32
+    L.omniseg_debug_get_profile.argtypes = [vp, vp, i32, C.POINTER(i32)]
+    L.omniseg_debug_get_profile.restype = i32
     _lib = L
     return L
 
@@ -167,6 +172,18 @@ class Omniseg:
         _check(load().omniseg_get_timings(self.h, out.ctypes.data, 11))
         return out
 
+    def set_profile(self, on=True):
+        _check(load().omniseg_debug_set_profile(self.h, 1 if on else 0))
+
+    def profile(self):
+        """dict(ms, flops, launches, layers=[(ms, flops, launches), ...]) of the conv launches."""
+        import numpy as np
+        nl = C.c_int()
+        out = np.zeros(3 + 3 * 64, np.float64)
+        _check(load().omniseg_debug_get_profile(self.h, out.ctypes.data, out.size, C.byref(nl)))
+        layers = [tuple(out[3 + 3 * i:6 + 3 * i]) for i in range(nl.value)]
+        return dict(ms=out[0], flops=out[1], launches=int(out[2]), layers=layers)
+
     def predict_tiles(self, tiles_u8, tasks, with_F=False, with_g=False, c_bottleneck=None):
         """tiles_u8: n x P x P x 3 uint8; tasks: list of (class, scale index)."""
         import numpy as np
@@ -179,7 +196,7 @@ class Omniseg:
                                                   _ptr(out_g), _ptr(out_F)))
         return out_p, out_F, out_g
 
-    def conv(self, x, w, b, stride=1, r=None, mode=0):
+    def conv(self, x, w, b, stride=1, r=None, mode=0, split=False):
         """x: float32 [B][H][W][Cin]; w: [Cout][k][k][Cin]; returns float32 output."""
         import numpy as np
         x = np.ascontiguousarray(x, np.float32)
@@ -193,5 +210,5 @@ class Omniseg:
         y = np.zeros((B, Ho, Wo, Cout), np.float32)
         rr = None if r is None else np.ascontiguousarray(r, np.float32)
         _check(load().omniseg_debug_conv(self.h, _ptr(x), B, H, W, Cin, _ptr(w), _ptr(b), Cout, k, stride,
-                                         _ptr(rr), mode, _ptr(y)))
+                                         _ptr(rr), mode | (16 if split else 0), _ptr(y)))
         return y

@@ -37,6 +37,8 @@ def _ref(x, w, b, stride, r, mode):
             y = np.maximum(y + r[i], 0)
         elif mode == 2:
             y = r[i] + nn.up2(y)
+        elif mode == 3 and r is not None:
+            y = y + r[i]
         out.append(y)
     return np.stack(out)
 
@@ -60,21 +62,47 @@ CASES = [
 ]
 
 
+SPLIT_CASES = [c for i, c in enumerate(CASES) if i % 3 == 1 or c[7] == 2]
+
+
 @pytest.mark.parametrize("B,H,W,Cin,Cout,k,stride,mode", CASES)
 def test_conv_parity(h, B, H, W, Cin, Cout, k, stride, mode):
+    _run(h, B, H, W, Cin, Cout, k, stride, mode, False)
+
+
+@pytest.mark.parametrize("B,H,W,Cin,Cout,k,stride,mode", SPLIT_CASES)
+def test_conv_parity_split(h, B, H, W, Cin, Cout, k, stride, mode):
+    """x2 precision: fp32 inputs stored as hi + lo fp16; the result must be fp32-grade:
+    |err| <= 2^-20 |ref| + 1e-5 (two fp16 roundings of a residual, fp32 accumulation)."""
+    _run(h, B, H, W, Cin, Cout, k, stride, mode, True)
+
+
+def _run(h, B, H, W, Cin, Cout, k, stride, mode, split):
     rng = np.random.default_rng(B * 1000 + H + Cin + Cout + k + stride + mode)
-    x = _f16(rng.standard_normal((B, H, W, Cin)))
+    x = rng.standard_normal((B, H, W, Cin)) if split else _f16(rng.standard_normal((B, H, W, Cin)))
     w = _f16(rng.standard_normal((Cout, k, k, Cin)) * np.sqrt(2.0 / (k * k * Cin)))
     b = rng.standard_normal(Cout).astype(np.float32).astype(np.float64) * 0.1
     Ho, Wo = (H - 1) // stride + 1, (W - 1) // stride + 1
     r = None
     if mode == 1:
-        r = _f16(rng.standard_normal((B, Ho, Wo, Cout)))
+        r = rng.standard_normal((B, Ho, Wo, Cout))
     elif mode == 2:
-        r = _f16(rng.standard_normal((B, 2 * Ho, 2 * Wo, Cout)))
+        r = rng.standard_normal((B, 2 * Ho, 2 * Wo, Cout))
+    if r is not None and not split:
+        r = _f16(r)
+    if split:   # the GPU sees fp32-rounded inputs
+        x = x.astype(np.float32).astype(np.float64)
+        r = None if r is None else r.astype(np.float32).astype(np.float64)
     ref = _ref(x, w, b, stride, r, mode)
-    got = h.conv(x, w, b, stride=stride, r=r, mode=mode)
+    got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split)
     err = np.abs(got - ref)
-    bound = TOL_REL * np.abs(ref) + 1e-3
+    if split:
+        # fp32 accumulation over K terms: |err| <= K eps32 sum|terms| (worst case); use the
+        # sum of |terms| (conv of |x| with |w|) as the scale, plus the two output roundings
+        ref_abs = _ref(np.abs(x), np.abs(w), np.abs(b), stride, None if r is None else np.abs(r),
+                       3 if mode != 2 else 2)
+        bound = 2.0 ** -18 * np.abs(ref_abs) + 2.0 ** -21 * np.abs(ref) + 1e-6
+    else:
+        bound = TOL_REL * np.abs(ref) + 1e-3
     assert got.shape == ref.shape
     assert (err <= bound).all(), f"max err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"
