@@ -34,9 +34,14 @@ def arch_dict(levels=5, base=32, ncls=6, scale_codes=SCALE_CODES_4, slide_mag=40
 
 def arch_string(a: dict) -> str:
     """Format an arch dict as the key=value string omniseg_create() takes."""
-    return ("levels={levels};base={base};head={head};ncls={ncls};scale_codes={sc};"
-            "slide_mag={slide_mag};dtype={dtype};batch={batch}").format(
-                sc=",".join(str(s) for s in a["scale_codes"]), **a)
+    s = ("levels={levels};base={base};head={head};ncls={ncls};scale_codes={sc};"
+         "slide_mag={slide_mag};dtype={dtype};batch={batch}").format(
+             sc=",".join(str(s) for s in a["scale_codes"]), **a)
+    if a.get("xlevels") is not None:
+        s += ";xlevels=%d" % a["xlevels"]
+    if a.get("xa") is not None:
+        s += ";xa=%d" % a["xa"]
+    return s
 
 
 def channels(a: dict):

@@ -9,8 +9,12 @@ namespace osg {
 
 struct ConvPlan {
   CUtensorMap tmA, tmB;  // activation (4-D NHWC) and weight (2-D [Cout][taps*Cin]) TMA maps
+  CUtensorMap tmO, tmR;  // output / residual maps of the TMA epilogue (unused for kUpAdd)
   ConvArgs args;
   int bn, bk, stages, mode, grid;
+  int rows_R = 0;        // > 0: the multi-row 3x3 kernel (conv3_rows_kernel) with R blocks
+  int nz_R = 0;          // > 0: the no-swizzle multi-row 3x3 kernel (conv3_nz_kernel)
+  int hb = 1;
   bool bf16;
   double flops;          // algorithmic FLOPs of one launch (2 * M * N * K)
 };

@@ -5,6 +5,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_set>
 #include <type_traits>
@@ -41,7 +42,7 @@ CUtensorMapSwizzle swz(int bytes) {
 template <typename T, int BN, int BK>
 struct Cfg {
   static constexpr int kStageBytes = ConvSmem<BN, BK, 1>::kStage;
-  static constexpr int kStages0 = (200 * 1024) / kStageBytes;
+  static constexpr int kStages0 = kStageBudget / kStageBytes;
   static constexpr int STAGES = kStages0 > 8 ? 8 : (kStages0 < 2 ? 2 : kStages0);
   using Smem = ConvSmem<BN, BK, STAGES>;
 };
@@ -59,7 +60,7 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.args);
+    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args);
   };
   switch (p.mode) {
     case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kReluBias>); break;
@@ -69,8 +70,69 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
   }
 }
 
+template <typename T, int BN, int HB>
+void launch_rows(const ConvPlan& p, cudaStream_t s) {
+  constexpr int R = RowsCfg::R(BN);
+  constexpr int BK = RowsCfg::BK(BN, HB);
+  constexpr int ST = RowsCfg::STAGES(BN, HB);
+  static_assert(ST >= 2, "multi-row tile does not fit shared memory");
+  constexpr int smem = RowsSmem<BN, BK, R, R * HB + 2, 128 / HB, ST>::kTotal;
+  auto go = [&](auto kern) {
+    static std::mutex mu;
+    static std::unordered_set<const void*> done;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (done.insert(reinterpret_cast<const void*>(kern)).second)
+        OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args);
+  };
+  switch (p.mode) {
+    case kReluBias: go(conv3_rows_kernel<T, BN, BK, R, HB, ST, kReluBias>); break;
+    case kResidualRelu: go(conv3_rows_kernel<T, BN, BK, R, HB, ST, kResidualRelu>); break;
+    default: go(conv3_rows_kernel<T, BN, BK, R, HB, ST, kBias>); break;
+  }
+}
+
+template <typename T, int BN>
+void launch_nz(const ConvPlan& p, cudaStream_t s) {
+  constexpr int R = NzCfg::R(BN);
+  constexpr int ST = NzCfg::STAGES(BN);
+  static_assert(ST >= 2, "no-swizzle tile does not fit shared memory");
+  constexpr int smem = NzSmem<BN, R, ST>::kTotal;
+  auto go = [&](auto kern) {
+    static std::mutex mu;
+    static std::unordered_set<const void*> done;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (done.insert(reinterpret_cast<const void*>(kern)).second)
+        OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args);
+  };
+  switch (p.mode) {
+    case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias>); break;
+    case kResidualRelu: go(conv3_nz_kernel<T, BN, R, ST, kResidualRelu>); break;
+    default: go(conv3_nz_kernel<T, BN, R, ST, kBias>); break;
+  }
+}
+
 template <typename T>
 void dispatch(const ConvPlan& p, cudaStream_t s) {
+  if (p.nz_R > 0) {
+    if (p.bn == 16) return launch_nz<T, 16>(p, s);
+    if (p.bn == 32) return launch_nz<T, 32>(p, s);
+    if (p.bn == 64) return launch_nz<T, 64>(p, s);
+    throw Error(-1, "unsupported no-swizzle conv shape");
+  }
+  if (p.rows_R > 0) {
+#define OS_RCASE(N_, H_) \
+  if (p.bn == N_ && p.hb == H_) return launch_rows<T, N_, H_>(p, s);
+    OS_RCASE(16, 1) OS_RCASE(32, 1) OS_RCASE(64, 1) OS_RCASE(128, 1)
+    OS_RCASE(16, 2) OS_RCASE(32, 2) OS_RCASE(64, 2) OS_RCASE(128, 2)
+#undef OS_RCASE
+    throw Error(-1, "unsupported multi-row conv shape");
+  }
 #define OS_CASE(N_, K_) \
   if (p.bn == N_ && p.bk == K_) return launch_tpl<T, N_, K_>(p, s);
   OS_CASE(16, 16) OS_CASE(16, 32) OS_CASE(16, 64)
@@ -84,7 +146,7 @@ void dispatch(const ConvPlan& p, cudaStream_t s) {
 
 int stages_for(int bn, int bk) {
   const int a = 128 * bk * 2, b = ((bn * bk * 2 + 1023) / 1024) * 1024;
-  int st = (200 * 1024) / (a + b);
+  int st = kStageBudget / (a + b);
   return st > 8 ? 8 : (st < 2 ? 2 : st);
 }
 }  // namespace
@@ -135,16 +197,51 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.tiles_y = Ho / a.hb;
   a.n_tiles_n = Cout / p.bn;
   a.kchunks = Cin / p.bk;
+  // no-swizzle multi-row variant (conv3_nz_kernel): 3x3 stride 1, width >= 128, N <= 64
+  if (k == 3 && stride == 1 && mode != kUpAdd && p.bn <= 64 && a.hb == 1 && Cout == p.bn && Cin % 16 == 0 &&
+      a.tiles_y % NzCfg::R(p.bn) == 0 && getenv("OMNISEG_NO_NZ") == nullptr) {
+    const int R = NzCfg::R(p.bn);
+    // A: 5-D view {8 ch, W, H, Cin/8, B} with the chunk dimension (16-B stride) outside the
+    // pixel dimensions, box {8, 130, R+2, 2, 1} -> smem [chunk][row][px][16 B]
+    cuuint64_t dims[5] = {8, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)(Cin / 8), (cuuint64_t)B};
+    cuuint64_t strides[4] = {(cuuint64_t)Cin * 2, (cuuint64_t)Win * Cin * 2, 16, (cuuint64_t)Hin * Win * Cin * 2};
+    cuuint32_t box[5] = {8, 130, (cuuint32_t)(R + 2), 2, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    const CUtensorMapDataType dt0 = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUresult r = encode_fn()(&p.tmA, dt0, 5, const_cast<void*>(in), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
+      p.nz_R = R;
+      p.bk = 16;
+      a.kchunks = Cin / 16;
+      a.tiles_y /= R;
+    }
+  }
+  // multi-row variant for 3x3 stride-1 convs with N <= 128 (see conv3_rows_kernel)
+  if (p.nz_R == 0 && k == 3 && stride == 1 && mode != kUpAdd && p.bn <= 128 && (a.hb == 1 || a.hb == 2) &&
+      Cout == p.bn && getenv("OMNISEG_NO_ROWS") == nullptr) {
+    const int R = RowsCfg::R(p.bn);
+    const int bk = RowsCfg::BK(p.bn, a.hb);
+    if (a.tiles_y % R == 0 && Cin % bk == 0) {
+      p.rows_R = R;
+      p.hb = a.hb;
+      p.bk = bk;
+      a.kchunks = Cin / bk;
+      a.tiles_y /= R;
+    }
+  }
   a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
   a.bias = bias;
   a.res = res;
   a.out = out;
   a.split = split_out ? 1 : 0;
   const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  {
+  if (p.nz_R == 0) {
     cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B};
     cuuint64_t strides[3] = {(cuuint64_t)Cin * 2, (cuuint64_t)Win * Cin * 2, (cuuint64_t)Hin * Win * Cin * 2};
     cuuint32_t box[4] = {(cuuint32_t)p.bk, (cuuint32_t)(a.wb * stride), (cuuint32_t)(a.hb * stride), 1};
+    if (p.rows_R > 0) box[2] = (cuuint32_t)(p.rows_R * a.hb + 2);
     cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
     CUresult r = encode_fn()(&p.tmA, dt, 4, const_cast<void*>(in), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz(p.bk * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -162,9 +259,34 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
   }
-  p.stages = stages_for(p.bn, p.bk);
+  {
+    // output / residual maps for the TMA epilogue: [B][Ho][Wo][Cst], one warp box
+    // = CH channels x (bw x bh) pixels, 64-B (CH=32) / 32-B (CH=16) swizzle
+    const int CH = p.bn < 32 ? p.bn : 32;
+    const int Cst = split_out ? 2 * Cout : Cout;
+    const int bw = a.wb < 32 ? a.wb : 32, bh = 32 / bw;
+    cuuint64_t dims[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)Cst * 2, (cuuint64_t)Wo * Cst * 2, (cuuint64_t)Ho * Wo * Cst * 2};
+    cuuint32_t box[4] = {(cuuint32_t)CH, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUtensorMapSwizzle sw = CH == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    if (mode != kUpAdd) {
+      CUresult r = encode_fn()(&p.tmO, dt, 4, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(out) failed: " + std::to_string((int)r));
+      if (res) {
+        r = encode_fn()(&p.tmR, dt, 4, const_cast<void*>(res), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(res) failed: " + std::to_string((int)r));
+      } else {
+        p.tmR = p.tmO;
+      }
+    }
+  }
+  p.stages = (p.rows_R > 0 || p.nz_R > 0) ? 0 : stages_for(p.bn, p.bk);
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
   p.flops = 2.0 * (double)B * Ho * Wo * Cout * (double)k * k * Cin;
+  p.hb = a.hb;
   return p;
 }
 

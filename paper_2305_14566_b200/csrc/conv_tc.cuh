@@ -113,13 +113,118 @@ __device__ __forceinline__ void store_row(const float (&v)[CH], T* base, size_t 
   }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// TMA epilogue (modes 0, 1, 3): each epilogue warp owns 32 M rows = a bw x bh pixel box.
+// TMEM -> registers -> bias (+ residual from a TMA-loaded smem tile) -> ReLU -> 16-bit
+// (hi, and lo in the x2 mode) -> swizzled STS -> one TMA store per box. The smem images
+// use the 64-B (CH = 32) / 32-B (CH = 16) swizzle of the output / residual tensor maps.
+template <int CH>
+struct EpiTile {
+  static constexpr int kRow = CH * 2;
+  static constexpr int kBuf = 32 * kRow;
+  static constexpr int kWarpBytes = 4 * kBuf;   // out hi, out lo, res hi, res lo
+  static constexpr int kBytes = 4 * kWarpBytes; // 4 epilogue warps
+  static __device__ __forceinline__ uint32_t off(int r, int j) {
+    if constexpr (CH == 32)
+      return r * 64 + 16 * (j ^ ((r >> 1) & 3));
+    else
+      return r * 32 + 16 * (j ^ ((r >> 2) & 1));
+  }
+};
+
+struct EpiState {
+  uint8_t* buf;        // this warp's 4 buffers
+  uint64_t* rbar;      // this warp's residual mbarrier
+  uint32_t rphase;
+};
+
+// One CH-wide chunk of the warp's 32 rows. (xb, yb, b): box origin; n0: first channel.
+template <typename T, int CH, int MODE>
+__device__ __forceinline__ void epi_chunk(EpiState& es, const CUtensorMap* tmO, const CUtensorMap* tmR,
+                                          uint32_t taddr, const float* bias, int n0, int Cout, int split,
+                                          int xb, int yb, int b, uint32_t lane) {
+  using E = EpiTile<CH>;
+  uint8_t* out_hi = es.buf;
+  uint8_t* out_lo = es.buf + E::kBuf;
+  uint8_t* res_hi = es.buf + 2 * E::kBuf;
+  uint8_t* res_lo = es.buf + 3 * E::kBuf;
+  if constexpr (MODE == kResidualRelu) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(es.rbar, (split ? 2 : 1) * E::kBuf);
+      ptx::tma_load_4d(res_hi, tmR, es.rbar, n0, xb, yb, b);
+      if (split) ptx::tma_load_4d(res_lo, tmR, es.rbar, Cout + n0, xb, yb, b);
+    }
+  }
+  uint32_t u[32];
+  if constexpr (CH == 32) {
+    ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(u));
+  } else {
+    ptx::tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
+  }
+  ptx::tmem_ld_wait();
+  float v[CH];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(bias + n0 + j);
+  if constexpr (MODE == kResidualRelu) {
+    ptx::mbar_wait(es.rbar, es.rphase);
+    es.rphase ^= 1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !split) break;
+      const uint8_t* rb = h ? res_lo : res_hi;
+#pragma unroll
+      for (int j = 0; j < CH / 8; ++j) {
+        const uint4 rv = *reinterpret_cast<const uint4*>(rb + E::off(lane, j));
+        const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = StoreT<T>::unpack(rr[e]);
+          v[8 * j + 2 * e] += f.x;
+          v[8 * j + 2 * e + 1] += f.y;
+        }
+      }
+    }
+  }
+  if constexpr (MODE != kBias) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) v[j] = fmaxf(v[j], 0.0f);
+  }
+  if (lane == 0) ptx::bulk_wait_read0();  // previous stores of this warp done reading smem
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < CH / 8; ++j) {
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = StoreT<T>::pack(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+    *reinterpret_cast<uint4*>(out_hi + E::off(lane, j)) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (split) {
+      uint32_t l[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 hv = StoreT<T>::unpack(o[e]);
+        l[e] = StoreT<T>::pack(v[8 * j + 2 * e] - hv.x, v[8 * j + 2 * e + 1] - hv.y);
+      }
+      *reinterpret_cast<uint4*>(out_lo + E::off(lane, j)) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+  }
+  ptx::fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    ptx::tma_store_4d(tmO, out_hi, n0, xb, yb, b);
+    if (split) ptx::tma_store_4d(tmO, out_lo, Cout + n0, xb, yb, b);
+    ptx::bulk_commit();
+  }
+}
+
 template <int BN, int BK, int STAGES>
 struct ConvSmem {
   static constexpr int kA = 128 * BK * 2;
   static constexpr int kB = ((BN * BK * 2 + 1023) / 1024) * 1024;
   static constexpr int kStage = kA + kB;
-  static constexpr int kBars = (2 * STAGES + 4) * 8 + 16;
-  static constexpr int kTotal = STAGES * kStage + kBars + 1024;  // + alignment slack
+  static constexpr int kBars = (2 * STAGES + 8) * 8 + 16;
+  static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
+  static constexpr int kTotal = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                                           : (2 * BN <= 256) ? 256 : 512;
   static constexpr uint32_t kLayout = BK == 64 ? 2u : BK == 32 ? 4u : 6u;  // SW128 / SW64 / SW32
@@ -129,6 +234,7 @@ struct ConvSmem {
 template <typename T, int BN, int BK, int STAGES, int MODE>
 __global__ void __launch_bounds__(256, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                    const ConvArgs args) {
   using S = ConvSmem<BN, BK, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -137,7 +243,8 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // 4 residual barriers (one per epilogue warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 4);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -153,6 +260,7 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
+    for (int a = 0; a < 4; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -235,6 +343,11 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;               // TMEM lane quadrant of this warp
     const int row = q * 32 + lane;        // M row = pixel within the tile
     const int py = row / args.wb, px = row - (row / args.wb) * args.wb;
+    constexpr int CH = BN < 32 ? BN : 32;
+    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[q], 0};
+    const int bw = args.wb < 32 ? args.wb : 32;
+    const int box_dx = (q * 32) % args.wb, box_dy = (q * 32) / args.wb;
+    (void)bw;
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -248,46 +361,405 @@ __global__ void __launch_bounds__(256, 1)
       const int y = ty * args.hb + py, x = tx * args.wb + px;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      constexpr int CH = BN < 32 ? BN : 32;
 #pragma unroll 1
       for (int c = 0; c < BN; c += CH) {
-        uint32_t u[32];
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
-        if constexpr (CH == 32) {
-          ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(u));
-        } else {
-          ptx::tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
-        }
-        ptx::tmem_ld_wait();
         const int n0 = nt * BN + c;
-        float v[CH];
-#pragma unroll
-        for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(args.bias + n0 + j);
         if constexpr (MODE == kUpAdd) {
+          uint32_t u[32];
+          if constexpr (CH == 32) {
+            ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(u));
+          } else {
+            ptx::tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
+          }
+          ptx::tmem_ld_wait();
+          float v[CH];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(args.bias + n0 + j);
           const size_t W2 = 2 * (size_t)args.Wo;
 #pragma unroll 1
           for (int a = 0; a < 4; ++a) {
             const size_t pix = ((size_t)b * 2 * args.Ho + 2 * y + (a >> 1)) * W2 + 2 * x + (a & 1);
-            float u[CH];
+            float uu[CH];
 #pragma unroll
-            for (int j = 0; j < CH; ++j) u[j] = v[j];
-            add_row<T, CH>(u, static_cast<const T*>(args.res), pix, n0, args.Cout, args.split);
-            store_row<T, CH>(u, static_cast<T*>(args.out), pix, n0, args.Cout, args.split);
+            for (int j = 0; j < CH; ++j) uu[j] = v[j];
+            add_row<T, CH>(uu, static_cast<const T*>(args.res), pix, n0, args.Cout, args.split);
+            store_row<T, CH>(uu, static_cast<T*>(args.out), pix, n0, args.Cout, args.split);
           }
         } else {
-          const size_t pix = ((size_t)b * args.Ho + y) * args.Wo + x;
-          if constexpr (MODE == kResidualRelu)
-            add_row<T, CH>(v, static_cast<const T*>(args.res), pix, n0, args.Cout, args.split);
-          if constexpr (MODE != kBias) {
-#pragma unroll
-            for (int j = 0; j < CH; ++j) v[j] = fmaxf(v[j], 0.0f);
-          }
-          store_row<T, CH>(v, static_cast<T*>(args.out), pix, n0, args.Cout, args.split);
+          epi_chunk<T, CH, MODE>(es, &tmO, &tmR, taddr, args.bias, n0, args.Cout, args.split,
+                                 tx * args.wb + box_dx, ty * args.hb + box_dy, b, lane);
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Multi-row variant for 3x3 stride-1 convolutions with N <= 128 (the thin, bandwidth-bound
+// levels). One work item = R vertically adjacent 128-pixel M blocks (R * hb image rows of
+// one wb-wide column segment) x one N tile. For each (dx, K chunk) a single TMA box of
+// R*hb + 2 input rows (dx-shifted, zero-filled outside the image) serves all three dy taps
+// of all R blocks: the A operand of block r, tap dy starts (r*hb + dy)*wb pixels into the
+// box, a multiple of 8 rows, so it stays aligned to the swizzle atom. The three B boxes
+// (taps (0,dx), (1,dx), (2,dx)) are shared by the R blocks. Per 128 output pixels this
+// moves 3(R*hb+2)/(R*hb) instead of 9 input rows and 9/R instead of 9 weight tiles through
+// L2 -> SMEM. Accumulators: R x BN TMEM columns, double buffered (2 R BN <= 512).
+// Compile-time tile configuration of the multi-row kernel: R = 256/BN blocks (so two
+// accumulator buffers fill the 512 TMEM columns), the largest K chunk giving >= 3 stages in
+// 200 KB of shared memory (else 16 with >= 2 stages).
+constexpr int kStageBudget = 168 * 1024;  // smem for the operand ring (the TMA epilogue takes 32 KB)
+
+struct RowsCfg {
+  static constexpr int stage_bytes(int bn, int bk, int r, int hb) {
+    return (((r * hb + 2) * (128 / hb) * bk * 2 + 1023) / 1024) * 1024 + 3 * (((bn * bk * 2 + 1023) / 1024) * 1024);
+  }
+  static constexpr int R(int bn) { return 256 / bn; }
+  static constexpr int BK(int bn, int hb) {
+    return 3 * stage_bytes(bn, 64, R(bn), hb) <= kStageBudget   ? 64
+           : 3 * stage_bytes(bn, 32, R(bn), hb) <= kStageBudget ? 32
+                                                                : 16;
+  }
+  static constexpr int STAGES(int bn, int hb) {
+    return kStageBudget / stage_bytes(bn, BK(bn, hb), R(bn), hb) > 6
+               ? 6
+               : kStageBudget / stage_bytes(bn, BK(bn, hb), R(bn), hb);
+  }
+};
+
+template <int BN, int BK, int R, int ROWS, int WB, int STAGES>
+struct RowsSmem {
+  static constexpr int kA = ((ROWS * WB * BK * 2 + 1023) / 1024) * 1024;
+  static constexpr int kBt = ((BN * BK * 2 + 1023) / 1024) * 1024;  // one tap's B tile
+  static constexpr int kStage = kA + 3 * kBt;
+  static constexpr int kBars = (2 * STAGES + 8) * 8 + 16;
+  static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
+  static constexpr int kTotal = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes + 1024;
+  static constexpr uint32_t kTmemCols = (2 * R * BN <= 32) ? 32 : (2 * R * BN <= 64) ? 64 : (2 * R * BN <= 128) ? 128
+                                         : (2 * R * BN <= 256) ? 256 : 512;
+  static constexpr uint32_t kLayout = BK == 64 ? 2u : BK == 32 ? 4u : 6u;
+  static constexpr uint32_t kSBO = 8 * BK * 2;
+};
+
+template <typename T, int BN, int BK, int R, int HB, int STAGES, int MODE>
+__global__ void __launch_bounds__(256, 1)
+    conv3_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
+                      const ConvArgs args) {
+  constexpr int WB = 128 / HB;
+  constexpr int ROWS = R * HB + 2;
+  using S = RowsSmem<BN, BK, R, ROWS, WB, STAGES>;
+  static_assert(2 * R * BN <= 512, "TMEM");
+  static_assert(WB % 8 == 0, "swizzle alignment of the shifted A operands");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;  // 4 residual barriers (one per epilogue warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 4);
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    for (int a = 0; a < 4; ++a) ptx::mbar_init(&rbar[a], 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kiters = 3 * args.kchunks;  // (dx, kc)
+  constexpr uint32_t kTx = ROWS * WB * BK * 2 + 3 * BN * BK * 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
+        const int nt = w % args.n_tiles_n;
+        int m = w / args.n_tiles_n;
+        const int tx = m % args.tiles_x;
+        m /= args.tiles_x;
+        const int tyg = m % args.tiles_y;
+        const int b = m / args.tiles_y;
+        const int x0 = tx * WB - 1;
+        const int y0 = tyg * R * HB - 1;
+        for (int it = 0; it < kiters; ++it) {
+          const int dx = it / args.kchunks;
+          const int kc = it - dx * args.kchunks;
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStage;
+          ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+          ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0, b);
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)
+            ptx::tma_load_2d(sa + S::kA + dy * S::kBt, &tmB, &full[stage], (dy * 3 + dx) * args.Cin + kc * BK,
+                             nt * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+        const int acc = local & 1;
+        ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_base = tmem_base + acc * R * BN;
+        for (int it = 0; it < kiters; ++it) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+            const uint32_t sb = sa + S::kA + dy * S::kBt;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const uint32_t a0 = sa + (uint32_t)((r * HB + dy) * WB * BK * 2);
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint64_t da = ptx::smem_desc(a0 + k * 32, S::kSBO, S::kLayout);
+                const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBO, S::kLayout);
+                ptx::mma_f16(d_base + r * BN, da, db, idesc, (it | dy | k) != 0);
+              }
+            }
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    constexpr int CH = BN < 32 ? BN : 32;
+    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[q], 0};
+    const int box_dx = (q * 32) % WB, box_dy = (q * 32) / WB;
+    int local = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int nt = w % args.n_tiles_n;
+      int m = w / args.n_tiles_n;
+      const int tx = m % args.tiles_x;
+      m /= args.tiles_x;
+      const int tyg = m % args.tiles_y;
+      const int b = m / args.tiles_y;
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll 1
+      for (int r = 0; r < R; ++r) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += CH) {
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
+          epi_chunk<T, CH, MODE>(es, &tmO, &tmR, taddr, args.bias, nt * BN + c, args.Cout, args.split,
+                                 tx * WB + box_dx, tyg * R * HB + r * HB + box_dy, b, lane);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Multi-row 3x3 stride-1 kernel with a NO-SWIZZLE A operand (image width >= 128, N <= 64):
+// per 16-channel K chunk one 5-D TMA box brings (R+2) input rows x 130 pixels (the x halo
+// included, OOB zero-filled) into smem as [8-ch chunk][row][pixel][16 B]. In the K-major
+// no-swizzle UMMA layout every pixel is one 16-B core-matrix row, so the operand of block
+// r, tap (dy, dx) simply starts ((r+dy)*130 + dx)*16 B into the box: all 9 taps of all R
+// blocks come from one load (~(R+2)/R input reads per output instead of 9). Weights: 9
+// per-tap SW32 boxes per chunk, shared by the R blocks.
+template <int BN, int R, int STAGES>
+struct NzSmem {
+  static constexpr int kPx = 130;
+  static constexpr int kChunkStride = (R + 2) * kPx * 16;                 // LBO of the A operand
+  static constexpr int kA = ((2 * kChunkStride + 1023) / 1024) * 1024;  // two 8-ch chunks (K = 16)
+  static constexpr int kBt = ((BN * 32 + 1023) / 1024) * 1024;          // one tap's BN x 16 B tile
+  static constexpr int kStage = kA + 9 * kBt;
+  static constexpr int kBars = (2 * STAGES + 8) * 8 + 16;
+  static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
+  static constexpr int kTotal = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes + 1024;
+  static constexpr uint32_t kTmemCols = (2 * R * BN <= 256) ? 256 : 512;
+};
+
+struct NzCfg {
+  static constexpr int R(int bn) { return 256 / bn; }
+  static constexpr int stage_bytes(int bn) {
+    return ((2 * (R(bn) + 2) * 130 * 16 + 1023) / 1024) * 1024 + 9 * (((bn * 32 + 1023) / 1024) * 1024);
+  }
+  static constexpr int STAGES(int bn) {
+    return kStageBudget / stage_bytes(bn) > 6 ? 6 : kStageBudget / stage_bytes(bn);
+  }
+};
+
+template <typename T, int BN, int R, int STAGES, int MODE>
+__global__ void __launch_bounds__(256, 1)
+    conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
+                    const ConvArgs args) {
+  using S = NzSmem<BN, R, STAGES>;
+  static_assert(2 * R * BN <= 512, "TMEM");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 4);
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    for (int a = 0; a < 4; ++a) ptx::mbar_init(&rbar[a], 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kiters = args.kchunks;  // 16-channel chunks
+  constexpr uint32_t kTx = 2 * S::kChunkStride + 9 * BN * 32;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
+        const int nt = w % args.n_tiles_n;
+        int m = w / args.n_tiles_n;
+        const int tx = m % args.tiles_x;
+        m /= args.tiles_x;
+        const int tyg = m % args.tiles_y;
+        const int b = m / args.tiles_y;
+        const int x0 = tx * 128 - 1;
+        const int y0 = tyg * R - 1;
+        for (int kc = 0; kc < kiters; ++kc) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStage;
+          ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+          ptx::tma_load_5d(sa, &tmA, &full[stage], 0, x0, y0, 2 * kc, b);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap)
+            ptx::tma_load_2d(sa + S::kA + tap * S::kBt, &tmB, &full[stage], tap * args.Cin + kc * 16, nt * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+        const int acc = local & 1;
+        ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_base = tmem_base + acc * R * BN;
+        for (int kc = 0; kc < kiters; ++kc) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int dy = tap / 3, dx = tap % 3;
+            const uint64_t db = ptx::smem_desc(sa + S::kA + tap * S::kBt, 8 * 32, 6u);  // SW32, 8 rows x 32 B
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const uint32_t a0 = sa + (uint32_t)(((r + dy) * S::kPx + dx) * 16);
+              const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
+              ptx::mma_f16(d_base + r * BN, da, db, idesc, (kc | tap) != 0);
+            }
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    constexpr int CH = BN < 32 ? BN : 32;
+    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[q], 0};
+    int local = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int nt = w % args.n_tiles_n;
+      int m = w / args.n_tiles_n;
+      const int tx = m % args.tiles_x;
+      m /= args.tiles_x;
+      const int tyg = m % args.tiles_y;
+      const int b = m / args.tiles_y;
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll 1
+      for (int r = 0; r < R; ++r) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += CH) {
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
+          epi_chunk<T, CH, MODE>(es, &tmO, &tmR, taddr, args.bias, nt * BN + c, args.Cout, args.split,
+                                 tx * 128 + q * 32, tyg * R + r, b, lane);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
   __syncthreads();

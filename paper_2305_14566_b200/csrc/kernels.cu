@@ -436,12 +436,18 @@ __global__ void controller_kernel(const float* g, int Cb, const float* Wc, const
 // z = W3 ReLU(W2 ReLU(W1 F + b1) + b2) + b3, p = 1/(1+e^-z) (north_star dynamic head),
 // and the fixed-point stitch acc += (1 << 28) + round(p 2^20) into the task's canvas
 // (R12: order-independent integer atomics). Debug mode writes p instead.
+// Each thread handles HPX consecutive pixels so every shared-memory weight load (float4)
+// feeds HPX FMAs (the one-load-per-FMA form was L1-bound).
+constexpr int HPX = 4;
+constexpr int kThetaPad = 156;  // 153 rounded up to a float4 multiple
 template <typename T>
-__global__ void head_stitch_kernel(const T* D0, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
-                                   const float* theta, int ntasks, const uint32_t* tiles, int first,
-                                   HeadTaskTable tt, int S, int Hp, int Wp, int pad, float* out_p, float* out_F) {
-  __shared__ float sth[kMaxTasks * kTheta];
-  __shared__ float sw[kHead * 64];
+__global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, int C0, int split, int P,
+                                                          const float* Wpre, const float* bpre, const float* theta,
+                                                          int ntasks, const uint32_t* tiles, int first,
+                                                          HeadTaskTable tt, int S, int Hp, int Wp, int pad,
+                                                          float* out_p, float* out_F) {
+  __shared__ __align__(16) float sth[kMaxTasks * kThetaPad];
+  __shared__ __align__(16) float sw[kHead * 64];
   __shared__ float sb[kHead];
   const int b = blockIdx.y;
   int lf = 0, ty = 0, tx = 0;
@@ -452,65 +458,132 @@ __global__ void head_stitch_kernel(const T* D0, int C0p, int C0, int split, int 
     tx = id & 0x7FFF;
   }
   const int f = 1 << lf;
-  for (int i = threadIdx.x; i < ntasks * kTheta; i += blockDim.x) sth[i] = theta[(int64_t)b * ntasks * kTheta + i];
+  for (int i = threadIdx.x; i < ntasks * kTheta; i += blockDim.x) {
+    const int t = i / kTheta, j = i - t * kTheta;
+    sth[t * kThetaPad + j] = theta[(int64_t)b * ntasks * kTheta + i];
+  }
   for (int i = threadIdx.x; i < kHead * C0; i += blockDim.x) sw[i] = Wpre[i];
   if (threadIdx.x < kHead) sb[threadIdx.x] = bpre[threadIdx.x];
   __syncthreads();
-  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pix >= P * P) return;
-  const T* d = D0 + ((int64_t)b * P * P + pix) * (split ? 2 * C0p : C0p);
-  float F[kHead];
+  const int pix0 = (blockIdx.x * blockDim.x + threadIdx.x) * HPX;
+  if (pix0 >= P * P) return;  // P*P is a multiple of HPX (P % 16 == 0)
+  const int cs = split ? 2 * C0p : C0p;
+  const T* d = D0 + ((int64_t)b * P * P + pix0) * cs;
+  float F[HPX][kHead];
 #pragma unroll
-  for (int o = 0; o < kHead; ++o) F[o] = sb[o];
+  for (int q = 0; q < HPX; ++q)
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) F[q][o] = sb[o];
   for (int c = 0; c < C0; c += 8) {
-    uint4 u = *reinterpret_cast<const uint4*>(d + c);
-    uint4 ul = split ? *reinterpret_cast<const uint4*>(d + C0p + c) : make_uint4(0, 0, 0, 0);
-    const T* e = reinterpret_cast<const T*>(&u);
-    const T* el = reinterpret_cast<const T*>(&ul);
+    float xv[HPX][8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float xv = float(e[k]) + (split ? float(el[k]) : 0.f);
+    for (int q = 0; q < HPX; ++q) {
+      const uint4 u = *reinterpret_cast<const uint4*>(d + (int64_t)q * cs + c);
+      const T* e = reinterpret_cast<const T*>(&u);
 #pragma unroll
-      for (int o = 0; o < kHead; ++o) F[o] = fmaf(sw[o * C0 + c + k], xv, F[o]);
+      for (int k = 0; k < 8; ++k) xv[q][k] = float(e[k]);
+      if (split) {
+        const uint4 ul = *reinterpret_cast<const uint4*>(d + (int64_t)q * cs + C0p + c);
+        const T* el = reinterpret_cast<const T*>(&ul);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xv[q][k] += float(el[k]);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      const float4 w0 = *reinterpret_cast<const float4*>(sw + o * C0 + c);
+      const float4 w1 = *reinterpret_cast<const float4*>(sw + o * C0 + c + 4);
+#pragma unroll
+      for (int q = 0; q < HPX; ++q) {
+        float a = F[q][o];
+        a = fmaf(w0.x, xv[q][0], a);
+        a = fmaf(w0.y, xv[q][1], a);
+        a = fmaf(w0.z, xv[q][2], a);
+        a = fmaf(w0.w, xv[q][3], a);
+        a = fmaf(w1.x, xv[q][4], a);
+        a = fmaf(w1.y, xv[q][5], a);
+        a = fmaf(w1.z, xv[q][6], a);
+        a = fmaf(w1.w, xv[q][7], a);
+        F[q][o] = a;
+      }
     }
   }
   if (out_F) {
 #pragma unroll
-    for (int o = 0; o < kHead; ++o) out_F[((int64_t)b * P * P + pix) * kHead + o] = F[o];
+    for (int q = 0; q < HPX; ++q)
+#pragma unroll
+      for (int o = 0; o < kHead; ++o) out_F[((int64_t)b * P * P + pix0 + q) * kHead + o] = F[q][o];
   }
-  const int y = pix / P, x = pix % P;
   const int Ey = Hp / f, Ex = Wp / f;
   const int oy = min(ty * S, Ey - P), ox = min(tx * S, Ex - P);
-  const int cy = oy + y - pad / f, cx = ox + x - pad / f;
   for (int t = 0; t < ntasks; ++t) {
     if (tiles && tt.log2f[t] != lf) continue;
-    const float* th = sth + t * kTheta;
-    float h1[kHead], h2[kHead];
+    const float* th = sth + t * kThetaPad;
+    float h1[HPX][kHead], h2[HPX][kHead];
 #pragma unroll
     for (int o = 0; o < kHead; ++o) {
-      float s = th[64 + o];
+      const float4 w0 = *reinterpret_cast<const float4*>(th + o * 8);
+      const float4 w1 = *reinterpret_cast<const float4*>(th + o * 8 + 4);
+      const float bo = th[64 + o];
 #pragma unroll
-      for (int i = 0; i < kHead; ++i) s = fmaf(th[o * 8 + i], F[i], s);
-      h1[o] = fmaxf(s, 0.f);
+      for (int q = 0; q < HPX; ++q) {
+        float a = bo;
+        a = fmaf(w0.x, F[q][0], a);
+        a = fmaf(w0.y, F[q][1], a);
+        a = fmaf(w0.z, F[q][2], a);
+        a = fmaf(w0.w, F[q][3], a);
+        a = fmaf(w1.x, F[q][4], a);
+        a = fmaf(w1.y, F[q][5], a);
+        a = fmaf(w1.z, F[q][6], a);
+        a = fmaf(w1.w, F[q][7], a);
+        h1[q][o] = fmaxf(a, 0.f);
+      }
     }
 #pragma unroll
     for (int o = 0; o < kHead; ++o) {
-      float s = th[136 + o];
+      const float4 w0 = *reinterpret_cast<const float4*>(th + 72 + o * 8);
+      const float4 w1 = *reinterpret_cast<const float4*>(th + 72 + o * 8 + 4);
+      const float bo = th[136 + o];
 #pragma unroll
-      for (int i = 0; i < kHead; ++i) s = fmaf(th[72 + o * 8 + i], h1[i], s);
-      h2[o] = fmaxf(s, 0.f);
+      for (int q = 0; q < HPX; ++q) {
+        float a = bo;
+        a = fmaf(w0.x, h1[q][0], a);
+        a = fmaf(w0.y, h1[q][1], a);
+        a = fmaf(w0.z, h1[q][2], a);
+        a = fmaf(w0.w, h1[q][3], a);
+        a = fmaf(w1.x, h1[q][4], a);
+        a = fmaf(w1.y, h1[q][5], a);
+        a = fmaf(w1.z, h1[q][6], a);
+        a = fmaf(w1.w, h1[q][7], a);
+        h2[q][o] = fmaxf(a, 0.f);
+      }
     }
-    float z = th[152];
+    const float4 w30 = *reinterpret_cast<const float4*>(th + 144);
+    const float4 w31 = *reinterpret_cast<const float4*>(th + 148);
+    const float b3 = th[152];
 #pragma unroll
-    for (int i = 0; i < kHead; ++i) z = fmaf(th[144 + i], h2[i], z);
-    const float p = 1.0f / (1.0f + expf(-z));
-    if (out_p) {
-      out_p[(((int64_t)b * ntasks + t) * P * P) + pix] = p;
-    } else {
-      const int Ht = tt.Ht[t], Wt = tt.Wt[t];
-      if (cy >= 0 && cy < Ht && cx >= 0 && cx < Wt && cy >= tt.row0[t] && cy < tt.row1[t]) {
-        const uint32_t q = __float2uint_rn(p * 1048576.0f);
-        atomicAdd(tt.canvas[t] + (int64_t)(cy - tt.row0[t]) * Wt + cx, (1u << 28) + q);
+    for (int q = 0; q < HPX; ++q) {
+      float z = b3;
+      z = fmaf(w30.x, h2[q][0], z);
+      z = fmaf(w30.y, h2[q][1], z);
+      z = fmaf(w30.z, h2[q][2], z);
+      z = fmaf(w30.w, h2[q][3], z);
+      z = fmaf(w31.x, h2[q][4], z);
+      z = fmaf(w31.y, h2[q][5], z);
+      z = fmaf(w31.z, h2[q][6], z);
+      z = fmaf(w31.w, h2[q][7], z);
+      const float p = 1.0f / (1.0f + expf(-z));
+      const int pix = pix0 + q;
+      if (out_p) {
+        out_p[(((int64_t)b * ntasks + t) * P * P) + pix] = p;
+      } else {
+        const int y = pix / P, x = pix % P;
+        const int cy = oy + y - pad / f, cx = ox + x - pad / f;
+        const int Wt = tt.Wt[t];
+        if (cy >= 0 && cy < tt.Ht[t] && cx >= 0 && cx < Wt && cy >= tt.row0[t] && cy < tt.row1[t]) {
+          const uint32_t qv = __float2uint_rn(p * 1048576.0f);
+          atomicAdd(tt.canvas[t] + (int64_t)(cy - tt.row0[t]) * Wt + cx, (1u << 28) + qv);
+        }
       }
     }
   }
@@ -628,8 +701,8 @@ template <typename T>
 void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
                  const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
                  int Hp, int Wp, int pad, float* out_p, float* out_F, cudaStream_t s) {
-  dim3 grid((P * P + 255) / 256, n);
-  head_stitch_kernel<T><<<grid, 256, 0, s>>>(D0, C0p, C0, split, P, Wpre, bpre, theta, ntasks, tiles, first, tt, S, Hp, Wp,
+  dim3 grid((P * P / HPX + 127) / 128, n);
+  head_stitch_kernel<T><<<grid, 128, 0, s>>>(D0, C0p, C0, split, P, Wpre, bpre, theta, ntasks, tiles, first, tt, S, Hp, Wp,
                                              pad, out_p, out_F);
 }
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area,

@@ -95,6 +95,9 @@ struct Arch {
   std::vector<int> scale_codes{5, 10, 20, 40};
   bool bf16 = false;
   bool split = false;  // "x2" precision: activations stored as hi + lo 16-bit pairs
+  int xlevels = -1;    // x2 only for tensors at U-Net levels < xlevels (-1: all levels)
+  int xa = 1;          // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
+  bool sp(int level) const { return split && level < (xlevels < 0 ? 64 : xlevels); }
 };
 
 Arch parse_arch(const char* s) {
@@ -124,6 +127,8 @@ Arch parse_arch(const char* s) {
     else if (k == "slide_mag") a.slide_mag = toi(v);
     else if (k == "batch") a.batch = toi(v);
     else if (k == "device") a.device = toi(v);
+    else if (k == "xlevels") a.xlevels = toi(v);
+    else if (k == "xa") a.xa = toi(v);
     else if (k == "dtype") {
       OS_REQUIRE(v == "fp16" || v == "bf16" || v == "fp16x2" || v == "bf16x2",
                  "arch: dtype must be fp16, bf16, fp16x2 or bf16x2");
@@ -306,10 +311,11 @@ void load_weights(omniseg* h, const float* blob) {
     o += n;
     return p;
   };
-  auto conv = [&](Layer& dst, int co, int k, int ci, int stride) {
+  // in_level: U-Net level of the layer's input tensor (x2 inputs duplicate the K axis)
+  auto conv = [&](Layer& dst, int co, int k, int ci, int stride, int in_level) {
     const float* w = take((size_t)co * k * k * ci);
     const float* b = take(co);
-    upload_conv<T>(dst, w, b, ci, co, k, stride, pad16(ci), pad16(co), a.split ? 2 : 1);
+    upload_conv<T>(dst, w, b, ci, co, k, stride, pad16(ci), pad16(co), a.sp(in_level) ? 2 : 1);
   };
   {
     const float* w = take((size_t)h->C[0] * 27);
@@ -323,14 +329,14 @@ void load_weights(omniseg* h, const float* blob) {
   h->dec_a.resize(L);
   h->dec_b.resize(L);
   for (int l = 0; l < L; ++l) {
-    conv(h->enc_a[l], h->C[l], 3, h->C[l], 1);
-    conv(h->enc_b[l], h->C[l], 3, h->C[l], 1);
-    if (l < L - 1) conv(h->down[l], h->C[l + 1], 3, h->C[l], 2);
+    conv(h->enc_a[l], h->C[l], 3, h->C[l], 1, l);
+    conv(h->enc_b[l], h->C[l], 3, h->C[l], 1, a.xa ? l : 1000);
+    if (l < L - 1) conv(h->down[l], h->C[l + 1], 3, h->C[l], 2, l);
   }
   for (int l = L - 2; l >= 0; --l) {
-    conv(h->up[l], h->C[l], 1, h->C[l + 1], 1);
-    conv(h->dec_a[l], h->C[l], 3, h->C[l], 1);
-    conv(h->dec_b[l], h->C[l], 3, h->C[l], 1);
+    conv(h->up[l], h->C[l], 1, h->C[l + 1], 1, l + 1);
+    conv(h->dec_a[l], h->C[l], 3, h->C[l], 1, l);
+    conv(h->dec_b[l], h->C[l], 3, h->C[l], 1, a.xa ? l : 1000);
   }
   {
     const float* w = take((size_t)kHead * h->C[0]);
@@ -369,7 +375,7 @@ void ensure_workspace(omniseg* h, int P) {
   if (h->ws_P == P && h->ws_B == B) return;
   check_patch(h, P);
   const int L = h->arch.levels;
-  const size_t es = h->arch.split ? 4 : 2;  // 16-bit storage (x2: hi + lo)
+  // 16-bit storage; x2 levels hold hi + lo
   h->X0.ensure((size_t)B * P * P * 32 * 2);  // exact u8 values: never split
   h->lv.clear();
   h->lv.resize(L);
@@ -377,7 +383,7 @@ void ensure_workspace(omniseg* h, int P) {
     LevelBufs& q = h->lv[l];
     q.P = P >> l;
     q.C = h->Cp[l];
-    const size_t n = (size_t)B * q.P * q.P * q.C * es;
+    const size_t n = (size_t)B * q.P * q.P * q.C * (h->arch.sp(l) ? 4 : 2);
     q.E.ensure(n);
     q.A.ensure(n);
     q.Bt.ensure(n);
@@ -389,31 +395,32 @@ void ensure_workspace(omniseg* h, int P) {
   h->dec_plans.clear();
   h->enc_layers.clear();
   h->dec_layers.clear();
-  auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode) {
+  // out_level: U-Net level of the output (and residual / skip) tensor
+  auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int out_level) {
     return make_conv_plan(bf, in, B, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
-                          res, out, h->arch.split);
+                          res, out, h->arch.sp(out_level));
   };
-  auto enc = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode) {
-    h->enc_plans.push_back(plan(ly, in, Hin, res, out, mode));
+  auto enc = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol) {
+    h->enc_plans.push_back(plan(ly, in, Hin, res, out, mode, ol));
     h->enc_layers.push_back(&ly);
   };
-  auto dec = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode) {
-    h->dec_plans.push_back(plan(ly, in, Hin, res, out, mode));
+  auto dec = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol) {
+    h->dec_plans.push_back(plan(ly, in, Hin, res, out, mode, ol));
     h->dec_layers.push_back(&ly);
   };
-  enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias);
+  enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias, 0);
   for (int l = 0; l < L; ++l) {
     LevelBufs& q = h->lv[l];
-    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias);
-    enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu);
-    if (l < L - 1) enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias);
+    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, h->arch.xa ? l : 1000);
+    enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l);
+    if (l < L - 1) enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias, l + 1);
   }
   for (int l = L - 2; l >= 0; --l) {
     LevelBufs& q = h->lv[l];
     const void* D = (l + 1 == L - 1) ? h->lv[l + 1].E.p : h->lv[l + 1].A.p;
-    dec(h->up[l], D, q.P / 2, q.E.p, q.A.p, kUpAdd);
-    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias);
-    dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu);
+    dec(h->up[l], D, q.P / 2, q.E.p, q.A.p, kUpAdd, l);
+    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, h->arch.xa ? l : 1000);
+    dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu, l);
   }
   h->ws_P = P;
   h->ws_B = B;
@@ -523,7 +530,7 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
     h->conv_launches++;
   }
   const LevelBufs& bl = h->lv[L - 1];
-  launch_gap<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->arch.split, h->g.as<float>(), s);
+  launch_gap<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->arch.sp(L - 1), h->g.as<float>(), s);
   launch_controller(h->g.as<float>(), n, h->C[L - 1], h->Wc.as<float>(), h->bc.as<float>(), h->arch.ncls,
                     (int)h->arch.scale_codes.size(), h->task_cls.as<int>(), h->task_scl.as<int>(), ntasks,
                     h->theta.as<float>(), s);
@@ -534,7 +541,7 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
     run_conv_prof(h, h->dec_plans[i], *h->dec_layers[i], (int)(h->enc_plans.size() + i), n);
     h->conv_launches++;
   }
-  launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.split, P, h->Wpre.as<float>(), h->bpre.as<float>(),
+  launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.sp(0), P, h->Wpre.as<float>(), h->bpre.as<float>(),
                  h->theta.as<float>(), ntasks, tiles, first, tt, S, Hp, Wp, pad, out_p, out_F, s);
   h->launches++;
   OS_CUDA(cudaGetLastError());

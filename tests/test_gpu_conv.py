@@ -59,6 +59,13 @@ CASES = [
     (3, 8, 16, 32, 16, 3, 1, 3),
     (1, 512, 512, 32, 32, 3, 1, 0),
     (1, 32, 32, 48, 48, 3, 1, 1),   # 48 channels: K chunk 16, N tile 16
+    # multi-row 3x3 kernel (conv3_rows_kernel): N<=128, hb in {1,2}
+    (1, 256, 256, 16, 16, 3, 1, 1),   # R=16
+    (1, 256, 256, 64, 64, 3, 1, 0),   # R=4, BK=32
+    (1, 128, 128, 128, 128, 3, 1, 1), # R=2
+    (2, 64, 64, 64, 64, 3, 1, 3),     # hb=2
+    (1, 4, 128, 32, 32, 3, 1, 0),     # tiles_y % R != 0 -> per-tap kernel
+    (3, 16, 128, 32, 32, 3, 1, 1),    # ragged: 3 images, 2 row groups each
 ]
 
 
