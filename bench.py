@@ -106,15 +106,6 @@ def dist_env():
     return world, rank, local
 
 
-def bands(Hp, world, S):
-    """Row bands of the padded 40x frame, boundaries multiples of 8*S."""
-    unit = 8 * S
-    nb = (Hp + unit - 1) // unit
-    cuts = [min(Hp, (nb * r // world) * unit) for r in range(world + 1)]
-    cuts[-1] = Hp
-    return [(cuts[r], cuts[r + 1]) for r in range(world)]
-
-
 # ------------------------------------------------------------------ reference arm (oracle)
 def oracle_sample(w, slide_rows_fn, n_tiles=1, strip=512):
     """Oracle (as it stands) on a bounded sample of the workload: the front end on a
@@ -204,6 +195,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from omniseg_inputs import arch_string, geometry, render, workload
     from paper_2305_14566_b200 import Omniseg
+    from paper_2305_14566_b200 import dist as D
     from paper_2305_14566_b200 import lib as L
 
     w = workload(int(a.workload.replace("cfg", "")))
@@ -214,13 +206,11 @@ def main():
     H, W = w.H, w.W
     Hp = (H + 2 * w.pad + 127) // 128 * 128
     fmax = max(w.arch["slide_mag"] // s for s in w.scales)
-    halo = w.patch * fmax + 64
     if world > 1:
-        row0, row1 = bands(Hp, world, w.stride)[rank]
+        row0, row1 = D.band_partition(Hp, world, w.stride)[rank]
+        b0, b1 = D.band_slide_rows(H, w.pad, w.patch, fmax, row0, row1)
     else:
-        row0, row1 = 0, Hp
-    b0 = max(0, min(H, row0 - w.pad - halo)) if world > 1 else 0
-    b1 = max(0, min(H, row1 - w.pad + halo)) if world > 1 else H
+        row0, row1, b0, b1 = 0, Hp, 0, H
     dev = torch.device("cuda", local)
     t0 = time.time()
     g = geometry(w.slide)
@@ -240,11 +230,7 @@ def main():
     prob = torch.empty(max(ncan, 1), dtype=torch.float32, device=dev)
     mask = torch.empty(max(ncan, 1), dtype=torch.uint8, device=dev)
     area = torch.zeros(len(w.scales), dtype=torch.int64, device=dev)
-    if world > 1:
-        uid = torch.cuda.nccl.unique_id() if rank == 0 else None
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        h.comm_init(obj[0], world, rank)
+    D.init_comm(h, world, rank)
 
     def step(src, p_out, m_out, a_out):
         if world > 1:

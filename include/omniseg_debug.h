@@ -37,6 +37,14 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
                        const float* w, const float* b, int Cout, int k, int stride,
                        const float* r, int mode, float* y);
 
+/* Single-GPU emulation of the multi-GPU band path: inject the global pad colour (3 u8)
+ * and global interior histogram (256 u64) that the NCCL broadcast / all-reduce would
+ * deliver, so that omniseg_segment_band on one GPU without a communicator reproduces a
+ * rank's result. NULL arguments switch injection off. */
+int omniseg_debug_band_globals(omniseg_t* h, const uint8_t* pc, const uint64_t* hist);
+/* The pad colour and the (global) histogram used by the last segment call. */
+int omniseg_debug_get_detection(const omniseg_t* h, uint8_t* pc, uint64_t* hist);
+
 /* Per-launch CUDA-event timing of every tcgen05 convolution (on the library's stream),
  * accumulated over calls until the next set_profile. on = 0 disables; either call resets. */
 int omniseg_debug_set_profile(omniseg_t* h, int on);

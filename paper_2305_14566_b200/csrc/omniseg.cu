@@ -215,6 +215,12 @@ struct omniseg {
   std::vector<double> layer_ms, layer_flops, layer_n;
   double prof_ms = 0, prof_flops = 0, prof_launches = 0;
 
+  // debug: injected global detection state for single-GPU band emulation
+  bool inject = false;
+  uint8_t inj_pc[4] = {0, 0, 0, 0};
+  unsigned long long inj_hist[256] = {};
+  unsigned long long last_hist[256] = {};
+
   // NCCL
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
@@ -582,6 +588,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   h->state.ensure(sizeof(DevState));
   DevState* st = h->state.as<DevState>();
   if (b0 == 0) launch_pad_colour(dslide, W, st, s);
+  if (h->inject) OS_CUDA(cudaMemcpyAsync(st, h->inj_pc, 4, cudaMemcpyHostToDevice, s));
   if (h->world > 1) {
     g_nccl.check(g_nccl.broadcast(st, st, 4, ncclUint8, 0, h->comm, s), "ncclBroadcast(pad colour)");
   }
@@ -628,6 +635,8 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
               h->hist.as<unsigned long long>(), s);
   if (h->world > 1)
     g_nccl.check(g_nccl.allReduce(h->hist.p, h->hist.p, 256, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(hist)");
+  if (h->inject) OS_CUDA(cudaMemcpyAsync(h->hist.p, h->inj_hist, 256 * 8, cudaMemcpyHostToDevice, s));
+  OS_CUDA(cudaMemcpyAsync(h->last_hist, h->hist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
   launch_otsu(h->hist.as<unsigned long long>(), st, s);
   launch_fg(h->gm.as<uint8_t>(), h->fg.as<uint8_t>(), W8, m0, m1, ir0, ir1, ic0, ic1, st, s);
   // candidate grids (canonical order: factor descending, row, col)
@@ -1069,6 +1078,32 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
     return fail(e);
   } catch (const std::exception& e) {
     return fail(Error(-2, e.what()));
+  }
+}
+
+int omniseg_debug_band_globals(omniseg_t* h, const uint8_t* pc, const uint64_t* hist) {
+  if (!h) return fail(Error(-1, "band_globals: NULL handle"));
+  if (!pc || !hist) {
+    h->inject = false;
+    return 0;
+  }
+  h->inject = true;
+  for (int c = 0; c < 3; ++c) h->inj_pc[c] = pc[c];
+  h->inj_pc[3] = 0;
+  for (int i = 0; i < 256; ++i) h->inj_hist[i] = hist[i];
+  return 0;
+}
+
+int omniseg_debug_get_detection(const omniseg_t* h, uint8_t* pc, uint64_t* hist) {
+  try {
+    OS_REQUIRE(h && pc && hist, "get_detection: NULL argument");
+    DevState st;
+    OS_CUDA(cudaMemcpy(&st, h->state.p, sizeof(st), cudaMemcpyDeviceToHost));
+    for (int c = 0; c < 3; ++c) pc[c] = st.pc[c];
+    for (int i = 0; i < 256; ++i) hist[i] = h->last_hist[i];
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
   }
 }
 

@@ -19,7 +19,7 @@ SYMBOLS = ("omniseg_create", "omniseg_segment_slide", "omniseg_output_size", "om
            "omniseg_segment_band", "omniseg_band_rows", "omniseg_get_tiles", "omniseg_get_fgmask",
            "omniseg_get_timings", "omniseg_set_stream", "omniseg_last_error", "omniseg_destroy",
            "omniseg_debug_predict_tiles", "omniseg_debug_conv", "omniseg_debug_set_profile",
-           "omniseg_debug_get_profile")
+           "omniseg_debug_get_profile", "omniseg_debug_band_globals", "omniseg_debug_get_detection")
 
 
 class OmnisegError(RuntimeError):
@@ -70,6 +70,10 @@ def load(path: str = LIB_PATH):
     L.omniseg_debug_set_profile.restype = i32
     L.omniseg_debug_get_profile.argtypes = [vp, vp, i32, C.POINTER(i32)]
     L.omniseg_debug_get_profile.restype = i32
+    L.omniseg_debug_band_globals.argtypes = [vp, vp, vp]
+    L.omniseg_debug_band_globals.restype = i32
+    L.omniseg_debug_get_detection.argtypes = [vp, vp, vp]
+    L.omniseg_debug_get_detection.restype = i32
     _lib = L
     return L
 
@@ -171,6 +175,22 @@ class Omniseg:
         out = np.zeros(11, np.float64)
         _check(load().omniseg_get_timings(self.h, out.ctypes.data, 11))
         return out
+
+    def band_globals(self, pc=None, hist=None):
+        import numpy as np
+        if pc is None:
+            _check(load().omniseg_debug_band_globals(self.h, None, None))
+            return
+        pc = np.ascontiguousarray(pc, np.uint8)
+        hist = np.ascontiguousarray(hist, np.uint64)
+        _check(load().omniseg_debug_band_globals(self.h, pc.ctypes.data, hist.ctypes.data))
+
+    def detection(self):
+        import numpy as np
+        pc = np.zeros(3, np.uint8)
+        hist = np.zeros(256, np.uint64)
+        _check(load().omniseg_debug_get_detection(self.h, pc.ctypes.data, hist.ctypes.data))
+        return pc, hist
 
     def set_profile(self, on=True):
         _check(load().omniseg_debug_set_profile(self.h, 1 if on else 0))

@@ -1,0 +1,84 @@
+"""Multi-GPU band path emulated on one GPU: every rank's omniseg_segment_band runs on the
+same GPU, with the global pad colour and Otsu histogram that the NCCL collectives would
+deliver injected (omniseg_debug_band_globals). Owned canvas rows must be BIT-IDENTICAL
+to the single-GPU omniseg_segment_slide run (fixed-point stitch, R12), kept
+tiles must be exactly the full-slide tiles that intersect the band, and the band areas
+must sum to the full areas."""
+import numpy as np
+import pytest
+
+from omniseg_inputs import arch_dict, arch_string, make_slide, make_weights
+
+pytestmark = pytest.mark.gpu
+
+H, W, PAD, P, S = 3072, 1024, 128, 256, 128
+SCALES, CLASSES = (1, 2, 4), (0, 1, 1)
+
+
+@pytest.fixture(scope="module")
+def setup(gpu_lib):
+    from paper_2305_14566_b200 import Omniseg
+    a = arch_dict(levels=3, base=8, ncls=2, scale_codes=(1, 2, 4), slide_mag=4, batch=16)
+    blob = make_weights(a, 1)
+    spec = dict(kind="blobs", seed=31, W=W, H=H, n_blobs=14, axes=(60, 260), rings=True, nuclei=True)
+    slide = make_slide(spec).numpy()
+    h = Omniseg(arch_string(a), blob)
+    n = sum(h.output_size(H, W, s) for s in SCALES)
+    prob = np.zeros(n, np.float32)
+    mask = np.zeros(n, np.uint8)
+    area = np.zeros(len(SCALES), np.uint64)
+    h.segment_slide(slide, H, W, PAD, P, S, SCALES, CLASSES, prob, mask, area)
+    pc, hist = h.detection()
+    return a, blob, slide, h, prob, mask, area, pc, hist, h.tiles()
+
+
+def _split(arr, a):
+    out, o = [], 0
+    for s in SCALES:
+        f = a["slide_mag"] // s
+        hh, ww = (H + f - 1) // f, (W + f - 1) // f
+        out.append(arr[o:o + hh * ww].reshape(hh, ww))
+        o += hh * ww
+    return out
+
+
+def _window_rows(v, Hp):
+    f = 1 << (v >> 30)
+    oy = min(((v >> 15) & 0x7FFF) * S, Hp // f - P)
+    return oy * f, (oy + P) * f
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bands_bit_exact(setup, world):
+    from paper_2305_14566_b200 import Omniseg
+    from paper_2305_14566_b200 import dist as D
+    a, blob, slide, h_full, prob, mask, area, pc, hist, tiles_full = setup
+    Hp, _ = D.padded_extent(H, W, PAD)
+    fmax = max(a["slide_mag"] // s for s in SCALES)
+    P_full, M_full = _split(prob, a), _split(mask, a)
+    area_sum = np.zeros(len(SCALES), np.uint64)
+    h = Omniseg(arch_string(a), blob)
+    h.band_globals(pc, hist)
+    for (row0, row1) in D.band_partition(Hp, world, S):
+        b0, b1 = D.band_slide_rows(H, PAD, P, fmax, row0, row1)
+        own = [D.owned_canvas_rows(H, PAD, a["slide_mag"] // s, row0, row1) for s in SCALES]
+        n = sum((r1 - r0) * ((W + f - 1) // f) for (r0, r1), f in zip(own, [a["slide_mag"] // s for s in SCALES]))
+        bp = np.zeros(max(n, 1), np.float32)
+        bm = np.zeros(max(n, 1), np.uint8)
+        ba = np.zeros(len(SCALES), np.uint64)
+        h.segment_band(np.ascontiguousarray(slide[b0:b1]), H, W, row0, row1, PAD, P, S, SCALES, CLASSES, bp, bm, ba)
+        o = 0
+        for t, ((r0, r1), s) in enumerate(zip(own, SCALES)):
+            f = a["slide_mag"] // s
+            ww = (W + f - 1) // f
+            got_p = bp[o:o + (r1 - r0) * ww].reshape(r1 - r0, ww)
+            got_m = bm[o:o + (r1 - r0) * ww].reshape(r1 - r0, ww)
+            assert (got_p.view(np.uint32) == P_full[t][r0:r1].view(np.uint32)).all(), (row0, t)
+            assert (got_m == M_full[t][r0:r1]).all()
+            o += (r1 - r0) * ww
+        area_sum += ba
+        band_tiles = set(h.tiles().tolist())
+        expect = {v for v in tiles_full.tolist() if _window_rows(v, Hp)[0] < row1 and _window_rows(v, Hp)[1] > row0}
+        assert band_tiles == expect
+        _, t_band, gp_band = h.fgmask()
+    assert (area_sum == area).all()
