@@ -52,6 +52,27 @@ struct FrontParams {
   int own8_0, own8_1;    // level-8 rows owned (histogram counts only these)
 };
 
+// Per-task stitch targets passed by value to the head (kernel or fused epilogue).
+struct HeadTaskTable {
+  uint32_t* canvas[kMaxTasks];  // fixed-point accumulators, rows [row0, row1) of the task canvas
+  int Ht[kMaxTasks], Wt[kMaxTasks];
+  int row0[kMaxTasks], row1[kMaxTasks];
+  int log2f[kMaxTasks];
+};
+
+// Everything the dynamic head + stitch needs (fused into the last decoder conv).
+struct HeadArgs {
+  const float* Wpre;    // [8][C0] precls weights (fp32)
+  const float* bpre;    // [8]
+  const float* theta;   // [B][ntasks][153] controller output
+  int ntasks, C0, P, S, Hp, Wp, pad;
+  const uint32_t* tiles;  // kept-tile ids (NULL: debug windows, every task applies)
+  int first;              // index of batch tile 0 in `tiles`
+  float* out_p;           // debug: [B][ntasks][P][P] probabilities instead of stitching
+  float* out_F;           // debug: [B][P][P][8]
+  HeadTaskTable tt;
+};
+
 __host__ __device__ inline uint32_t pack_tile(int log2f, int ty, int tx) {
   return (uint32_t(log2f) << 30) | (uint32_t(ty) << 15) | uint32_t(tx);
 }

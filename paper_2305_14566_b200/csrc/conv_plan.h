@@ -16,6 +16,7 @@ struct ConvPlan {
   int nz_R = 0;          // > 0: the no-swizzle multi-row 3x3 kernel (conv3_nz_kernel)
   int hb = 1;
   bool bf16;
+  HeadArgs head{};       // kHead mode (fused dynamic head + stitch), set by the caller per launch
   double flops;          // algorithmic FLOPs of one launch (2 * M * N * K)
 };
 

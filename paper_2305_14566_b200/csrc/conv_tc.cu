@@ -108,17 +108,19 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args);
+    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head);
   };
   switch (p.mode) {
     case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias>); break;
     case kResidualRelu: go(conv3_nz_kernel<T, BN, R, ST, kResidualRelu>); break;
+    case kHeadFused: go(conv3_nz_kernel<T, BN, R, ST, kHeadFused>); break;
     default: go(conv3_nz_kernel<T, BN, R, ST, kBias>); break;
   }
 }
 
 template <typename T>
 void dispatch(const ConvPlan& p, cudaStream_t s) {
+  if (p.mode == kHeadFused && p.nz_R == 0) throw Error(-1, "fused head needs the no-swizzle conv kernel");
   if (p.nz_R > 0) {
     if (p.bn == 16) return launch_nz<T, 16>(p, s);
     if (p.bn == 32) return launch_nz<T, 32>(p, s);

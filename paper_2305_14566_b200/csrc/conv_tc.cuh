@@ -22,11 +22,12 @@
 
 #include <type_traits>
 
+#include "common.cuh"
 #include "ptx.cuh"
 
 namespace osg {
 
-enum ConvMode : int { kReluBias = 0, kResidualRelu = 1, kUpAdd = 2, kBias = 3 };
+enum ConvMode : int { kReluBias = 0, kResidualRelu = 1, kUpAdd = 2, kBias = 3, kHeadFused = 4 };
 
 struct ConvArgs {
   int B, Ho, Wo;          // conv output grid (mode 2: the low-resolution grid)
@@ -123,7 +124,7 @@ template <int CH>
 struct EpiTile {
   static constexpr int kRow = CH * 2;
   static constexpr int kBuf = 32 * kRow;
-  static constexpr int kWarpBytes = 4 * kBuf;   // out hi, out lo, res hi, res lo
+  static constexpr int kWarpBytes = 6 * kBuf;   // out hi, out lo, 2 x (res hi, res lo)
   static constexpr int kBytes = 4 * kWarpBytes; // 4 epilogue warps
   static __device__ __forceinline__ uint32_t off(int r, int j) {
     if constexpr (CH == 32)
@@ -134,28 +135,34 @@ struct EpiTile {
 };
 
 struct EpiState {
-  uint8_t* buf;        // this warp's 4 buffers
-  uint64_t* rbar;      // this warp's residual mbarrier
-  uint32_t rphase;
+  uint8_t* buf;         // this warp's 6 buffers
+  uint64_t* rbar;       // this warp's 2 residual mbarriers (double-buffered prefetch)
+  uint32_t rphase[2];
 };
 
-// One CH-wide chunk of the warp's 32 rows. (xb, yb, b): box origin; n0: first channel.
-template <typename T, int CH, int MODE>
-__device__ __forceinline__ void epi_chunk(EpiState& es, const CUtensorMap* tmO, const CUtensorMap* tmR,
-                                          uint32_t taddr, const float* bias, int n0, int Cout, int split,
-                                          int xb, int yb, int b, uint32_t lane) {
+// Issue the TMA loads of one residual chunk into buffer slot `slot` (lane 0).
+template <int CH>
+__device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUtensorMap* tmR, int n0, int Cout,
+                                              int split, int xb, int yb, int b, uint32_t lane) {
   using E = EpiTile<CH>;
-  uint8_t* out_hi = es.buf;
-  uint8_t* out_lo = es.buf + E::kBuf;
-  uint8_t* res_hi = es.buf + 2 * E::kBuf;
-  uint8_t* res_lo = es.buf + 3 * E::kBuf;
-  if constexpr (MODE == kResidualRelu) {
-    if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(es.rbar, (split ? 2 : 1) * E::kBuf);
-      ptx::tma_load_4d(res_hi, tmR, es.rbar, n0, xb, yb, b);
-      if (split) ptx::tma_load_4d(res_lo, tmR, es.rbar, Cout + n0, xb, yb, b);
-    }
+  if (lane == 0) {
+    uint8_t* hi = es.buf + (2 + 2 * slot) * E::kBuf;
+    ptx::mbar_arrive_expect_tx(&es.rbar[slot], (split ? 2 : 1) * E::kBuf);
+    ptx::tma_load_4d(hi, tmR, &es.rbar[slot], n0, xb, yb, b);
+    if (split) ptx::tma_load_4d(hi + E::kBuf, tmR, &es.rbar[slot], Cout + n0, xb, yb, b);
   }
+}
+
+// Accumulator -> bias (+ residual from a TMA-loaded smem tile) -> ReLU (MODE != kBias), for
+// one CH-wide chunk of the warp's 32 rows. (xb, yb, b): box origin; n0: first channel.
+// The residual of this chunk was issued earlier into `slot` (epi_res_issue).
+template <typename T, int CH, int MODE>
+__device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t taddr, const float* bias, int n0,
+                                           int split, uint32_t lane, float (&v)[CH]) {
+  using E = EpiTile<CH>;
+  uint8_t* res_hi = es.buf + (2 + 2 * slot) * E::kBuf;
+  uint8_t* res_lo = res_hi + E::kBuf;
+  constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
   uint32_t u[32];
   if constexpr (CH == 32) {
     ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(u));
@@ -163,12 +170,11 @@ __device__ __forceinline__ void epi_chunk(EpiState& es, const CUtensorMap* tmO, 
     ptx::tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
   }
   ptx::tmem_ld_wait();
-  float v[CH];
 #pragma unroll
   for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(bias + n0 + j);
-  if constexpr (MODE == kResidualRelu) {
-    ptx::mbar_wait(es.rbar, es.rphase);
-    es.rphase ^= 1;
+  if constexpr (kRes) {
+    ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
+    es.rphase[slot] ^= 1;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (h == 1 && !split) break;
@@ -185,11 +191,24 @@ __device__ __forceinline__ void epi_chunk(EpiState& es, const CUtensorMap* tmO, 
         }
       }
     }
+    __syncwarp();  // every lane has read the residual tile before it is reloaded
   }
   if constexpr (MODE != kBias) {
 #pragma unroll
     for (int j = 0; j < CH; ++j) v[j] = fmaxf(v[j], 0.0f);
   }
+}
+
+// One CH-wide chunk: values -> 16-bit (hi, + lo in x2) -> swizzled STS -> TMA store.
+template <typename T, int CH, int MODE>
+__device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensorMap* tmO, uint32_t taddr,
+                                          const float* bias, int n0, int Cout, int split, int xb, int yb, int b,
+                                          uint32_t lane) {
+  using E = EpiTile<CH>;
+  uint8_t* out_hi = es.buf;
+  uint8_t* out_lo = es.buf + E::kBuf;
+  float v[CH];
+  epi_values<T, CH, MODE>(es, slot, taddr, bias, n0, split, lane, v);
   if (lane == 0) ptx::bulk_wait_read0();  // previous stores of this warp done reading smem
   __syncwarp();
 #pragma unroll
@@ -217,12 +236,108 @@ __device__ __forceinline__ void epi_chunk(EpiState& es, const CUtensorMap* tmO, 
   }
 }
 
+// Fused dynamic head + stitch (MODE kHeadFused, last decoder conv, CH = BN = all C0 channels):
+// D0 = ReLU(acc + b + U0) (the storage-rounded value in plain 16-bit modes, the exact fp32
+// value in x2 modes, i.e. hi + lo to 2^-22), F = precls(D0), then per task of the tile's
+// scale z = W3 ReLU(W2 ReLU(W1 F + b1) + b2) + b3, p = sigmoid(z), and the fixed-point
+// canvas atomics of kernels.cu's head_stitch_kernel. D0 itself is never written.
+template <typename T, int CH>
+__device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr, const float* bias, int split,
+                                         int xb, int yb, int b, uint32_t lane, const HeadArgs& ha, const float* s_w,
+                                         const float* s_b, const float* s_th, int lf, int oy, int ox) {
+  float v[CH];
+  epi_values<T, CH, kHeadFused>(es, slot, taddr, bias, 0, split, lane, v);
+  if (!split) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) v[j] = float(T(v[j]));
+  }
+  // precls with the weights padded to CH columns (zeros beyond C0): fully unrolled, v stays
+  // in registers, one float4 shared load per 4 FMAs
+  float F[kHead];
+#pragma unroll
+  for (int o = 0; o < kHead; ++o) {
+    float a = s_b[o];
+#pragma unroll
+    for (int j = 0; j < CH; j += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(s_w + o * CH + j);
+      a = fmaf(w4.x, v[j], a);
+      a = fmaf(w4.y, v[j + 1], a);
+      a = fmaf(w4.z, v[j + 2], a);
+      a = fmaf(w4.w, v[j + 3], a);
+    }
+    F[o] = a;
+  }
+  const int y = yb, x = xb + (int)lane;  // hb = 1: the warp's 32 pixels of one row
+  if (ha.out_F) {
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) ha.out_F[(((int64_t)b * ha.P + y) * ha.P + x) * kHead + o] = F[o];
+  }
+  const int f = 1 << lf;
+  for (int t = 0; t < ha.ntasks; ++t) {
+    if (ha.tiles && ha.tt.log2f[t] != lf) continue;
+    const float* th = s_th + t * 156;
+    float h1[kHead], h2[kHead];
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + o * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + o * 8 + 4);
+      float a = th[64 + o];
+      a = fmaf(a4.x, F[0], a);
+      a = fmaf(a4.y, F[1], a);
+      a = fmaf(a4.z, F[2], a);
+      a = fmaf(a4.w, F[3], a);
+      a = fmaf(b4.x, F[4], a);
+      a = fmaf(b4.y, F[5], a);
+      a = fmaf(b4.z, F[6], a);
+      a = fmaf(b4.w, F[7], a);
+      h1[o] = fmaxf(a, 0.f);
+    }
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + 72 + o * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + 72 + o * 8 + 4);
+      float a = th[136 + o];
+      a = fmaf(a4.x, h1[0], a);
+      a = fmaf(a4.y, h1[1], a);
+      a = fmaf(a4.z, h1[2], a);
+      a = fmaf(a4.w, h1[3], a);
+      a = fmaf(b4.x, h1[4], a);
+      a = fmaf(b4.y, h1[5], a);
+      a = fmaf(b4.z, h1[6], a);
+      a = fmaf(b4.w, h1[7], a);
+      h2[o] = fmaxf(a, 0.f);
+    }
+    const float4 c4 = *reinterpret_cast<const float4*>(th + 144);
+    const float4 d4 = *reinterpret_cast<const float4*>(th + 148);
+    float z = th[152];
+    z = fmaf(c4.x, h2[0], z);
+    z = fmaf(c4.y, h2[1], z);
+    z = fmaf(c4.z, h2[2], z);
+    z = fmaf(c4.w, h2[3], z);
+    z = fmaf(d4.x, h2[4], z);
+    z = fmaf(d4.y, h2[5], z);
+    z = fmaf(d4.z, h2[6], z);
+    z = fmaf(d4.w, h2[7], z);
+    const float p = 1.0f / (1.0f + expf(-z));
+    if (ha.out_p) {
+      ha.out_p[(((int64_t)b * ha.ntasks + t) * ha.P + y) * ha.P + x] = p;
+    } else {
+      const int cy = oy + y - ha.pad / f, cx = ox + x - ha.pad / f;
+      const int Wt = ha.tt.Wt[t];
+      if (cy >= 0 && cy < ha.tt.Ht[t] && cx >= 0 && cx < Wt && cy >= ha.tt.row0[t] && cy < ha.tt.row1[t]) {
+        const uint32_t qv = __float2uint_rn(p * 1048576.0f);
+        atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, (1u << 28) + qv);
+      }
+    }
+  }
+}
+
 template <int BN, int BK, int STAGES>
 struct ConvSmem {
   static constexpr int kA = 128 * BK * 2;
   static constexpr int kB = ((BN * BK * 2 + 1023) / 1024) * 1024;
   static constexpr int kStage = kA + kB;
-  static constexpr int kBars = (2 * STAGES + 8) * 8 + 16;
+  static constexpr int kBars = (2 * STAGES + 12) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   static constexpr int kTotal = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
@@ -237,14 +352,15 @@ __global__ void __launch_bounds__(256, 1)
                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                    const ConvArgs args) {
   using S = ConvSmem<BN, BK, STAGES>;
+  static_assert(S::kTotal <= 227 * 1024, "shared memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;  // 4 residual barriers (one per epilogue warp)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 4);
+  uint64_t* rbar = tempty + 2;  // 8 residual barriers (two per epilogue warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 8);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -260,7 +376,7 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
-    for (int a = 0; a < 4; ++a) ptx::mbar_init(&rbar[a], 1);
+    for (int a = 0; a < 8; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -344,7 +460,7 @@ __global__ void __launch_bounds__(256, 1)
     const int row = q * 32 + lane;        // M row = pixel within the tile
     const int py = row / args.wb, px = row - (row / args.wb) * args.wb;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[q], 0};
+    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}};
     const int bw = args.wb < 32 ? args.wb : 32;
     const int box_dx = (q * 32) % args.wb, box_dy = (q * 32) / args.wb;
     (void)bw;
@@ -361,10 +477,17 @@ __global__ void __launch_bounds__(256, 1)
       const int y = ty * args.hb + py, x = tx * args.wb + px;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      constexpr bool kRes = MODE == kResidualRelu;
+      const int xb = tx * args.wb + box_dx, yb = ty * args.hb + box_dy;
+      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb, b, lane);
 #pragma unroll 1
       for (int c = 0; c < BN; c += CH) {
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
         const int n0 = nt * BN + c;
+        const int slot = (c / CH) & 1;
+        if constexpr (kRes) {
+          if (c + CH < BN) epi_res_issue<CH>(es, slot ^ 1, &tmR, n0 + CH, args.Cout, args.split, xb, yb, b, lane);
+        }
         if constexpr (MODE == kUpAdd) {
           uint32_t u[32];
           if constexpr (CH == 32) {
@@ -387,8 +510,7 @@ __global__ void __launch_bounds__(256, 1)
             store_row<T, CH>(uu, static_cast<T*>(args.out), pix, n0, args.Cout, args.split);
           }
         } else {
-          epi_chunk<T, CH, MODE>(es, &tmO, &tmR, taddr, args.bias, n0, args.Cout, args.split,
-                                 tx * args.wb + box_dx, ty * args.hb + box_dy, b, lane);
+          epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, n0, args.Cout, args.split, xb, yb, b, lane);
         }
       }
       ptx::tc_fence_before();
@@ -441,7 +563,7 @@ struct RowsSmem {
   static constexpr int kA = ((ROWS * WB * BK * 2 + 1023) / 1024) * 1024;
   static constexpr int kBt = ((BN * BK * 2 + 1023) / 1024) * 1024;  // one tap's B tile
   static constexpr int kStage = kA + 3 * kBt;
-  static constexpr int kBars = (2 * STAGES + 8) * 8 + 16;
+  static constexpr int kBars = (2 * STAGES + 12) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   static constexpr int kTotal = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes + 1024;
   static constexpr uint32_t kTmemCols = (2 * R * BN <= 32) ? 32 : (2 * R * BN <= 64) ? 64 : (2 * R * BN <= 128) ? 128
@@ -458,6 +580,7 @@ __global__ void __launch_bounds__(256, 1)
   constexpr int WB = 128 / HB;
   constexpr int ROWS = R * HB + 2;
   using S = RowsSmem<BN, BK, R, ROWS, WB, STAGES>;
+  static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
   static_assert(WB % 8 == 0, "swizzle alignment of the shifted A operands");
   extern __shared__ uint8_t smem_raw[];
@@ -466,8 +589,8 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;  // 4 residual barriers (one per epilogue warp)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 4);
+  uint64_t* rbar = tempty + 2;  // 8 residual barriers (two per epilogue warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 8);
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   if (warp == 0 && lane == 0) {
@@ -481,7 +604,7 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
-    for (int a = 0; a < 4; ++a) ptx::mbar_init(&rbar[a], 1);
+    for (int a = 0; a < 8; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -564,7 +687,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[q], 0};
+    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}};
     const int box_dx = (q * 32) % WB, box_dy = (q * 32) / WB;
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
@@ -577,14 +700,24 @@ __global__ void __launch_bounds__(256, 1)
       const int b = m / args.tiles_y;
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
+      constexpr bool kRes = MODE == kResidualRelu;
+      constexpr int NC = BN / CH;
+      const int xb = tx * WB + box_dx;
+      const int yb0 = tyg * R * HB + box_dy;
+      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb0, b, lane);
 #pragma unroll 1
-      for (int r = 0; r < R; ++r) {
-#pragma unroll 1
-        for (int c = 0; c < BN; c += CH) {
-          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
-          epi_chunk<T, CH, MODE>(es, &tmO, &tmR, taddr, args.bias, nt * BN + c, args.Cout, args.split,
-                                 tx * WB + box_dx, tyg * R * HB + r * HB + box_dy, b, lane);
+      for (int i = 0; i < R * NC; ++i) {
+        const int r = i / NC, c = (i - r * NC) * CH;
+        const int slot = i & 1;
+        if constexpr (kRes) {
+          if (i + 1 < R * NC) {
+            const int r1 = (i + 1) / NC, c1 = (i + 1 - r1 * NC) * CH;
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, yb0 + r1 * HB, b, lane);
+          }
         }
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
+        epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
+                               yb0 + r * HB, b, lane);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
@@ -614,9 +747,12 @@ struct NzSmem {
   static constexpr int kA = ((2 * kChunkStride + 1023) / 1024) * 1024;  // two 8-ch chunks (K = 16)
   static constexpr int kBt = ((BN * 32 + 1023) / 1024) * 1024;          // one tap's BN x 16 B tile
   static constexpr int kStage = kA + 9 * kBt;
-  static constexpr int kBars = (2 * STAGES + 8) * 8 + 16;
+  static constexpr int kBars = (2 * STAGES + 12) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
-  static constexpr int kTotal = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes + 1024;
+  static constexpr int kHeadOff = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes;
+  static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
+  static constexpr int kHeadBytes = (kHeadTasks * 156 + kHead * 64 + kHead) * 4;
+  static constexpr int kTotal = kHeadOff + kHeadBytes + 1024;
   static constexpr uint32_t kTmemCols = (2 * R * BN <= 256) ? 256 : 512;
 };
 
@@ -634,8 +770,9 @@ template <typename T, int BN, int R, int STAGES, int MODE>
 __global__ void __launch_bounds__(256, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
-                    const ConvArgs args) {
+                    const ConvArgs args, const __grid_constant__ HeadArgs hargs) {
   using S = NzSmem<BN, R, STAGES>;
+  static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -643,8 +780,8 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 4);
+  uint64_t* rbar = tempty + 2;  // 8 residual barriers (two per epilogue warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 8);
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   if (warp == 0 && lane == 0) {
@@ -658,7 +795,7 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
-    for (int a = 0; a < 4; ++a) ptx::mbar_init(&rbar[a], 1);
+    for (int a = 0; a < 8; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -735,7 +872,18 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[q], 0};
+    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}};
+    float* s_th = reinterpret_cast<float*>(smem + S::kHeadOff);
+    float* s_w = s_th + S::kHeadTasks * 156;
+    float* s_b = s_w + kHead * 64;
+    const int et = q * 32 + (int)lane;  // 0..127 over the epilogue warps
+    if constexpr (MODE == kHeadFused) {
+      for (int i = et; i < kHead * CH; i += 128) {
+        const int o = i / CH, j = i - o * CH;
+        s_w[i] = j < hargs.C0 ? hargs.Wpre[o * hargs.C0 + j] : 0.f;
+      }
+      if (et < kHead) s_b[et] = hargs.bpre[et];
+    }
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -745,15 +893,46 @@ __global__ void __launch_bounds__(256, 1)
       m /= args.tiles_x;
       const int tyg = m % args.tiles_y;
       const int b = m / args.tiles_y;
+      int lf = 0, oy = 0, ox = 0;
+      if constexpr (MODE == kHeadFused) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous work item's theta no longer read
+        const int nth = hargs.ntasks * kTheta;
+        for (int i = et; i < nth; i += 128) {
+          const int t = i / kTheta;
+          s_th[t * 156 + (i - t * kTheta)] = hargs.theta[(int64_t)b * nth + i];
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (hargs.tiles) {
+          const uint32_t id = hargs.tiles[hargs.first + b];
+          lf = id >> 30;
+          const int f = 1 << lf;
+          oy = min((int)((id >> 15) & 0x7FFF) * hargs.S, hargs.Hp / f - hargs.P);
+          ox = min((int)(id & 0x7FFF) * hargs.S, hargs.Wp / f - hargs.P);
+        }
+      }
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
+      constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
+      constexpr int NC = BN / CH;
+      const int xb = tx * 128 + q * 32;
+      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, tyg * R, b, lane);
 #pragma unroll 1
-      for (int r = 0; r < R; ++r) {
-#pragma unroll 1
-        for (int c = 0; c < BN; c += CH) {
-          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
-          epi_chunk<T, CH, MODE>(es, &tmO, &tmR, taddr, args.bias, nt * BN + c, args.Cout, args.split,
-                                 tx * 128 + q * 32, tyg * R + r, b, lane);
+      for (int i = 0; i < R * NC; ++i) {
+        const int r = i / NC, c = (i - r * NC) * CH;
+        const int slot = i & 1;
+        if constexpr (kRes) {
+          if (i + 1 < R * NC) {
+            const int r1 = (i + 1) / NC, c1 = (i + 1 - r1 * NC) * CH;
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1, b, lane);
+          }
+        }
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
+        if constexpr (MODE == kHeadFused) {
+          epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b, lane, hargs, s_w, s_b, s_th,
+                          lf, oy, ox);
+        } else {
+          epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
+                                 tyg * R + r, b, lane);
         }
       }
       ptx::tc_fence_before();

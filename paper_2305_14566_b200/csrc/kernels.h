@@ -16,13 +16,6 @@ struct DevState {
   int pad_;
 };
 
-// Per-task stitch targets passed by value to the head kernel.
-struct HeadTaskTable {
-  uint32_t* canvas[kMaxTasks];  // fixed-point accumulators, rows [row0, row1) of the task canvas
-  int Ht[kMaxTasks], Wt[kMaxTasks];
-  int row0[kMaxTasks], row1[kMaxTasks];
-  int log2f[kMaxTasks];
-};
 
 void launch_pad_colour(const uint8_t* slide, int64_t W, DevState* st, cudaStream_t s);
 void launch_pyramid(const FrontParams& p, const DevState* st, uint32_t* L2, uint32_t* L4, uint32_t* L8,

@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -193,6 +194,8 @@ struct omniseg {
   };
   std::vector<ConvPlan> enc_plans, dec_plans;
   std::vector<const Layer*> enc_layers, dec_layers;
+  ConvPlan head_plan{};   // dec0.b with the dynamic head + stitch fused into its epilogue
+  bool head_fusable = false;
 
   // front end / canvases
   DevBuf slide, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
@@ -428,6 +431,16 @@ void ensure_workspace(omniseg* h, int P) {
     dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, h->arch.xa ? l : 1000);
     dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu, l);
   }
+  // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
+  h->head_fusable = false;
+  if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr) {
+    LevelBufs& q = h->lv[0];
+    ConvPlan hp = plan(h->dec_b[0], q.Bt.p, q.P, q.A.p, q.A.p, kHeadFused, 0);
+    if (hp.nz_R > 0 && hp.bn == h->Cp[0] && h->C[0] <= 32) {
+      h->head_plan = hp;
+      h->head_fusable = true;
+    }
+  }
   h->ws_P = P;
   h->ws_B = B;
 }
@@ -542,14 +555,40 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
                     h->theta.as<float>(), s);
   h->launches += 2;
   if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, h->g.p, (size_t)n * h->C[L - 1] * 4, cudaMemcpyDefault, s));
-  for (size_t i = 0; i < h->dec_plans.size(); ++i) {
-    set_conv_batch(h->dec_plans[i], n);
-    run_conv_prof(h, h->dec_plans[i], *h->dec_layers[i], (int)(h->enc_plans.size() + i), n);
+  const bool fuse = h->head_fusable && ntasks <= 8;
+  const size_t ndec = h->dec_plans.size();
+  for (size_t i = 0; i < ndec; ++i) {
+    if (fuse && i + 1 == ndec) {
+      ConvPlan& hp = h->head_plan;
+      set_conv_batch(hp, n);
+      HeadArgs& ha = hp.head;
+      ha.Wpre = h->Wpre.as<float>();
+      ha.bpre = h->bpre.as<float>();
+      ha.theta = h->theta.as<float>();
+      ha.ntasks = ntasks;
+      ha.C0 = h->C[0];
+      ha.P = P;
+      ha.S = S;
+      ha.Hp = Hp;
+      ha.Wp = Wp;
+      ha.pad = pad;
+      ha.tiles = tiles;
+      ha.first = first;
+      ha.out_p = out_p;
+      ha.out_F = out_F;
+      ha.tt = tt;
+      run_conv_prof(h, hp, *h->dec_layers[i], (int)(h->enc_plans.size() + i), n);
+    } else {
+      set_conv_batch(h->dec_plans[i], n);
+      run_conv_prof(h, h->dec_plans[i], *h->dec_layers[i], (int)(h->enc_plans.size() + i), n);
+    }
     h->conv_launches++;
   }
-  launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.sp(0), P, h->Wpre.as<float>(), h->bpre.as<float>(),
-                 h->theta.as<float>(), ntasks, tiles, first, tt, S, Hp, Wp, pad, out_p, out_F, s);
-  h->launches++;
+  if (!fuse) {
+    launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.sp(0), P, h->Wpre.as<float>(),
+                   h->bpre.as<float>(), h->theta.as<float>(), ntasks, tiles, first, tt, S, Hp, Wp, pad, out_p, out_F, s);
+    h->launches++;
+  }
   OS_CUDA(cudaGetLastError());
 }
 
