@@ -24,9 +24,11 @@ struct ConvPlan {
 // K-major), fp32 bias; output grid Ho = ceil(Hin/stride) etc. `res` per ConvMode.
 // split_out: res/out use the hi|lo split layout (x2 precision); for split inputs the
 // caller passes Cin = 2 x channels and weights duplicated along K ([W | W]).
+// B = images per launch (work items); B_in / B_res / B_out = batch extents of the input,
+// residual and output tensors (default B; the args.b_* offsets select the images).
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
                         const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
-                        bool split_out = false);
+                        bool split_out = false, int B_in = -1, int B_res = -1, int B_out = -1);
 void set_conv_batch(ConvPlan& p, int B);
 void run_conv(const ConvPlan& p, cudaStream_t s);
 int num_sms();

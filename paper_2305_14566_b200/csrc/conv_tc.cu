@@ -165,7 +165,10 @@ int num_sms() {
 
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
                         const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
-                        bool split_out) {
+                        bool split_out, int B_in, int B_res, int B_out) {
+  if (B_in < 0) B_in = B;
+  if (B_res < 0) B_res = B;
+  if (B_out < 0) B_out = B;
   OS_REQUIRE(Cin % 16 == 0 && Cout % 16 == 0, "conv channels must be multiples of 16");
   OS_REQUIRE(k == 1 || k == 3, "conv kernel size must be 1 or 3");
   OS_REQUIRE(stride == 1 || stride == 2, "conv stride must be 1 or 2");
@@ -205,7 +208,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     const int R = NzCfg::R(p.bn);
     // A: 5-D view {8 ch, W, H, Cin/8, B} with the chunk dimension (16-B stride) outside the
     // pixel dimensions, box {8, 130, R+2, 2, 1} -> smem [chunk][row][px][16 B]
-    cuuint64_t dims[5] = {8, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)(Cin / 8), (cuuint64_t)B};
+    cuuint64_t dims[5] = {8, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)(Cin / 8), (cuuint64_t)B_in};
     cuuint64_t strides[4] = {(cuuint64_t)Cin * 2, (cuuint64_t)Win * Cin * 2, 16, (cuuint64_t)Hin * Win * Cin * 2};
     cuuint32_t box[5] = {8, 130, (cuuint32_t)(R + 2), 2, 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
@@ -240,7 +243,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.split = split_out ? 1 : 0;
   const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   if (p.nz_R == 0) {
-    cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B};
+    cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B_in};
     cuuint64_t strides[3] = {(cuuint64_t)Cin * 2, (cuuint64_t)Win * Cin * 2, (cuuint64_t)Hin * Win * Cin * 2};
     cuuint32_t box[4] = {(cuuint32_t)p.bk, (cuuint32_t)(a.wb * stride), (cuuint32_t)(a.hb * stride), 1};
     if (p.rows_R > 0) box[2] = (cuuint32_t)(p.rows_R * a.hb + 2);
@@ -267,7 +270,8 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     const int CH = p.bn < 32 ? p.bn : 32;
     const int Cst = split_out ? 2 * Cout : Cout;
     const int bw = a.wb < 32 ? a.wb : 32, bh = 32 / bw;
-    cuuint64_t dims[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B};
+    cuuint64_t dims[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B_out};
+    cuuint64_t dims_r[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B_res};
     cuuint64_t strides[3] = {(cuuint64_t)Cst * 2, (cuuint64_t)Wo * Cst * 2, (cuuint64_t)Ho * Wo * Cst * 2};
     cuuint32_t box[4] = {(cuuint32_t)CH, (cuuint32_t)bw, (cuuint32_t)bh, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
@@ -277,7 +281,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(out) failed: " + std::to_string((int)r));
       if (res) {
-        r = encode_fn()(&p.tmR, dt, 4, const_cast<void*>(res), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        r = encode_fn()(&p.tmR, dt, 4, const_cast<void*>(res), dims_r, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(res) failed: " + std::to_string((int)r));
       } else {

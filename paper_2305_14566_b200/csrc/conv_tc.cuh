@@ -42,6 +42,9 @@ struct ConvArgs {
   const void* res;        // residual (mode 1, [B][Ho][Wo][Cout]) or skip (mode 2, [B][2Ho][2Wo][Cout])
   void* out;              // [B][Ho][Wo][Cout] (mode 2: [B][2Ho][2Wo][Cout])
   int split;              // res/out stored as [Cout] hi | [Cout] lo per pixel (x2 precision mode)
+  // batch-index offsets of the tensors (a launch over images [0, B) of the work space reads
+  // input image b + b_in, residual b + b_res, writes b + b_out, head tile b + b_head)
+  int b_in, b_res, b_out, b_head;
 };
 
 template <typename T>
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(256, 1)
           uint8_t* sa = smem + stage * S::kStage;
           uint8_t* sb = sa + S::kA;
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0 + dy, b);
+          ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0 + dy, b + args.b_in);
           ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
           if (++stage == STAGES) {
             stage = 0;
@@ -479,14 +482,14 @@ __global__ void __launch_bounds__(256, 1)
       ptx::tc_fence_after();
       constexpr bool kRes = MODE == kResidualRelu;
       const int xb = tx * args.wb + box_dx, yb = ty * args.hb + box_dy;
-      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb, b, lane);
+      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb, b + args.b_res, lane);
 #pragma unroll 1
       for (int c = 0; c < BN; c += CH) {
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
         const int n0 = nt * BN + c;
         const int slot = (c / CH) & 1;
         if constexpr (kRes) {
-          if (c + CH < BN) epi_res_issue<CH>(es, slot ^ 1, &tmR, n0 + CH, args.Cout, args.split, xb, yb, b, lane);
+          if (c + CH < BN) epi_res_issue<CH>(es, slot ^ 1, &tmR, n0 + CH, args.Cout, args.split, xb, yb, b + args.b_res, lane);
         }
         if constexpr (MODE == kUpAdd) {
           uint32_t u[32];
@@ -502,15 +505,18 @@ __global__ void __launch_bounds__(256, 1)
           const size_t W2 = 2 * (size_t)args.Wo;
 #pragma unroll 1
           for (int a = 0; a < 4; ++a) {
-            const size_t pix = ((size_t)b * 2 * args.Ho + 2 * y + (a >> 1)) * W2 + 2 * x + (a & 1);
+            const size_t pin = (size_t)(2 * y + (a >> 1)) * W2 + 2 * x + (a & 1);
+            const size_t img = (size_t)2 * args.Ho * W2;
             float uu[CH];
 #pragma unroll
             for (int j = 0; j < CH; ++j) uu[j] = v[j];
-            add_row<T, CH>(uu, static_cast<const T*>(args.res), pix, n0, args.Cout, args.split);
-            store_row<T, CH>(uu, static_cast<T*>(args.out), pix, n0, args.Cout, args.split);
+            add_row<T, CH>(uu, static_cast<const T*>(args.res), (size_t)(b + args.b_res) * img + pin, n0, args.Cout,
+                           args.split);
+            store_row<T, CH>(uu, static_cast<T*>(args.out), (size_t)(b + args.b_out) * img + pin, n0, args.Cout,
+                             args.split);
           }
         } else {
-          epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, n0, args.Cout, args.split, xb, yb, b, lane);
+          epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, n0, args.Cout, args.split, xb, yb, b + args.b_out, lane);
         }
       }
       ptx::tc_fence_before();
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__(256, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0, b);
+          ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0, b + args.b_in);
 #pragma unroll
           for (int dy = 0; dy < 3; ++dy)
             ptx::tma_load_2d(sa + S::kA + dy * S::kBt, &tmB, &full[stage], (dy * 3 + dx) * args.Cin + kc * BK,
@@ -704,7 +710,7 @@ __global__ void __launch_bounds__(256, 1)
       constexpr int NC = BN / CH;
       const int xb = tx * WB + box_dx;
       const int yb0 = tyg * R * HB + box_dy;
-      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb0, b, lane);
+      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb0, b + args.b_res, lane);
 #pragma unroll 1
       for (int i = 0; i < R * NC; ++i) {
         const int r = i / NC, c = (i - r * NC) * CH;
@@ -712,12 +718,12 @@ __global__ void __launch_bounds__(256, 1)
         if constexpr (kRes) {
           if (i + 1 < R * NC) {
             const int r1 = (i + 1) / NC, c1 = (i + 1 - r1 * NC) * CH;
-            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, yb0 + r1 * HB, b, lane);
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, yb0 + r1 * HB, b + args.b_res, lane);
           }
         }
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
         epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
-                               yb0 + r * HB, b, lane);
+                               yb0 + r * HB, b + args.b_out, lane);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
@@ -823,7 +829,7 @@ __global__ void __launch_bounds__(256, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          ptx::tma_load_5d(sa, &tmA, &full[stage], 0, x0, y0, 2 * kc, b);
+          ptx::tma_load_5d(sa, &tmA, &full[stage], 0, x0, y0, 2 * kc, b + args.b_in);
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap)
             ptx::tma_load_2d(sa + S::kA + tap * S::kBt, &tmB, &full[stage], tap * args.Cin + kc * 16, nt * BN);
@@ -899,11 +905,11 @@ __global__ void __launch_bounds__(256, 1)
         const int nth = hargs.ntasks * kTheta;
         for (int i = et; i < nth; i += 128) {
           const int t = i / kTheta;
-          s_th[t * 156 + (i - t * kTheta)] = hargs.theta[(int64_t)b * nth + i];
+          s_th[t * 156 + (i - t * kTheta)] = hargs.theta[(int64_t)(b + args.b_head) * nth + i];
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (hargs.tiles) {
-          const uint32_t id = hargs.tiles[hargs.first + b];
+          const uint32_t id = hargs.tiles[hargs.first + b + args.b_head];
           lf = id >> 30;
           const int f = 1 << lf;
           oy = min((int)((id >> 15) & 0x7FFF) * hargs.S, hargs.Hp / f - hargs.P);
@@ -915,7 +921,7 @@ __global__ void __launch_bounds__(256, 1)
       constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
       constexpr int NC = BN / CH;
       const int xb = tx * 128 + q * 32;
-      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, tyg * R, b, lane);
+      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, tyg * R, b + args.b_res, lane);
 #pragma unroll 1
       for (int i = 0; i < R * NC; ++i) {
         const int r = i / NC, c = (i - r * NC) * CH;
@@ -923,16 +929,16 @@ __global__ void __launch_bounds__(256, 1)
         if constexpr (kRes) {
           if (i + 1 < R * NC) {
             const int r1 = (i + 1) / NC, c1 = (i + 1 - r1 * NC) * CH;
-            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1, b, lane);
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res, lane);
           }
         }
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
         if constexpr (MODE == kHeadFused) {
-          epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b, lane, hargs, s_w, s_b, s_th,
-                          lf, oy, ox);
+          epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs, s_w,
+                          s_b, s_th, lf, oy, ox);
         } else {
           epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
-                                 tyg * R + r, b, lane);
+                                 tyg * R + r, b + args.b_out, lane);
         }
       }
       ptx::tc_fence_before();

@@ -196,6 +196,13 @@ struct omniseg {
   std::vector<const Layer*> enc_layers, dec_layers;
   ConvPlan head_plan{};   // dec0.b with the dynamic head + stitch fused into its epilogue
   bool head_fusable = false;
+  // level-0 micro-batching: the level-0 layers run one tile at a time on single-tile
+  // scratch tensors (h0, t, U0) that stay L2-resident; only E0 (the skip) and the gather
+  // output live in HBM. Plans: stem, enc0.a, enc0.b | up0, dec0.a, dec0.b(head or plain)
+  bool mb0 = false;
+  DevBuf s_h0, s_t, s_U0;
+  ConvPlan mb_enc[3], mb_dec[3], mb_head{};
+  bool mb_head_ok = false;
 
   // front end / canvases
   DevBuf slide, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
@@ -431,6 +438,39 @@ void ensure_workspace(omniseg* h, int P) {
     dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, h->arch.xa ? l : 1000);
     dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu, l);
   }
+  // level-0 micro-batching (see the handle); opt-in with OMNISEG_MB0=1 (measured slower: single-tile
+  // launches are too small to reach a pipelined steady state)
+  h->mb0 = false;
+  if (getenv("OMNISEG_MB0") != nullptr && L >= 3) {
+    LevelBufs& q0 = h->lv[0];
+    const size_t t1 = (size_t)P * P * q0.C * (h->arch.sp(0) ? 4 : 2);
+    const size_t t1a = (size_t)P * P * q0.C * ((h->arch.sp(0) && h->arch.xa) ? 4 : 2);
+    h->s_h0.ensure(t1);
+    h->s_t.ensure(t1a);
+    h->s_U0.ensure(t1);
+    auto mplan = [&](const Layer& ly, const void* in, int Hin, int Bin, const void* res, int Bres, void* out, int Bout,
+                     int mode, int ol) {
+      return make_conv_plan(bf, in, 1, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
+                            res, out, h->arch.sp(ol), Bin, Bres, Bout);
+    };
+    const int la = h->arch.xa ? 0 : 1000;
+    const void* D1 = (1 == L - 1) ? h->lv[1].E.p : h->lv[1].A.p;
+    h->mb_enc[0] = mplan(h->stem, h->X0.p, P, B, nullptr, 1, h->s_h0.p, 1, kReluBias, 0);
+    h->mb_enc[1] = mplan(h->enc_a[0], h->s_h0.p, P, 1, nullptr, 1, h->s_t.p, 1, kReluBias, la);
+    h->mb_enc[2] = mplan(h->enc_b[0], h->s_t.p, P, 1, h->s_h0.p, 1, q0.E.p, B, kResidualRelu, 0);
+    h->mb_dec[0] = mplan(h->up[0], D1, P / 2, B, q0.E.p, B, h->s_U0.p, 1, kUpAdd, 0);
+    h->mb_dec[1] = mplan(h->dec_a[0], h->s_U0.p, P, 1, nullptr, 1, h->s_t.p, 1, kReluBias, la);
+    h->mb_dec[2] = mplan(h->dec_b[0], h->s_t.p, P, 1, h->s_U0.p, 1, q0.A.p, B, kResidualRelu, 0);
+    h->mb_head_ok = false;
+    if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr) {
+      ConvPlan hp = mplan(h->dec_b[0], h->s_t.p, P, 1, h->s_U0.p, 1, h->s_U0.p, 1, kHeadFused, 0);
+      if (hp.nz_R > 0 && hp.bn == h->Cp[0] && h->C[0] <= 32) {
+        h->mb_head = hp;
+        h->mb_head_ok = true;
+      }
+    }
+    h->mb0 = true;
+  }
   // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
   h->head_fusable = false;
   if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr) {
@@ -538,12 +578,46 @@ void collect_profile(omniseg* h) {
 }
 
 // Run trunk + GAP/controller + head for `n` tiles already gathered into X0.
+void fill_head(HeadArgs& ha, omniseg* h, int ntasks, int P, int S, int Hp, int Wp, int pad, const uint32_t* tiles,
+               int first, const HeadTaskTable& tt, float* out_p, float* out_F) {
+  ha.Wpre = h->Wpre.as<float>();
+  ha.bpre = h->bpre.as<float>();
+  ha.theta = h->theta.as<float>();
+  ha.ntasks = ntasks;
+  ha.C0 = h->C[0];
+  ha.P = P;
+  ha.S = S;
+  ha.Hp = Hp;
+  ha.Wp = Wp;
+  ha.pad = pad;
+  ha.tiles = tiles;
+  ha.first = first;
+  ha.out_p = out_p;
+  ha.out_F = out_F;
+  ha.tt = tt;
+}
+
 template <typename T>
 void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int first, const HeadTaskTable& tt,
                         int ntasks, int S, int Hp, int Wp, int pad, float* out_p, float* out_F, float* out_g) {
   const int L = h->arch.levels;
   cudaStream_t s = h->stream;
-  for (size_t i = 0; i < h->enc_plans.size(); ++i) {
+  const bool mb = h->mb0;
+  const size_t ne = h->enc_plans.size();
+  // ---------------- encoder
+  if (mb) {
+    for (int i = 0; i < n; ++i) {
+      for (int k = 0; k < 3; ++k) {
+        ConvPlan& pl = h->mb_enc[k];
+        pl.args.b_in = k == 0 ? i : 0;
+        pl.args.b_res = 0;
+        pl.args.b_out = k == 2 ? i : 0;
+        run_conv_prof(h, pl, *h->enc_layers[k], k, 1);
+        h->conv_launches++;
+      }
+    }
+  }
+  for (size_t i = mb ? 3 : 0; i < ne; ++i) {
     set_conv_batch(h->enc_plans[i], n);
     run_conv_prof(h, h->enc_plans[i], *h->enc_layers[i], (int)i, n);
     h->conv_launches++;
@@ -555,36 +629,39 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
                     h->theta.as<float>(), s);
   h->launches += 2;
   if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, h->g.p, (size_t)n * h->C[L - 1] * 4, cudaMemcpyDefault, s));
-  const bool fuse = h->head_fusable && ntasks <= 8;
+  // ---------------- decoder
   const size_t ndec = h->dec_plans.size();
-  for (size_t i = 0; i < ndec; ++i) {
+  const bool fuse = (mb ? h->mb_head_ok : h->head_fusable) && ntasks <= 8;
+  bool head_done = false;
+  for (size_t i = 0; i < (mb ? ndec - 3 : ndec); ++i) {
     if (fuse && i + 1 == ndec) {
       ConvPlan& hp = h->head_plan;
       set_conv_batch(hp, n);
-      HeadArgs& ha = hp.head;
-      ha.Wpre = h->Wpre.as<float>();
-      ha.bpre = h->bpre.as<float>();
-      ha.theta = h->theta.as<float>();
-      ha.ntasks = ntasks;
-      ha.C0 = h->C[0];
-      ha.P = P;
-      ha.S = S;
-      ha.Hp = Hp;
-      ha.Wp = Wp;
-      ha.pad = pad;
-      ha.tiles = tiles;
-      ha.first = first;
-      ha.out_p = out_p;
-      ha.out_F = out_F;
-      ha.tt = tt;
-      run_conv_prof(h, hp, *h->dec_layers[i], (int)(h->enc_plans.size() + i), n);
+      fill_head(hp.head, h, ntasks, P, S, Hp, Wp, pad, tiles, first, tt, out_p, out_F);
+      run_conv_prof(h, hp, *h->dec_layers[i], (int)(ne + i), n);
+      head_done = true;
     } else {
       set_conv_batch(h->dec_plans[i], n);
-      run_conv_prof(h, h->dec_plans[i], *h->dec_layers[i], (int)(h->enc_plans.size() + i), n);
+      run_conv_prof(h, h->dec_plans[i], *h->dec_layers[i], (int)(ne + i), n);
     }
     h->conv_launches++;
   }
-  if (!fuse) {
+  if (mb) {
+    if (fuse) fill_head(h->mb_head.head, h, ntasks, P, S, Hp, Wp, pad, tiles, first, tt, out_p, out_F);
+    for (int i = 0; i < n; ++i) {
+      for (int k = 0; k < 3; ++k) {
+        ConvPlan& pl = (k == 2 && fuse) ? h->mb_head : h->mb_dec[k];
+        pl.args.b_in = k == 0 ? i : 0;
+        pl.args.b_res = k == 0 ? i : 0;
+        pl.args.b_out = (k == 2 && !fuse) ? i : 0;
+        pl.args.b_head = i;
+        run_conv_prof(h, pl, *h->dec_layers[ndec - 3 + k], (int)(ne + ndec - 3 + k), 1);
+        h->conv_launches++;
+      }
+    }
+    head_done = fuse;
+  }
+  if (!head_done) {
     launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.sp(0), P, h->Wpre.as<float>(),
                    h->bpre.as<float>(), h->theta.as<float>(), ntasks, tiles, first, tt, S, Hp, Wp, pad, out_p, out_F, s);
     h->launches++;
