@@ -171,10 +171,11 @@ def run_reference(a):
 
 
 def tile_estimate(w):
-    """Kept-tile count of the workload from the GPU path's last run if recorded, else the
-    SURVEY §8(d) estimate (only used to extrapolate the oracle sample)."""
-    est = {"cfg1_tiny": 46, "cfg2_single_scale": 160, "cfg3_multiscale": 1800, "cfg4_needle_biopsy": 10900}
-    p = os.path.join(ROOT, "profiles", "kept_tiles.json")
+    """Kept-tile count of the workload as computed by the ORACLE front end
+    (tests/golden/kept_tiles.json, written by scripts/oracle_tile_counts.py); only used to
+    extrapolate the oracle's timing sample. Falls back to the SURVEY §8(d) estimate."""
+    est = {"cfg5_sweep_fg95": 31874}
+    p = os.path.join(ROOT, "tests", "golden", "kept_tiles.json")
     try:
         with open(p) as f:
             return json.load(f)[w.name]
@@ -307,11 +308,12 @@ def main():
     if rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
         try:
             t_fe, t_tile = oracle_sample(w, lambda r0, r1: render(g, r0, r1).numpy())
-            T = t_fe * H / 512 + t_tile * n_tiles
+            n_or = tile_estimate(w)
+            T = t_fe * H / 512 + t_tile * n_or
             cpu = {"value": H * W / 1e6 / T, "unit": "Mpx/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"oracle (fp64 numpy) front end on a 512-row strip ({t_fe:.2f} s) + one 512^2 window "
                              f"through trunk+head+stitch ({t_tile:.2f} s), extrapolated to {H} rows and "
-                             f"{n_tiles} kept tiles"}
+                             f"{n_or} kept tiles (oracle tile plan)"}
         except Exception as e:  # the baseline must never break the bench line
             cpu = {"value": None, "unit": "Mpx/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"failed: {e}"}

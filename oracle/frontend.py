@@ -108,7 +108,7 @@ def detection(padded: np.ndarray, H: int, W: int, pad: int, k: int = 7, guard: i
     t = Otsu threshold, g_pad = luma of the pad colour, fg = foreground mask u8).
     Interior = level-8 rows [pad/8, pad/8 + H//8), cols likewise (pixels wholly
     inside the slide). fg = interior & gm <= t & gm <= g_pad - guard (tissue is the
-    darker side; the guard is DESIGN.md reading R5)."""
+    darker side; the guard is DESIGN.md reading R7)."""
     assert pad % 8 == 0
     L8 = level(padded, 8)
     g8 = luma(L8)
@@ -160,3 +160,48 @@ def tile_plan(fg: np.ndarray, Hp: int, Wp: int, factors, P: int, S: int):
                     n += 1
         grids[f] = (len(oys), len(oxs), n)
     return kept, grids
+
+
+def padded_window(slide: np.ndarray, pad: int, pc, r0: int, r1: int, c0: int, c1: int) -> np.ndarray:
+    """Rows [r0, r1) x cols [c0, c1) of the padded slide (pad_slide) without materialising
+    the whole frame: slide pixels where they exist, the pad colour elsewhere."""
+    H, W, _ = slide.shape
+    out = np.empty((r1 - r0, c1 - c0, 3), np.uint8)
+    out[:, :] = np.asarray(pc, np.uint8)
+    ys, ye = max(r0, pad), min(r1, pad + H)
+    xs, xe = max(c0, pad), min(c1, pad + W)
+    if ys < ye and xs < xe:
+        out[ys - r0:ye - r0, xs - c0:xe - c0] = slide[ys - pad:ye - pad, xs - pad:xe - pad]
+    return out
+
+
+def detection_chunked(slide: np.ndarray, pad: int, rows_per_chunk: int = 4096, k: int = 7, guard: int = 16):
+    """`detection` evaluated on a padded frame too large to materialise: level 8 is a
+    block-local mean, so computing it over row windows that are multiples of 8 rows and
+    concatenating is identical to `level(pad_slide(slide), 8)`; the median, histogram,
+    Otsu and foreground then run on the (small) whole level-8 grid exactly as in
+    `detection`."""
+    H, W, _ = slide.shape
+    Hp, Wp = padded_extent(H, W, pad)
+    pc = pad_colour(slide)
+    step = rows_per_chunk // 8 * 8
+    L8 = np.concatenate([level(padded_window(slide, pad, pc, r, min(Hp, r + step), 0, Wp), 8)
+                         for r in range(0, Hp, step)])
+    g8 = luma(L8)
+    gm = median_blur(g8, k)
+    r0, c0 = pad // 8, pad // 8
+    r1, c1 = r0 + H // 8, c0 + W // 8
+    interior = np.zeros(gm.shape, bool)
+    interior[r0:r1, c0:c1] = True
+    hist = np.bincount(gm[interior].ravel(), minlength=256).astype(np.int64)
+    t = otsu_threshold(hist)
+    g_pad = int(luma(pc.astype(np.uint8)[None, None, :])[0, 0])
+    fg = interior & (gm.astype(np.int64) <= t) & (gm.astype(np.int64) <= g_pad - guard)
+    return dict(g8=g8, gm=gm, hist=hist, t=t, g_pad=g_pad, fg=fg.astype(np.uint8), pc=pc, Hp=Hp, Wp=Wp)
+
+
+def level_window(slide: np.ndarray, pad: int, pc, f: int, oy: int, ox: int, P: int) -> np.ndarray:
+    """The P x P window at level f with origin (oy, ox) (level-f padded coordinates),
+    computed from the 40x padded region it averages (identical to slicing `level`)."""
+    win = padded_window(slide, pad, pc, oy * f, (oy + P) * f, ox * f, (ox + P) * f)
+    return level(win, f)

@@ -1,0 +1,106 @@
+"""Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py times
+(fp16x2, batch 64, device-resident slide and outputs):
+
+* front end bit-exact at full size: Otsu t, g_pad, the level-8 foreground mask and the
+  kept-tile list, against the oracle's detection (evaluated row-chunked, identical to the
+  whole-frame definition: tests/test_oracle_frontend.py) and tile plan;
+* the probability canvas on sampled pixels that the oracle computes one by one (every
+  kept window covering the pixel through the fp64 trunk + head, averaged): |dp| <= 1e-2,
+  and the mask agrees wherever the oracle probability is not within 1e-2 of 1/2.
+"""
+import numpy as np
+import pytest
+import torch
+
+from omniseg_inputs import arch_string, geometry, render, workload
+from oracle import frontend as fe
+from oracle import net as nn
+from oracle import pipeline as op
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _unpack(ids, Hp, Wp, P, S):
+    out = []
+    for v in ids.tolist():
+        f = 1 << (v >> 30)
+        out.append((f, min(((v >> 15) & 0x7FFF) * S, Hp // f - P), min((v & 0x7FFF) * S, Wp // f - P)))
+    return out
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_fullsize_front_end_and_sampled_probabilities(gpu_lib, cfg):
+    from paper_2305_14566_b200 import Omniseg
+    w = workload(cfg)
+    H, W, P, S, pad = w.H, w.W, w.patch, w.stride, w.pad
+    slide_d = render(geometry(w.slide), device="cuda", chunk_rows=2048)
+    slide = slide_d.cpu().numpy()
+    h = Omniseg(arch_string(w.arch), w.weights())
+    sizes = [h.output_size(H, W, s) for s in w.scales]
+    prob = torch.empty(sum(sizes), dtype=torch.float32, device="cuda")
+    mask = torch.empty(sum(sizes), dtype=torch.uint8, device="cuda")
+    h.segment_slide(slide_d, H, W, pad, P, S, w.scales, w.classes, prob, mask, None)
+    torch.cuda.synchronize()
+    prob, mask = prob.cpu().numpy(), mask.cpu().numpy()
+    # ---- front end, bit-exact
+    det = fe.detection_chunked(slide, pad)
+    fg, t, gpad = h.fgmask()
+    assert t == det["t"] and gpad == det["g_pad"]
+    assert (fg == det["fg"]).all()
+    arch = nn.parse_arch(arch_string(w.arch))
+    tf = op.task_factors(arch, w.scales)
+    kept, _ = fe.tile_plan(det["fg"], det["Hp"], det["Wp"], [f for f, _ in tf], P, S)
+    got = _unpack(h.tiles(), det["Hp"], det["Wp"], P, S)
+    assert got == kept
+    # ---- sampled probabilities
+    net = nn.unpack_weights(arch, w.weights())
+    rng = np.random.default_rng(cfg)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    cache, checked, budget = {}, 0, 10
+    for ti, (f, s_idx) in enumerate(tf):
+        Ht, Wt = (H + f - 1) // f, (W + f - 1) // f
+        pt = prob[offs[ti]:offs[ti + 1]].reshape(Ht, Wt)
+        mt = mask[offs[ti]:offs[ti + 1]].reshape(Ht, Wt)
+        cand = []
+        pos = np.argwhere(mt == 1)
+        if len(pos):
+            cand += [tuple(pos[i]) for i in rng.choice(len(pos), min(2, len(pos)), replace=False)]
+        cov = np.argwhere(pt > 0)
+        if len(cov):
+            cand += [tuple(cov[i]) for i in rng.choice(len(cov), min(2, len(cov)), replace=False)]
+        for (cy, cx) in cand:
+            tiles = op.covering_tiles(kept, f, pad, P, int(cy), int(cx))
+            need = [k for k in tiles if k not in cache]
+            if len(cache) + len(need) > budget:
+                continue
+            for (ff, oy, ox) in need:
+                win = fe.level_window(slide, pad, det["pc"], ff, oy, ox, P)
+                tasks = [(c, s) for c, (f2, s) in zip(w.classes, tf) if f2 == ff]
+                Fr, Er = nn.trunk(net, arch, win)
+                g = nn.gap(Er)
+                cache[(ff, oy, ox)] = {(c, s): nn.head(Fr, nn.controller(net, arch, g, c, s)) for c, s in tasks}
+            # the chosen pixel and its 24x24 neighbourhood wherever the covering windows are cached
+            for yy in range(max(0, cy - 12), min(Ht, cy + 12)):
+                for xx in range(max(0, cx - 12), min(Wt, cx + 12)):
+                    tl = op.covering_tiles(kept, f, pad, P, yy, xx)
+                    if any(k not in cache for k in tl):
+                        continue
+                    ps = [cache[(ff, oy, ox)][(w.classes[ti], s_idx)][yy + pad // f - oy, xx + pad // f - ox]
+                          for (ff, oy, ox) in tl]
+                    p_ref = float(np.mean(ps)) if ps else 0.0
+                    assert abs(float(pt[yy, xx]) - p_ref) <= 1e-2, (ti, yy, xx, pt[yy, xx], p_ref)
+                    if abs(p_ref - 0.5) > 1e-2:
+                        assert int(mt[yy, xx]) == int(p_ref >= 0.5)
+                    checked += 1
+    assert checked >= 500
+
+
+def test_synthetic_slide_cpu_gpu_identical(gpu_lib):
+    """The seeded generator gives byte-identical windows on CPU and GPU (bench generates
+    slides on the GPU, the oracle side on the CPU)."""
+    for cfg in (3, 4, 5):
+        g = geometry(workload(cfg).slide)
+        for (r0, c0) in ((0, 0), (5000, 3000), (g["H"] - 300, g["W"] - 700)):
+            a = render(g, r0, r0 + 256, c0, c0 + 512).numpy()
+            b = render(g, r0, r0 + 256, c0, c0 + 512, device="cuda").cpu().numpy()
+            assert (a == b).all(), (cfg, r0, c0)

@@ -248,3 +248,17 @@ def test_all_tissue_full_grid():
     assert det["fg"].sum() >= 64 * 64 - 4 * 9 and det["fg"][:8].sum() == 0
     kept, grids = fe.tile_plan(det["fg"], p.shape[0], p.shape[1], [1], 128, 128)
     assert grids[1] == (5, 5, 25) and len(kept) == 25
+
+
+def test_chunked_detection_equals_whole_frame():
+    """The memory-bounded evaluation (row windows) equals the whole-frame definition."""
+    from omniseg_inputs import make_slide, workload
+    w = workload(1)
+    s = make_slide(w.slide).numpy()
+    p = fe.pad_slide(s, w.pad)
+    a = fe.detection(p, 1024, 1024, w.pad)
+    b = fe.detection_chunked(s, w.pad, rows_per_chunk=256)
+    assert a["t"] == b["t"] and (a["fg"] == b["fg"]).all() and (a["hist"] == b["hist"]).all()
+    assert a["g_pad"] == b["g_pad"]
+    L1 = fe.level(p, 4)
+    assert (fe.level_window(s, w.pad, fe.pad_colour(s), 4, 40, 12, 64) == L1[40:104, 12:76]).all()
