@@ -42,7 +42,7 @@ CUtensorMapSwizzle swz(int bytes) {
 template <typename T, int BN, int BK>
 struct Cfg {
   static constexpr int kStageBytes = ConvSmem<BN, BK, 1>::kStage;
-  static constexpr int kStages0 = kStageBudget / kStageBytes;
+  static constexpr int kStages0 = kStageBudgetTap / kStageBytes;
   static constexpr int STAGES = kStages0 > 8 ? 8 : (kStages0 < 2 ? 2 : kStages0);
   using Smem = ConvSmem<BN, BK, STAGES>;
 };
@@ -148,7 +148,7 @@ void dispatch(const ConvPlan& p, cudaStream_t s) {
 
 int stages_for(int bn, int bk) {
   const int a = 128 * bk * 2, b = ((bn * bk * 2 + 1023) / 1024) * 1024;
-  int st = kStageBudget / (a + b);
+  int st = kStageBudgetTap / (a + b);
   return st > 8 ? 8 : (st < 2 ? 2 : st);
 }
 }  // namespace
@@ -276,6 +276,19 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     cuuint32_t box[4] = {(cuuint32_t)CH, (cuuint32_t)bw, (cuuint32_t)bh, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const CUtensorMapSwizzle sw = CH == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    if (mode == kUpAdd && a.wb >= 32) {
+      // up-add: full-resolution skip / output, one box = 64 output pixels of one row
+      cuuint64_t d2[4] = {(cuuint64_t)Cst, (cuuint64_t)(2 * Wo), (cuuint64_t)(2 * Ho), (cuuint64_t)B_out};
+      cuuint64_t d2r[4] = {(cuuint64_t)Cst, (cuuint64_t)(2 * Wo), (cuuint64_t)(2 * Ho), (cuuint64_t)B_res};
+      cuuint64_t st2[3] = {(cuuint64_t)Cst * 2, (cuuint64_t)2 * Wo * Cst * 2, (cuuint64_t)4 * Ho * Wo * Cst * 2};
+      cuuint32_t bx2[4] = {(cuuint32_t)CH, 64, 1, 1};
+      CUresult r = encode_fn()(&p.tmO, dt, 4, out, d2, st2, bx2, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(up out) failed: " + std::to_string((int)r));
+      r = encode_fn()(&p.tmR, dt, 4, const_cast<void*>(res), d2r, st2, bx2, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(up skip) failed: " + std::to_string((int)r));
+    }
     if (mode != kUpAdd) {
       CUresult r = encode_fn()(&p.tmO, dt, 4, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -342,7 +342,11 @@ struct ConvSmem {
   static constexpr int kStage = kA + kB;
   static constexpr int kBars = (2 * STAGES + 12) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
-  static constexpr int kTotal = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes + 1024;  // + alignment slack
+  // epilogue smem: the TMA epilogue tiles, or the up-add tiles (4 x 64 rows x CH ch per warp)
+  static constexpr int kCH = BN < 32 ? BN : 32;
+  static constexpr int kUpBytes = 4 * 4 * 64 * kCH * 2;
+  static constexpr int kEpiBytes = EpiTile<kCH>::kBytes > kUpBytes ? EpiTile<kCH>::kBytes : kUpBytes;
+  static constexpr int kTotal = kEpiOff + kEpiBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                                           : (2 * BN <= 256) ? 256 : 512;
   static constexpr uint32_t kLayout = BK == 64 ? 2u : BK == 32 ? 4u : 6u;  // SW128 / SW64 / SW32
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(256, 1)
   using S = ConvSmem<BN, BK, STAGES>;
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(256, 1)
     const int row = q * 32 + lane;        // M row = pixel within the tile
     const int py = row / args.wb, px = row - (row / args.wb) * args.wb;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}};
+    EpiState es{smem + S::kEpiOff + q * (S::kEpiBytes / 4), &rbar[2 * q], {0, 0}};
     const int bw = args.wb < 32 ? args.wb : 32;
     const int box_dx = (q * 32) % args.wb, box_dy = (q * 32) / args.wb;
     (void)bw;
@@ -502,18 +506,71 @@ __global__ void __launch_bounds__(256, 1)
           float v[CH];
 #pragma unroll
           for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(args.bias + n0 + j);
-          const size_t W2 = 2 * (size_t)args.Wo;
+          if (args.wb >= 32) {
+            // TMA path: the warp's 32 low-res pixels (one row) -> two output rows of 64 pixels
+            using E = EpiTile<CH>;
+            constexpr int kUB = 64 * CH * 2;  // one 64-row buffer
+            uint8_t* sk_hi = es.buf;
+            uint8_t* sk_lo = es.buf + kUB;
+            uint8_t* o_hi = es.buf + 2 * kUB;
+            uint8_t* o_lo = es.buf + 3 * kUB;
 #pragma unroll 1
-          for (int a = 0; a < 4; ++a) {
-            const size_t pin = (size_t)(2 * y + (a >> 1)) * W2 + 2 * x + (a & 1);
-            const size_t img = (size_t)2 * args.Ho * W2;
-            float uu[CH];
+            for (int a = 0; a < 2; ++a) {
+              const int ox = 2 * xb, oyy = 2 * yb + a;
+              if (lane == 0) {
+                ptx::mbar_arrive_expect_tx(&es.rbar[0], (args.split ? 2 : 1) * kUB);
+                ptx::tma_load_4d(sk_hi, &tmR, &es.rbar[0], n0, ox, oyy, b + args.b_res);
+                if (args.split) ptx::tma_load_4d(sk_lo, &tmR, &es.rbar[0], args.Cout + n0, ox, oyy, b + args.b_res);
+              }
+              ptx::mbar_wait(&es.rbar[0], es.rphase[0]);
+              es.rphase[0] ^= 1;
+              if (lane == 0) ptx::bulk_wait_read0();
+              __syncwarp();
 #pragma unroll
-            for (int j = 0; j < CH; ++j) uu[j] = v[j];
-            add_row<T, CH>(uu, static_cast<const T*>(args.res), (size_t)(b + args.b_res) * img + pin, n0, args.Cout,
-                           args.split);
-            store_row<T, CH>(uu, static_cast<T*>(args.out), (size_t)(b + args.b_out) * img + pin, n0, args.Cout,
+              for (int q2 = 0; q2 < 2; ++q2) {
+                const int rr = 2 * (int)lane + q2;
+#pragma unroll
+                for (int j = 0; j < CH / 8; ++j) {
+                  const uint4 h4 = *reinterpret_cast<const uint4*>(sk_hi + E::off(rr, j));
+                  uint4 l4 = make_uint4(0, 0, 0, 0);
+                  if (args.split) l4 = *reinterpret_cast<const uint4*>(sk_lo + E::off(rr, j));
+                  const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+                  uint32_t o[4], l[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 fh = StoreT<T>::unpack(hh[e]);
+                    const float2 fl = StoreT<T>::unpack(ll[e]);
+                    const float x0 = fh.x + fl.x + v[8 * j + 2 * e], x1 = fh.y + fl.y + v[8 * j + 2 * e + 1];
+                    o[e] = StoreT<T>::pack(x0, x1);
+                    const float2 hv = StoreT<T>::unpack(o[e]);
+                    l[e] = StoreT<T>::pack(x0 - hv.x, x1 - hv.y);
+                  }
+                  *reinterpret_cast<uint4*>(o_hi + E::off(rr, j)) = make_uint4(o[0], o[1], o[2], o[3]);
+                  if (args.split) *reinterpret_cast<uint4*>(o_lo + E::off(rr, j)) = make_uint4(l[0], l[1], l[2], l[3]);
+                }
+              }
+              ptx::fence_proxy_async();
+              __syncwarp();
+              if (lane == 0) {
+                ptx::tma_store_4d(&tmO, o_hi, n0, ox, oyy, b + args.b_out);
+                if (args.split) ptx::tma_store_4d(&tmO, o_lo, args.Cout + n0, ox, oyy, b + args.b_out);
+                ptx::bulk_commit();
+              }
+            }
+          } else {
+            const size_t W2 = 2 * (size_t)args.Wo;
+#pragma unroll 1
+            for (int a = 0; a < 4; ++a) {
+              const size_t pin = (size_t)(2 * y + (a >> 1)) * W2 + 2 * x + (a & 1);
+              const size_t img = (size_t)2 * args.Ho * W2;
+              float uu[CH];
+#pragma unroll
+              for (int j = 0; j < CH; ++j) uu[j] = v[j];
+              add_row<T, CH>(uu, static_cast<const T*>(args.res), (size_t)(b + args.b_res) * img + pin, n0, args.Cout,
                              args.split);
+              store_row<T, CH>(uu, static_cast<T*>(args.out), (size_t)(b + args.b_out) * img + pin, n0, args.Cout,
+                               args.split);
+            }
           }
         } else {
           epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, n0, args.Cout, args.split, xb, yb, b + args.b_out, lane);
@@ -545,7 +602,8 @@ __global__ void __launch_bounds__(256, 1)
 // Compile-time tile configuration of the multi-row kernel: R = 256/BN blocks (so two
 // accumulator buffers fill the 512 TMEM columns), the largest K chunk giving >= 3 stages in
 // 200 KB of shared memory (else 16 with >= 2 stages).
-constexpr int kStageBudget = 168 * 1024;  // smem for the operand ring (the TMA epilogue takes 32 KB)
+constexpr int kStageBudget = 168 * 1024;     // smem for the operand ring (the TMA epilogue takes 48 KB)
+constexpr int kStageBudgetTap = 156 * 1024;  // per-tap kernel (its up-add epilogue takes 64 KB)
 
 struct RowsCfg {
   static constexpr int stage_bytes(int bn, int bk, int r, int hb) {
@@ -590,7 +648,7 @@ __global__ void __launch_bounds__(256, 1)
   static_assert(2 * R * BN <= 512, "TMEM");
   static_assert(WB % 8 == 0, "swizzle alignment of the shifted A operands");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -781,7 +839,7 @@ __global__ void __launch_bounds__(256, 1)
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
