@@ -94,12 +94,12 @@ void launch_rows(const ConvPlan& p, cudaStream_t s) {
   }
 }
 
-template <typename T, int BN>
+template <typename T, int BN, bool DYF>
 void launch_nz(const ConvPlan& p, cudaStream_t s) {
   constexpr int R = NzCfg::R(BN);
   constexpr int ST = NzCfg::STAGES(BN);
   static_assert(ST >= 2, "no-swizzle tile does not fit shared memory");
-  constexpr int smem = NzSmem<BN, R, ST>::kTotal;
+  constexpr int smem = NzSmem<BN, R, ST, DYF>::kTotal;
   auto go = [&](auto kern) {
     static std::mutex mu;
     static std::unordered_set<const void*> done;
@@ -111,10 +111,10 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
     kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head);
   };
   switch (p.mode) {
-    case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias>); break;
-    case kResidualRelu: go(conv3_nz_kernel<T, BN, R, ST, kResidualRelu>); break;
-    case kHeadFused: go(conv3_nz_kernel<T, BN, R, ST, kHeadFused>); break;
-    default: go(conv3_nz_kernel<T, BN, R, ST, kBias>); break;
+    case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;
+    case kResidualRelu: go(conv3_nz_kernel<T, BN, R, ST, kResidualRelu, DYF>); break;
+    case kHeadFused: go(conv3_nz_kernel<T, BN, R, ST, kHeadFused, DYF>); break;
+    default: go(conv3_nz_kernel<T, BN, R, ST, kBias, DYF>); break;
   }
 }
 
@@ -122,9 +122,10 @@ template <typename T>
 void dispatch(const ConvPlan& p, cudaStream_t s) {
   if (p.mode == kHeadFused && p.nz_R == 0) throw Error(-1, "fused head needs the no-swizzle conv kernel");
   if (p.nz_R > 0) {
-    if (p.bn == 16) return launch_nz<T, 16>(p, s);
-    if (p.bn == 32) return launch_nz<T, 32>(p, s);
-    if (p.bn == 64) return launch_nz<T, 64>(p, s);
+    static const bool dyf = getenv("OMNISEG_NO_DYF") == nullptr;
+    if (p.bn == 16) return dyf ? launch_nz<T, 16, true>(p, s) : launch_nz<T, 16, false>(p, s);
+    if (p.bn == 32) return dyf ? launch_nz<T, 32, true>(p, s) : launch_nz<T, 32, false>(p, s);
+    if (p.bn == 64) return dyf ? launch_nz<T, 64, true>(p, s) : launch_nz<T, 64, false>(p, s);
     throw Error(-1, "unsupported no-swizzle conv shape");
   }
   if (p.rows_R > 0) {

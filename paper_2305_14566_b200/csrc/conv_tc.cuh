@@ -804,12 +804,14 @@ __global__ void __launch_bounds__(256, 1)
 // r, tap (dy, dx) simply starts ((r+dy)*130 + dx)*16 B into the box: all 9 taps of all R
 // blocks come from one load (~(R+2)/R input reads per output instead of 9). Weights: 9
 // per-tap SW32 boxes per chunk, shared by the R blocks.
-template <int BN, int R, int STAGES>
+template <int BN, int R, int STAGES, bool DYF = false>
 struct NzSmem {
   static constexpr int kPx = 130;
   static constexpr int kChunkStride = (R + 2) * kPx * 16;                 // LBO of the A operand
   static constexpr int kA = ((2 * kChunkStride + 1023) / 1024) * 1024;  // two 8-ch chunks (K = 16)
-  static constexpr int kBt = ((BN * 32 + 1023) / 1024) * 1024;          // one tap's BN x 16 B tile
+  // one tap's BN x 16-channel weight tile (SW32); the dy-stacked variant packs the three dy
+  // tiles of one dx back to back, so they must be exactly BN*32 bytes apart
+  static constexpr int kBt = DYF ? BN * 32 : ((BN * 32 + 1023) / 1024) * 1024;
   static constexpr int kStage = kA + 9 * kBt;
   static constexpr int kBars = (2 * STAGES + 12) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
@@ -830,12 +832,20 @@ struct NzCfg {
   }
 };
 
-template <typename T, int BN, int R, int STAGES, int MODE>
+// DYF ("dy-fused"): the three dy weight tiles of a dx are stacked along N, so ONE MMA with
+// ONE A fetch (input row i, shift dx) produces the contributions to output rows i+1, i, i-1
+// (N = 3 BN; 2 BN / BN at the band edges). The R accumulators are laid out in reverse row
+// order (row r at column (R-1-r) BN) so those three are contiguous; because one MMA covers
+// accumulators first-written by different MMAs, they are zeroed by the epilogue
+// (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
+// tensor-core operand traffic than one MMA per (tap, row).
+template <typename T, int BN, int R, int STAGES, int MODE, bool DYF>
 __global__ void __launch_bounds__(256, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                     const ConvArgs args, const __grid_constant__ HeadArgs hargs) {
-  using S = NzSmem<BN, R, STAGES>;
+  using S = NzSmem<BN, R, STAGES, DYF>;
+  static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
   extern __shared__ uint8_t smem_raw[];
@@ -889,8 +899,10 @@ __global__ void __launch_bounds__(256, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
           ptx::tma_load_5d(sa, &tmA, &full[stage], 0, x0, y0, 2 * kc, b + args.b_in);
 #pragma unroll
-          for (int tap = 0; tap < 9; ++tap)
-            ptx::tma_load_2d(sa + S::kA + tap * S::kBt, &tmB, &full[stage], tap * args.Cin + kc * 16, nt * BN);
+          for (int tap = 0; tap < 9; ++tap) {
+            const int slot = DYF ? (tap % 3) * 3 + tap / 3 : tap;  // DYF: [dx][dy] order
+            ptx::tma_load_2d(sa + S::kA + slot * S::kBt, &tmB, &full[stage], tap * args.Cin + kc * 16, nt * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -900,28 +912,50 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
+      constexpr bool kBf = std::is_same<T, __nv_bfloat16>::value;
+      constexpr uint32_t idesc = ptx::idesc_f16(128, BN, kBf);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
         const int acc = local & 1;
-        ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        // DYF: the epilogue zeroes every buffer and arrives once up front (real phases)
+        ptx::mbar_wait(&tempty[acc], DYF ? ((local >> 1) & 1) : (((local >> 1) & 1) ^ 1));
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + acc * R * BN;
         for (int kc = 0; kc < kiters; ++kc) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
+          if constexpr (DYF) {
 #pragma unroll
-          for (int tap = 0; tap < 9; ++tap) {
-            const int dy = tap / 3, dx = tap % 3;
-            const uint64_t db = ptx::smem_desc(sa + S::kA + tap * S::kBt, 8 * 32, 6u);  // SW32, 8 rows x 32 B
+            for (int dx = 0; dx < 3; ++dx) {
+              const uint32_t sbd = sa + S::kA + dx * 3 * S::kBt;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const uint32_t a0 = sa + (uint32_t)(((r + dy) * S::kPx + dx) * 16);
-              const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
-              ptx::mma_f16(d_base + r * BN, da, db, idesc, (kc | tap) != 0);
+              for (int i = -1; i <= R; ++i) {
+                const int r_hi = i + 1 < R - 1 ? i + 1 : R - 1;
+                const int r_lo = i - 1 > 0 ? i - 1 : 0;
+                const int nrows = r_hi - r_lo + 1;
+                const int dy0 = i - r_hi + 1;
+                const uint32_t a0 = sa + (uint32_t)(((i + 1) * S::kPx + dx) * 16);
+                const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
+                const uint64_t db = ptx::smem_desc(sbd + dy0 * BN * 32, 8 * 32, 6u);
+                const uint32_t id = nrows == 3 ? ptx::idesc_f16(128, 3 * BN, kBf)
+                                  : nrows == 2 ? ptx::idesc_f16(128, 2 * BN, kBf) : idesc;
+                ptx::mma_f16(d_base + (R - 1 - r_hi) * BN, da, db, id, 1u);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+              const int dy = tap / 3, dx = tap % 3;
+              const uint64_t db = ptx::smem_desc(sa + S::kA + tap * S::kBt, 8 * 32, 6u);  // SW32, 8 rows x 32 B
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const uint32_t a0 = sa + (uint32_t)(((r + dy) * S::kPx + dx) * 16);
+                const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
+                ptx::mma_f16(d_base + r * BN, da, db, idesc, (kc | tap) != 0);
+              }
             }
           }
           ptx::mma_commit(&empty[stage]);
@@ -947,6 +981,14 @@ __global__ void __launch_bounds__(256, 1)
         s_w[i] = j < hargs.C0 ? hargs.Wpre[o * hargs.C0 + j] : 0.f;
       }
       if (et < kHead) s_b[et] = hargs.bpre[et];
+    }
+    if constexpr (DYF) {
+      // zero both accumulator buffers (this warp's lanes) and release them to the MMA warp
+      for (int c = 0; c < 2 * R * BN; c += 16) ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + c);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[0]);
+      ptx::mbar_arrive(&tempty[1]);
     }
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
@@ -990,7 +1032,8 @@ __global__ void __launch_bounds__(256, 1)
             epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res, lane);
           }
         }
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (DYF ? (R - 1 - r) : r) * BN + c;
         if constexpr (MODE == kHeadFused) {
           epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs, s_w,
                           s_b, s_th, lf, oy, ox);
@@ -998,6 +1041,11 @@ __global__ void __launch_bounds__(256, 1)
           epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
                                  tyg * R + r, b + args.b_out, lane);
         }
+      }
+      if constexpr (DYF) {
+        for (int c = 0; c < R * BN; c += 16)
+          ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + c);
+        ptx::tmem_st_wait();
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
