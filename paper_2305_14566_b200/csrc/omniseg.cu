@@ -705,7 +705,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   DevState* st = h->state.as<DevState>();
   if (b0 == 0) launch_pad_colour(dslide, W, st, s);
   if (h->inject) OS_CUDA(cudaMemcpyAsync(st, h->inj_pc, 4, cudaMemcpyHostToDevice, s));
-  if (h->world > 1) {
+  if (h->comm) {
     g_nccl.check(g_nccl.broadcast(st, st, 4, ncclUint8, 0, h->comm, s), "ncclBroadcast(pad colour)");
   }
   bool needf[4] = {false, false, false, false};
@@ -749,7 +749,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   const int ir0 = pad / 8, ir1 = (int)(pad / 8 + H / 8), ic0 = pad / 8, ic1 = (int)(pad / 8 + W / 8);
   launch_hist(h->gm.as<uint8_t>(), W8, std::max(ir0, fp.own8_0), std::min(ir1, fp.own8_1), ic0, ic1,
               h->hist.as<unsigned long long>(), s);
-  if (h->world > 1)
+  if (h->comm)
     g_nccl.check(g_nccl.allReduce(h->hist.p, h->hist.p, 256, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(hist)");
   if (h->inject) OS_CUDA(cudaMemcpyAsync(h->hist.p, h->inj_hist, 256 * 8, cudaMemcpyHostToDevice, s));
   OS_CUDA(cudaMemcpyAsync(h->last_hist, h->hist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
@@ -851,7 +851,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
                     h->area.as<unsigned long long>() + t, s);
     h->launches++;
   }
-  if (h->world > 1)
+  if (h->comm)
     g_nccl.check(g_nccl.allReduce(h->area.p, h->area.p, tk.n, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(area)");
   record(h, 4);
   if (out_prob && !prob_dev)
@@ -986,7 +986,7 @@ int omniseg_comm_init(omniseg_t* h, const void* id, int world, int rank) {
     OS_REQUIRE(h && id, "comm_init: NULL argument");
     OS_REQUIRE(world >= 1 && rank >= 0 && rank < world, "comm_init: bad world/rank");
     OS_CUDA(cudaSetDevice(h->device));
-    if (world == 1) {
+    if (world == 1 && getenv("OMNISEG_FORCE_NCCL") == nullptr) {
       h->world = 1;
       h->rank = 0;
       return 0;

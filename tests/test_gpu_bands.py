@@ -82,3 +82,22 @@ def test_bands_bit_exact(setup, world):
         assert band_tiles == expect
         _, t_band, gp_band = h.fgmask()
     assert (area_sum == area).all()
+
+
+def test_nccl_plumbing_world1(setup, monkeypatch):
+    """The real NCCL path (dlopen'ed libnccl, communicator from a torch-generated unique id,
+    pad-colour broadcast, histogram and area all-reduces) with a communicator of size 1:
+    the single band [0, Hp) must reproduce segment_slide bit for bit."""
+    import torch
+    from paper_2305_14566_b200 import Omniseg
+    from paper_2305_14566_b200 import dist as D
+    monkeypatch.setenv("OMNISEG_FORCE_NCCL", "1")
+    a, blob, slide, h_full, prob, mask, area, pc, hist, tiles_full = setup
+    h = Omniseg(arch_string(a), blob)
+    h.comm_init(torch.cuda.nccl.unique_id(), 1, 0)
+    Hp, _ = D.padded_extent(H, W, PAD)
+    bp = np.zeros_like(prob)
+    bm = np.zeros_like(mask)
+    ba = np.zeros_like(area)
+    h.segment_band(slide, H, W, 0, Hp, PAD, P, S, SCALES, CLASSES, bp, bm, ba)
+    assert (bp.view(np.uint32) == prob.view(np.uint32)).all() and (bm == mask).all() and (ba == area).all()
