@@ -99,7 +99,11 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   constexpr int R = NzCfg::R(BN);
   constexpr int ST = NzCfg::STAGES(BN);
   static_assert(ST >= 2, "no-swizzle tile does not fit shared memory");
-  constexpr int smem = NzSmem<BN, R, ST, DYF>::kTotal;
+  constexpr int smem_plain = NzSmem<BN, R, ST, DYF, 4>::kTotal;
+  constexpr int smem_head = NzSmem<BN, R, ST, DYF, 8>::kTotal;
+  static_assert(smem_head <= 227 * 1024, "fused-head smem");
+  const int smem = p.mode == kHeadFused ? smem_head : smem_plain;
+  const int threads = p.mode == kHeadFused ? 384 : 256;
   auto go = [&](auto kern) {
     static std::mutex mu;
     static std::unordered_set<const void*> done;
@@ -108,7 +112,7 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head);
+    kern<<<p.grid, threads, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head);
   };
   switch (p.mode) {
     case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;

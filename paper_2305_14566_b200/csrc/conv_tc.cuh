@@ -138,9 +138,10 @@ struct EpiTile {
 };
 
 struct EpiState {
-  uint8_t* buf;         // this warp's 6 buffers
+  uint8_t* buf;         // this warp's 6 buffers (out hi, out lo, 2 x residual hi/lo)
   uint64_t* rbar;       // this warp's 2 residual mbarriers (double-buffered prefetch)
   uint32_t rphase[2];
+  int res_base = 2;     // buffer index of residual slot 0 (0 when the warp has no out buffers)
 };
 
 // Issue the TMA loads of one residual chunk into buffer slot `slot` (lane 0).
@@ -149,7 +150,7 @@ __device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUte
                                               int split, int xb, int yb, int b, uint32_t lane) {
   using E = EpiTile<CH>;
   if (lane == 0) {
-    uint8_t* hi = es.buf + (2 + 2 * slot) * E::kBuf;
+    uint8_t* hi = es.buf + (es.res_base + 2 * slot) * E::kBuf;
     ptx::mbar_arrive_expect_tx(&es.rbar[slot], (split ? 2 : 1) * E::kBuf);
     ptx::tma_load_4d(hi, tmR, &es.rbar[slot], n0, xb, yb, b);
     if (split) ptx::tma_load_4d(hi + E::kBuf, tmR, &es.rbar[slot], Cout + n0, xb, yb, b);
@@ -163,7 +164,7 @@ template <typename T, int CH, int MODE>
 __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t taddr, const float* bias, int n0,
                                            int split, uint32_t lane, float (&v)[CH]) {
   using E = EpiTile<CH>;
-  uint8_t* res_hi = es.buf + (2 + 2 * slot) * E::kBuf;
+  uint8_t* res_hi = es.buf + (es.res_base + 2 * slot) * E::kBuf;
   uint8_t* res_lo = res_hi + E::kBuf;
   constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
   uint32_t u[32];
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(256, 1)
 // r, tap (dy, dx) simply starts ((r+dy)*130 + dx)*16 B into the box: all 9 taps of all R
 // blocks come from one load (~(R+2)/R input reads per output instead of 9). Weights: 9
 // per-tap SW32 boxes per chunk, shared by the R blocks.
-template <int BN, int R, int STAGES, bool DYF = false>
+template <int BN, int R, int STAGES, bool DYF = false, int EW = 4>
 struct NzSmem {
   static constexpr int kPx = 130;
   static constexpr int kChunkStride = (R + 2) * kPx * 16;                 // LBO of the A operand
@@ -813,9 +814,12 @@ struct NzSmem {
   // tiles of one dx back to back, so they must be exactly BN*32 bytes apart
   static constexpr int kBt = DYF ? BN * 32 : ((BN * 32 + 1023) / 1024) * 1024;
   static constexpr int kStage = kA + 9 * kBt;
-  static constexpr int kBars = (2 * STAGES + 12) * 8 + 16;
+  static constexpr int kBars = (2 * STAGES + 24) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
-  static constexpr int kHeadOff = kEpiOff + EpiTile<(BN < 32 ? BN : 32)>::kBytes;
+  // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
+  static constexpr int kWarpEpi = EW == 4 ? EpiTile<(BN < 32 ? BN : 32)>::kWarpBytes
+                                          : 4 * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
+  static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
   static constexpr int kHeadBytes = (kHeadTasks * 156 + kHead * 64 + kHead) * 4;
   static constexpr int kTotal = kHeadOff + kHeadBytes + 1024;
@@ -840,11 +844,12 @@ struct NzCfg {
 // (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
 // tensor-core operand traffic than one MMA per (tap, row).
 template <typename T, int BN, int R, int STAGES, int MODE, bool DYF>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(MODE == kHeadFused ? 384 : 256, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                     const ConvArgs args, const __grid_constant__ HeadArgs hargs) {
-  using S = NzSmem<BN, R, STAGES, DYF>;
+  constexpr int EW = MODE == kHeadFused ? 8 : 4;  // epilogue warps (2 per TMEM lane quadrant for the head)
+  using S = NzSmem<BN, R, STAGES, DYF, EW>;
   static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
@@ -854,8 +859,8 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;  // 8 residual barriers (two per epilogue warp)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 8);
+  uint64_t* rbar = tempty + 2;  // two residual barriers per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * EW);
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   if (warp == 0 && lane == 0) {
@@ -867,9 +872,9 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 128);
+      ptx::mbar_init(&tempty[a], 32 * EW);
     }
-    for (int a = 0; a < 8; ++a) ptx::mbar_init(&rbar[a], 1);
+    for (int a = 0; a < 2 * EW; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -968,23 +973,28 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
+    const int q = warp & 3;            // TMEM lane quadrant
+    const int ew = warp - 4;           // epilogue warp index
+    constexpr int NH = EW / 4;         // warps per quadrant (they alternate rows)
+    const int half = ew / 4;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}};
+    EpiState es{smem + S::kEpiOff + ew * S::kWarpEpi, &rbar[2 * ew], {0, 0}, EW == 4 ? 2 : 0};
     float* s_th = reinterpret_cast<float*>(smem + S::kHeadOff);
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;
-    const int et = q * 32 + (int)lane;  // 0..127 over the epilogue warps
+    const int et = ew * 32 + (int)lane;  // 0 .. 32*EW-1 over the epilogue warps
     if constexpr (MODE == kHeadFused) {
-      for (int i = et; i < kHead * CH; i += 128) {
+      for (int i = et; i < kHead * CH; i += 32 * EW) {
         const int o = i / CH, j = i - o * CH;
         s_w[i] = j < hargs.C0 ? hargs.Wpre[o * hargs.C0 + j] : 0.f;
       }
       if (et < kHead) s_b[et] = hargs.bpre[et];
     }
     if constexpr (DYF) {
-      // zero both accumulator buffers (this warp's lanes) and release them to the MMA warp
-      for (int c = 0; c < 2 * R * BN; c += 16) ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + c);
+      // zero both accumulator buffers (this warp's lanes; the NH warps of a quadrant split the
+      // columns) and release them to the MMA warp
+      for (int c = half * (2 * R * BN / NH); c < (half + 1) * (2 * R * BN / NH); c += 16)
+        ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + c);
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[0]);
@@ -1001,13 +1011,13 @@ __global__ void __launch_bounds__(256, 1)
       const int b = m / args.tiles_y;
       int lf = 0, oy = 0, ox = 0;
       if constexpr (MODE == kHeadFused) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous work item's theta no longer read
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // previous theta no longer read
         const int nth = hargs.ntasks * kTheta;
-        for (int i = et; i < nth; i += 128) {
+        for (int i = et; i < nth; i += 32 * EW) {
           const int t = i / kTheta;
           s_th[t * 156 + (i - t * kTheta)] = hargs.theta[(int64_t)(b + args.b_head) * nth + i];
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
         if (hargs.tiles) {
           const uint32_t id = hargs.tiles[hargs.first + b + args.b_head];
           lf = id >> 30;
@@ -1021,14 +1031,16 @@ __global__ void __launch_bounds__(256, 1)
       constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
       constexpr int NC = BN / CH;
       const int xb = tx * 128 + q * 32;
-      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, tyg * R, b + args.b_res, lane);
+      constexpr int RM = R / NH;  // rows of this warp: r = j * NH + half
+      if constexpr (kRes)
+        epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, tyg * R + half, b + args.b_res, lane);
 #pragma unroll 1
-      for (int i = 0; i < R * NC; ++i) {
-        const int r = i / NC, c = (i - r * NC) * CH;
+      for (int i = 0; i < RM * NC; ++i) {
+        const int r = (i / NC) * NH + half, c = (i % NC) * CH;
         const int slot = i & 1;
         if constexpr (kRes) {
-          if (i + 1 < R * NC) {
-            const int r1 = (i + 1) / NC, c1 = (i + 1 - r1 * NC) * CH;
+          if (i + 1 < RM * NC) {
+            const int r1 = ((i + 1) / NC) * NH + half, c1 = ((i + 1) % NC) * CH;
             epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res, lane);
           }
         }
@@ -1043,8 +1055,11 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       if constexpr (DYF) {
-        for (int c = 0; c < R * BN; c += 16)
-          ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + c);
+        for (int j = 0; j < RM; ++j) {
+          const int r = j * NH + half;
+          for (int c = 0; c < BN; c += 16)
+            ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (R - 1 - r) * BN + c);
+        }
         ptx::tmem_st_wait();
       }
       ptx::tc_fence_before();

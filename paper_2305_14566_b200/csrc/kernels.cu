@@ -399,20 +399,33 @@ __global__ void gather_raw_kernel(const uint8_t* tiles, int n, int P, T* X) {
 // ------------------------------------------------------------------ K7 GAP + controller
 // g[b][c] = mean over the bottleneck's h x w pixels (fixed summation order), fp32.
 // (x2 precision: a pixel holds [C] hi | [C] lo; the value is hi + lo.)
+// Block = 32 channels x 8 pixel slices (coalesced 64-B channel rows); each thread sums its
+// slice in pixel order, then the 8 slice sums are added in a fixed order: deterministic.
 template <typename T>
-__global__ void gap_kernel(const T* E, int hw, int C, int split, float* g) {
+__global__ void __launch_bounds__(256) gap_kernel(const T* E, int hw, int C, int split, float* g) {
+  __shared__ float part[8][33];
   const int b = blockIdx.y;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+  const int cl = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
   const int cs = split ? 2 * C : C;
-  const T* p = E + (int64_t)b * hw * cs + c;
   float s = 0.f;
-  for (int i = 0; i < hw; ++i) {
-    float v = float(p[(int64_t)i * cs]);
-    if (split) v += float(p[(int64_t)i * cs + C]);
-    s += v;
+  if (c < C) {
+    const T* p = E + (int64_t)b * hw * cs + c;
+    const int per = (hw + 7) / 8, i0 = sl * per, i1 = min(hw, i0 + per);
+    for (int i = i0; i < i1; ++i) {
+      float v = float(p[(int64_t)i * cs]);
+      if (split) v += float(p[(int64_t)i * cs + C]);
+      s += v;
+    }
   }
-  g[(int64_t)b * C + c] = s / float(hw);
+  part[sl][cl] = s;
+  __syncthreads();
+  if (sl == 0 && c < C) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][cl];
+    g[(int64_t)b * C + c] = t / float(hw);
+  }
 }
 
 // theta[b][t][j] = Wc[j] . [g_b ; onehot(cls_t) ; onehot(scl_t)] + bc[j]   (north_star controller)
@@ -689,8 +702,8 @@ void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s)
 }
 template <typename T>
 void launch_gap(const T* E, int n, int hw, int C, int split, float* g, cudaStream_t s) {
-  dim3 grid((C + 127) / 128, n);
-  gap_kernel<T><<<grid, 128, 0, s>>>(E, hw, C, split, g);
+  dim3 grid((C + 31) / 32, n);
+  gap_kernel<T><<<grid, 256, 0, s>>>(E, hw, C, split, g);
 }
 void launch_controller(const float* g, int n, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
                        const int* task_cls, const int* task_scl, int ntasks, float* theta, cudaStream_t s) {
