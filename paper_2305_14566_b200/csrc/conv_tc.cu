@@ -97,13 +97,18 @@ void launch_rows(const ConvPlan& p, cudaStream_t s) {
 template <typename T, int BN, bool DYF>
 void launch_nz(const ConvPlan& p, cudaStream_t s) {
   constexpr int R = NzCfg::R(BN);
-  constexpr int ST = NzCfg::STAGES(BN);
-  static_assert(ST >= 2, "no-swizzle tile does not fit shared memory");
-  constexpr int smem_plain = NzSmem<BN, R, ST, DYF, 4>::kTotal;
-  constexpr int smem_head = NzSmem<BN, R, ST, DYF, 8>::kTotal;
-  static_assert(smem_head <= 227 * 1024, "fused-head smem");
-  const int smem = p.mode == kHeadFused ? smem_head : smem_plain;
-  const int threads = p.mode == kHeadFused ? 384 : 256;
+  constexpr int ST = NzCfg::STAGES(BN, 4, false);   // plain epilogue (4 warps)
+  constexpr int STR = NzCfg::STAGES(BN, 8, false);  // residual epilogue (8 warps)
+  constexpr int STH = NzCfg::STAGES(BN, 8, true);   // fused head (8 warps, residual slots only)
+  static_assert(ST >= 2 && STR >= 2 && STH >= 2, "no-swizzle tile does not fit shared memory");
+  int smem = NzSmem<BN, R, ST, DYF, 4, false>::kTotal, threads = 256;
+  if (p.mode == kResidualRelu) {
+    smem = NzSmem<BN, R, STR, DYF, 8, false>::kTotal;
+    threads = 384;
+  } else if (p.mode == kHeadFused) {
+    smem = NzSmem<BN, R, STH, DYF, 8, true>::kTotal;
+    threads = 384;
+  }
   auto go = [&](auto kern) {
     static std::mutex mu;
     static std::unordered_set<const void*> done;
@@ -116,8 +121,8 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   };
   switch (p.mode) {
     case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;
-    case kResidualRelu: go(conv3_nz_kernel<T, BN, R, ST, kResidualRelu, DYF>); break;
-    case kHeadFused: go(conv3_nz_kernel<T, BN, R, ST, kHeadFused, DYF>); break;
+    case kResidualRelu: go(conv3_nz_kernel<T, BN, R, STR, kResidualRelu, DYF>); break;
+    case kHeadFused: go(conv3_nz_kernel<T, BN, R, STH, kHeadFused, DYF>); break;
     default: go(conv3_nz_kernel<T, BN, R, ST, kBias, DYF>); break;
   }
 }

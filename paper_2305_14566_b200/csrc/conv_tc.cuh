@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(256, 1)
 // r, tap (dy, dx) simply starts ((r+dy)*130 + dx)*16 B into the box: all 9 taps of all R
 // blocks come from one load (~(R+2)/R input reads per output instead of 9). Weights: 9
 // per-tap SW32 boxes per chunk, shared by the R blocks.
-template <int BN, int R, int STAGES, bool DYF = false, int EW = 4>
+template <int BN, int R, int STAGES, bool DYF = false, int EW = 4, bool HEAD = false>
 struct NzSmem {
   static constexpr int kPx = 130;
   static constexpr int kChunkStride = (R + 2) * kPx * 16;                 // LBO of the A operand
@@ -817,11 +817,11 @@ struct NzSmem {
   static constexpr int kBars = (2 * STAGES + 24) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
-  static constexpr int kWarpEpi = EW == 4 ? EpiTile<(BN < 32 ? BN : 32)>::kWarpBytes
-                                          : 4 * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
+  static constexpr int kWarpEpi = HEAD ? 4 * EpiTile<(BN < 32 ? BN : 32)>::kBuf   // residual slots only
+                                       : EpiTile<(BN < 32 ? BN : 32)>::kWarpBytes;
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
-  static constexpr int kHeadBytes = (kHeadTasks * 156 + kHead * 64 + kHead) * 4;
+  static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 : 0;
   static constexpr int kTotal = kHeadOff + kHeadBytes + 1024;
   static constexpr uint32_t kTmemCols = (2 * R * BN <= 256) ? 256 : 512;
 };
@@ -831,8 +831,12 @@ struct NzCfg {
   static constexpr int stage_bytes(int bn) {
     return ((2 * (R(bn) + 2) * 130 * 16 + 1023) / 1024) * 1024 + 9 * (((bn * 32 + 1023) / 1024) * 1024);
   }
-  static constexpr int STAGES(int bn) {
-    return kStageBudget / stage_bytes(bn) > 6 ? 6 : kStageBudget / stage_bytes(bn);
+  // ring depth from what the epilogue (ew warps; head: residual slots only) leaves of 227 KB
+  static constexpr int STAGES(int bn, int ew = 4, bool head = false) {
+    return budget(bn, ew, head) / stage_bytes(bn) > 6 ? 6 : budget(bn, ew, head) / stage_bytes(bn);
+  }
+  static constexpr int budget(int bn, int ew, bool head) {
+    return 227 * 1024 - 3 * 1024 - ew * (head ? 4 : 6) * 32 * (bn < 32 ? bn : 32) * 2 - (head ? 7680 : 0);
   }
 };
 
@@ -844,12 +848,14 @@ struct NzCfg {
 // (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
 // tensor-core operand traffic than one MMA per (tap, row).
 template <typename T, int BN, int R, int STAGES, int MODE, bool DYF>
-__global__ void __launch_bounds__(MODE == kHeadFused ? 384 : 256, 1)
+__global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) ? 384 : 256, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                     const ConvArgs args, const __grid_constant__ HeadArgs hargs) {
-  constexpr int EW = MODE == kHeadFused ? 8 : 4;  // epilogue warps (2 per TMEM lane quadrant for the head)
-  using S = NzSmem<BN, R, STAGES, DYF, EW>;
+  // epilogue warps: 8 (2 per TMEM lane quadrant, alternating rows) for the residual and
+  // fused-head epilogues, whose per-row work exceeds the MMA time of thin layers; 4 otherwise
+  constexpr int EW = (MODE == kHeadFused || MODE == kResidualRelu) ? 8 : 4;
+  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused>;
   static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
@@ -978,7 +984,7 @@ __global__ void __launch_bounds__(MODE == kHeadFused ? 384 : 256, 1)
     constexpr int NH = EW / 4;         // warps per quadrant (they alternate rows)
     const int half = ew / 4;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + ew * S::kWarpEpi, &rbar[2 * ew], {0, 0}, EW == 4 ? 2 : 0};
+    EpiState es{smem + S::kEpiOff + ew * S::kWarpEpi, &rbar[2 * ew], {0, 0}, MODE == kHeadFused ? 0 : 2};
     float* s_th = reinterpret_cast<float*>(smem + S::kHeadOff);
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libomniseg.so")
+LIB_PATH = os.environ.get("OMNISEG_LIB", os.path.join(HERE, "lib", "libomniseg.so"))
 
 _lib = None
 
