@@ -10,6 +10,7 @@ namespace osg {
 struct ConvPlan {
   CUtensorMap tmA, tmB;  // activation (4-D NHWC) and weight (2-D [Cout][taps*Cin]) TMA maps
   CUtensorMap tmO, tmR;  // output / residual maps of the TMA epilogue (unused for kUpAdd)
+  LoMaps lo;             // e4m3 / e5m2 maps of the F8 lo parts (input, weights, output, residual)
   ConvArgs args;
   int bn, bk, stages, mode, grid;
   int rows_R = 0;        // > 0: the multi-row 3x3 kernel (conv3_rows_kernel) with R blocks
@@ -22,13 +23,15 @@ struct ConvPlan {
 
 // Plan one convolution: input [B][Hin][Win][Cin], weights [Cout][k][k][Cin] (16-bit,
 // K-major), fp32 bias; output grid Ho = ceil(Hin/stride) etc. `res` per ConvMode.
-// split_out: res/out use the hi|lo split layout (x2 precision); for split inputs the
-// caller passes Cin = 2 x channels and weights duplicated along K ([W | W]).
+// split_out: StoreKind of res/out. in_kind: StoreKind of the input; for x2 inputs the
+// caller passes Cin = 2 x channels and weights duplicated along K ([W | W]); for F8 inputs
+// Cin = channels, w = fp16 weights and w_lo = e5m2(W * 2^-6) bytes of the same layout.
 // B = images per launch (work items); B_in / B_res / B_out = batch extents of the input,
 // residual and output tensors (default B; the args.b_* offsets select the images).
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
                         const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
-                        bool split_out = false, int B_in = -1, int B_res = -1, int B_out = -1);
+                        int split_out = 0, int B_in = -1, int B_res = -1, int B_out = -1, int in_kind = 0,
+                        const void* w_lo = nullptr);
 void set_conv_batch(ConvPlan& p, int B);
 void run_conv(const ConvPlan& p, cudaStream_t s);
 int num_sms();

@@ -60,7 +60,7 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args);
+    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
   };
   switch (p.mode) {
     case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kReluBias>); break;
@@ -85,7 +85,7 @@ void launch_rows(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args);
+    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
   };
   switch (p.mode) {
     case kReluBias: go(conv3_rows_kernel<T, BN, BK, R, HB, ST, kReluBias>); break;
@@ -117,7 +117,7 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, threads, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head);
+    kern<<<p.grid, threads, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head, p.lo);
   };
   switch (p.mode) {
     case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;
@@ -175,13 +175,16 @@ int num_sms() {
 
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
                         const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
-                        bool split_out, int B_in, int B_res, int B_out) {
+                        int split_out, int B_in, int B_res, int B_out, int in_kind, const void* w_lo) {
   if (B_in < 0) B_in = B;
   if (B_res < 0) B_res = B;
   if (B_out < 0) B_out = B;
   OS_REQUIRE(Cin % 16 == 0 && Cout % 16 == 0, "conv channels must be multiples of 16");
   OS_REQUIRE(k == 1 || k == 3, "conv kernel size must be 1 or 3");
   OS_REQUIRE(stride == 1 || stride == 2, "conv stride must be 1 or 2");
+  const bool f8in = in_kind == kStoreF8;
+  OS_REQUIRE(!f8in || (Cin % 32 == 0 && w_lo != nullptr && !bf16), "F8 input needs Cin % 32 == 0, fp16 and lo weights");
+  OS_REQUIRE(split_out != kStoreF8 || (Cout % 32 == 0 && !bf16), "F8 output needs Cout % 32 == 0 and fp16");
   ConvPlan p{};
   p.mode = mode;
   p.bf16 = bf16;
@@ -212,6 +215,12 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.tiles_y = Ho / a.hb;
   a.n_tiles_n = Cout / p.bn;
   a.kchunks = Cin / p.bk;
+  a.kch_lo = f8in ? Cin / p.bk : 0;
+  // input pixel bytes and the element count of its (hi) channel axis
+  const uint64_t in_px = f8in ? 3ull * Cin : 2ull * Cin;
+  const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapDataType d8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const void* in_lo = f8in ? static_cast<const uint8_t*>(in) + 2 * Cin : nullptr;
   // no-swizzle multi-row variant (conv3_nz_kernel): 3x3 stride 1, width >= 128, N <= 64
   if (k == 3 && stride == 1 && mode != kUpAdd && p.bn <= 64 && a.hb == 1 && Cout == p.bn && Cin % 16 == 0 &&
       a.tiles_y % NzCfg::R(p.bn) == 0 && getenv("OMNISEG_NO_NZ") == nullptr) {
@@ -219,17 +228,24 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     // A: 5-D view {8 ch, W, H, Cin/8, B} with the chunk dimension (16-B stride) outside the
     // pixel dimensions, box {8, 130, R+2, 2, 1} -> smem [chunk][row][px][16 B]
     cuuint64_t dims[5] = {8, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)(Cin / 8), (cuuint64_t)B_in};
-    cuuint64_t strides[4] = {(cuuint64_t)Cin * 2, (cuuint64_t)Win * Cin * 2, 16, (cuuint64_t)Hin * Win * Cin * 2};
+    cuuint64_t strides[4] = {in_px, (cuuint64_t)Win * in_px, 16, (cuuint64_t)Hin * Win * in_px};
     cuuint32_t box[5] = {8, 130, (cuuint32_t)(R + 2), 2, 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    const CUtensorMapDataType dt0 = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    CUresult r = encode_fn()(&p.tmA, dt0, 5, const_cast<void*>(in), dims, strides, box, es,
+    CUresult r = encode_fn()(&p.tmA, dt, 5, const_cast<void*>(in), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS && f8in) {
+      // lo: {16 e4m3, W, H, Cin/16, B}, the same 16-B core-matrix rows
+      cuuint64_t d2[5] = {16, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)(Cin / 16), (cuuint64_t)B_in};
+      cuuint32_t b2[5] = {16, 130, (cuuint32_t)(R + 2), 2, 1};
+      r = encode_fn()(&p.lo.A, d8, 5, const_cast<void*>(in_lo), d2, strides, b2, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r == CUDA_SUCCESS) {
       p.nz_R = R;
       p.bk = 16;
       a.kchunks = Cin / 16;
+      a.kch_lo = f8in ? Cin / 32 : 0;
       a.tiles_y /= R;
     }
   }
@@ -238,23 +254,24 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
       Cout == p.bn && getenv("OMNISEG_NO_ROWS") == nullptr) {
     const int R = RowsCfg::R(p.bn);
     const int bk = RowsCfg::BK(p.bn, a.hb);
-    if (a.tiles_y % R == 0 && Cin % bk == 0) {
+    if (a.tiles_y % R == 0 && Cin % bk == 0 && (!f8in || bk >= 32)) {
       p.rows_R = R;
       p.hb = a.hb;
       p.bk = bk;
       a.kchunks = Cin / bk;
+      a.kch_lo = f8in ? Cin / bk : 0;
       a.tiles_y /= R;
     }
   }
+  OS_REQUIRE(!f8in || p.nz_R > 0 || p.bk >= 32, "F8 input needs K chunks of >= 32 channels");
   a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
   a.bias = bias;
   a.res = res;
   a.out = out;
-  a.split = split_out ? 1 : 0;
-  const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  a.split = split_out;
   if (p.nz_R == 0) {
     cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B_in};
-    cuuint64_t strides[3] = {(cuuint64_t)Cin * 2, (cuuint64_t)Win * Cin * 2, (cuuint64_t)Hin * Win * Cin * 2};
+    cuuint64_t strides[3] = {in_px, (cuuint64_t)Win * in_px, (cuuint64_t)Hin * Win * in_px};
     cuuint32_t box[4] = {(cuuint32_t)p.bk, (cuuint32_t)(a.wb * stride), (cuuint32_t)(a.hb * stride), 1};
     if (p.rows_R > 0) box[2] = (cuuint32_t)(p.rows_R * a.hb + 2);
     cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
@@ -262,6 +279,11 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz(p.bk * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(A) failed: " + std::to_string((int)r));
+    if (f8in) {
+      r = encode_fn()(&p.lo.A, d8, 4, const_cast<void*>(in_lo), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swz(p.bk), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(A lo) failed: " + std::to_string((int)r));
+    }
   }
   {
     const int taps = k * k;
@@ -273,40 +295,59 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz(p.bk * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
+    if (f8in) {
+      // lo weights: e5m2 bytes [Cout][taps*Cin]; a lo chunk is bk (nz: 32) bytes wide
+      const int bkl = p.nz_R > 0 ? 32 : p.bk;
+      cuuint64_t s1[1] = {(cuuint64_t)taps * Cin};
+      cuuint32_t b1[2] = {(cuuint32_t)bkl, (cuuint32_t)p.bn};
+      r = encode_fn()(&p.lo.B, d8, 2, const_cast<void*>(w_lo), dims, s1, b1, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swz(bkl), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(B lo) failed: " + std::to_string((int)r));
+    }
   }
   {
-    // output / residual maps for the TMA epilogue: [B][Ho][Wo][Cst], one warp box
-    // = CH channels x (bw x bh) pixels, 64-B (CH=32) / 32-B (CH=16) swizzle
+    // output / residual maps for the TMA epilogue: [B][Ho][Wo][C], one warp box = CH channels
+    // x (bw x bh) pixels, 64-B (CH=32) / 32-B (CH=16) swizzle; x2 stores [C hi | C lo] per
+    // pixel (lo at channel Cout), F8 a fp16 hi map + an e4m3 lo map (CH-byte rows, 32-B / no swizzle)
     const int CH = p.bn < 32 ? p.bn : 32;
-    const int Cst = split_out ? 2 * Cout : Cout;
+    const bool f8o = split_out == kStoreF8;
+    const int Cst = split_out == kStoreX2 ? 2 * Cout : Cout;
+    const uint64_t opx = f8o ? 3ull * Cout : 2ull * Cst;
     const int bw = a.wb < 32 ? a.wb : 32, bh = 32 / bw;
     cuuint64_t dims[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B_out};
     cuuint64_t dims_r[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B_res};
-    cuuint64_t strides[3] = {(cuuint64_t)Cst * 2, (cuuint64_t)Wo * Cst * 2, (cuuint64_t)Ho * Wo * Cst * 2};
+    cuuint64_t strides[3] = {opx, (cuuint64_t)Wo * opx, (cuuint64_t)Ho * Wo * opx};
     cuuint32_t box[4] = {(cuuint32_t)CH, (cuuint32_t)bw, (cuuint32_t)bh, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const CUtensorMapSwizzle sw = CH == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    const CUtensorMapSwizzle swl = CH == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    auto enc = [&](CUtensorMap* m, CUtensorMapDataType t, const void* base, const cuuint64_t* d, const cuuint64_t* st,
+                   const cuuint32_t* bx, CUtensorMapSwizzle z, const char* what) {
+      CUresult r = encode_fn()(m, t, 4, const_cast<void*>(base), d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, z,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(-2, std::string("cuTensorMapEncodeTiled(") + what + ") failed: " +
+                                                 std::to_string((int)r));
+    };
+    auto lo_of = [&](const void* base) { return static_cast<const void*>(static_cast<const uint8_t*>(base) + 2 * Cout); };
     if (mode == kUpAdd && a.wb >= 32) {
       // up-add: full-resolution skip / output, one box = 64 output pixels of one row
       cuuint64_t d2[4] = {(cuuint64_t)Cst, (cuuint64_t)(2 * Wo), (cuuint64_t)(2 * Ho), (cuuint64_t)B_out};
       cuuint64_t d2r[4] = {(cuuint64_t)Cst, (cuuint64_t)(2 * Wo), (cuuint64_t)(2 * Ho), (cuuint64_t)B_res};
-      cuuint64_t st2[3] = {(cuuint64_t)Cst * 2, (cuuint64_t)2 * Wo * Cst * 2, (cuuint64_t)4 * Ho * Wo * Cst * 2};
+      cuuint64_t st2[3] = {opx, 2ull * Wo * opx, 4ull * Ho * Wo * opx};
       cuuint32_t bx2[4] = {(cuuint32_t)CH, 64, 1, 1};
-      CUresult r = encode_fn()(&p.tmO, dt, 4, out, d2, st2, bx2, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(up out) failed: " + std::to_string((int)r));
-      r = encode_fn()(&p.tmR, dt, 4, const_cast<void*>(res), d2r, st2, bx2, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(up skip) failed: " + std::to_string((int)r));
+      enc(&p.tmO, dt, out, d2, st2, bx2, sw, "up out");
+      enc(&p.tmR, dt, res, d2r, st2, bx2, sw, "up skip");
+      if (f8o) {
+        enc(&p.lo.O, d8, lo_of(out), d2, st2, bx2, swl, "up out lo");
+        enc(&p.lo.R, d8, lo_of(res), d2r, st2, bx2, swl, "up skip lo");
+      }
     }
     if (mode != kUpAdd) {
-      CUresult r = encode_fn()(&p.tmO, dt, 4, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(out) failed: " + std::to_string((int)r));
+      enc(&p.tmO, dt, out, dims, strides, box, sw, "out");
+      if (f8o) enc(&p.lo.O, d8, lo_of(out), dims, strides, box, swl, "out lo");
       if (res) {
-        r = encode_fn()(&p.tmR, dt, 4, const_cast<void*>(res), dims_r, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(res) failed: " + std::to_string((int)r));
+        enc(&p.tmR, dt, res, dims_r, strides, box, sw, "res");
+        if (f8o) enc(&p.lo.R, d8, lo_of(res), dims_r, strides, box, swl, "res lo");
       } else {
         p.tmR = p.tmO;
       }

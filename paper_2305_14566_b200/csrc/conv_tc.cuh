@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include <type_traits>
 
@@ -28,6 +29,22 @@
 namespace osg {
 
 enum ConvMode : int { kReluBias = 0, kResidualRelu = 1, kUpAdd = 2, kBias = 3, kHeadFused = 4 };
+
+// Storage of an activation tensor, per pixel (R9):
+//   kStorePlain  [C] 16-bit
+//   kStoreX2     [C] hi | [C] lo, both 16-bit (hi = round(v), lo = round(v - hi))
+//   kStoreF8     [C] fp16 hi | [C] e4m3 lo8 = sat(round((v - hi) * 2^6)), 3C bytes per pixel.
+// A convolution over an F8 input runs its K loop over the hi chunks (kind::f16, 16-bit
+// weights) and then the lo chunks (kind::f8f6f4, E5M2 weights W * 2^-6) into ONE fp32
+// accumulator: (lo 2^6)(W 2^-6) = lo W.
+enum StoreKind : int { kStorePlain = 0, kStoreX2 = 1, kStoreF8 = 2 };
+constexpr float kLoScale = 64.0f;
+constexpr float kLoInv = 1.0f / 64.0f;
+
+// fp8 TMA maps of an F8 tensor's lo part (input A, lo weights B, output O, residual R).
+struct LoMaps {
+  CUtensorMap A, B, O, R;
+};
 
 struct ConvArgs {
   int B, Ho, Wo;          // conv output grid (mode 2: the low-resolution grid)
@@ -41,7 +58,8 @@ struct ConvArgs {
   const float* bias;      // [Cout]
   const void* res;        // residual (mode 1, [B][Ho][Wo][Cout]) or skip (mode 2, [B][2Ho][2Wo][Cout])
   void* out;              // [B][Ho][Wo][Cout] (mode 2: [B][2Ho][2Wo][Cout])
-  int split;              // res/out stored as [Cout] hi | [Cout] lo per pixel (x2 precision mode)
+  int split;              // StoreKind of res/out
+  int kch_lo;             // F8 input: number of lo K chunks (after the kchunks hi chunks), else 0
   // batch-index offsets of the tensors (a launch over images [0, B) of the work space reads
   // input image b + b_in, residual b + b_res, writes b + b_out, head tile b + b_head)
   int b_in, b_res, b_out, b_head;
@@ -72,11 +90,77 @@ struct StoreT<__nv_bfloat16> {
   }
 };
 
+// ---- F8 lo helpers: e4m3 pairs, low byte = first value
+__device__ __forceinline__ uint32_t f8_pack4(float a, float b, float c, float d) {
+  const uint32_t p0 = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+  const uint32_t p1 = __nv_cvt_float2_to_fp8x2(make_float2(c, d), __NV_SATFINITE, __NV_E4M3);
+  return p0 | (p1 << 16);
+}
+__device__ __forceinline__ float2 f8_unpack2(uint32_t u16) {
+  const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(u16 & 0xFFFFu), __NV_E4M3);
+  const float2 f = __half22float2(__half2(hr));
+  return make_float2(f.x * kLoInv, f.y * kLoInv);
+}
+// 16 values -> 16 fp16 hi (two uint4) + 16 e4m3 lo (one uint4)
+__device__ __forceinline__ void split_f8_16(const float* v, uint4& h0, uint4& h1, uint4& lo) {
+  uint32_t h[8], l[4];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) h[e] = StoreT<__half>::pack(v[2 * e], v[2 * e + 1]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 a = StoreT<__half>::unpack(h[2 * e]), b = StoreT<__half>::unpack(h[2 * e + 1]);
+    l[e] = f8_pack4((v[4 * e] - a.x) * kLoScale, (v[4 * e + 1] - a.y) * kLoScale, (v[4 * e + 2] - b.x) * kLoScale,
+                    (v[4 * e + 3] - b.y) * kLoScale);
+  }
+  h0 = make_uint4(h[0], h[1], h[2], h[3]);
+  h1 = make_uint4(h[4], h[5], h[6], h[7]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+// v[0..16) += the 16 lo values of one uint4 of e4m3
+__device__ __forceinline__ void add_f8_16(float* v, const uint4& q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 a = f8_unpack2(w[e]), b = f8_unpack2(w[e] >> 16);
+    v[4 * e] += a.x;
+    v[4 * e + 1] += a.y;
+    v[4 * e + 2] += b.x;
+    v[4 * e + 3] += b.y;
+  }
+}
+// smem image of one F8 lo box row of CH bytes: 32-B swizzle (CH = 32) / none (CH = 16)
+template <int CH>
+__device__ __forceinline__ uint32_t lo_off(int r, int j) {
+  if constexpr (CH == 32)
+    return r * 32 + 16 * (j ^ ((r >> 2) & 1));
+  else
+    return r * 16;
+}
+
 // Row I/O of the epilogue. A pixel's channels are stored either plain ([C]) or split
 // ([C] hi | [C] lo, hi = round(v), lo = round(v - hi): the "x2" precision mode in which
 // the next convolution runs its K loop over both halves with the same exact weights).
 template <typename T, int CH>
 __device__ __forceinline__ void add_row(float (&v)[CH], const T* base, size_t pix, int n0, int C, int split) {
+  if (split == kStoreF8) {
+    const uint8_t* px = reinterpret_cast<const uint8_t*>(base) + pix * 3 * (size_t)C;
+    const uint4* hs = reinterpret_cast<const uint4*>(px + 2 * n0);
+    const uint4* ls = reinterpret_cast<const uint4*>(px + 2 * (size_t)C + n0);
+#pragma unroll
+    for (int j = 0; j < CH / 8; ++j) {
+      const uint4 rv = __ldg(hs + j);
+      const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = StoreT<T>::unpack(rr[e]);
+        v[8 * j + 2 * e] += f.x;
+        v[8 * j + 2 * e + 1] += f.y;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CH / 16; ++j) add_f8_16(v + 16 * j, __ldg(ls + j));
+    return;
+  }
   const size_t stride = split ? 2 * (size_t)C : (size_t)C;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -97,6 +181,14 @@ __device__ __forceinline__ void add_row(float (&v)[CH], const T* base, size_t pi
 }
 template <typename T, int CH>
 __device__ __forceinline__ void store_row(const float (&v)[CH], T* base, size_t pix, int n0, int C, int split) {
+  if (split == kStoreF8) {
+    uint8_t* px = reinterpret_cast<uint8_t*>(base) + pix * 3 * (size_t)C;
+    uint4* hs = reinterpret_cast<uint4*>(px + 2 * n0);
+    uint4* ls = reinterpret_cast<uint4*>(px + 2 * (size_t)C + n0);
+#pragma unroll
+    for (int j = 0; j < CH / 16; ++j) split_f8_16(v + 16 * j, hs[2 * j], hs[2 * j + 1], ls[j]);
+    return;
+  }
   const size_t stride = split ? 2 * (size_t)C : (size_t)C;
   uint4* hs = reinterpret_cast<uint4*>(base + pix * stride + n0);
 #pragma unroll
@@ -145,15 +237,20 @@ struct EpiState {
 };
 
 // Issue the TMA loads of one residual chunk into buffer slot `slot` (lane 0).
+// F8: the lo part comes from the fp8 map tmR2 (CH bytes per row).
 template <int CH>
-__device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUtensorMap* tmR, int n0, int Cout,
-                                              int split, int xb, int yb, int b, uint32_t lane) {
+__device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUtensorMap* tmR, const CUtensorMap* tmR2,
+                                              int n0, int Cout, int split, int xb, int yb, int b, uint32_t lane) {
   using E = EpiTile<CH>;
   if (lane == 0) {
     uint8_t* hi = es.buf + (es.res_base + 2 * slot) * E::kBuf;
-    ptx::mbar_arrive_expect_tx(&es.rbar[slot], (split ? 2 : 1) * E::kBuf);
+    const uint32_t tx = split == kStoreF8 ? E::kBuf + 32 * CH : (split ? 2 : 1) * E::kBuf;
+    ptx::mbar_arrive_expect_tx(&es.rbar[slot], tx);
     ptx::tma_load_4d(hi, tmR, &es.rbar[slot], n0, xb, yb, b);
-    if (split) ptx::tma_load_4d(hi + E::kBuf, tmR, &es.rbar[slot], Cout + n0, xb, yb, b);
+    if (split == kStoreF8)
+      ptx::tma_load_4d(hi + E::kBuf, tmR2, &es.rbar[slot], n0, xb, yb, b);
+    else if (split)
+      ptx::tma_load_4d(hi + E::kBuf, tmR, &es.rbar[slot], Cout + n0, xb, yb, b);
   }
 }
 
@@ -179,9 +276,13 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
   if constexpr (kRes) {
     ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
     es.rphase[slot] ^= 1;
+    if (split == kStoreF8) {
+#pragma unroll
+      for (int j = 0; j < CH / 16; ++j) add_f8_16(v + 16 * j, *reinterpret_cast<const uint4*>(res_lo + lo_off<CH>(lane, j)));
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if (h == 1 && !split) break;
+      if (h == 1 && split != kStoreX2) break;
       const uint8_t* rb = h ? res_lo : res_hi;
 #pragma unroll
       for (int j = 0; j < CH / 8; ++j) {
@@ -205,9 +306,9 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
 
 // One CH-wide chunk: values -> 16-bit (hi, + lo in x2) -> swizzled STS -> TMA store.
 template <typename T, int CH, int MODE>
-__device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensorMap* tmO, uint32_t taddr,
-                                          const float* bias, int n0, int Cout, int split, int xb, int yb, int b,
-                                          uint32_t lane) {
+__device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensorMap* tmO, const CUtensorMap* tmO2,
+                                          uint32_t taddr, const float* bias, int n0, int Cout, int split, int xb,
+                                          int yb, int b, uint32_t lane) {
   using E = EpiTile<CH>;
   uint8_t* out_hi = es.buf;
   uint8_t* out_lo = es.buf + E::kBuf;
@@ -215,6 +316,24 @@ __device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensor
   epi_values<T, CH, MODE>(es, slot, taddr, bias, n0, split, lane, v);
   if (lane == 0) ptx::bulk_wait_read0();  // previous stores of this warp done reading smem
   __syncwarp();
+  if (split == kStoreF8) {
+#pragma unroll
+    for (int j = 0; j < CH / 16; ++j) {
+      uint4 h0, h1, lo;
+      split_f8_16(v + 16 * j, h0, h1, lo);
+      *reinterpret_cast<uint4*>(out_hi + E::off(lane, 2 * j)) = h0;
+      *reinterpret_cast<uint4*>(out_hi + E::off(lane, 2 * j + 1)) = h1;
+      *reinterpret_cast<uint4*>(out_lo + lo_off<CH>(lane, j)) = lo;
+    }
+    ptx::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_4d(tmO, out_hi, n0, xb, yb, b);
+      ptx::tma_store_4d(tmO2, out_lo, n0, xb, yb, b);
+      ptx::bulk_commit();
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < CH / 8; ++j) {
     uint32_t o[4];
@@ -352,13 +471,15 @@ struct ConvSmem {
                                                           : (2 * BN <= 256) ? 256 : 512;
   static constexpr uint32_t kLayout = BK == 64 ? 2u : BK == 32 ? 4u : 6u;  // SW128 / SW64 / SW32
   static constexpr uint32_t kSBO = 8 * BK * 2;                              // 8 rows of BK*2 bytes
+  static constexpr uint32_t kLayoutLo = BK == 64 ? 4u : 6u;                 // F8 lo rows: BK bytes
+  static constexpr uint32_t kSBOLo = 8 * BK;
 };
 
 template <typename T, int BN, int BK, int STAGES, int MODE>
 __global__ void __launch_bounds__(256, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
-                   const ConvArgs args) {
+                   const ConvArgs args, const __grid_constant__ LoMaps lo) {
   using S = ConvSmem<BN, BK, STAGES>;
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   extern __shared__ uint8_t smem_raw[];
@@ -395,8 +516,10 @@ __global__ void __launch_bounds__(256, 1)
 
   const int r = args.ksize >> 1;
   const int taps = args.ksize * args.ksize;
-  const int kiters = taps * args.kchunks;
+  const int kct = args.kchunks + args.kch_lo;  // hi chunks, then (F8 input) lo chunks
+  const int kiters = taps * kct;
   constexpr uint32_t kTx = S::kA + BN * BK * 2;
+  constexpr uint32_t kTxLo = 128 * BK + BN * BK;  // F8 lo chunk: BK bytes per row
 
   if (warp == 0) {
     if (lane == 0) {
@@ -413,15 +536,22 @@ __global__ void __launch_bounds__(256, 1)
         const int x0 = tx * args.wb * args.stride - r;
         const int y0 = ty * args.hb * args.stride - r;
         for (int it = 0; it < kiters; ++it) {
-          const int tap = it / args.kchunks;
-          const int kc = it - tap * args.kchunks;
+          const int tap = it / kct;
+          const int kc = it - tap * kct;
           const int dy = tap / args.ksize, dx = tap - (tap / args.ksize) * args.ksize;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
           uint8_t* sb = sa + S::kA;
-          ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0 + dy, b + args.b_in);
-          ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
+          if (kc < args.kchunks) {
+            ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+            ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0 + dy, b + args.b_in);
+            ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
+          } else {
+            const int kl = kc - args.kchunks;
+            ptx::mbar_arrive_expect_tx(&full[stage], kTxLo);
+            ptx::tma_load_4d(sa, &lo.A, &full[stage], kl * BK, x0 + dx, y0 + dy, b + args.b_in);
+            ptx::tma_load_2d(sb, &lo.B, &full[stage], tap * args.Cin + kl * BK, nt * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -433,6 +563,7 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
+      constexpr uint32_t idesc8 = ptx::idesc_f8(128, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -447,11 +578,21 @@ __global__ void __launch_bounds__(256, 1)
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
           const uint32_t sb = sa + S::kA;
+          if (it % kct < args.kchunks) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBO, S::kLayout);
-            const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBO, S::kLayout);
-            ptx::mma_f16(d_tmem, da, db, idesc, (it | k) != 0);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBO, S::kLayout);
+              const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBO, S::kLayout);
+              ptx::mma_f16(d_tmem, da, db, idesc, (it | k) != 0);
+            }
+          } else if constexpr (BK >= 32) {
+            // F8 lo chunk: BK bytes per row (SW64 / SW32), 32 K per MMA
+#pragma unroll
+            for (int k = 0; k < BK / 32; ++k) {
+              const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBOLo, S::kLayoutLo);
+              const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBOLo, S::kLayoutLo);
+              ptx::mma_f8(d_tmem, da, db, idesc8, 1u);
+            }
           }
           ptx::mma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -487,14 +628,16 @@ __global__ void __launch_bounds__(256, 1)
       ptx::tc_fence_after();
       constexpr bool kRes = MODE == kResidualRelu;
       const int xb = tx * args.wb + box_dx, yb = ty * args.hb + box_dy;
-      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb, b + args.b_res, lane);
+      if constexpr (kRes)
+        epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, yb, b + args.b_res, lane);
 #pragma unroll 1
       for (int c = 0; c < BN; c += CH) {
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
         const int n0 = nt * BN + c;
         const int slot = (c / CH) & 1;
         if constexpr (kRes) {
-          if (c + CH < BN) epi_res_issue<CH>(es, slot ^ 1, &tmR, n0 + CH, args.Cout, args.split, xb, yb, b + args.b_res, lane);
+          if (c + CH < BN)
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, &lo.R, n0 + CH, args.Cout, args.split, xb, yb, b + args.b_res, lane);
         }
         if constexpr (MODE == kUpAdd) {
           uint32_t u[32];
@@ -516,17 +659,56 @@ __global__ void __launch_bounds__(256, 1)
             uint8_t* o_hi = es.buf + 2 * kUB;
             uint8_t* o_lo = es.buf + 3 * kUB;
 #pragma unroll 1
+            const bool f8 = args.split == kStoreF8;
             for (int a = 0; a < 2; ++a) {
               const int ox = 2 * xb, oyy = 2 * yb + a;
               if (lane == 0) {
-                ptx::mbar_arrive_expect_tx(&es.rbar[0], (args.split ? 2 : 1) * kUB);
+                ptx::mbar_arrive_expect_tx(&es.rbar[0], f8 ? kUB + kUB / 2 : (args.split ? 2 : 1) * kUB);
                 ptx::tma_load_4d(sk_hi, &tmR, &es.rbar[0], n0, ox, oyy, b + args.b_res);
-                if (args.split) ptx::tma_load_4d(sk_lo, &tmR, &es.rbar[0], args.Cout + n0, ox, oyy, b + args.b_res);
+                if (f8)
+                  ptx::tma_load_4d(sk_lo, &lo.R, &es.rbar[0], n0, ox, oyy, b + args.b_res);
+                else if (args.split)
+                  ptx::tma_load_4d(sk_lo, &tmR, &es.rbar[0], args.Cout + n0, ox, oyy, b + args.b_res);
               }
               ptx::mbar_wait(&es.rbar[0], es.rphase[0]);
               es.rphase[0] ^= 1;
               if (lane == 0) ptx::bulk_wait_read0();
               __syncwarp();
+              if (f8) {
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                  const int rr = 2 * (int)lane + q2;
+                  float x[CH];
+#pragma unroll
+                  for (int j = 0; j < CH / 8; ++j) {
+                    const uint4 h4 = *reinterpret_cast<const uint4*>(sk_hi + E::off(rr, j));
+                    const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                      const float2 fh = StoreT<T>::unpack(hh[e]);
+                      x[8 * j + 2 * e] = fh.x + v[8 * j + 2 * e];
+                      x[8 * j + 2 * e + 1] = fh.y + v[8 * j + 2 * e + 1];
+                    }
+                  }
+#pragma unroll
+                  for (int j = 0; j < CH / 16; ++j) {
+                    add_f8_16(x + 16 * j, *reinterpret_cast<const uint4*>(sk_lo + lo_off<CH>(rr, j)));
+                    uint4 h0, h1, l4;
+                    split_f8_16(x + 16 * j, h0, h1, l4);
+                    *reinterpret_cast<uint4*>(o_hi + E::off(rr, 2 * j)) = h0;
+                    *reinterpret_cast<uint4*>(o_hi + E::off(rr, 2 * j + 1)) = h1;
+                    *reinterpret_cast<uint4*>(o_lo + lo_off<CH>(rr, j)) = l4;
+                  }
+                }
+                ptx::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                  ptx::tma_store_4d(&tmO, o_hi, n0, ox, oyy, b + args.b_out);
+                  ptx::tma_store_4d(&lo.O, o_lo, n0, ox, oyy, b + args.b_out);
+                  ptx::bulk_commit();
+                }
+                continue;
+              }
 #pragma unroll
               for (int q2 = 0; q2 < 2; ++q2) {
                 const int rr = 2 * (int)lane + q2;
@@ -574,7 +756,8 @@ __global__ void __launch_bounds__(256, 1)
             }
           }
         } else {
-          epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, n0, args.Cout, args.split, xb, yb, b + args.b_out, lane);
+          epi_chunk<T, CH, MODE>(es, slot, &tmO, &lo.O, taddr, args.bias, n0, args.Cout, args.split, xb, yb,
+                                 b + args.b_out, lane);
         }
       }
       ptx::tc_fence_before();
@@ -635,13 +818,15 @@ struct RowsSmem {
                                          : (2 * R * BN <= 256) ? 256 : 512;
   static constexpr uint32_t kLayout = BK == 64 ? 2u : BK == 32 ? 4u : 6u;
   static constexpr uint32_t kSBO = 8 * BK * 2;
+  static constexpr uint32_t kLayoutLo = BK == 64 ? 4u : 6u;  // F8 lo rows: BK bytes
+  static constexpr uint32_t kSBOLo = 8 * BK;
 };
 
 template <typename T, int BN, int BK, int R, int HB, int STAGES, int MODE>
 __global__ void __launch_bounds__(256, 1)
     conv3_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
-                      const ConvArgs args) {
+                      const ConvArgs args, const __grid_constant__ LoMaps lo) {
   constexpr int WB = 128 / HB;
   constexpr int ROWS = R * HB + 2;
   using S = RowsSmem<BN, BK, R, ROWS, WB, STAGES>;
@@ -677,8 +862,10 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int kiters = 3 * args.kchunks;  // (dx, kc)
+  const int kct = args.kchunks + args.kch_lo;  // hi chunks, then (F8 input) lo chunks
+  const int kiters = 3 * kct;                   // (dx, kc)
   constexpr uint32_t kTx = ROWS * WB * BK * 2 + 3 * BN * BK * 2;
+  constexpr uint32_t kTxLo = ROWS * WB * BK + 3 * BN * BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -694,15 +881,19 @@ __global__ void __launch_bounds__(256, 1)
         const int x0 = tx * WB - 1;
         const int y0 = tyg * R * HB - 1;
         for (int it = 0; it < kiters; ++it) {
-          const int dx = it / args.kchunks;
-          const int kc = it - dx * args.kchunks;
+          const int dx = it / kct;
+          const int kc = it - dx * kct;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
-          ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0, b + args.b_in);
+          const bool hi = kc < args.kchunks;
+          const int kk = hi ? kc : kc - args.kchunks;
+          const CUtensorMap* mA = hi ? &tmA : &lo.A;
+          const CUtensorMap* mB = hi ? &tmB : &lo.B;
+          ptx::mbar_arrive_expect_tx(&full[stage], hi ? kTx : kTxLo);
+          ptx::tma_load_4d(sa, mA, &full[stage], kk * BK, x0 + dx, y0, b + args.b_in);
 #pragma unroll
           for (int dy = 0; dy < 3; ++dy)
-            ptx::tma_load_2d(sa + S::kA + dy * S::kBt, &tmB, &full[stage], (dy * 3 + dx) * args.Cin + kc * BK,
+            ptx::tma_load_2d(sa + S::kA + dy * S::kBt, mB, &full[stage], (dy * 3 + dx) * args.Cin + kk * BK,
                              nt * BN);
           if (++stage == STAGES) {
             stage = 0;
@@ -714,6 +905,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
+      constexpr uint32_t idesc8 = ptx::idesc_f8(128, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -726,6 +918,31 @@ __global__ void __launch_bounds__(256, 1)
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
+          if (it % kct >= args.kchunks) {
+            if constexpr (BK >= 32) {
+              // F8 lo chunk: BK bytes per row, 32 K per MMA (always accumulates: hi chunks precede)
+#pragma unroll
+              for (int dy = 0; dy < 3; ++dy) {
+                const uint32_t sb = sa + S::kA + dy * S::kBt;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                  const uint32_t a0 = sa + (uint32_t)((r * HB + dy) * WB * BK);
+#pragma unroll
+                  for (int k = 0; k < BK / 32; ++k) {
+                    const uint64_t da = ptx::smem_desc(a0 + k * 32, S::kSBOLo, S::kLayoutLo);
+                    const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBOLo, S::kLayoutLo);
+                    ptx::mma_f8(d_base + r * BN, da, db, idesc8, 1u);
+                  }
+                }
+              }
+            }
+            ptx::mma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
 #pragma unroll
           for (int dy = 0; dy < 3; ++dy) {
             const uint32_t sb = sa + S::kA + dy * S::kBt;
@@ -769,7 +986,8 @@ __global__ void __launch_bounds__(256, 1)
       constexpr int NC = BN / CH;
       const int xb = tx * WB + box_dx;
       const int yb0 = tyg * R * HB + box_dy;
-      if constexpr (kRes) epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, yb0, b + args.b_res, lane);
+      if constexpr (kRes)
+        epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, yb0, b + args.b_res, lane);
 #pragma unroll 1
       for (int i = 0; i < R * NC; ++i) {
         const int r = i / NC, c = (i - r * NC) * CH;
@@ -777,11 +995,12 @@ __global__ void __launch_bounds__(256, 1)
         if constexpr (kRes) {
           if (i + 1 < R * NC) {
             const int r1 = (i + 1) / NC, c1 = (i + 1 - r1 * NC) * CH;
-            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, yb0 + r1 * HB, b + args.b_res, lane);
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, &lo.R, nt * BN + c1, args.Cout, args.split, xb, yb0 + r1 * HB,
+                              b + args.b_res, lane);
           }
         }
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
-        epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
+        epi_chunk<T, CH, MODE>(es, slot, &tmO, &lo.O, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
                                yb0 + r * HB, b + args.b_out, lane);
       }
       ptx::tc_fence_before();
@@ -851,7 +1070,7 @@ template <typename T, int BN, int R, int STAGES, int MODE, bool DYF>
 __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) ? 384 : 256, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
-                    const ConvArgs args, const __grid_constant__ HeadArgs hargs) {
+                    const ConvArgs args, const __grid_constant__ HeadArgs hargs, const __grid_constant__ LoMaps lo) {
   // epilogue warps: 8 (2 per TMEM lane quadrant, alternating rows) for the residual and
   // fused-head epilogues, whose per-row work exceeds the MMA time of thin layers; 4 otherwise
   constexpr int EW = (MODE == kHeadFused || MODE == kResidualRelu) ? 8 : 4;
@@ -888,7 +1107,8 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int kiters = args.kchunks;  // 16-channel chunks
+  // 32-byte K chunks: kchunks hi chunks (16 fp16 channels), then kch_lo F8 lo chunks (32 e4m3)
+  const int kiters = args.kchunks + args.kch_lo;
   constexpr uint32_t kTx = 2 * S::kChunkStride + 9 * BN * 32;
 
   if (warp == 0) {
@@ -907,12 +1127,15 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
         for (int kc = 0; kc < kiters; ++kc) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
+          const bool hi = kc < args.kchunks;
+          const int kk = hi ? kc : kc - args.kchunks;
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          ptx::tma_load_5d(sa, &tmA, &full[stage], 0, x0, y0, 2 * kc, b + args.b_in);
+          ptx::tma_load_5d(sa, hi ? &tmA : &lo.A, &full[stage], 0, x0, y0, 2 * kk, b + args.b_in);
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const int slot = DYF ? (tap % 3) * 3 + tap / 3 : tap;  // DYF: [dx][dy] order
-            ptx::tma_load_2d(sa + S::kA + slot * S::kBt, &tmB, &full[stage], tap * args.Cin + kc * 16, nt * BN);
+            ptx::tma_load_2d(sa + S::kA + slot * S::kBt, hi ? &tmB : &lo.B, &full[stage],
+                             tap * args.Cin + kk * (hi ? 16 : 32), nt * BN);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -938,6 +1161,7 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
+          const bool f8 = kc >= args.kchunks;  // F8 lo chunk: same smem image, kind::f8f6f4
           if constexpr (DYF) {
 #pragma unroll
             for (int dx = 0; dx < 3; ++dx) {
@@ -951,9 +1175,14 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
                 const uint32_t a0 = sa + (uint32_t)(((i + 1) * S::kPx + dx) * 16);
                 const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
                 const uint64_t db = ptx::smem_desc(sbd + dy0 * BN * 32, 8 * 32, 6u);
-                const uint32_t id = nrows == 3 ? ptx::idesc_f16(128, 3 * BN, kBf)
-                                  : nrows == 2 ? ptx::idesc_f16(128, 2 * BN, kBf) : idesc;
-                ptx::mma_f16(d_base + (R - 1 - r_hi) * BN, da, db, id, 1u);
+                if (f8) {
+                  const uint32_t id8 = ptx::idesc_f8(128, nrows * BN);
+                  ptx::mma_f8(d_base + (R - 1 - r_hi) * BN, da, db, id8, 1u);
+                } else {
+                  const uint32_t id = nrows == 3 ? ptx::idesc_f16(128, 3 * BN, kBf)
+                                    : nrows == 2 ? ptx::idesc_f16(128, 2 * BN, kBf) : idesc;
+                  ptx::mma_f16(d_base + (R - 1 - r_hi) * BN, da, db, id, 1u);
+                }
               }
             }
           } else {
@@ -965,7 +1194,10 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
               for (int r = 0; r < R; ++r) {
                 const uint32_t a0 = sa + (uint32_t)(((r + dy) * S::kPx + dx) * 16);
                 const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
-                ptx::mma_f16(d_base + r * BN, da, db, idesc, (kc | tap) != 0);
+                if (f8)
+                  ptx::mma_f8(d_base + r * BN, da, db, ptx::idesc_f8(128, BN), 1u);
+                else
+                  ptx::mma_f16(d_base + r * BN, da, db, idesc, (kc | tap) != 0);
               }
             }
           }
@@ -1039,7 +1271,7 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
       const int xb = tx * 128 + q * 32;
       constexpr int RM = R / NH;  // rows of this warp: r = j * NH + half
       if constexpr (kRes)
-        epi_res_issue<CH>(es, 0, &tmR, nt * BN, args.Cout, args.split, xb, tyg * R + half, b + args.b_res, lane);
+        epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, tyg * R + half, b + args.b_res, lane);
 #pragma unroll 1
       for (int i = 0; i < RM * NC; ++i) {
         const int r = (i / NC) * NH + half, c = (i % NC) * CH;
@@ -1047,7 +1279,8 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
         if constexpr (kRes) {
           if (i + 1 < RM * NC) {
             const int r1 = ((i + 1) / NC) * NH + half, c1 = ((i + 1) % NC) * CH;
-            epi_res_issue<CH>(es, slot ^ 1, &tmR, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res, lane);
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, &lo.R, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1,
+                              b + args.b_res, lane);
           }
         }
         const uint32_t taddr =
@@ -1056,7 +1289,7 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
           epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs, s_w,
                           s_b, s_th, lf, oy, ox);
         } else {
-          epi_chunk<T, CH, MODE>(es, slot, &tmO, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
+          epi_chunk<T, CH, MODE>(es, slot, &tmO, &lo.O, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
                                  tyg * R + r, b + args.b_out, lane);
         }
       }

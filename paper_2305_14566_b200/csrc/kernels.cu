@@ -6,6 +6,7 @@
 //   DESIGN.md §2 reading). Integer stages are bit-exact by construction.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -396,6 +397,22 @@ __global__ void gather_raw_kernel(const uint8_t* tiles, int n, int P, T* X) {
   for (int k = 0; k < 32; ++k) dst[k] = T(v[k]);
 }
 
+// f8 storage (conv_tc.cuh kStoreF8): pixel = [C] fp16 hi | [C] e4m3 lo * 2^6, 3C bytes
+__device__ __forceinline__ float f8lo(uint8_t u) {
+  const __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)u, __NV_E4M3);
+  return __half2float(__half(h)) * (1.0f / 64.0f);
+}
+// value of channel c of pixel i (hi + lo) for storage kind `split` (0 plain, 1 x2, 2 f8)
+template <typename T>
+__device__ __forceinline__ float act_value(const T* base, int64_t i, int c, int C, int split) {
+  if (split == 2) {
+    const uint8_t* px = reinterpret_cast<const uint8_t*>(base) + i * 3 * (int64_t)C;
+    return __half2float(*reinterpret_cast<const __half*>(px + 2 * c)) + f8lo(px[2 * C + c]);
+  }
+  if (split == 1) return float(base[i * 2 * C + c]) + float(base[i * 2 * C + C + c]);
+  return float(base[i * C + c]);
+}
+
 // ------------------------------------------------------------------ K7 GAP + controller
 // g[b][c] = mean over the bottleneck's h x w pixels (fixed summation order), fp32.
 // (x2 precision: a pixel holds [C] hi | [C] lo; the value is hi + lo.)
@@ -407,16 +424,10 @@ __global__ void __launch_bounds__(256) gap_kernel(const T* E, int hw, int C, int
   const int b = blockIdx.y;
   const int cl = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
-  const int cs = split ? 2 * C : C;
   float s = 0.f;
   if (c < C) {
-    const T* p = E + (int64_t)b * hw * cs + c;
     const int per = (hw + 7) / 8, i0 = sl * per, i1 = min(hw, i0 + per);
-    for (int i = i0; i < i1; ++i) {
-      float v = float(p[(int64_t)i * cs]);
-      if (split) v += float(p[(int64_t)i * cs + C]);
-      s += v;
-    }
+    for (int i = i0; i < i1; ++i) s += act_value(E, (int64_t)b * hw + i, c, C, split);
   }
   part[sl][cl] = s;
   __syncthreads();
@@ -480,8 +491,9 @@ __global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, 
   __syncthreads();
   const int pix0 = (blockIdx.x * blockDim.x + threadIdx.x) * HPX;
   if (pix0 >= P * P) return;  // P*P is a multiple of HPX (P % 16 == 0)
-  const int cs = split ? 2 * C0p : C0p;
+  const int cs = split == 1 ? 2 * C0p : C0p;
   const T* d = D0 + ((int64_t)b * P * P + pix0) * cs;
+  const uint8_t* d8 = reinterpret_cast<const uint8_t*>(D0) + ((int64_t)b * P * P + pix0) * 3 * C0p;
   float F[HPX][kHead];
 #pragma unroll
   for (int q = 0; q < HPX; ++q)
@@ -491,6 +503,16 @@ __global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, 
     float xv[HPX][8];
 #pragma unroll
     for (int q = 0; q < HPX; ++q) {
+      if (split == 2) {
+        const uint8_t* px = d8 + (int64_t)q * 3 * C0p;
+        const uint4 u = *reinterpret_cast<const uint4*>(px + 2 * c);
+        const __half* e = reinterpret_cast<const __half*>(&u);
+        const uint2 l = *reinterpret_cast<const uint2*>(px + 2 * C0p + c);
+        const uint8_t* lb = reinterpret_cast<const uint8_t*>(&l);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xv[q][k] = __half2float(e[k]) + f8lo(lb[k]);
+        continue;
+      }
       const uint4 u = *reinterpret_cast<const uint4*>(d + (int64_t)q * cs + c);
       const T* e = reinterpret_cast<const T*>(&u);
 #pragma unroll
@@ -635,7 +657,12 @@ __global__ void f32_to_t_kernel(const float* in, T* out, int64_t rows, int cin, 
   const int c = i % cpad;
   const float v = c < cin ? in[r * cin + c] : 0.f;
   const T hi = T(v);
-  if (split) {
+  if (split == 2) {
+    uint8_t* px = reinterpret_cast<uint8_t*>(out) + r * 3 * cpad;
+    const __half h = __float2half_rn(v);
+    *reinterpret_cast<__half*>(px + 2 * c) = h;
+    px[2 * cpad + c] = (uint8_t)__nv_cvt_float_to_fp8((v - __half2float(h)) * 64.0f, __NV_SATFINITE, __NV_E4M3);
+  } else if (split) {
     out[r * 2 * cpad + c] = hi;
     out[r * 2 * cpad + cpad + c] = T(v - float(hi));
   } else {
@@ -648,7 +675,7 @@ __global__ void t_to_f32_kernel(const T* in, float* out, int64_t rows, int cout,
   if (i >= rows * cout) return;
   const int64_t r = i / cout;
   const int c = i % cout;
-  out[i] = split ? float(in[r * 2 * cpad + c]) + float(in[r * 2 * cpad + cpad + c]) : float(in[r * cpad + c]);
+  out[i] = act_value(in, r, c, cpad, split);
 }
 
 // ==================================================================== host launchers

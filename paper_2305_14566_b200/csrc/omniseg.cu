@@ -4,6 +4,7 @@
 // of kernels.cu and conv_tc.cu.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -95,10 +96,14 @@ struct Arch {
   int levels = 5, base = 32, head = 8, ncls = 6, slide_mag = 40, batch = 64, device = -1;
   std::vector<int> scale_codes{5, 10, 20, 40};
   bool bf16 = false;
-  bool split = false;  // "x2" precision: activations stored as hi + lo 16-bit pairs
-  int xlevels = -1;    // x2 only for tensors at U-Net levels < xlevels (-1: all levels)
-  int xa = 1;          // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
-  bool sp(int level) const { return split && level < (xlevels < 0 ? 64 : xlevels); }
+  int split = kStorePlain;  // StoreKind of the activations: fp16/bf16 plain, x2 (hi + lo 16-bit), f8 (fp16 + e4m3 lo)
+  int xlevels = -1;         // split storage only for tensors at U-Net levels < xlevels (-1: all levels)
+  int xa = 1;               // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
+  int sp(int level) const { return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain; }
+  // bytes per channel of a tensor stored with kind k
+  static int bpc(int k) { return k == kStoreX2 ? 4 : k == kStoreF8 ? 3 : 2; }
+  // channel padding: 16 (MMA K step), 32 in the f8 mode (an e4m3 MMA consumes 32 channels)
+  int padc(int c) const { return split == kStoreF8 ? (c + 31) / 32 * 32 : (c + 15) / 16 * 16; }
 };
 
 Arch parse_arch(const char* s) {
@@ -131,10 +136,10 @@ Arch parse_arch(const char* s) {
     else if (k == "xlevels") a.xlevels = toi(v);
     else if (k == "xa") a.xa = toi(v);
     else if (k == "dtype") {
-      OS_REQUIRE(v == "fp16" || v == "bf16" || v == "fp16x2" || v == "bf16x2",
-                 "arch: dtype must be fp16, bf16, fp16x2 or bf16x2");
+      OS_REQUIRE(v == "fp16" || v == "bf16" || v == "fp16x2" || v == "bf16x2" || v == "fp16f8",
+                 "arch: dtype must be fp16, bf16, fp16x2, bf16x2 or fp16f8");
       a.bf16 = v.rfind("bf16", 0) == 0;
-      a.split = v.size() > 4;
+      a.split = v == "fp16f8" ? kStoreF8 : v.size() > 4 ? kStoreX2 : kStorePlain;
     } else if (k == "scale_codes") {
       a.scale_codes.clear();
       std::stringstream s2(v);
@@ -159,7 +164,9 @@ int pad16(int c) { return (c + 15) / 16 * 16; }
 
 struct Layer {
   DevBuf w;      // [coutp][k*k][cinp] 16-bit
+  DevBuf wlo;    // f8 inputs: [coutp][k*k][cinp] e5m2 bytes of W * 2^-6 (the lo term's weights)
   DevBuf b;      // [coutp] fp32
+  int in_kind = 0;  // StoreKind of the layer's input
   int cin = 0, cout = 0, cinp = 0, coutp = 0, k = 3, stride = 1;
   int alg_k = 0; // algorithmic K if not k*k*cin (the stem: 27)
 };
@@ -196,14 +203,6 @@ struct omniseg {
   std::vector<const Layer*> enc_layers, dec_layers;
   ConvPlan head_plan{};   // dec0.b with the dynamic head + stitch fused into its epilogue
   bool head_fusable = false;
-  // level-0 micro-batching: the level-0 layers run one tile at a time on single-tile
-  // scratch tensors (h0, t, U0) that stay L2-resident; only E0 (the skip) and the gather
-  // output live in HBM. Plans: stem, enc0.a, enc0.b | up0, dec0.a, dec0.b(head or plain)
-  bool mb0 = false;
-  DevBuf s_h0, s_t, s_U0;
-  ConvPlan mb_enc[3], mb_dec[3], mb_head{};
-  bool mb_head_ok = false;
-
   // front end / canvases
   DevBuf slide, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
   std::vector<uint32_t> h_tiles;
@@ -259,10 +258,13 @@ __nv_bfloat16 to16<__nv_bfloat16>(float v) {
 }
 
 // Upload one conv: blob order [cout][k][k][cin] fp32 -> device [coutp][k*k][cinp] 16-bit.
-// kdup = 2 for split (hi|lo) inputs: the K axis of every tap is [W | W].
+// x2 inputs: the K axis of every tap is [W | W] (kdup = 2). f8 inputs: also the lo weights
+// e5m2(W * 2^-6), RNE and saturating (R9).
 template <typename T>
 void upload_conv(Layer& L, const float* w, const float* b, int cin, int cout, int k, int stride, int cinp, int coutp,
-                 int kdup = 1) {
+                 int in_kind = kStorePlain) {
+  const int kdup = in_kind == kStoreX2 ? 2 : 1;
+  L.in_kind = in_kind;
   L.cin = cin;
   L.cout = cout;
   L.cinp = cinp * kdup;
@@ -282,6 +284,16 @@ void upload_conv(Layer& L, const float* w, const float* b, int cin, int cout, in
   L.b.ensure(hb.size() * sizeof(float));
   OS_CUDA(cudaMemcpy(L.w.p, hw.data(), hw.size() * sizeof(T), cudaMemcpyHostToDevice));
   OS_CUDA(cudaMemcpy(L.b.p, hb.data(), hb.size() * sizeof(float), cudaMemcpyHostToDevice));
+  if (in_kind == kStoreF8) {
+    std::vector<uint8_t> hl((size_t)coutp * k * k * cinp, 0);
+    for (int o = 0; o < cout; ++o)
+      for (int t = 0; t < k * k; ++t)
+        for (int c = 0; c < cin; ++c)
+          hl[((size_t)o * k * k + t) * cinp + c] = (uint8_t)__nv_cvt_float_to_fp8(
+              w[((size_t)o * k * k + t) * cin + c] * kLoInv, __NV_SATFINITE, __NV_E5M2);
+    L.wlo.ensure(hl.size());
+    OS_CUDA(cudaMemcpy(L.wlo.p, hl.data(), hl.size(), cudaMemcpyHostToDevice));
+  }
 }
 
 // Stem as a 1x1 conv over the 32-channel im2col input of the gather kernel:
@@ -331,7 +343,7 @@ void load_weights(omniseg* h, const float* blob) {
   auto conv = [&](Layer& dst, int co, int k, int ci, int stride, int in_level) {
     const float* w = take((size_t)co * k * k * ci);
     const float* b = take(co);
-    upload_conv<T>(dst, w, b, ci, co, k, stride, pad16(ci), pad16(co), a.sp(in_level) ? 2 : 1);
+    upload_conv<T>(dst, w, b, ci, co, k, stride, a.padc(ci), a.padc(co), a.sp(in_level));
   };
   {
     const float* w = take((size_t)h->C[0] * 27);
@@ -391,22 +403,22 @@ void ensure_workspace(omniseg* h, int P) {
   if (h->ws_P == P && h->ws_B == B) return;
   check_patch(h, P);
   const int L = h->arch.levels;
-  // 16-bit storage; x2 levels hold hi + lo
-  h->X0.ensure((size_t)B * P * P * 32 * 2);  // exact u8 values: never split
+  const Arch& ar = h->arch;
+  h->X0.ensure((size_t)B * P * P * 32 * 2);  // exact u8 values in 16-bit: never split
   h->lv.clear();
   h->lv.resize(L);
   for (int l = 0; l < L; ++l) {
     LevelBufs& q = h->lv[l];
     q.P = P >> l;
     q.C = h->Cp[l];
-    const size_t n = (size_t)B * q.P * q.P * q.C * (h->arch.sp(l) ? 4 : 2);
+    const size_t n = (size_t)B * q.P * q.P * q.C * Arch::bpc(ar.sp(l));
     q.E.ensure(n);
     q.A.ensure(n);
     q.Bt.ensure(n);
   }
   h->g.ensure((size_t)B * h->C[L - 1] * 4);
   h->theta.ensure((size_t)B * kMaxTasks * kTheta * 4);
-  const bool bf = h->arch.bf16;
+  const bool bf = ar.bf16;
   h->enc_plans.clear();
   h->dec_plans.clear();
   h->enc_layers.clear();
@@ -414,7 +426,7 @@ void ensure_workspace(omniseg* h, int P) {
   // out_level: U-Net level of the output (and residual / skip) tensor
   auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int out_level) {
     return make_conv_plan(bf, in, B, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
-                          res, out, h->arch.sp(out_level));
+                          res, out, ar.sp(out_level), -1, -1, -1, ly.in_kind, ly.wlo.p);
   };
   auto enc = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol) {
     h->enc_plans.push_back(plan(ly, in, Hin, res, out, mode, ol));
@@ -427,7 +439,7 @@ void ensure_workspace(omniseg* h, int P) {
   enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias, 0);
   for (int l = 0; l < L; ++l) {
     LevelBufs& q = h->lv[l];
-    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, h->arch.xa ? l : 1000);
+    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000);
     enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l);
     if (l < L - 1) enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias, l + 1);
   }
@@ -435,41 +447,8 @@ void ensure_workspace(omniseg* h, int P) {
     LevelBufs& q = h->lv[l];
     const void* D = (l + 1 == L - 1) ? h->lv[l + 1].E.p : h->lv[l + 1].A.p;
     dec(h->up[l], D, q.P / 2, q.E.p, q.A.p, kUpAdd, l);
-    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, h->arch.xa ? l : 1000);
+    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000);
     dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu, l);
-  }
-  // level-0 micro-batching (see the handle); opt-in with OMNISEG_MB0=1 (measured slower: single-tile
-  // launches are too small to reach a pipelined steady state)
-  h->mb0 = false;
-  if (getenv("OMNISEG_MB0") != nullptr && L >= 3) {
-    LevelBufs& q0 = h->lv[0];
-    const size_t t1 = (size_t)P * P * q0.C * (h->arch.sp(0) ? 4 : 2);
-    const size_t t1a = (size_t)P * P * q0.C * ((h->arch.sp(0) && h->arch.xa) ? 4 : 2);
-    h->s_h0.ensure(t1);
-    h->s_t.ensure(t1a);
-    h->s_U0.ensure(t1);
-    auto mplan = [&](const Layer& ly, const void* in, int Hin, int Bin, const void* res, int Bres, void* out, int Bout,
-                     int mode, int ol) {
-      return make_conv_plan(bf, in, 1, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
-                            res, out, h->arch.sp(ol), Bin, Bres, Bout);
-    };
-    const int la = h->arch.xa ? 0 : 1000;
-    const void* D1 = (1 == L - 1) ? h->lv[1].E.p : h->lv[1].A.p;
-    h->mb_enc[0] = mplan(h->stem, h->X0.p, P, B, nullptr, 1, h->s_h0.p, 1, kReluBias, 0);
-    h->mb_enc[1] = mplan(h->enc_a[0], h->s_h0.p, P, 1, nullptr, 1, h->s_t.p, 1, kReluBias, la);
-    h->mb_enc[2] = mplan(h->enc_b[0], h->s_t.p, P, 1, h->s_h0.p, 1, q0.E.p, B, kResidualRelu, 0);
-    h->mb_dec[0] = mplan(h->up[0], D1, P / 2, B, q0.E.p, B, h->s_U0.p, 1, kUpAdd, 0);
-    h->mb_dec[1] = mplan(h->dec_a[0], h->s_U0.p, P, 1, nullptr, 1, h->s_t.p, 1, kReluBias, la);
-    h->mb_dec[2] = mplan(h->dec_b[0], h->s_t.p, P, 1, h->s_U0.p, 1, q0.A.p, B, kResidualRelu, 0);
-    h->mb_head_ok = false;
-    if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr) {
-      ConvPlan hp = mplan(h->dec_b[0], h->s_t.p, P, 1, h->s_U0.p, 1, h->s_U0.p, 1, kHeadFused, 0);
-      if (hp.nz_R > 0 && hp.bn == h->Cp[0] && h->C[0] <= 32) {
-        h->mb_head = hp;
-        h->mb_head_ok = true;
-      }
-    }
-    h->mb0 = true;
   }
   // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
   h->head_fusable = false;
@@ -602,22 +581,9 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
                         int ntasks, int S, int Hp, int Wp, int pad, float* out_p, float* out_F, float* out_g) {
   const int L = h->arch.levels;
   cudaStream_t s = h->stream;
-  const bool mb = h->mb0;
   const size_t ne = h->enc_plans.size();
   // ---------------- encoder
-  if (mb) {
-    for (int i = 0; i < n; ++i) {
-      for (int k = 0; k < 3; ++k) {
-        ConvPlan& pl = h->mb_enc[k];
-        pl.args.b_in = k == 0 ? i : 0;
-        pl.args.b_res = 0;
-        pl.args.b_out = k == 2 ? i : 0;
-        run_conv_prof(h, pl, *h->enc_layers[k], k, 1);
-        h->conv_launches++;
-      }
-    }
-  }
-  for (size_t i = mb ? 3 : 0; i < ne; ++i) {
+  for (size_t i = 0; i < ne; ++i) {
     set_conv_batch(h->enc_plans[i], n);
     run_conv_prof(h, h->enc_plans[i], *h->enc_layers[i], (int)i, n);
     h->conv_launches++;
@@ -631,9 +597,9 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
   if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, h->g.p, (size_t)n * h->C[L - 1] * 4, cudaMemcpyDefault, s));
   // ---------------- decoder
   const size_t ndec = h->dec_plans.size();
-  const bool fuse = (mb ? h->mb_head_ok : h->head_fusable) && ntasks <= 8;
+  const bool fuse = h->head_fusable && ntasks <= 8;
   bool head_done = false;
-  for (size_t i = 0; i < (mb ? ndec - 3 : ndec); ++i) {
+  for (size_t i = 0; i < ndec; ++i) {
     if (fuse && i + 1 == ndec) {
       ConvPlan& hp = h->head_plan;
       set_conv_batch(hp, n);
@@ -645,21 +611,6 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
       run_conv_prof(h, h->dec_plans[i], *h->dec_layers[i], (int)(ne + i), n);
     }
     h->conv_launches++;
-  }
-  if (mb) {
-    if (fuse) fill_head(h->mb_head.head, h, ntasks, P, S, Hp, Wp, pad, tiles, first, tt, out_p, out_F);
-    for (int i = 0; i < n; ++i) {
-      for (int k = 0; k < 3; ++k) {
-        ConvPlan& pl = (k == 2 && fuse) ? h->mb_head : h->mb_dec[k];
-        pl.args.b_in = k == 0 ? i : 0;
-        pl.args.b_res = k == 0 ? i : 0;
-        pl.args.b_out = (k == 2 && !fuse) ? i : 0;
-        pl.args.b_head = i;
-        run_conv_prof(h, pl, *h->dec_layers[ndec - 3 + k], (int)(ne + ndec - 3 + k), 1);
-        h->conv_launches++;
-      }
-    }
-    head_done = fuse;
   }
   if (!head_done) {
     launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.sp(0), P, h->Wpre.as<float>(),
@@ -913,7 +864,7 @@ omniseg_t* omniseg_create(const char* arch, const void* weights, size_t nbytes) 
     const int L = h->arch.levels;
     for (int l = 0; l < L; ++l) {
       h->C.push_back(h->arch.base << l);
-      h->Cp.push_back(pad16(h->arch.base << l));
+      h->Cp.push_back(h->arch.padc(h->arch.base << l));
     }
     h->nin = h->C[L - 1] + h->arch.ncls + (int)h->arch.scale_codes.size();
     OS_REQUIRE(weights != nullptr, "weights is NULL");
@@ -1142,7 +1093,8 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
                        int Cout, int k, int stride, const float* r, int mode, float* y) {
   try {
     OS_REQUIRE(h && x && w && b && y, "debug_conv: NULL argument");
-    const int split = (mode & 16) ? 1 : 0;
+    // mode | 16: x2 storage of input / residual / output; mode | 32: f8 storage
+    const int split = (mode & 32) ? kStoreF8 : (mode & 16) ? kStoreX2 : kStorePlain;
     mode &= 15;
     OS_REQUIRE(mode >= 0 && mode <= 3, "debug_conv: bad mode");
     OS_REQUIRE((mode != 1 && mode != 2) || r, "debug_conv: mode needs r");
@@ -1150,27 +1102,29 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
     OS_CUDA(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
     const bool bf = h->arch.bf16;
-    const int cinp = pad16(Cin), coutp = pad16(Cout);
+    const int pc = split == kStoreF8 ? 32 : 16;
+    const int cinp = (Cin + pc - 1) / pc * pc, coutp = (Cout + pc - 1) / pc * pc;
     const int Ho = (H - 1) / stride + 1, Wo = (W - 1) / stride + 1;
     const int oh = mode == 2 ? 2 * Ho : Ho, ow = mode == 2 ? 2 * Wo : Wo;
-    const int sm = split ? 2 : 1;
+    const int sm = split == kStoreX2 ? 2 : 1;
+    const int bpc = Arch::bpc(split);
     Layer L;
     std::vector<float> wv(w, w + (size_t)Cout * k * k * Cin), bv(b, b + Cout);
     if (bf)
-      upload_conv<__nv_bfloat16>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp, sm);
+      upload_conv<__nv_bfloat16>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp, split);
     else
-      upload_conv<__half>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp, sm);
+      upload_conv<__half>(L, wv.data(), bv.data(), Cin, Cout, k, stride, cinp, coutp, split);
     DevBuf f32in, xin, rin, f32r, out, f32o;
     const int64_t rows_in = (int64_t)B * H * W, rows_out = (int64_t)B * oh * ow;
     f32in.ensure(rows_in * Cin * 4);
-    xin.ensure(rows_in * cinp * 2 * sm);
+    xin.ensure(rows_in * cinp * bpc);
     OS_CUDA(cudaMemcpyAsync(f32in.p, x, rows_in * Cin * 4, cudaMemcpyHostToDevice, s));
     if (r) {
       f32r.ensure(rows_out * Cout * 4);
-      rin.ensure(rows_out * coutp * 2 * sm);
+      rin.ensure(rows_out * coutp * bpc);
       OS_CUDA(cudaMemcpyAsync(f32r.p, r, rows_out * Cout * 4, cudaMemcpyHostToDevice, s));
     }
-    out.ensure(rows_out * coutp * 2 * sm);
+    out.ensure(rows_out * coutp * bpc);
     f32o.ensure(rows_out * Cout * 4);
     if (bf) {
       launch_f32_to_t<__nv_bfloat16>(f32in.as<float>(), xin.as<__nv_bfloat16>(), rows_in, Cin, cinp, split, s);
@@ -1181,7 +1135,7 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
       if (r) launch_f32_to_t<__half>(f32r.as<float>(), rin.as<__half>(), rows_out, Cout, coutp, split, s);
     }
     ConvPlan p = make_conv_plan(bf, xin.p, B, H, W, cinp * sm, L.w.p, L.b.as<float>(), coutp, k, stride, mode,
-                                r ? rin.p : nullptr, out.p, split != 0);
+                                r ? rin.p : nullptr, out.p, split, -1, -1, -1, split, L.wlo.p);
     run_conv(p, s);
     if (bf)
       launch_t_to_f32<__nv_bfloat16>(out.as<__nv_bfloat16>(), f32o.as<float>(), rows_out, Cout, coutp, split, s);

@@ -28,7 +28,7 @@ def stitched(cfg, crop, xls):
         a = dict(w.arch)
         if isinstance(xl, str):
             k, v = xl.split("=")
-            a[k] = int(v)
+            a[k] = int(v) if v.lstrip("-").isdigit() else v
         else:
             a["xlevels"] = xl
         h = Omniseg(arch_string(a), w.weights())

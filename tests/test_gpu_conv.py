@@ -84,6 +84,34 @@ def test_conv_parity_split(h, B, H, W, Cin, Cout, k, stride, mode):
     _run(h, B, H, W, Cin, Cout, k, stride, mode, True)
 
 
+@pytest.mark.parametrize("B,H,W,Cin,Cout,k,stride,mode", [c for c in CASES if c[3] % 32 == 0] +
+                         [(1, 128, 128, 32, 32, 3, 1, 3), (1, 64, 64, 32, 64, 3, 1, 1), (1, 32, 32, 96, 96, 3, 1, 0)])
+def test_conv_parity_f8(h, B, H, W, Cin, Cout, k, stride, mode):
+    """f8 precision (R9): fp32 inputs stored as fp16 hi + e4m3 lo (x 2^6), the lo
+    term multiplied by e5m2(W 2^-6) into the same fp32 accumulator. The reference applies
+    exactly those roundings (torch's RNE float8 casts) to x, r and the lo weights, so what
+    remains is the fp32 accumulation order and the f8 rounding of the stored output:
+    |err| <= 2^-18 sum|terms| + 2^-14 |ref| + 2^-15. Dropping the lo term or mis-scaling it
+    errs by ~2^-12 |ref| and fails."""
+    _run(h, B, H, W, Cin, Cout, k, stride, mode, "f8")
+
+
+def _f8_store(a):
+    """fp32 -> stored f8 pair value: fp16 hi + e4m3 RNE-saturated lo (x 2^6) / 2^6."""
+    import torch
+    a32 = np.asarray(a, np.float32)
+    hi = a32.astype(np.float16).astype(np.float32)
+    lo = torch.from_numpy(((a32 - hi) * 64.0).astype(np.float32)).clamp(-448, 448)
+    lo = lo.to(torch.float8_e4m3fn).to(torch.float64).numpy() / 64.0
+    return hi.astype(np.float64) + lo, hi.astype(np.float64), lo
+
+
+def _e5m2_lo_weights(w):
+    import torch
+    t = torch.from_numpy((np.asarray(w, np.float64) / 64.0).astype(np.float32))
+    return t.to(torch.float8_e5m2).to(torch.float64).numpy() * 64.0
+
+
 def _run(h, B, H, W, Cin, Cout, k, stride, mode, split):
     rng = np.random.default_rng(B * 1000 + H + Cin + Cout + k + stride + mode)
     x = rng.standard_normal((B, H, W, Cin)) if split else _f16(rng.standard_normal((B, H, W, Cin)))
@@ -100,6 +128,28 @@ def _run(h, B, H, W, Cin, Cout, k, stride, mode, split):
     if split:   # the GPU sees fp32-rounded inputs
         x = x.astype(np.float32).astype(np.float64)
         r = None if r is None else r.astype(np.float32).astype(np.float64)
+    if split == "f8":
+        _, xhi, xlo = _f8_store(x)
+        rs = None if r is None else _f8_store(r)[0]
+        wlo = _e5m2_lo_weights(w)
+        pre = np.stack([nn.conv2d(xhi[i], w, b, stride) + nn.conv2d(xlo[i], wlo, np.zeros_like(b), stride)
+                        for i in range(B)])
+        if mode == 0:
+            ref = np.maximum(pre, 0)
+        elif mode == 1:
+            ref = np.maximum(pre + rs, 0)
+        elif mode == 2:
+            ref = rs + np.stack([nn.up2(p) for p in pre])
+        else:
+            ref = pre if rs is None else pre + rs
+        got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split)
+        ref_abs = _ref(np.abs(x), np.abs(w), np.abs(b), stride, None if r is None else np.abs(r),
+                       3 if mode != 2 else 2)
+        bound = 2.0 ** -18 * np.abs(ref_abs) + 2.0 ** -14 * np.abs(ref) + 2.0 ** -15
+        err = np.abs(got - ref)
+        assert got.shape == ref.shape
+        assert (err <= bound).all(), f"max err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"
+        return
     ref = _ref(x, w, b, stride, r, mode)
     got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split)
     err = np.abs(got - ref)

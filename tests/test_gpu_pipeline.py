@@ -79,6 +79,20 @@ def cfg1(gpu_lib):
     return w, slide, ref, h, prob, mask, area
 
 
+def test_cfg1_f8_gated(gpu_lib):
+    """fp16f8 precision (fp16 hi + e4m3 lo activations, R9): the full gates --
+    tile list / fg bit-exact, |dp| <= 1e-2, masks >= 99.9% with flips only near 0.5."""
+    w = workload(1)
+    w.arch["dtype"] = "fp16f8"
+    slide, ref = _cfg1_ref()
+    h, prob, mask, area = run_gpu(w, slide)
+    H, W = slide.shape[:2]
+    Hp, Wp = fe.padded_extent(H, W, w.pad)
+    assert unpack_tiles(h.tiles(), Hp, Wp, w.patch, w.stride) == ref["kept"]
+    dmax, agree = check_prob_mask(prob.reshape(H, W), mask.reshape(H, W), ref["prob"][0], ref["mask"][0], "f8")
+    print(f"fp16f8: max |dp| {dmax:.4g}, mask agreement {agree:.5f}")
+
+
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
 def test_cfg1_16bit_storage_numerics_report(gpu_lib, dtype):
     """Plain 16-bit activation storage (BASELINE configs' 'bf16 activations', and fp16):
