@@ -5,6 +5,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_set>
@@ -265,6 +266,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   }
   OS_REQUIRE(!f8in || p.nz_R > 0 || p.bk >= 32, "F8 input needs K chunks of >= 32 channels");
   a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
+  if (const char* d = getenv("OMNISEG_DBG")) a.dbg = atoi(d);
   a.bias = bias;
   a.res = res;
   a.out = out;
@@ -368,13 +370,35 @@ void set_conv_batch(ConvPlan& p, int B) {
   p.flops = 2.0 * (double)B * a.Ho * a.Wo * a.Cout * (double)a.ksize * a.ksize * a.Cin;
 }
 
-void run_conv(const ConvPlan& p, cudaStream_t s) {
-  if (p.args.num_work <= 0) return;
+void run_conv(const ConvPlan& p0, cudaStream_t s) {
+  if (p0.args.num_work <= 0) return;
+  ConvPlan p = p0;
+  static unsigned long long* dbuf = nullptr;
+  if ((p.args.dbg & 8) && p.nz_R > 0) {  // experiment: MMA-warp cycle counters
+    if (!dbuf) OS_CUDA(cudaMalloc(&dbuf, 148 * 4 * 8));
+    p.args.dbg_out = dbuf;
+  } else {
+    p.args.dbg &= ~8;
+  }
   if (p.bf16)
     dispatch<__nv_bfloat16>(p, s);
   else
     dispatch<__half>(p, s);
   OS_CUDA(cudaGetLastError());
+  if (p.args.dbg & 8) {
+    unsigned long long h[148 * 4];
+    OS_CUDA(cudaStreamSynchronize(s));
+    OS_CUDA(cudaMemcpy(h, dbuf, sizeof(h), cudaMemcpyDeviceToHost));
+    double a = 0, te = 0, fu = 0, n = 0;
+    for (int i = 0; i < p.grid; ++i) {
+      a += h[4 * i];
+      te += h[4 * i + 1];
+      fu += h[4 * i + 2];
+      n += h[4 * i + 3];
+    }
+    fprintf(stderr, "[nz BN=%d Cin=%d mode=%d] per item: total %.0f, wait tempty %.0f, wait full %.0f cycles (%.0f items/CTA)\n",
+            p.bn, p.args.Cin, p.mode, a / n, te / n, fu / n, n / p.grid);
+  }
 }
 
 }  // namespace osg

@@ -63,6 +63,9 @@ struct ConvArgs {
   // batch-index offsets of the tensors (a launch over images [0, B) of the work space reads
   // input image b + b_in, residual b + b_res, writes b + b_out, head tile b + b_head)
   int b_in, b_res, b_out, b_head;
+  int dbg;  // experiments only (OMNISEG_DBG, conv3_nz_kernel): 1 skip epilogue math/stores, 2 skip MMAs, 4 skip loads,
+            // 8 record MMA-warp cycle counters into dbg_out[blockIdx.x][4]
+  unsigned long long* dbg_out;
 };
 
 template <typename T>
@@ -560,8 +563,8 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------------------ MMA issuer (warp-collective)
       constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
       constexpr uint32_t idesc8 = ptx::idesc_f8(128, BN);
       int stage = 0;
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBO, S::kLayout);
               const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBO, S::kLayout);
-              ptx::mma_f16(d_tmem, da, db, idesc, (it | k) != 0);
+              ptx::mma_f16_w(d_tmem, da, db, idesc, (it | k) != 0);
             }
           } else if constexpr (BK >= 32) {
             // F8 lo chunk: BK bytes per row (SW64 / SW32), 32 K per MMA
@@ -591,16 +594,16 @@ __global__ void __launch_bounds__(256, 1)
             for (int k = 0; k < BK / 32; ++k) {
               const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBOLo, S::kLayoutLo);
               const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBOLo, S::kLayoutLo);
-              ptx::mma_f8(d_tmem, da, db, idesc8, 1u);
+              ptx::mma_f8_w(d_tmem, da, db, idesc8, 1u);
             }
           }
-          ptx::mma_commit(&empty[stage]);
+          ptx::mma_commit_w(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tfull[acc]);
+        ptx::mma_commit_w(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -903,7 +906,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // MMA issuer (warp-collective)
       constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
       constexpr uint32_t idesc8 = ptx::idesc_f8(128, BN);
       int stage = 0;
@@ -931,12 +934,12 @@ __global__ void __launch_bounds__(256, 1)
                   for (int k = 0; k < BK / 32; ++k) {
                     const uint64_t da = ptx::smem_desc(a0 + k * 32, S::kSBOLo, S::kLayoutLo);
                     const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBOLo, S::kLayoutLo);
-                    ptx::mma_f8(d_base + r * BN, da, db, idesc8, 1u);
+                    ptx::mma_f8_w(d_base + r * BN, da, db, idesc8, 1u);
                   }
                 }
               }
             }
-            ptx::mma_commit(&empty[stage]);
+            ptx::mma_commit_w(&empty[stage]);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -953,17 +956,17 @@ __global__ void __launch_bounds__(256, 1)
               for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t da = ptx::smem_desc(a0 + k * 32, S::kSBO, S::kLayout);
                 const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBO, S::kLayout);
-                ptx::mma_f16(d_base + r * BN, da, db, idesc, (it | dy | k) != 0);
+                ptx::mma_f16_w(d_base + r * BN, da, db, idesc, (it | dy | k) != 0);
               }
             }
           }
-          ptx::mma_commit(&empty[stage]);
+          ptx::mma_commit_w(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tfull[acc]);
+        ptx::mma_commit_w(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -1059,6 +1062,47 @@ struct NzCfg {
   }
 };
 
+// The MMAs of one 32-byte K chunk of conv3_nz_kernel (warp-collective issue). F8: the lo
+// chunk (e4m3 activations x e5m2 weights, kind::f8f6f4); otherwise 16-bit (kind::f16).
+template <int BN, int R, bool DYF, bool F8, bool BF, typename S>
+__device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int kc) {
+  if constexpr (DYF) {
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      const uint32_t sbd = sa + S::kA + dx * 3 * S::kBt;
+#pragma unroll
+      for (int i = -1; i <= R; ++i) {
+        const int r_hi = i + 1 < R - 1 ? i + 1 : R - 1;
+        const int r_lo = i - 1 > 0 ? i - 1 : 0;
+        const int nrows = r_hi - r_lo + 1;
+        const int dy0 = i - r_hi + 1;
+        const uint32_t a0 = sa + (uint32_t)(((i + 1) * S::kPx + dx) * 16);
+        const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
+        const uint64_t db = ptx::smem_desc(sbd + dy0 * BN * 32, 8 * 32, 6u);
+        if constexpr (F8)
+          ptx::mma_f8_w(d_base + (R - 1 - r_hi) * BN, da, db, ptx::idesc_f8(128, nrows * BN), 1u);
+        else
+          ptx::mma_f16_w(d_base + (R - 1 - r_hi) * BN, da, db, ptx::idesc_f16(128, nrows * BN, BF), 1u);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+      const int dy = tap / 3, dx = tap % 3;
+      const uint64_t db = ptx::smem_desc(sa + S::kA + tap * S::kBt, 8 * 32, 6u);  // SW32, 8 rows x 32 B
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t a0 = sa + (uint32_t)(((r + dy) * S::kPx + dx) * 16);
+        const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
+        if constexpr (F8)
+          ptx::mma_f8_w(d_base + r * BN, da, db, ptx::idesc_f8(128, BN), 1u);
+        else
+          ptx::mma_f16_w(d_base + r * BN, da, db, ptx::idesc_f16(128, BN, BF), (kc | tap) != 0);
+      }
+    }
+  }
+}
+
 // DYF ("dy-fused"): the three dy weight tiles of a dx are stacked along N, so ONE MMA with
 // ONE A fetch (input row i, shift dx) produces the contributions to output rows i+1, i, i-1
 // (N = 3 BN; 2 BN / BN at the band edges). The R accumulators are laid out in reverse row
@@ -1129,6 +1173,14 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
           uint8_t* sa = smem + stage * S::kStage;
           const bool hi = kc < args.kchunks;
           const int kk = hi ? kc : kc - args.kchunks;
+          if (args.dbg & 4) {
+            ptx::mbar_arrive(&full[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
           ptx::tma_load_5d(sa, hi ? &tmA : &lo.A, &full[stage], 0, x0, y0, 2 * kk, b + args.b_in);
 #pragma unroll
@@ -1145,69 +1197,46 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // MMA issuer (warp-collective; the hi/lo kind branch is per chunk, outside the MMA loops)
       constexpr bool kBf = std::is_same<T, __nv_bfloat16>::value;
-      constexpr uint32_t idesc = ptx::idesc_f16(128, BN, kBf);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
+      unsigned long long c_te = 0, c_full = 0, c_all = 0, t_start = clock64();
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
         const int acc = local & 1;
         // DYF: the epilogue zeroes every buffer and arrives once up front (real phases)
+        unsigned long long t0 = clock64();
         ptx::mbar_wait(&tempty[acc], DYF ? ((local >> 1) & 1) : (((local >> 1) & 1) ^ 1));
+        c_te += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + acc * R * BN;
         for (int kc = 0; kc < kiters; ++kc) {
+          t0 = clock64();
           ptx::mbar_wait(&full[stage], phase);
+          c_full += clock64() - t0;
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
-          const bool f8 = kc >= args.kchunks;  // F8 lo chunk: same smem image, kind::f8f6f4
-          if constexpr (DYF) {
-#pragma unroll
-            for (int dx = 0; dx < 3; ++dx) {
-              const uint32_t sbd = sa + S::kA + dx * 3 * S::kBt;
-#pragma unroll
-              for (int i = -1; i <= R; ++i) {
-                const int r_hi = i + 1 < R - 1 ? i + 1 : R - 1;
-                const int r_lo = i - 1 > 0 ? i - 1 : 0;
-                const int nrows = r_hi - r_lo + 1;
-                const int dy0 = i - r_hi + 1;
-                const uint32_t a0 = sa + (uint32_t)(((i + 1) * S::kPx + dx) * 16);
-                const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
-                const uint64_t db = ptx::smem_desc(sbd + dy0 * BN * 32, 8 * 32, 6u);
-                if (f8) {
-                  const uint32_t id8 = ptx::idesc_f8(128, nrows * BN);
-                  ptx::mma_f8(d_base + (R - 1 - r_hi) * BN, da, db, id8, 1u);
-                } else {
-                  const uint32_t id = nrows == 3 ? ptx::idesc_f16(128, 3 * BN, kBf)
-                                    : nrows == 2 ? ptx::idesc_f16(128, 2 * BN, kBf) : idesc;
-                  ptx::mma_f16(d_base + (R - 1 - r_hi) * BN, da, db, id, 1u);
-                }
-              }
-            }
+          if (args.dbg & 2) {
+          } else if (kc >= args.kchunks) {  // F8 lo chunk: same smem image, kind::f8f6f4
+            nz_mma_chunk<BN, R, DYF, true, kBf, S>(sa, d_base, kc);
           } else {
-#pragma unroll
-            for (int tap = 0; tap < 9; ++tap) {
-              const int dy = tap / 3, dx = tap % 3;
-              const uint64_t db = ptx::smem_desc(sa + S::kA + tap * S::kBt, 8 * 32, 6u);  // SW32, 8 rows x 32 B
-#pragma unroll
-              for (int r = 0; r < R; ++r) {
-                const uint32_t a0 = sa + (uint32_t)(((r + dy) * S::kPx + dx) * 16);
-                const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
-                if (f8)
-                  ptx::mma_f8(d_base + r * BN, da, db, ptx::idesc_f8(128, BN), 1u);
-                else
-                  ptx::mma_f16(d_base + r * BN, da, db, idesc, (kc | tap) != 0);
-              }
-            }
+            nz_mma_chunk<BN, R, DYF, false, kBf, S>(sa, d_base, kc);
           }
-          ptx::mma_commit(&empty[stage]);
+          ptx::mma_commit_w(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tfull[acc]);
+        ptx::mma_commit_w(&tfull[acc]);
+      }
+      c_all = clock64() - t_start;
+      if ((args.dbg & 8) && lane == 0) {
+        args.dbg_out[blockIdx.x * 4 + 0] = c_all;
+        args.dbg_out[blockIdx.x * 4 + 1] = c_te;
+        args.dbg_out[blockIdx.x * 4 + 2] = c_full;
+        args.dbg_out[blockIdx.x * 4 + 3] = local;
       }
     }
   } else if (warp >= 4) {
@@ -1285,7 +1314,12 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
         }
         const uint32_t taddr =
             tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (DYF ? (R - 1 - r) : r) * BN + c;
-        if constexpr (MODE == kHeadFused) {
+        if (args.dbg & 1) {
+          if constexpr (kRes) {
+            ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
+            es.rphase[slot] ^= 1;
+          }
+        } else if constexpr (MODE == kHeadFused) {
           epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs, s_w,
                           s_b, s_th, lf, oy, ox);
         } else {
