@@ -23,6 +23,8 @@ struct ConvPlan {
 
 // Plan one convolution: input [B][Hin][Win][Cin], weights [Cout][k][k][Cin] (16-bit,
 // K-major), fp32 bias; output grid Ho = ceil(Hin/stride) etc. `res` per ConvMode.
+// in_rc / res_rc / out_rc: tensors in the row-chunked layout [B][H][16-B chunk][W][16 B] (hi
+// chunks, then lo chunks) instead of NHWC; an RC input requires nz_eligible().
 // split_out: StoreKind of res/out. in_kind: StoreKind of the input; for x2 inputs the
 // caller passes Cin = 2 x channels and weights duplicated along K ([W | W]); for F8 inputs
 // Cin = channels, w = fp16 weights and w_lo = e5m2(W * 2^-6) bytes of the same layout.
@@ -31,7 +33,9 @@ struct ConvPlan {
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
                         const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
                         int split_out = 0, int B_in = -1, int B_res = -1, int B_out = -1, int in_kind = 0,
-                        const void* w_lo = nullptr);
+                        const void* w_lo = nullptr, int in_rc = 0, int res_rc = 0, int out_rc = 0);
+// The no-swizzle multi-row conv (the only reader of row-chunked inputs) applies to this shape.
+bool nz_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode);
 void set_conv_batch(ConvPlan& p, int B);
 void run_conv(const ConvPlan& p, cudaStream_t s);
 int num_sms();

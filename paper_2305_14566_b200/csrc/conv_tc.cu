@@ -174,9 +174,17 @@ int num_sms() {
   return n;
 }
 
+bool nz_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode) {
+  int bn = 256;
+  while (Cout % bn) bn >>= 1;
+  return k == 3 && stride == 1 && mode != kUpAdd && bn <= 64 && Cout == bn && Cin % 16 == 0 && Win >= 128 &&
+         Win % 128 == 0 && Hin % NzCfg::R(bn) == 0;
+}
+
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
                         const float* bias, int Cout, int k, int stride, int mode, const void* res, void* out,
-                        int split_out, int B_in, int B_res, int B_out, int in_kind, const void* w_lo) {
+                        int split_out, int B_in, int B_res, int B_out, int in_kind, const void* w_lo, int in_rc,
+                        int res_rc, int out_rc) {
   if (B_in < 0) B_in = B;
   if (B_res < 0) B_res = B;
   if (B_out < 0) B_out = B;
@@ -222,33 +230,35 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const CUtensorMapDataType d8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
   const void* in_lo = f8in ? static_cast<const uint8_t*>(in) + 2 * Cin : nullptr;
-  // no-swizzle multi-row variant (conv3_nz_kernel): 3x3 stride 1, width >= 128, N <= 64
-  if (k == 3 && stride == 1 && mode != kUpAdd && p.bn <= 64 && a.hb == 1 && Cout == p.bn && Cin % 16 == 0 &&
-      a.tiles_y % NzCfg::R(p.bn) == 0 && getenv("OMNISEG_NO_NZ") == nullptr) {
+  a.in_rc = in_rc;
+  a.res_rc = res_rc;
+  a.out_rc = out_rc;
+  {
+    const int Wout = mode == kUpAdd ? 2 * Wo : Wo;  // up-add: the full-resolution output
+    OS_REQUIRE(!out_rc || (Wout >= 128 && Wout % 128 == 0 && (mode != kUpAdd || (!res_rc && a.wb >= 32))),
+               "row-chunked output needs width >= 128 (up-add: NHWC skip)");
+  }
+  // no-swizzle multi-row variant (conv3_nz_kernel): 3x3 stride 1, width >= 128, N <= 64, and
+  // the input in the row-chunked layout (which only that kernel reads)
+  OS_REQUIRE(!in_rc || nz_eligible(Hin, Win, Cin, Cout, k, stride, mode), "row-chunked input needs the nz conv");
+  if (in_rc) {
     const int R = NzCfg::R(p.bn);
-    // A: 5-D view {8 ch, W, H, Cin/8, B} with the chunk dimension (16-B stride) outside the
-    // pixel dimensions, box {8, 130, R+2, 2, 1} -> smem [chunk][row][px][16 B]
-    cuuint64_t dims[5] = {8, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)(Cin / 8), (cuuint64_t)B_in};
-    cuuint64_t strides[4] = {in_px, (cuuint64_t)Win * in_px, 16, (cuuint64_t)Hin * Win * in_px};
-    cuuint32_t box[5] = {8, 130, (cuuint32_t)(R + 2), 2, 1};
+    // A: 5-D u8 view {128 B = 8 px of one chunk, W/8 units, chunk, H, B} of [B][H][chunk][W][16 B],
+    // box {128, 18, 2, R+2, 1} -> smem [row][chunk][144 px][16 B]
+    const uint64_t nch = in_px / 16;
+    cuuint64_t dims[5] = {128, (cuuint64_t)Win / 8, nch, (cuuint64_t)Hin, (cuuint64_t)B_in};
+    cuuint64_t strides[4] = {128, (cuuint64_t)Win * 16, nch * Win * 16, (cuuint64_t)Hin * nch * Win * 16};
+    cuuint32_t box[5] = {128, 18, 2, (cuuint32_t)(R + 2), 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    CUresult r = encode_fn()(&p.tmA, dt, 5, const_cast<void*>(in), dims, strides, box, es,
+    CUresult r = encode_fn()(&p.tmA, d8, 5, const_cast<void*>(in), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r == CUDA_SUCCESS && f8in) {
-      // lo: {16 e4m3, W, H, Cin/16, B}, the same 16-B core-matrix rows
-      cuuint64_t d2[5] = {16, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)(Cin / 16), (cuuint64_t)B_in};
-      cuuint32_t b2[5] = {16, 130, (cuuint32_t)(R + 2), 2, 1};
-      r = encode_fn()(&p.lo.A, d8, 5, const_cast<void*>(in_lo), d2, strides, b2, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    }
-    if (r == CUDA_SUCCESS) {
-      p.nz_R = R;
-      p.bk = 16;
-      a.kchunks = Cin / 16;
-      a.kch_lo = f8in ? Cin / 32 : 0;
-      a.tiles_y /= R;
-    }
+    if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(A rc) failed: " + std::to_string((int)r));
+    p.nz_R = R;
+    p.bk = 16;
+    a.kchunks = Cin / 16;
+    a.kch_lo = f8in ? Cin / 32 : 0;
+    a.tiles_y /= R;
   }
   // multi-row variant for 3x3 stride-1 convs with N <= 128 (see conv3_rows_kernel)
   if (p.nz_R == 0 && k == 3 && stride == 1 && mode != kUpAdd && p.bn <= 128 && (a.hb == 1 || a.hb == 2) &&
@@ -331,23 +341,49 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
                                                  std::to_string((int)r));
     };
     auto lo_of = [&](const void* base) { return static_cast<const void*>(static_cast<const uint8_t*>(base) + 2 * Cout); };
+    // row-chunked out / residual: 5-D u8 {128 B, W/8, chunk, H, B}; box = 32 (up-add: 64) pixels x the
+    // chunks of CH channels (hi; x2 lo: the same box at chunk Cout/8 + ..; F8 lo: CH/16 chunks)
+    auto enc_rc = [&](CUtensorMap* m, const void* base, int Wd, int Hd, int Bd, int px, int chunks, const char* what) {
+      const uint64_t nch = opx / 16;
+      // 128-B units of 8 pixels as the inner box dimension (16-B TMA rows are issue-limited)
+      cuuint64_t d5[5] = {128, (cuuint64_t)Wd / 8, nch, (cuuint64_t)Hd, (cuuint64_t)Bd};
+      cuuint64_t s5[4] = {128, (cuuint64_t)Wd * 16, nch * Wd * 16, (cuuint64_t)Hd * nch * Wd * 16};
+      cuuint32_t b5[5] = {128, (cuuint32_t)px / 8, (cuuint32_t)chunks, 1, 1};
+      cuuint32_t e5[5] = {1, 1, 1, 1, 1};
+      CUresult r = encode_fn()(m, d8, 5, const_cast<void*>(base), d5, s5, b5, e5, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(-2, std::string("cuTensorMapEncodeTiled(") + what + ") failed: " +
+                                                 std::to_string((int)r));
+    };
     if (mode == kUpAdd && a.wb >= 32) {
       // up-add: full-resolution skip / output, one box = 64 output pixels of one row
       cuuint64_t d2[4] = {(cuuint64_t)Cst, (cuuint64_t)(2 * Wo), (cuuint64_t)(2 * Ho), (cuuint64_t)B_out};
       cuuint64_t d2r[4] = {(cuuint64_t)Cst, (cuuint64_t)(2 * Wo), (cuuint64_t)(2 * Ho), (cuuint64_t)B_res};
       cuuint64_t st2[3] = {opx, 2ull * Wo * opx, 4ull * Ho * Wo * opx};
       cuuint32_t bx2[4] = {(cuuint32_t)CH, 64, 1, 1};
-      enc(&p.tmO, dt, out, d2, st2, bx2, sw, "up out");
-      enc(&p.tmR, dt, res, d2r, st2, bx2, sw, "up skip");
-      if (f8o) {
-        enc(&p.lo.O, d8, lo_of(out), d2, st2, bx2, swl, "up out lo");
-        enc(&p.lo.R, d8, lo_of(res), d2r, st2, bx2, swl, "up skip lo");
+      if (out_rc) {
+        enc_rc(&p.tmO, out, 2 * Wo, 2 * Ho, B_out, 64, CH / 8, "up out rc");
+        if (f8o) enc_rc(&p.lo.O, out, 2 * Wo, 2 * Ho, B_out, 64, CH / 16, "up out lo rc");
+      } else {
+        enc(&p.tmO, dt, out, d2, st2, bx2, sw, "up out");
+        if (f8o) enc(&p.lo.O, d8, lo_of(out), d2, st2, bx2, swl, "up out lo");
       }
+      enc(&p.tmR, dt, res, d2r, st2, bx2, sw, "up skip");
+      if (f8o) enc(&p.lo.R, d8, lo_of(res), d2r, st2, bx2, swl, "up skip lo");
     }
     if (mode != kUpAdd) {
-      enc(&p.tmO, dt, out, dims, strides, box, sw, "out");
-      if (f8o) enc(&p.lo.O, d8, lo_of(out), dims, strides, box, swl, "out lo");
-      if (res) {
+      if (out_rc) {
+        enc_rc(&p.tmO, out, Wo, Ho, B_out, 32, CH / 8, "out rc");
+        if (f8o) enc_rc(&p.lo.O, out, Wo, Ho, B_out, 32, CH / 16, "out lo rc");
+      } else {
+        enc(&p.tmO, dt, out, dims, strides, box, sw, "out");
+        if (f8o) enc(&p.lo.O, d8, lo_of(out), dims, strides, box, swl, "out lo");
+      }
+      if (res && res_rc) {
+        enc_rc(&p.tmR, res, Wo, Ho, B_res, 32, CH / 8, "res rc");
+        if (f8o) enc_rc(&p.lo.R, res, Wo, Ho, B_res, 32, CH / 16, "res lo rc");
+      } else if (res) {
         enc(&p.tmR, dt, res, dims_r, strides, box, sw, "res");
         if (f8o) enc(&p.lo.R, d8, lo_of(res), dims_r, strides, box, swl, "res lo");
       } else {

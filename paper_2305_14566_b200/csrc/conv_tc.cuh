@@ -63,6 +63,9 @@ struct ConvArgs {
   // batch-index offsets of the tensors (a launch over images [0, B) of the work space reads
   // input image b + b_in, residual b + b_res, writes b + b_out, head tile b + b_head)
   int b_in, b_res, b_out, b_head;
+  // row-chunked (RC) layout flags of the input / residual / output tensors: [B][H][chunk][W][16 B]
+  // with the 16-B chunks of a pixel in the order hi chunks, then lo chunks; else NHWC
+  int in_rc, res_rc, out_rc;
   int dbg;  // experiments only (OMNISEG_DBG, conv3_nz_kernel): 1 skip epilogue math/stores, 2 skip MMAs, 4 skip loads,
             // 8 record MMA-warp cycle counters into dbg_out[blockIdx.x][4]
   unsigned long long* dbg_out;
@@ -237,10 +240,25 @@ struct EpiState {
   uint64_t* rbar;       // this warp's 2 residual mbarriers (double-buffered prefetch)
   uint32_t rphase[2];
   int res_base = 2;     // buffer index of residual slot 0 (0 when the warp has no out buffers)
+  int res_rc = 0;       // residual / output tensors in the row-chunked layout (see ConvArgs)
+  int out_rc = 0;
 };
 
-// Issue the TMA loads of one residual chunk into buffer slot `slot` (lane 0).
-// F8: the lo part comes from the fp8 map tmR2 (CH bytes per row).
+// smem image offsets of one warp box (32 pixels x CH channels). NHWC boxes are 64-B (CH = 32)
+// / 32-B (CH = 16) swizzled pixel rows; row-chunked (RC) boxes are [16-B chunk][32 px][16 B].
+// j16: index of a 16-bit 8-channel unit; j8: index of an e4m3 16-channel unit.
+template <int CH>
+__device__ __forceinline__ uint32_t off16(int rc, int px, int j16) {
+  return rc ? (uint32_t)(j16 * 512 + px * 16) : EpiTile<CH>::off(px, j16);
+}
+template <int CH>
+__device__ __forceinline__ uint32_t off8(int rc, int px, int j8) {
+  return rc ? (uint32_t)(j8 * 512 + px * 16) : lo_off<CH>(px, j8);
+}
+
+// Issue the TMA loads of one residual chunk into buffer slot `slot` (lane 0). F8: the lo part
+// comes from the e4m3 map tmR2. RC: 5-D maps {128 B = 8 px, W/8, chunk, H, B}; the chunks of channels
+// [n0, n0 + CH) are n0/8.. (hi), C/8 + n0/8.. (x2 lo) and C/8 + n0/16.. (F8 lo).
 template <int CH>
 __device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUtensorMap* tmR, const CUtensorMap* tmR2,
                                               int n0, int Cout, int split, int xb, int yb, int b, uint32_t lane) {
@@ -249,6 +267,14 @@ __device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUte
     uint8_t* hi = es.buf + (es.res_base + 2 * slot) * E::kBuf;
     const uint32_t tx = split == kStoreF8 ? E::kBuf + 32 * CH : (split ? 2 : 1) * E::kBuf;
     ptx::mbar_arrive_expect_tx(&es.rbar[slot], tx);
+    if (es.res_rc) {
+      ptx::tma_load_5d(hi, tmR, &es.rbar[slot], 0, xb / 8, n0 / 8, yb, b);
+      if (split == kStoreF8)
+        ptx::tma_load_5d(hi + E::kBuf, tmR2, &es.rbar[slot], 0, xb / 8, Cout / 8 + n0 / 16, yb, b);
+      else if (split)
+        ptx::tma_load_5d(hi + E::kBuf, tmR, &es.rbar[slot], 0, xb / 8, Cout / 8 + n0 / 8, yb, b);
+      return;
+    }
     ptx::tma_load_4d(hi, tmR, &es.rbar[slot], n0, xb, yb, b);
     if (split == kStoreF8)
       ptx::tma_load_4d(hi + E::kBuf, tmR2, &es.rbar[slot], n0, xb, yb, b);
@@ -277,11 +303,13 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
 #pragma unroll
   for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(bias + n0 + j);
   if constexpr (kRes) {
+    const int rc = es.res_rc;
     ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
     es.rphase[slot] ^= 1;
     if (split == kStoreF8) {
 #pragma unroll
-      for (int j = 0; j < CH / 16; ++j) add_f8_16(v + 16 * j, *reinterpret_cast<const uint4*>(res_lo + lo_off<CH>(lane, j)));
+      for (int j = 0; j < CH / 16; ++j)
+        add_f8_16(v + 16 * j, *reinterpret_cast<const uint4*>(res_lo + off8<CH>(rc, lane, j)));
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -289,7 +317,7 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
       const uint8_t* rb = h ? res_lo : res_hi;
 #pragma unroll
       for (int j = 0; j < CH / 8; ++j) {
-        const uint4 rv = *reinterpret_cast<const uint4*>(rb + E::off(lane, j));
+        const uint4 rv = *reinterpret_cast<const uint4*>(rb + off16<CH>(rc, lane, j));
         const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -307,14 +335,14 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
   }
 }
 
-// One CH-wide chunk: values -> 16-bit (hi, + lo in x2) -> swizzled STS -> TMA store.
+// One CH-wide chunk: values -> 16-bit (hi, + lo in x2 / F8) -> STS -> TMA store.
 template <typename T, int CH, int MODE>
 __device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensorMap* tmO, const CUtensorMap* tmO2,
                                           uint32_t taddr, const float* bias, int n0, int Cout, int split, int xb,
                                           int yb, int b, uint32_t lane) {
-  using E = EpiTile<CH>;
   uint8_t* out_hi = es.buf;
-  uint8_t* out_lo = es.buf + E::kBuf;
+  uint8_t* out_lo = es.buf + EpiTile<CH>::kBuf;
+  const int rc = es.out_rc;
   float v[CH];
   epi_values<T, CH, MODE>(es, slot, taddr, bias, n0, split, lane, v);
   if (lane == 0) ptx::bulk_wait_read0();  // previous stores of this warp done reading smem
@@ -324,40 +352,44 @@ __device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensor
     for (int j = 0; j < CH / 16; ++j) {
       uint4 h0, h1, lo;
       split_f8_16(v + 16 * j, h0, h1, lo);
-      *reinterpret_cast<uint4*>(out_hi + E::off(lane, 2 * j)) = h0;
-      *reinterpret_cast<uint4*>(out_hi + E::off(lane, 2 * j + 1)) = h1;
-      *reinterpret_cast<uint4*>(out_lo + lo_off<CH>(lane, j)) = lo;
+      *reinterpret_cast<uint4*>(out_hi + off16<CH>(rc, lane, 2 * j)) = h0;
+      *reinterpret_cast<uint4*>(out_hi + off16<CH>(rc, lane, 2 * j + 1)) = h1;
+      *reinterpret_cast<uint4*>(out_lo + off8<CH>(rc, lane, j)) = lo;
     }
-    ptx::fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) {
-      ptx::tma_store_4d(tmO, out_hi, n0, xb, yb, b);
-      ptx::tma_store_4d(tmO2, out_lo, n0, xb, yb, b);
-      ptx::bulk_commit();
-    }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int j = 0; j < CH / 8; ++j) {
-    uint32_t o[4];
+    for (int j = 0; j < CH / 8; ++j) {
+      uint32_t o[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) o[e] = StoreT<T>::pack(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
-    *reinterpret_cast<uint4*>(out_hi + E::off(lane, j)) = make_uint4(o[0], o[1], o[2], o[3]);
-    if (split) {
-      uint32_t l[4];
+      for (int e = 0; e < 4; ++e) o[e] = StoreT<T>::pack(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(out_hi + off16<CH>(rc, lane, j)) = make_uint4(o[0], o[1], o[2], o[3]);
+      if (split) {
+        uint32_t l[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 hv = StoreT<T>::unpack(o[e]);
-        l[e] = StoreT<T>::pack(v[8 * j + 2 * e] - hv.x, v[8 * j + 2 * e + 1] - hv.y);
+        for (int e = 0; e < 4; ++e) {
+          const float2 hv = StoreT<T>::unpack(o[e]);
+          l[e] = StoreT<T>::pack(v[8 * j + 2 * e] - hv.x, v[8 * j + 2 * e + 1] - hv.y);
+        }
+        *reinterpret_cast<uint4*>(out_lo + off16<CH>(rc, lane, j)) = make_uint4(l[0], l[1], l[2], l[3]);
       }
-      *reinterpret_cast<uint4*>(out_lo + E::off(lane, j)) = make_uint4(l[0], l[1], l[2], l[3]);
     }
   }
   ptx::fence_proxy_async();
   __syncwarp();
   if (lane == 0) {
-    ptx::tma_store_4d(tmO, out_hi, n0, xb, yb, b);
-    if (split) ptx::tma_store_4d(tmO, out_lo, Cout + n0, xb, yb, b);
+    if (rc) {
+      ptx::tma_store_5d(tmO, out_hi, 0, xb / 8, n0 / 8, yb, b);
+      if (split == kStoreF8)
+        ptx::tma_store_5d(tmO2, out_lo, 0, xb / 8, Cout / 8 + n0 / 16, yb, b);
+      else if (split)
+        ptx::tma_store_5d(tmO, out_lo, 0, xb / 8, Cout / 8 + n0 / 8, yb, b);
+    } else {
+      ptx::tma_store_4d(tmO, out_hi, n0, xb, yb, b);
+      if (split == kStoreF8)
+        ptx::tma_store_4d(tmO2, out_lo, n0, xb, yb, b);
+      else if (split)
+        ptx::tma_store_4d(tmO, out_lo, Cout + n0, xb, yb, b);
+    }
     ptx::bulk_commit();
   }
 }
@@ -612,7 +644,7 @@ __global__ void __launch_bounds__(256, 1)
     const int row = q * 32 + lane;        // M row = pixel within the tile
     const int py = row / args.wb, px = row - (row / args.wb) * args.wb;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * (S::kEpiBytes / 4), &rbar[2 * q], {0, 0}};
+    EpiState es{smem + S::kEpiOff + q * (S::kEpiBytes / 4), &rbar[2 * q], {0, 0}, 2, args.res_rc, args.out_rc};
     const int bw = args.wb < 32 ? args.wb : 32;
     const int box_dx = (q * 32) % args.wb, box_dy = (q * 32) / args.wb;
     (void)bw;
@@ -661,8 +693,27 @@ __global__ void __launch_bounds__(256, 1)
             uint8_t* sk_lo = es.buf + kUB;
             uint8_t* o_hi = es.buf + 2 * kUB;
             uint8_t* o_lo = es.buf + 3 * kUB;
-#pragma unroll 1
             const bool f8 = args.split == kStoreF8;
+            const int orc = args.out_rc;  // RC output: [chunk][64 px][16 B] boxes; the skip stays NHWC
+            auto oo16 = [&](int rr, int j) { return orc ? (uint32_t)(j * 1024 + rr * 16) : E::off(rr, j); };
+            auto oo8 = [&](int rr, int j) { return orc ? (uint32_t)(j * 1024 + rr * 16) : lo_off<CH>(rr, j); };
+            auto ostore = [&](int ox, int oyy) {
+              if (orc) {
+                ptx::tma_store_5d(&tmO, o_hi, 0, ox / 8, n0 / 8, oyy, b + args.b_out);
+                if (f8)
+                  ptx::tma_store_5d(&lo.O, o_lo, 0, ox / 8, args.Cout / 8 + n0 / 16, oyy, b + args.b_out);
+                else if (args.split)
+                  ptx::tma_store_5d(&tmO, o_lo, 0, ox / 8, args.Cout / 8 + n0 / 8, oyy, b + args.b_out);
+              } else {
+                ptx::tma_store_4d(&tmO, o_hi, n0, ox, oyy, b + args.b_out);
+                if (f8)
+                  ptx::tma_store_4d(&lo.O, o_lo, n0, ox, oyy, b + args.b_out);
+                else if (args.split)
+                  ptx::tma_store_4d(&tmO, o_lo, args.Cout + n0, ox, oyy, b + args.b_out);
+              }
+              ptx::bulk_commit();
+            };
+#pragma unroll 1
             for (int a = 0; a < 2; ++a) {
               const int ox = 2 * xb, oyy = 2 * yb + a;
               if (lane == 0) {
@@ -698,18 +749,14 @@ __global__ void __launch_bounds__(256, 1)
                     add_f8_16(x + 16 * j, *reinterpret_cast<const uint4*>(sk_lo + lo_off<CH>(rr, j)));
                     uint4 h0, h1, l4;
                     split_f8_16(x + 16 * j, h0, h1, l4);
-                    *reinterpret_cast<uint4*>(o_hi + E::off(rr, 2 * j)) = h0;
-                    *reinterpret_cast<uint4*>(o_hi + E::off(rr, 2 * j + 1)) = h1;
-                    *reinterpret_cast<uint4*>(o_lo + lo_off<CH>(rr, j)) = l4;
+                    *reinterpret_cast<uint4*>(o_hi + oo16(rr, 2 * j)) = h0;
+                    *reinterpret_cast<uint4*>(o_hi + oo16(rr, 2 * j + 1)) = h1;
+                    *reinterpret_cast<uint4*>(o_lo + oo8(rr, j)) = l4;
                   }
                 }
                 ptx::fence_proxy_async();
                 __syncwarp();
-                if (lane == 0) {
-                  ptx::tma_store_4d(&tmO, o_hi, n0, ox, oyy, b + args.b_out);
-                  ptx::tma_store_4d(&lo.O, o_lo, n0, ox, oyy, b + args.b_out);
-                  ptx::bulk_commit();
-                }
+                if (lane == 0) ostore(ox, oyy);
                 continue;
               }
 #pragma unroll
@@ -731,17 +778,13 @@ __global__ void __launch_bounds__(256, 1)
                     const float2 hv = StoreT<T>::unpack(o[e]);
                     l[e] = StoreT<T>::pack(x0 - hv.x, x1 - hv.y);
                   }
-                  *reinterpret_cast<uint4*>(o_hi + E::off(rr, j)) = make_uint4(o[0], o[1], o[2], o[3]);
-                  if (args.split) *reinterpret_cast<uint4*>(o_lo + E::off(rr, j)) = make_uint4(l[0], l[1], l[2], l[3]);
+                  *reinterpret_cast<uint4*>(o_hi + oo16(rr, j)) = make_uint4(o[0], o[1], o[2], o[3]);
+                  if (args.split) *reinterpret_cast<uint4*>(o_lo + oo16(rr, j)) = make_uint4(l[0], l[1], l[2], l[3]);
                 }
               }
               ptx::fence_proxy_async();
               __syncwarp();
-              if (lane == 0) {
-                ptx::tma_store_4d(&tmO, o_hi, n0, ox, oyy, b + args.b_out);
-                if (args.split) ptx::tma_store_4d(&tmO, o_lo, args.Cout + n0, ox, oyy, b + args.b_out);
-                ptx::bulk_commit();
-              }
+              if (lane == 0) ostore(ox, oyy);
             }
           } else {
             const size_t W2 = 2 * (size_t)args.Wo;
@@ -972,7 +1015,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}};
+    EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}, 2, args.res_rc, args.out_rc};
     const int box_dx = (q * 32) % WB, box_dy = (q * 32) / WB;
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
@@ -1020,18 +1063,23 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-// Multi-row 3x3 stride-1 kernel with a NO-SWIZZLE A operand (image width >= 128, N <= 64):
-// per 16-channel K chunk one 5-D TMA box brings (R+2) input rows x 130 pixels (the x halo
-// included, OOB zero-filled) into smem as [8-ch chunk][row][pixel][16 B]. In the K-major
-// no-swizzle UMMA layout every pixel is one 16-B core-matrix row, so the operand of block
-// r, tap (dy, dx) simply starts ((r+dy)*130 + dx)*16 B into the box: all 9 taps of all R
-// blocks come from one load (~(R+2)/R input reads per output instead of 9). Weights: 9
-// per-tap SW32 boxes per chunk, shared by the R blocks.
+// Multi-row 3x3 stride-1 kernel with a NO-SWIZZLE A operand (image width >= 128, N <= 64).
+// The input is in the row-chunked (RC) layout [B][H][16-B chunk][W][16 B], so one image row
+// of one chunk is W*16 contiguous bytes. Per 32-byte K step (two chunks) one 5-D TMA box
+// {128 B = 8 px, 18 units, 2 chunks, R+2 rows, 1} brings the (R+2) input rows x 144 pixels
+// [x0 - 8, x0 + 136) (OOB zero-filled = the conv padding) into smem as [row][chunk][144 px]
+// [16 B] -- 128-B TMA rows (a 16-B inner box dimension is limited to 16 B per cycle per SM,
+// measured). In the K-major no-swizzle UMMA layout every pixel is one 16-B core-matrix row,
+// so the operand of block r, tap (dy, dx) starts at row r+dy, pixel 7+dx of the box (LBO =
+// the chunk plane): all 9 taps of all R blocks come from one load (~(R+2)/R input reads per
+// output). Weights: 9 per-tap SW32 boxes per chunk, shared by the R blocks.
 template <int BN, int R, int STAGES, bool DYF = false, int EW = 4, bool HEAD = false>
 struct NzSmem {
-  static constexpr int kPx = 130;
-  static constexpr int kChunkStride = (R + 2) * kPx * 16;                 // LBO of the A operand
-  static constexpr int kA = ((2 * kChunkStride + 1023) / 1024) * 1024;  // two 8-ch chunks (K = 16)
+  static constexpr int kPx = 144;                                   // 18 units of 8 pixels
+  static constexpr int kChunkStride = kPx * 16;                      // LBO of the A operand
+  static constexpr int kRowStride = 2 * kChunkStride;                // two chunks (K = 32 B) per row
+  static constexpr int kABytes = (R + 2) * kRowStride;
+  static constexpr int kA = ((kABytes + 1023) / 1024) * 1024;
   // one tap's BN x 16-channel weight tile (SW32); the dy-stacked variant packs the three dy
   // tiles of one dx back to back, so they must be exactly BN*32 bytes apart
   static constexpr int kBt = DYF ? BN * 32 : ((BN * 32 + 1023) / 1024) * 1024;
@@ -1049,9 +1097,11 @@ struct NzSmem {
 };
 
 struct NzCfg {
-  static constexpr int R(int bn) { return 256 / bn; }
+  // R output rows per work item: 2 R BN = 512 TMEM columns (two accumulator buffers), at most 8
+  // rows (the (R+2)-row input box must leave room for >= 2 ring stages)
+  static constexpr int R(int bn) { return 256 / bn < 8 ? 256 / bn : 8; }
   static constexpr int stage_bytes(int bn) {
-    return ((2 * (R(bn) + 2) * 130 * 16 + 1023) / 1024) * 1024 + 9 * (((bn * 32 + 1023) / 1024) * 1024);
+    return (((R(bn) + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + 9 * (((bn * 32 + 1023) / 1024) * 1024);
   }
   // ring depth from what the epilogue (ew warps; head: residual slots only) leaves of 227 KB
   static constexpr int STAGES(int bn, int ew = 4, bool head = false) {
@@ -1076,7 +1126,7 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
         const int r_lo = i - 1 > 0 ? i - 1 : 0;
         const int nrows = r_hi - r_lo + 1;
         const int dy0 = i - r_hi + 1;
-        const uint32_t a0 = sa + (uint32_t)(((i + 1) * S::kPx + dx) * 16);
+        const uint32_t a0 = sa + (uint32_t)((i + 1) * S::kRowStride + (7 + dx) * 16);
         const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
         const uint64_t db = ptx::smem_desc(sbd + dy0 * BN * 32, 8 * 32, 6u);
         if constexpr (F8)
@@ -1092,7 +1142,7 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
       const uint64_t db = ptx::smem_desc(sa + S::kA + tap * S::kBt, 8 * 32, 6u);  // SW32, 8 rows x 32 B
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const uint32_t a0 = sa + (uint32_t)(((r + dy) * S::kPx + dx) * 16);
+        const uint32_t a0 = sa + (uint32_t)((r + dy) * S::kRowStride + (7 + dx) * 16);
         const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
         if constexpr (F8)
           ptx::mma_f8_w(d_base + r * BN, da, db, ptx::idesc_f8(128, BN), 1u);
@@ -1153,7 +1203,7 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
   const uint32_t tmem_base = *tmem_slot;
   // 32-byte K chunks: kchunks hi chunks (16 fp16 channels), then kch_lo F8 lo chunks (32 e4m3)
   const int kiters = args.kchunks + args.kch_lo;
-  constexpr uint32_t kTx = 2 * S::kChunkStride + 9 * BN * 32;
+  constexpr uint32_t kTx = S::kABytes + 9 * BN * 32;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1166,7 +1216,7 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
         m /= args.tiles_x;
         const int tyg = m % args.tiles_y;
         const int b = m / args.tiles_y;
-        const int x0 = tx * 128 - 1;
+        const int u0 = tx * 16 - 1;  // first 8-pixel unit of the box (pixels [x0 - 8, x0 + 136))
         const int y0 = tyg * R - 1;
         for (int kc = 0; kc < kiters; ++kc) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -1182,7 +1232,8 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
             continue;
           }
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          ptx::tma_load_5d(sa, hi ? &tmA : &lo.A, &full[stage], 0, x0, y0, 2 * kk, b + args.b_in);
+          // chunks 2kc, 2kc+1 of the RC input: hi chunks first, then (F8) the lo chunks
+          ptx::tma_load_5d(sa, &tmA, &full[stage], 0, u0, 2 * kc, y0, b + args.b_in);
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const int slot = DYF ? (tap % 3) * 3 + tap / 3 : tap;  // DYF: [dx][dy] order
@@ -1245,7 +1296,8 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
     constexpr int NH = EW / 4;         // warps per quadrant (they alternate rows)
     const int half = ew / 4;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + ew * S::kWarpEpi, &rbar[2 * ew], {0, 0}, MODE == kHeadFused ? 0 : 2};
+    EpiState es{smem + S::kEpiOff + ew * S::kWarpEpi, &rbar[2 * ew], {0, 0}, MODE == kHeadFused ? 0 : 2, args.res_rc,
+                args.out_rc};
     float* s_th = reinterpret_cast<float*>(smem + S::kHeadOff);
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;

@@ -649,33 +649,51 @@ __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uin
 }
 
 // ------------------------------------------------------------------ conversions (debug / weights)
+// Byte offset of byte o of pixel r's channel data (pb bytes per pixel) in NHWC, or in the
+// row-chunked layout [B][H][16-B chunk][W][16 B] (rc_w = W > 0; conv_tc.cuh ConvArgs).
+__device__ __forceinline__ int64_t act_byte(int64_t r, int o, int pb, int rc_w) {
+  if (rc_w <= 0) return r * pb + o;
+  return (r / rc_w) * (int64_t)pb * rc_w + (int64_t)(o >> 4) * rc_w * 16 + (r % rc_w) * 16 + (o & 15);
+}
 template <typename T>
-__global__ void f32_to_t_kernel(const float* in, T* out, int64_t rows, int cin, int cpad, int split) {
+__global__ void f32_to_t_kernel(const float* in, T* out, int64_t rows, int cin, int cpad, int split, int rc_w) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * cpad) return;
   const int64_t r = i / cpad;
   const int c = i % cpad;
   const float v = c < cin ? in[r * cin + c] : 0.f;
   const T hi = T(v);
+  uint8_t* o8 = reinterpret_cast<uint8_t*>(out);
   if (split == 2) {
-    uint8_t* px = reinterpret_cast<uint8_t*>(out) + r * 3 * cpad;
     const __half h = __float2half_rn(v);
-    *reinterpret_cast<__half*>(px + 2 * c) = h;
-    px[2 * cpad + c] = (uint8_t)__nv_cvt_float_to_fp8((v - __half2float(h)) * 64.0f, __NV_SATFINITE, __NV_E4M3);
+    *reinterpret_cast<__half*>(o8 + act_byte(r, 2 * c, 3 * cpad, rc_w)) = h;
+    o8[act_byte(r, 2 * cpad + c, 3 * cpad, rc_w)] =
+        (uint8_t)__nv_cvt_float_to_fp8((v - __half2float(h)) * 64.0f, __NV_SATFINITE, __NV_E4M3);
   } else if (split) {
-    out[r * 2 * cpad + c] = hi;
-    out[r * 2 * cpad + cpad + c] = T(v - float(hi));
+    *reinterpret_cast<T*>(o8 + act_byte(r, 2 * c, 4 * cpad, rc_w)) = hi;
+    *reinterpret_cast<T*>(o8 + act_byte(r, 2 * cpad + 2 * c, 4 * cpad, rc_w)) = T(v - float(hi));
   } else {
-    out[i] = hi;
+    *reinterpret_cast<T*>(o8 + act_byte(r, 2 * c, 2 * cpad, rc_w)) = hi;
   }
 }
 template <typename T>
-__global__ void t_to_f32_kernel(const T* in, float* out, int64_t rows, int cout, int cpad, int split) {
+__global__ void t_to_f32_kernel(const T* in, float* out, int64_t rows, int cout, int cpad, int split, int rc_w) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * cout) return;
   const int64_t r = i / cout;
   const int c = i % cout;
-  out[i] = act_value(in, r, c, cpad, split);
+  const uint8_t* b8 = reinterpret_cast<const uint8_t*>(in);
+  float v;
+  if (split == 2) {
+    v = __half2float(*reinterpret_cast<const __half*>(b8 + act_byte(r, 2 * c, 3 * cpad, rc_w))) +
+        f8lo(b8[act_byte(r, 2 * cpad + c, 3 * cpad, rc_w)]);
+  } else if (split) {
+    v = float(*reinterpret_cast<const T*>(b8 + act_byte(r, 2 * c, 4 * cpad, rc_w))) +
+        float(*reinterpret_cast<const T*>(b8 + act_byte(r, 2 * cpad + 2 * c, 4 * cpad, rc_w)));
+  } else {
+    v = float(*reinterpret_cast<const T*>(b8 + act_byte(r, 2 * c, 2 * cpad, rc_w)));
+  }
+  out[i] = v;
 }
 
 // ==================================================================== host launchers
@@ -752,14 +770,14 @@ void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask,
   finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area);
 }
 template <typename T>
-void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, cudaStream_t s) {
+void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, int rc_w, cudaStream_t s) {
   int64_t n = rows * cpad;
-  f32_to_t_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cin, cpad, split);
+  f32_to_t_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cin, cpad, split, rc_w);
 }
 template <typename T>
-void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, int split, cudaStream_t s) {
+void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, int split, int rc_w, cudaStream_t s) {
   int64_t n = rows * cout;
-  t_to_f32_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cout, cpad, split);
+  t_to_f32_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, rows, cout, cpad, split, rc_w);
 }
 
 #define OS_INST(T)                                                                                                 \
@@ -770,8 +788,8 @@ void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, 
   template void launch_head<T>(const T*, int, int, int, int, int, const float*, const float*, const float*, int,        \
                                const uint32_t*, int, const HeadTaskTable&, int, int, int, int, float*, float*,     \
                                cudaStream_t);                                                                     \
-  template void launch_f32_to_t<T>(const float*, T*, int64_t, int, int, int, cudaStream_t);                       \
-  template void launch_t_to_f32<T>(const T*, float*, int64_t, int, int, int, cudaStream_t);
+  template void launch_f32_to_t<T>(const float*, T*, int64_t, int, int, int, int, cudaStream_t);                  \
+  template void launch_t_to_f32<T>(const T*, float*, int64_t, int, int, int, int, cudaStream_t);
 OS_INST(__half)
 OS_INST(__nv_bfloat16)
 

@@ -45,9 +45,9 @@ void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const fl
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area,
                      cudaStream_t s);
 template <typename T>
-void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, cudaStream_t s);
+void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, int rc_w, cudaStream_t s);
 template <typename T>
-void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, int split, cudaStream_t s);
+void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, int split, int rc_w, cudaStream_t s);
 
 // conv_tc.cu
 struct ConvPlan;  // opaque per-layer plan (TMA maps + launch config)

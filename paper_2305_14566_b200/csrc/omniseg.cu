@@ -193,6 +193,7 @@ struct omniseg {
   int ws_P = 0, ws_B = 0;
   DevBuf X0;
   std::vector<LevelBufs> lv;
+  std::vector<int> rc;  // per level: A_l / Bt_l stored row-chunked (see ensure_workspace)
   DevBuf g, theta, task_cls, task_scl;
   // plans in launch order for one batch (rebuilt with the workspace)
   struct Step {
@@ -423,38 +424,52 @@ void ensure_workspace(omniseg* h, int P) {
   h->dec_plans.clear();
   h->enc_layers.clear();
   h->dec_layers.clear();
+  // Tensor layouts. Per level l: A_l (stem / down / up output = the RB input
+  // and residual), Bt_l (conv_a output) and E_l (RB output: skip, down input; in the decoder
+  // E_l then receives D_l, the next up-conv's input). A_l and Bt_l are read only by the 3x3
+  // convs of their level: where those run the no-swizzle multi-row kernel (levels of width
+  // >= 128 and <= 64 channels) they are stored row-chunked (RC) for its 128-B TMA rows; E_l
+  // and every other tensor are NHWC.
+  h->rc.assign(L, 0);
+  for (int l = 0; l < L; ++l)
+    h->rc[l] = nz_eligible(P >> l, P >> l, h->enc_a[l].cinp, h->enc_a[l].coutp, 3, 1, kReluBias) &&
+               nz_eligible(P >> l, P >> l, h->enc_b[l].cinp, h->enc_b[l].coutp, 3, 1, kResidualRelu) &&
+               getenv("OMNISEG_NO_NZ") == nullptr;
   // out_level: U-Net level of the output (and residual / skip) tensor
-  auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int out_level) {
+  auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int out_level,
+                  int in_rc, int res_rc, int out_rc) {
     return make_conv_plan(bf, in, B, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
-                          res, out, ar.sp(out_level), -1, -1, -1, ly.in_kind, ly.wlo.p);
+                          res, out, ar.sp(out_level), -1, -1, -1, ly.in_kind, ly.wlo.p, in_rc, res_rc, out_rc);
   };
-  auto enc = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol) {
-    h->enc_plans.push_back(plan(ly, in, Hin, res, out, mode, ol));
+  auto enc = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol, int irc,
+                 int rrc, int orc) {
+    h->enc_plans.push_back(plan(ly, in, Hin, res, out, mode, ol, irc, rrc, orc));
     h->enc_layers.push_back(&ly);
   };
-  auto dec = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol) {
-    h->dec_plans.push_back(plan(ly, in, Hin, res, out, mode, ol));
+  auto dec = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol, int irc,
+                 int rrc, int orc) {
+    h->dec_plans.push_back(plan(ly, in, Hin, res, out, mode, ol, irc, rrc, orc));
     h->dec_layers.push_back(&ly);
   };
-  enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias, 0);
+  const auto& rc = h->rc;
+  enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias, 0, 0, 0, rc[0]);
   for (int l = 0; l < L; ++l) {
     LevelBufs& q = h->lv[l];
-    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000);
-    enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l);
-    if (l < L - 1) enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias, l + 1);
+    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000, rc[l], 0, rc[l]);
+    enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], 0);
+    if (l < L - 1) enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias, l + 1, 0, 0, rc[l + 1]);
   }
   for (int l = L - 2; l >= 0; --l) {
     LevelBufs& q = h->lv[l];
-    const void* D = (l + 1 == L - 1) ? h->lv[l + 1].E.p : h->lv[l + 1].A.p;
-    dec(h->up[l], D, q.P / 2, q.E.p, q.A.p, kUpAdd, l);
-    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000);
-    dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.A.p, kResidualRelu, l);
+    dec(h->up[l], h->lv[l + 1].E.p, q.P / 2, q.E.p, q.A.p, kUpAdd, l, 0, 0, rc[l]);
+    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000, rc[l], 0, rc[l]);
+    dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], 0);
   }
   // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
   h->head_fusable = false;
-  if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr) {
+  if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr && rc[0]) {
     LevelBufs& q = h->lv[0];
-    ConvPlan hp = plan(h->dec_b[0], q.Bt.p, q.P, q.A.p, q.A.p, kHeadFused, 0);
+    ConvPlan hp = plan(h->dec_b[0], q.Bt.p, q.P, q.A.p, q.E.p, kHeadFused, 0, rc[0], rc[0], 0);
     if (hp.nz_R > 0 && hp.bn == h->Cp[0] && h->C[0] <= 32) {
       h->head_plan = hp;
       h->head_fusable = true;
@@ -613,7 +628,7 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
     h->conv_launches++;
   }
   if (!head_done) {
-    launch_head<T>(h->lv[0].A.as<T>(), n, h->Cp[0], h->C[0], h->arch.sp(0), P, h->Wpre.as<float>(),
+    launch_head<T>(h->lv[0].E.as<T>(), n, h->Cp[0], h->C[0], h->arch.sp(0), P, h->Wpre.as<float>(),
                    h->bpre.as<float>(), h->theta.as<float>(), ntasks, tiles, first, tt, S, Hp, Wp, pad, out_p, out_F, s);
     h->launches++;
   }
@@ -1093,8 +1108,11 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
                        int Cout, int k, int stride, const float* r, int mode, float* y) {
   try {
     OS_REQUIRE(h && x && w && b && y, "debug_conv: NULL argument");
-    // mode | 16: x2 storage of input / residual / output; mode | 32: f8 storage
+    // mode | 16: x2 storage of input / residual / output; mode | 32: f8 storage; mode | 64:
+    // residual (not an up-add skip) and output row-chunked. The input is row-chunked exactly
+    // when the no-swizzle multi-row kernel applies (its only layout).
     const int split = (mode & 32) ? kStoreF8 : (mode & 16) ? kStoreX2 : kStorePlain;
+    const bool orc_req = (mode & 64) != 0;
     mode &= 15;
     OS_REQUIRE(mode >= 0 && mode <= 3, "debug_conv: bad mode");
     OS_REQUIRE((mode != 1 && mode != 2) || r, "debug_conv: mode needs r");
@@ -1126,21 +1144,28 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
     }
     out.ensure(rows_out * coutp * bpc);
     f32o.ensure(rows_out * Cout * 4);
+    const int in_rc = nz_eligible(H, W, cinp * sm, coutp, k, stride, mode) ? 1 : 0;
+    const int out_rc = orc_req && ow >= 128 && ow % 128 == 0 ? 1 : 0;
+    const int res_rc = out_rc && mode != 2 ? 1 : 0;
     if (bf) {
-      launch_f32_to_t<__nv_bfloat16>(f32in.as<float>(), xin.as<__nv_bfloat16>(), rows_in, Cin, cinp, split, s);
+      launch_f32_to_t<__nv_bfloat16>(f32in.as<float>(), xin.as<__nv_bfloat16>(), rows_in, Cin, cinp, split,
+                                     in_rc ? W : 0, s);
       if (r)
-        launch_f32_to_t<__nv_bfloat16>(f32r.as<float>(), rin.as<__nv_bfloat16>(), rows_out, Cout, coutp, split, s);
+        launch_f32_to_t<__nv_bfloat16>(f32r.as<float>(), rin.as<__nv_bfloat16>(), rows_out, Cout, coutp, split,
+                                       res_rc ? ow : 0, s);
     } else {
-      launch_f32_to_t<__half>(f32in.as<float>(), xin.as<__half>(), rows_in, Cin, cinp, split, s);
-      if (r) launch_f32_to_t<__half>(f32r.as<float>(), rin.as<__half>(), rows_out, Cout, coutp, split, s);
+      launch_f32_to_t<__half>(f32in.as<float>(), xin.as<__half>(), rows_in, Cin, cinp, split, in_rc ? W : 0, s);
+      if (r)
+        launch_f32_to_t<__half>(f32r.as<float>(), rin.as<__half>(), rows_out, Cout, coutp, split, res_rc ? ow : 0, s);
     }
     ConvPlan p = make_conv_plan(bf, xin.p, B, H, W, cinp * sm, L.w.p, L.b.as<float>(), coutp, k, stride, mode,
-                                r ? rin.p : nullptr, out.p, split, -1, -1, -1, split, L.wlo.p);
+                                r ? rin.p : nullptr, out.p, split, -1, -1, -1, split, L.wlo.p, in_rc, res_rc, out_rc);
     run_conv(p, s);
     if (bf)
-      launch_t_to_f32<__nv_bfloat16>(out.as<__nv_bfloat16>(), f32o.as<float>(), rows_out, Cout, coutp, split, s);
+      launch_t_to_f32<__nv_bfloat16>(out.as<__nv_bfloat16>(), f32o.as<float>(), rows_out, Cout, coutp, split,
+                                     out_rc ? ow : 0, s);
     else
-      launch_t_to_f32<__half>(out.as<__half>(), f32o.as<float>(), rows_out, Cout, coutp, split, s);
+      launch_t_to_f32<__half>(out.as<__half>(), f32o.as<float>(), rows_out, Cout, coutp, split, out_rc ? ow : 0, s);
     OS_CUDA(cudaMemcpyAsync(y, f32o.p, rows_out * Cout * 4, cudaMemcpyDeviceToHost, s));
     OS_CUDA(cudaStreamSynchronize(s));
     return 0;

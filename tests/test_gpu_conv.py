@@ -112,7 +112,24 @@ def _e5m2_lo_weights(w):
     return t.to(torch.float8_e5m2).to(torch.float64).numpy() * 64.0
 
 
-def _run(h, B, H, W, Cin, Cout, k, stride, mode, split):
+RC_CASES = [
+    (1, 128, 128, 32, 32, 3, 1, 1),   # nz, row-chunked residual + output
+    (2, 128, 128, 64, 64, 3, 1, 0),
+    (1, 256, 256, 32, 64, 3, 2, 0),   # stride-2 per-tap, row-chunked output (the down convs)
+    (1, 64, 64, 64, 32, 1, 1, 2),     # up-add, row-chunked output, NHWC skip
+    (1, 128, 128, 32, 32, 1, 1, 0),   # 1x1 per-tap (the stem), row-chunked output
+]
+
+
+@pytest.mark.parametrize("split", [False, "x2", "f8"])
+@pytest.mark.parametrize("B,H,W,Cin,Cout,k,stride,mode", RC_CASES)
+def test_conv_parity_row_chunked(h, B, H, W, Cin, Cout, k, stride, mode, split):
+    """Row-chunked residual / output layout ([B][H][16-B chunk][W][16 B]): the same
+    values as NHWC, for every storage kind."""
+    _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=True)
+
+
+def _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=False):
     rng = np.random.default_rng(B * 1000 + H + Cin + Cout + k + stride + mode)
     x = rng.standard_normal((B, H, W, Cin)) if split else _f16(rng.standard_normal((B, H, W, Cin)))
     w = _f16(rng.standard_normal((Cout, k, k, Cin)) * np.sqrt(2.0 / (k * k * Cin)))
@@ -142,7 +159,7 @@ def _run(h, B, H, W, Cin, Cout, k, stride, mode, split):
             ref = rs + np.stack([nn.up2(p) for p in pre])
         else:
             ref = pre if rs is None else pre + rs
-        got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split)
+        got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split, rc=rc)
         ref_abs = _ref(np.abs(x), np.abs(w), np.abs(b), stride, None if r is None else np.abs(r),
                        3 if mode != 2 else 2)
         bound = 2.0 ** -18 * np.abs(ref_abs) + 2.0 ** -14 * np.abs(ref) + 2.0 ** -15
@@ -151,7 +168,7 @@ def _run(h, B, H, W, Cin, Cout, k, stride, mode, split):
         assert (err <= bound).all(), f"max err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"
         return
     ref = _ref(x, w, b, stride, r, mode)
-    got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split)
+    got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split, rc=rc)
     err = np.abs(got - ref)
     if split:
         # fp32 accumulation over K terms: |err| <= K eps32 sum|terms| (worst case); use the
