@@ -15,6 +15,7 @@ struct ConvPlan {
   int bn, bk, stages, mode, grid;
   int rows_R = 0;        // > 0: the multi-row 3x3 kernel (conv3_rows_kernel) with R blocks
   int nz_R = 0;          // > 0: the no-swizzle multi-row 3x3 kernel (conv3_nz_kernel)
+  int s2_R = 0;          // > 0: the stride-2 row-chunked-input kernel (conv3s2_rc_kernel)
   int hb = 1;
   bool bf16;
   HeadArgs head{};       // kHead mode (fused dynamic head + stitch), set by the caller per launch
@@ -36,6 +37,8 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
                         const void* w_lo = nullptr, int in_rc = 0, int res_rc = 0, int out_rc = 0);
 // The no-swizzle multi-row conv (the only reader of row-chunked inputs) applies to this shape.
 bool nz_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode);
+// The stride-2 kernel over a row-chunked input (conv3s2_rc_kernel) applies to this shape.
+bool s2_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode);
 void set_conv_batch(ConvPlan& p, int B);
 void run_conv(const ConvPlan& p, cudaStream_t s);
 int num_sms();

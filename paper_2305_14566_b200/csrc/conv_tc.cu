@@ -40,19 +40,19 @@ CUtensorMapSwizzle swz(int bytes) {
   return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
 }
 
-template <typename T, int BN, int BK>
+template <typename T, int BN, int BK, bool UP>
 struct Cfg {
-  static constexpr int kStageBytes = ConvSmem<BN, BK, 1>::kStage;
-  static constexpr int kStages0 = kStageBudgetTap / kStageBytes;
+  static constexpr int kStageBytes = ConvSmem<BN, BK, 1, UP>::kStage;
+  static constexpr int kStages0 = (UP ? kStageBudgetTapUp : kStageBudgetTap) / kStageBytes;
   static constexpr int STAGES = kStages0 > 8 ? 8 : (kStages0 < 2 ? 2 : kStages0);
-  using Smem = ConvSmem<BN, BK, STAGES>;
+  using Smem = ConvSmem<BN, BK, STAGES, UP>;
 };
 
 template <typename T, int BN, int BK>
 void launch_tpl(const ConvPlan& p, cudaStream_t s) {
-  using C = Cfg<T, BN, BK>;
-  constexpr int smem = C::Smem::kTotal;
-  auto launch_mode = [&](auto kern) {
+  using C = Cfg<T, BN, BK, false>;
+  using CU = Cfg<T, BN, BK, true>;
+  auto launch_mode = [&](auto kern, int smem) {
     // all instantiations share one function-pointer type: remember each kernel separately
     static std::mutex mu;
     static std::unordered_set<const void*> done;
@@ -61,13 +61,14 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
+    kern<<<p.grid, p.mode == kUpAdd ? 384 : 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
   };
+  constexpr int sm = C::Smem::kTotal, smu = CU::Smem::kTotal;
   switch (p.mode) {
-    case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kReluBias>); break;
-    case kResidualRelu: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kResidualRelu>); break;
-    case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kUpAdd>); break;
-    default: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kBias>); break;
+    case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kReluBias>, sm); break;
+    case kResidualRelu: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kResidualRelu>, sm); break;
+    case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, CU::STAGES, kUpAdd>, smu); break;
+    default: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kBias>, sm); break;
   }
 }
 
@@ -128,8 +129,27 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   }
 }
 
+template <typename T, int BN>
+void launch_s2(const ConvPlan& p, cudaStream_t s) {
+  constexpr int R = S2Cfg::R(BN);
+  constexpr int ST = S2Cfg::STAGES(BN);
+  static_assert(ST >= 2, "stride-2 tile does not fit shared memory");
+  constexpr int smem = S2Smem<BN, R, ST>::kTotal;
+  auto kern = conv3s2_rc_kernel<T, BN, R, ST>;
+  static std::once_flag once;
+  std::call_once(once, [&] { OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); });
+  kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.args, p.lo);
+}
+
 template <typename T>
 void dispatch(const ConvPlan& p, cudaStream_t s) {
+  if (p.s2_R > 0) {
+    if (p.bn == 16) return launch_s2<T, 16>(p, s);
+    if (p.bn == 32) return launch_s2<T, 32>(p, s);
+    if (p.bn == 64) return launch_s2<T, 64>(p, s);
+    if (p.bn == 128) return launch_s2<T, 128>(p, s);
+    throw Error(-1, "unsupported stride-2 conv shape");
+  }
   if (p.mode == kHeadFused && p.nz_R == 0) throw Error(-1, "fused head needs the no-swizzle conv kernel");
   if (p.nz_R > 0) {
     static const bool dyf = getenv("OMNISEG_NO_DYF") == nullptr;
@@ -157,7 +177,7 @@ void dispatch(const ConvPlan& p, cudaStream_t s) {
   throw Error(-1, "unsupported conv tile shape");
 }
 
-int stages_for(int bn, int bk) {
+int stages_for(int bn, int bk) {  // informational (ConvPlan::stages): the non-up-add ring depth
   const int a = 128 * bk * 2, b = ((bn * bk * 2 + 1023) / 1024) * 1024;
   int st = kStageBudgetTap / (a + b);
   return st > 8 ? 8 : (st < 2 ? 2 : st);
@@ -172,6 +192,13 @@ int num_sms() {
     OS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   }
   return n;
+}
+
+bool s2_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode) {
+  int bn = 256;
+  while (Cout % bn) bn >>= 1;
+  return k == 3 && stride == 2 && mode == kReluBias && bn <= 128 && bn >= 16 && Cout == bn && Cin % 16 == 0 &&
+         Win % 128 == 0 && Hin % 2 == 0 && (Hin / 2) % S2Cfg::R(bn) == 0;
 }
 
 bool nz_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode) {
@@ -235,13 +262,35 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.out_rc = out_rc;
   {
     const int Wout = mode == kUpAdd ? 2 * Wo : Wo;  // up-add: the full-resolution output
-    OS_REQUIRE(!out_rc || (Wout >= 128 && Wout % 128 == 0 && (mode != kUpAdd || (!res_rc && a.wb >= 32))),
-               "row-chunked output needs width >= 128 (up-add: NHWC skip)");
+    OS_REQUIRE(!out_rc || (Wout >= 128 && Wout % 128 == 0 && (mode != kUpAdd || a.wb >= 32)),
+               "row-chunked output needs width >= 128");
+    OS_REQUIRE(!res_rc || (Wout >= 128 && Wout % 128 == 0 && (mode != kUpAdd || a.wb >= 32)),
+               "row-chunked residual / skip needs width >= 128");
   }
   // no-swizzle multi-row variant (conv3_nz_kernel): 3x3 stride 1, width >= 128, N <= 64, and
   // the input in the row-chunked layout (which only that kernel reads)
-  OS_REQUIRE(!in_rc || nz_eligible(Hin, Win, Cin, Cout, k, stride, mode), "row-chunked input needs the nz conv");
-  if (in_rc) {
+  OS_REQUIRE(!in_rc || nz_eligible(Hin, Win, Cin, Cout, k, stride, mode) ||
+                 s2_eligible(Hin, Win, Cin, Cout, k, stride, mode),
+             "row-chunked input needs the nz / stride-2 row-chunked conv");
+  if (in_rc && stride == 2) {
+    // stride-2 kernel: the same RC view, box {128, 18, 2, 2R+1, 1}; 128 input px -> 64 output px
+    const int R = S2Cfg::R(p.bn);
+    const uint64_t nch = in_px / 16;
+    cuuint64_t dims[5] = {128, (cuuint64_t)Win / 8, nch, (cuuint64_t)Hin, (cuuint64_t)B_in};
+    cuuint64_t strides[4] = {128, (cuuint64_t)Win * 16, nch * Win * 16, (cuuint64_t)Hin * nch * Win * 16};
+    cuuint32_t box[5] = {128, 18, 2, (cuuint32_t)(2 * R + 1), 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode_fn()(&p.tmA, d8, 5, const_cast<void*>(in), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(A rc s2) failed: " + std::to_string((int)r));
+    p.s2_R = R;
+    p.bk = 16;
+    a.kchunks = Cin / 16;
+    a.kch_lo = f8in ? Cin / 32 : 0;
+    a.tiles_x = Win / 128;
+    a.tiles_y = Ho / R;
+  } else if (in_rc) {
     const int R = NzCfg::R(p.bn);
     // A: 5-D u8 view {128 B = 8 px of one chunk, W/8 units, chunk, H, B} of [B][H][chunk][W][16 B],
     // box {128, 18, 2, R+2, 1} -> smem [row][chunk][144 px][16 B]
@@ -274,14 +323,14 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
       a.tiles_y /= R;
     }
   }
-  OS_REQUIRE(!f8in || p.nz_R > 0 || p.bk >= 32, "F8 input needs K chunks of >= 32 channels");
+  OS_REQUIRE(!f8in || p.nz_R > 0 || p.s2_R > 0 || p.bk >= 32, "F8 input needs K chunks of >= 32 channels");
   a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
   if (const char* d = getenv("OMNISEG_DBG")) a.dbg = atoi(d);
   a.bias = bias;
   a.res = res;
   a.out = out;
   a.split = split_out;
-  if (p.nz_R == 0) {
+  if (p.nz_R == 0 && p.s2_R == 0) {
     cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B_in};
     cuuint64_t strides[3] = {in_px, (cuuint64_t)Win * in_px, (cuuint64_t)Hin * Win * in_px};
     cuuint32_t box[4] = {(cuuint32_t)p.bk, (cuuint32_t)(a.wb * stride), (cuuint32_t)(a.hb * stride), 1};
@@ -309,7 +358,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
     if (f8in) {
       // lo weights: e5m2 bytes [Cout][taps*Cin]; a lo chunk is bk (nz: 32) bytes wide
-      const int bkl = p.nz_R > 0 ? 32 : p.bk;
+      const int bkl = (p.nz_R > 0 || p.s2_R > 0) ? 32 : p.bk;
       cuuint64_t s1[1] = {(cuuint64_t)taps * Cin};
       cuuint32_t b1[2] = {(cuuint32_t)bkl, (cuuint32_t)p.bn};
       r = encode_fn()(&p.lo.B, d8, 2, const_cast<void*>(w_lo), dims, s1, b1, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -325,7 +374,8 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     const bool f8o = split_out == kStoreF8;
     const int Cst = split_out == kStoreX2 ? 2 * Cout : Cout;
     const uint64_t opx = f8o ? 3ull * Cout : 2ull * Cst;
-    const int bw = a.wb < 32 ? a.wb : 32, bh = 32 / bw;
+    int bw = a.wb < 32 ? a.wb : 32, bh = 32 / bw;
+    if (p.s2_R > 0) bw = 16, bh = 1;  // stride-2 RC kernel: a warp stores 16 output pixels
     cuuint64_t dims[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B_out};
     cuuint64_t dims_r[4] = {(cuuint64_t)Cst, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)B_res};
     cuuint64_t strides[3] = {opx, (cuuint64_t)Wo * opx, (cuuint64_t)Ho * Wo * opx};
@@ -369,13 +419,18 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
         enc(&p.tmO, dt, out, d2, st2, bx2, sw, "up out");
         if (f8o) enc(&p.lo.O, d8, lo_of(out), d2, st2, bx2, swl, "up out lo");
       }
-      enc(&p.tmR, dt, res, d2r, st2, bx2, sw, "up skip");
-      if (f8o) enc(&p.lo.R, d8, lo_of(res), d2r, st2, bx2, swl, "up skip lo");
+      if (res_rc) {
+        enc_rc(&p.tmR, res, 2 * Wo, 2 * Ho, B_res, 64, CH / 8, "up skip rc");
+        if (f8o) enc_rc(&p.lo.R, res, 2 * Wo, 2 * Ho, B_res, 64, CH / 16, "up skip lo rc");
+      } else {
+        enc(&p.tmR, dt, res, d2r, st2, bx2, sw, "up skip");
+        if (f8o) enc(&p.lo.R, d8, lo_of(res), d2r, st2, bx2, swl, "up skip lo");
+      }
     }
     if (mode != kUpAdd) {
       if (out_rc) {
-        enc_rc(&p.tmO, out, Wo, Ho, B_out, 32, CH / 8, "out rc");
-        if (f8o) enc_rc(&p.lo.O, out, Wo, Ho, B_out, 32, CH / 16, "out lo rc");
+        enc_rc(&p.tmO, out, Wo, Ho, B_out, bw, CH / 8, "out rc");
+        if (f8o) enc_rc(&p.lo.O, out, Wo, Ho, B_out, bw, CH / 16, "out lo rc");
       } else {
         enc(&p.tmO, dt, out, dims, strides, box, sw, "out");
         if (f8o) enc(&p.lo.O, d8, lo_of(out), dims, strides, box, swl, "out lo");
@@ -391,7 +446,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
       }
     }
   }
-  p.stages = (p.rows_R > 0 || p.nz_R > 0) ? 0 : stages_for(p.bn, p.bk);
+  p.stages = (p.rows_R > 0 || p.nz_R > 0 || p.s2_R > 0) ? 0 : stages_for(p.bn, p.bk);
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
   p.flops = 2.0 * (double)B * Ho * Wo * Cout * (double)k * k * Cin;
   p.hb = a.hb;

@@ -490,17 +490,19 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
   }
 }
 
-template <int BN, int BK, int STAGES>
+template <int BN, int BK, int STAGES, bool UP = false>
 struct ConvSmem {
   static constexpr int kA = 128 * BK * 2;
   static constexpr int kB = ((BN * BK * 2 + 1023) / 1024) * 1024;
   static constexpr int kStage = kA + kB;
-  static constexpr int kBars = (2 * STAGES + 12) * 8 + 16;
+  static constexpr int kBars = (2 * STAGES + 4 + 16) * 8 + 16;  // full/empty, tfull/tempty, 2 x 8 epilogue warps
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // epilogue smem: the TMA epilogue tiles, or the up-add tiles (4 x 64 rows x CH ch per warp)
   static constexpr int kCH = BN < 32 ? BN : 32;
-  static constexpr int kUpBytes = 4 * 4 * 64 * kCH * 2;
-  static constexpr int kEpiBytes = EpiTile<kCH>::kBytes > kUpBytes ? EpiTile<kCH>::kBytes : kUpBytes;
+  // up-add: 8 epilogue warps x 2 slots x (skip hi, skip lo) 64-pixel buffers, the output
+  // computed in place over the skip
+  static constexpr int kUpBytes = 8 * 4 * 64 * kCH * 2;
+  static constexpr int kEpiBytes = UP ? kUpBytes : EpiTile<kCH>::kBytes;
   static constexpr int kTotal = kEpiOff + kEpiBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                                           : (2 * BN <= 256) ? 256 : 512;
@@ -511,11 +513,11 @@ struct ConvSmem {
 };
 
 template <typename T, int BN, int BK, int STAGES, int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(MODE == kUpAdd ? 384 : 256, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                    const ConvArgs args, const __grid_constant__ LoMaps lo) {
-  using S = ConvSmem<BN, BK, STAGES>;
+  using S = ConvSmem<BN, BK, STAGES, MODE == kUpAdd>;
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
@@ -523,8 +525,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;  // 8 residual barriers (two per epilogue warp)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 8);
+  // epilogue warps: 8 for the up-add (a pair per TMEM lane quadrant, one per output row), else 4
+  constexpr int EW = MODE == kUpAdd ? 8 : 4;
+  uint64_t* rbar = tempty + 2;  // two residual / skip barriers per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * EW);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -538,9 +542,9 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 128);
+      ptx::mbar_init(&tempty[a], 32 * EW);
     }
-    for (int a = 0; a < 8; ++a) ptx::mbar_init(&rbar[a], 1);
+    for (int a = 0; a < 2 * EW; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -641,13 +645,50 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int q = warp & 3;               // TMEM lane quadrant of this warp
+    const int ew = warp - 4, half = ew >> 2;
     const int row = q * 32 + lane;        // M row = pixel within the tile
     const int py = row / args.wb, px = row - (row / args.wb) * args.wb;
     constexpr int CH = BN < 32 ? BN : 32;
-    EpiState es{smem + S::kEpiOff + q * (S::kEpiBytes / 4), &rbar[2 * q], {0, 0}, 2, args.res_rc, args.out_rc};
+    EpiState es{smem + S::kEpiOff + ew * (S::kEpiBytes / EW), &rbar[2 * ew], {0, 0}, 2, args.res_rc, args.out_rc};
     const int bw = args.wb < 32 ? args.wb : 32;
     const int box_dx = (q * 32) % args.wb, box_dy = (q * 32) / args.wb;
     (void)bw;
+    // up-add (TMA path): the skip rows are double-buffered ACROSS work items (slot k & 1 holds the
+    // k-th load of this warp) so their HBM latency overlaps the previous row's math and stores
+    int up_k = 0;
+    auto up_issue = [&](int slot, int w2, int c2, int a2) {
+      if (lane != 0) return;
+      constexpr int kUB = 64 * CH * 2;
+      const bool f8 = args.split == kStoreF8;
+      const int nt2 = w2 % args.n_tiles_n;
+      int m2 = w2 / args.n_tiles_n;
+      const int tx2 = m2 % args.tiles_x;
+      m2 /= args.tiles_x;
+      const int ty2 = m2 % args.tiles_y;
+      const int b2 = m2 / args.tiles_y + args.b_res;
+      const int ox = 2 * (tx2 * args.wb + box_dx), oyy = 2 * (ty2 * args.hb + box_dy) + a2;
+      const int n0 = nt2 * BN + c2;
+      uint8_t* sk_hi = es.buf + 2 * slot * kUB;
+      uint8_t* sk_lo = sk_hi + kUB;
+      ptx::bulk_wait_read0();  // the store computed in place in this slot two steps ago has read it
+      ptx::mbar_arrive_expect_tx(&es.rbar[slot], f8 ? kUB + kUB / 2 : (args.split ? 2 : 1) * kUB);
+      if (args.res_rc) {
+        ptx::tma_load_5d(sk_hi, &tmR, &es.rbar[slot], 0, ox / 8, n0 / 8, oyy, b2);
+        if (f8)
+          ptx::tma_load_5d(sk_lo, &lo.R, &es.rbar[slot], 0, ox / 8, args.Cout / 8 + n0 / 16, oyy, b2);
+        else if (args.split)
+          ptx::tma_load_5d(sk_lo, &tmR, &es.rbar[slot], 0, ox / 8, args.Cout / 8 + n0 / 8, oyy, b2);
+      } else {
+        ptx::tma_load_4d(sk_hi, &tmR, &es.rbar[slot], n0, ox, oyy, b2);
+        if (f8)
+          ptx::tma_load_4d(sk_lo, &lo.R, &es.rbar[slot], n0, ox, oyy, b2);
+        else if (args.split)
+          ptx::tma_load_4d(sk_lo, &tmR, &es.rbar[slot], args.Cout + n0, ox, oyy, b2);
+      }
+    };
+    if constexpr (MODE == kUpAdd) {
+      if (args.wb >= 32 && (int)blockIdx.x < args.num_work) up_issue(0, blockIdx.x, 0, half);
+    }
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -659,12 +700,12 @@ __global__ void __launch_bounds__(256, 1)
       const int ty = m % args.tiles_y;
       const int b = m / args.tiles_y;
       const int y = ty * args.hb + py, x = tx * args.wb + px;
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
       constexpr bool kRes = MODE == kResidualRelu;
       const int xb = tx * args.wb + box_dx, yb = ty * args.hb + box_dy;
       if constexpr (kRes)
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, yb, b + args.b_res, lane);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < BN; c += CH) {
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
@@ -688,16 +729,15 @@ __global__ void __launch_bounds__(256, 1)
           if (args.wb >= 32) {
             // TMA path: the warp's 32 low-res pixels (one row) -> two output rows of 64 pixels
             using E = EpiTile<CH>;
-            constexpr int kUB = 64 * CH * 2;  // one 64-row buffer
-            uint8_t* sk_hi = es.buf;
-            uint8_t* sk_lo = es.buf + kUB;
-            uint8_t* o_hi = es.buf + 2 * kUB;
-            uint8_t* o_lo = es.buf + 3 * kUB;
+            constexpr int kUB = 64 * CH * 2;  // one 64-row buffer; 2 slots x (skip hi, skip lo)
             const bool f8 = args.split == kStoreF8;
             const int orc = args.out_rc;  // RC output: [chunk][64 px][16 B] boxes; the skip stays NHWC
             auto oo16 = [&](int rr, int j) { return orc ? (uint32_t)(j * 1024 + rr * 16) : E::off(rr, j); };
             auto oo8 = [&](int rr, int j) { return orc ? (uint32_t)(j * 1024 + rr * 16) : lo_off<CH>(rr, j); };
-            auto ostore = [&](int ox, int oyy) {
+            const int src = args.res_rc;  // RC skip: [chunk][64 px][16 B]
+            auto so16 = [&](int rr, int j) { return src ? (uint32_t)(j * 1024 + rr * 16) : E::off(rr, j); };
+            auto so8 = [&](int rr, int j) { return src ? (uint32_t)(j * 1024 + rr * 16) : lo_off<CH>(rr, j); };
+            auto ostore = [&](const uint8_t* o_hi, const uint8_t* o_lo, int ox, int oyy) {
               if (orc) {
                 ptx::tma_store_5d(&tmO, o_hi, 0, ox / 8, n0 / 8, oyy, b + args.b_out);
                 if (f8)
@@ -713,80 +753,87 @@ __global__ void __launch_bounds__(256, 1)
               }
               ptx::bulk_commit();
             };
-#pragma unroll 1
-            for (int a = 0; a < 2; ++a) {
+            {
+              // this warp's output row a = half; the skip of this (item, chunk) was issued one
+              // step ahead into slot up_k & 1: issue the next one (next chunk / item) now. The
+              // output is computed in place over the skip buffer and stored from there.
+              const int a = half;
               const int ox = 2 * xb, oyy = 2 * yb + a;
-              if (lane == 0) {
-                ptx::mbar_arrive_expect_tx(&es.rbar[0], f8 ? kUB + kUB / 2 : (args.split ? 2 : 1) * kUB);
-                ptx::tma_load_4d(sk_hi, &tmR, &es.rbar[0], n0, ox, oyy, b + args.b_res);
-                if (f8)
-                  ptx::tma_load_4d(sk_lo, &lo.R, &es.rbar[0], n0, ox, oyy, b + args.b_res);
-                else if (args.split)
-                  ptx::tma_load_4d(sk_lo, &tmR, &es.rbar[0], args.Cout + n0, ox, oyy, b + args.b_res);
+              const int slot = up_k & 1;
+              {
+                int w2 = w, c2 = c + CH;
+                if (c2 >= BN) c2 = 0, w2 += gridDim.x;
+                if (w2 < args.num_work) up_issue(slot ^ 1, w2, c2, a);
               }
-              ptx::mbar_wait(&es.rbar[0], es.rphase[0]);
-              es.rphase[0] ^= 1;
-              if (lane == 0) ptx::bulk_wait_read0();
-              __syncwarp();
-              if (f8) {
-#pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) {
-                  const int rr = 2 * (int)lane + q2;
-                  float x[CH];
-#pragma unroll
-                  for (int j = 0; j < CH / 8; ++j) {
-                    const uint4 h4 = *reinterpret_cast<const uint4*>(sk_hi + E::off(rr, j));
-                    const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                      const float2 fh = StoreT<T>::unpack(hh[e]);
-                      x[8 * j + 2 * e] = fh.x + v[8 * j + 2 * e];
-                      x[8 * j + 2 * e + 1] = fh.y + v[8 * j + 2 * e + 1];
-                    }
-                  }
-#pragma unroll
-                  for (int j = 0; j < CH / 16; ++j) {
-                    add_f8_16(x + 16 * j, *reinterpret_cast<const uint4*>(sk_lo + lo_off<CH>(rr, j)));
-                    uint4 h0, h1, l4;
-                    split_f8_16(x + 16 * j, h0, h1, l4);
-                    *reinterpret_cast<uint4*>(o_hi + oo16(rr, 2 * j)) = h0;
-                    *reinterpret_cast<uint4*>(o_hi + oo16(rr, 2 * j + 1)) = h1;
-                    *reinterpret_cast<uint4*>(o_lo + oo8(rr, j)) = l4;
-                  }
-                }
-                ptx::fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) ostore(ox, oyy);
-                continue;
-              }
+              ++up_k;
+              uint8_t* sk_hi = es.buf + 2 * slot * kUB;
+              uint8_t* sk_lo = sk_hi + kUB;
+              uint8_t* o_hi = sk_hi;
+              uint8_t* o_lo = sk_lo;
+              ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
+              es.rphase[slot] ^= 1;
+              // phase 1: skip + up-sampled conv value for the lane's two output pixels (all
+              // reads of the slot complete before phase 2 overwrites it in place -- the skip
+              // and output layouts may differ)
+              float x[2][CH];
 #pragma unroll
               for (int q2 = 0; q2 < 2; ++q2) {
                 const int rr = 2 * (int)lane + q2;
 #pragma unroll
                 for (int j = 0; j < CH / 8; ++j) {
-                  const uint4 h4 = *reinterpret_cast<const uint4*>(sk_hi + E::off(rr, j));
+                  const uint4 h4 = *reinterpret_cast<const uint4*>(sk_hi + so16(rr, j));
                   uint4 l4 = make_uint4(0, 0, 0, 0);
-                  if (args.split) l4 = *reinterpret_cast<const uint4*>(sk_lo + E::off(rr, j));
+                  if (args.split == kStoreX2) l4 = *reinterpret_cast<const uint4*>(sk_lo + so16(rr, j));
                   const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
-                  uint32_t o[4], l[4];
 #pragma unroll
                   for (int e = 0; e < 4; ++e) {
                     const float2 fh = StoreT<T>::unpack(hh[e]);
                     const float2 fl = StoreT<T>::unpack(ll[e]);
-                    const float x0 = fh.x + fl.x + v[8 * j + 2 * e], x1 = fh.y + fl.y + v[8 * j + 2 * e + 1];
-                    o[e] = StoreT<T>::pack(x0, x1);
-                    const float2 hv = StoreT<T>::unpack(o[e]);
-                    l[e] = StoreT<T>::pack(x0 - hv.x, x1 - hv.y);
+                    x[q2][8 * j + 2 * e] = fh.x + fl.x + v[8 * j + 2 * e];
+                    x[q2][8 * j + 2 * e + 1] = fh.y + fl.y + v[8 * j + 2 * e + 1];
                   }
-                  *reinterpret_cast<uint4*>(o_hi + oo16(rr, j)) = make_uint4(o[0], o[1], o[2], o[3]);
-                  if (args.split) *reinterpret_cast<uint4*>(o_lo + oo16(rr, j)) = make_uint4(l[0], l[1], l[2], l[3]);
+                }
+                if (f8) {
+#pragma unroll
+                  for (int j = 0; j < CH / 16; ++j)
+                    add_f8_16(x[q2] + 16 * j, *reinterpret_cast<const uint4*>(sk_lo + so8(rr, j)));
+                }
+              }
+              __syncwarp();
+              // phase 2: round to the storage kind and write in the output layout
+#pragma unroll
+              for (int q2 = 0; q2 < 2; ++q2) {
+                const int rr = 2 * (int)lane + q2;
+                if (f8) {
+#pragma unroll
+                  for (int j = 0; j < CH / 16; ++j) {
+                    uint4 h0, h1, l4;
+                    split_f8_16(x[q2] + 16 * j, h0, h1, l4);
+                    *reinterpret_cast<uint4*>(o_hi + oo16(rr, 2 * j)) = h0;
+                    *reinterpret_cast<uint4*>(o_hi + oo16(rr, 2 * j + 1)) = h1;
+                    *reinterpret_cast<uint4*>(o_lo + oo8(rr, j)) = l4;
+                  }
+                } else {
+#pragma unroll
+                  for (int j = 0; j < CH / 8; ++j) {
+                    uint32_t o[4], l[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                      const float x0 = x[q2][8 * j + 2 * e], x1 = x[q2][8 * j + 2 * e + 1];
+                      o[e] = StoreT<T>::pack(x0, x1);
+                      const float2 hv = StoreT<T>::unpack(o[e]);
+                      l[e] = StoreT<T>::pack(x0 - hv.x, x1 - hv.y);
+                    }
+                    *reinterpret_cast<uint4*>(o_hi + oo16(rr, j)) = make_uint4(o[0], o[1], o[2], o[3]);
+                    if (args.split) *reinterpret_cast<uint4*>(o_lo + oo16(rr, j)) = make_uint4(l[0], l[1], l[2], l[3]);
+                  }
                 }
               }
               ptx::fence_proxy_async();
               __syncwarp();
-              if (lane == 0) ostore(ox, oyy);
+              if (lane == 0) ostore(o_hi, o_lo, ox, oyy);
             }
-          } else {
+          } else if (half == 0) {
             const size_t W2 = 2 * (size_t)args.Wo;
 #pragma unroll 1
             for (int a = 0; a < 4; ++a) {
@@ -833,7 +880,8 @@ __global__ void __launch_bounds__(256, 1)
 // accumulator buffers fill the 512 TMEM columns), the largest K chunk giving >= 3 stages in
 // 200 KB of shared memory (else 16 with >= 2 stages).
 constexpr int kStageBudget = 168 * 1024;     // smem for the operand ring (the TMA epilogue takes 48 KB)
-constexpr int kStageBudgetTap = 156 * 1024;  // per-tap kernel (its up-add epilogue takes 64 KB)
+constexpr int kStageBudgetTap = 168 * 1024;    // per-tap kernel (its TMA epilogue takes 48 KB)
+constexpr int kStageBudgetTapUp = 96 * 1024;   // per-tap up-add kernel (its epilogue takes 128 KB)
 
 struct RowsCfg {
   static constexpr int stage_bytes(int bn, int bk, int r, int hb) {
@@ -1026,14 +1074,14 @@ __global__ void __launch_bounds__(256, 1)
       m /= args.tiles_x;
       const int tyg = m % args.tiles_y;
       const int b = m / args.tiles_y;
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ptx::tc_fence_after();
       constexpr bool kRes = MODE == kResidualRelu;
       constexpr int NC = BN / CH;
       const int xb = tx * WB + box_dx;
       const int yb0 = tyg * R * HB + box_dy;
       if constexpr (kRes)
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, yb0, b + args.b_res, lane);
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
 #pragma unroll 1
       for (int i = 0; i < R * NC; ++i) {
         const int r = i / NC, c = (i - r * NC) * CH;
@@ -1345,14 +1393,15 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
           ox = min((int)(id & 0x7FFF) * hargs.S, hargs.Wp / f - hargs.P);
         }
       }
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ptx::tc_fence_after();
       constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
       constexpr int NC = BN / CH;
       const int xb = tx * 128 + q * 32;
       constexpr int RM = R / NH;  // rows of this warp: r = j * NH + half
+      // the first residual chunk does not depend on the accumulator: issue it before waiting
       if constexpr (kRes)
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, tyg * R + half, b + args.b_res, lane);
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
 #pragma unroll 1
       for (int i = 0; i < RM * NC; ++i) {
         const int r = (i / NC) * NH + half, c = (i % NC) * CH;
@@ -1387,6 +1436,293 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
         }
         ptx::tmem_st_wait();
       }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace osg
+
+namespace osg {
+
+// ---------------------------------------------------------------------------------------
+// Stride-2 3x3 convolution over a ROW-CHUNKED input (the U-Net down convs of the levels whose
+// tensors are row-chunked). Like conv3_nz_kernel, one 5-D TMA box per 32-byte K step brings
+// 2R+1 full input rows x 144 pixels (128-B TMA rows) into smem; the M tile is 128 consecutive
+// INPUT pixels of one input row, so the MMA computes the stride-1 response at every input
+// column and the epilogue keeps the even ones (output pixel x0/2 + m/2 at TMEM lane m): 2x MMA
+// work for 1x loads -- a strided pixel walk is not a UMMA operand layout, and this layer's
+// MMA time is far below its load time. Only the even-row outputs are computed: input row i
+// of the box feeds output row i/2 (dy = 0) and i/2 - 1 (dy = 2) when i is even, (i-1)/2 (dy = 1)
+// when odd; with the R accumulators in reverse row order the even case is ONE MMA with the
+// [dy0 | dy2] weight tiles stacked along N (N = 2 BN). Accumulators are zeroed by the epilogue.
+template <int BN, int R, int STAGES>
+struct S2Smem {
+  static constexpr int kPx = 144;
+  static constexpr int kChunkStride = kPx * 16;
+  static constexpr int kRowStride = 2 * kChunkStride;
+  static constexpr int kABytes = (2 * R + 1) * kRowStride;
+  static constexpr int kA = ((kABytes + 1023) / 1024) * 1024;
+  static constexpr int kBt = BN * 32;  // one tap's BN x 32-B weight tile (SW32); per dx: [dy0][dy2][dy1]
+  static constexpr int kStage = kA + ((9 * kBt + 1023) / 1024) * 1024;
+  static constexpr int kBars = (2 * STAGES + 8) * 8 + 16;
+  static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
+  static constexpr int kCH = BN < 32 ? BN : 32;
+  static constexpr int kEpiBuf = 16 * kCH * 2;                 // 16 output pixels x CH 16-bit channels
+  static constexpr int kTotal = kEpiOff + 4 * 2 * kEpiBuf + 1024;
+  static constexpr uint32_t kTmemCols = (2 * R * BN <= 256) ? 256 : 512;
+};
+
+struct S2Cfg {
+  static constexpr int R(int bn) { return 256 / bn < 4 ? 256 / bn : 4; }
+  static constexpr int stage_bytes(int bn) {
+    return (((2 * R(bn) + 1) * 2 * 144 * 16 + 1023) / 1024) * 1024 + ((9 * bn * 32 + 1023) / 1024) * 1024;
+  }
+  static constexpr int STAGES(int bn) {
+    return (227 * 1024 - 3 * 1024 - 8 * 16 * (bn < 32 ? bn : 32) * 2) / stage_bytes(bn) > 4
+               ? 4
+               : (227 * 1024 - 3 * 1024 - 8 * 16 * (bn < 32 ? bn : 32) * 2) / stage_bytes(bn);
+  }
+};
+
+template <int BN, int R, bool F8, bool BF, typename S>
+__device__ __forceinline__ void s2_mma_chunk(uint32_t sa, uint32_t d_base) {
+#pragma unroll
+  for (int dx = 0; dx < 3; ++dx) {
+    const uint32_t sbd = sa + S::kA + dx * 3 * S::kBt;  // [dy0][dy2][dy1]
+#pragma unroll
+    for (int i = 0; i <= 2 * R; ++i) {
+      const uint32_t a0 = sa + (uint32_t)(i * S::kRowStride + (7 + dx) * 16);
+      const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
+      int col, n, slot;
+      if (i & 1) {  // dy = 1 -> output row (i-1)/2
+        col = (R - 1 - (i - 1) / 2) * BN;
+        n = BN;
+        slot = 2;
+      } else if (i == 0) {  // dy = 0 only -> row 0
+        col = (R - 1) * BN;
+        n = BN;
+        slot = 0;
+      } else if (i == 2 * R) {  // dy = 2 only -> row R-1
+        col = 0;
+        n = BN;
+        slot = 1;
+      } else {  // dy = 0 -> row i/2 and dy = 2 -> row i/2 - 1 (adjacent, reverse order)
+        col = (R - 1 - i / 2) * BN;
+        n = 2 * BN;
+        slot = 0;
+      }
+      const uint64_t db = ptx::smem_desc(sbd + slot * S::kBt, 8 * 32, 6u);
+      if constexpr (F8)
+        ptx::mma_f8_w(d_base + col, da, db, ptx::idesc_f8(128, n), 1u);
+      else
+        ptx::mma_f16_w(d_base + col, da, db, ptx::idesc_f16(128, n, BF), 1u);
+    }
+  }
+}
+
+template <typename T, int BN, int R, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    conv3s2_rc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmO, const ConvArgs args,
+                      const __grid_constant__ LoMaps lo) {
+  using S = S2Smem<BN, R, STAGES>;
+  constexpr int CH = S::kCH;
+  static_assert(2 * BN <= 256, "stacked N");
+  static_assert(S::kTotal <= 227 * 1024, "shared memory");
+  static_assert(2 * R * BN <= 512, "TMEM");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kiters = args.kchunks + args.kch_lo;
+  constexpr uint32_t kTx = S::kABytes + 9 * BN * 32;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
+        const int nt = w % args.n_tiles_n;
+        int m = w / args.n_tiles_n;
+        const int tx = m % args.tiles_x;  // 128 input pixels -> 64 output pixels
+        m /= args.tiles_x;
+        const int tyg = m % args.tiles_y;
+        const int b = m / args.tiles_y;
+        const int u0 = tx * 16 - 1;
+        const int y0 = 2 * tyg * R - 1;
+        for (int kc = 0; kc < kiters; ++kc) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStage;
+          const bool hi = kc < args.kchunks;
+          const int kk = hi ? kc : kc - args.kchunks;
+          ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+          ptx::tma_load_5d(sa, &tmA, &full[stage], 0, u0, 2 * kc, y0, b + args.b_in);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int dy = tap / 3, dx = tap % 3;
+            const int slot = dx * 3 + (dy == 0 ? 0 : dy == 2 ? 1 : 2);
+            ptx::tma_load_2d(sa + S::kA + slot * S::kBt, hi ? &tmB : &lo.B, &full[stage],
+                             tap * args.Cin + kk * (hi ? 16 : 32), nt * BN);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr bool kBf = std::is_same<T, __nv_bfloat16>::value;
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+      const int acc = local & 1;
+      ptx::mbar_wait(&tempty[acc], (local >> 1) & 1);  // the epilogue zeroes and arrives up front
+      ptx::tc_fence_after();
+      const uint32_t d_base = tmem_base + acc * R * BN;
+      for (int kc = 0; kc < kiters; ++kc) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
+        if (kc >= args.kchunks)
+          s2_mma_chunk<BN, R, true, kBf, S>(sa, d_base);
+        else
+          s2_mma_chunk<BN, R, false, kBf, S>(sa, d_base);
+        ptx::mma_commit_w(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ptx::mma_commit_w(&tfull[acc]);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue: even TMEM lanes are outputs
+    const int q = warp & 3;
+    uint8_t* o_hi = smem + S::kEpiOff + q * 2 * S::kEpiBuf;
+    uint8_t* o_lo = o_hi + S::kEpiBuf;
+    const int px = (int)lane >> 1;  // output pixel within the warp's 16
+    const bool even = (lane & 1) == 0;
+    const int rc = args.out_rc;
+    // NHWC box images: 16 rows of CH*2 bytes, 64-B (CH = 32) / 32-B swizzle; RC: [chunk][16 px][16 B]
+    auto o16 = [&](int j16) { return rc ? (uint32_t)(j16 * 256 + px * 16) : EpiTile<CH>::off(px, j16); };
+    auto o8 = [&](int j8) { return rc ? (uint32_t)(j8 * 256 + px * 16) : lo_off<CH>(px, j8); };
+    for (int c = 0; c < 2 * R * BN; c += 16) ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + c);
+    ptx::tmem_st_wait();
+    ptx::tc_fence_before();
+    ptx::mbar_arrive(&tempty[0]);
+    ptx::mbar_arrive(&tempty[1]);
+    int local = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int nt = w % args.n_tiles_n;
+      int m = w / args.n_tiles_n;
+      const int tx = m % args.tiles_x;
+      m /= args.tiles_x;
+      const int tyg = m % args.tiles_y;
+      const int b = m / args.tiles_y;
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
+      const int xo = tx * 64 + q * 16;
+#pragma unroll 1
+      for (int i = 0; i < R * (BN / CH); ++i) {
+        const int r = i / (BN / CH), c = (i % (BN / CH)) * CH;
+        const int n0 = nt * BN + c;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (R - 1 - r) * BN + c;
+        uint32_t u[32];
+        if constexpr (CH == 32) {
+          ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(u));
+        } else {
+          ptx::tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
+        }
+        ptx::tmem_ld_wait();
+        float v[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) v[j] = fmaxf(__uint_as_float(u[j]) + __ldg(args.bias + n0 + j), 0.0f);
+        if (lane == 0) ptx::bulk_wait_read0();
+        __syncwarp();
+        if (even) {
+          if (args.split == kStoreF8) {
+#pragma unroll
+            for (int j = 0; j < CH / 16; ++j) {
+              uint4 h0, h1, l4;
+              split_f8_16(v + 16 * j, h0, h1, l4);
+              *reinterpret_cast<uint4*>(o_hi + o16(2 * j)) = h0;
+              *reinterpret_cast<uint4*>(o_hi + o16(2 * j + 1)) = h1;
+              *reinterpret_cast<uint4*>(o_lo + o8(j)) = l4;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < CH / 8; ++j) {
+              uint32_t o[4], l[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                o[e] = StoreT<T>::pack(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+                const float2 hv = StoreT<T>::unpack(o[e]);
+                l[e] = StoreT<T>::pack(v[8 * j + 2 * e] - hv.x, v[8 * j + 2 * e + 1] - hv.y);
+              }
+              *reinterpret_cast<uint4*>(o_hi + o16(j)) = make_uint4(o[0], o[1], o[2], o[3]);
+              if (args.split) *reinterpret_cast<uint4*>(o_lo + o16(j)) = make_uint4(l[0], l[1], l[2], l[3]);
+            }
+          }
+        }
+        ptx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const int y = tyg * R + r, bo = b + args.b_out;
+          if (rc) {
+            ptx::tma_store_5d(&tmO, o_hi, 0, xo / 8, n0 / 8, y, bo);
+            if (args.split == kStoreF8)
+              ptx::tma_store_5d(&lo.O, o_lo, 0, xo / 8, args.Cout / 8 + n0 / 16, y, bo);
+            else if (args.split)
+              ptx::tma_store_5d(&tmO, o_lo, 0, xo / 8, args.Cout / 8 + n0 / 8, y, bo);
+          } else {
+            ptx::tma_store_4d(&tmO, o_hi, n0, xo, y, bo);
+            if (args.split == kStoreF8)
+              ptx::tma_store_4d(&lo.O, o_lo, n0, xo, y, bo);
+            else if (args.split)
+              ptx::tma_store_4d(&tmO, o_lo, args.Cout + n0, xo, y, bo);
+          }
+          ptx::bulk_commit();
+        }
+      }
+      for (int r = 0; r < R; ++r)
+        for (int c = 0; c < BN; c += 16)
+          ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (R - 1 - r) * BN + c);
+      ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
     }

@@ -193,7 +193,8 @@ struct omniseg {
   int ws_P = 0, ws_B = 0;
   DevBuf X0;
   std::vector<LevelBufs> lv;
-  std::vector<int> rc;  // per level: A_l / Bt_l stored row-chunked (see ensure_workspace)
+  std::vector<int> rc;   // per level: A_l / Bt_l stored row-chunked (see ensure_workspace)
+  std::vector<int> erc;  // per level: E_l (encoder output / skip) stored row-chunked
   DevBuf g, theta, task_cls, task_scl;
   // plans in launch order for one batch (rebuilt with the workspace)
   struct Step {
@@ -451,17 +452,27 @@ void ensure_workspace(omniseg* h, int P) {
     h->dec_plans.push_back(plan(ly, in, Hin, res, out, mode, ol, irc, rrc, orc));
     h->dec_layers.push_back(&ly);
   };
+  // E_l (the skip) is row-chunked too where the level is and its down conv can read it
+  // (conv3s2_rc_kernel); the decoder's D_l reuses the E_l buffer in NHWC (the next up-conv's
+  // per-tap A operand).
+  h->erc.assign(L, 0);
+  for (int l = 0; l + 1 < L; ++l)
+    h->erc[l] = h->rc[l] && s2_eligible(P >> l, P >> l, h->down[l].cinp, h->down[l].coutp, 3, 2, kReluBias) &&
+                h->down[l].coutp <= 64 &&  // the stride-2 kernel's 2x MMA work only pays off for thin N
+                getenv("OMNISEG_NO_S2") == nullptr;
   const auto& rc = h->rc;
+  const auto& erc = h->erc;
   enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias, 0, 0, 0, rc[0]);
   for (int l = 0; l < L; ++l) {
     LevelBufs& q = h->lv[l];
     enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000, rc[l], 0, rc[l]);
-    enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], 0);
-    if (l < L - 1) enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias, l + 1, 0, 0, rc[l + 1]);
+    enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], erc[l]);
+    if (l < L - 1)
+      enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias, l + 1, erc[l], 0, rc[l + 1]);
   }
   for (int l = L - 2; l >= 0; --l) {
     LevelBufs& q = h->lv[l];
-    dec(h->up[l], h->lv[l + 1].E.p, q.P / 2, q.E.p, q.A.p, kUpAdd, l, 0, 0, rc[l]);
+    dec(h->up[l], h->lv[l + 1].E.p, q.P / 2, q.E.p, q.A.p, kUpAdd, l, 0, erc[l], rc[l]);
     dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000, rc[l], 0, rc[l]);
     dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], 0);
   }
@@ -1113,6 +1124,7 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
     // when the no-swizzle multi-row kernel applies (its only layout).
     const int split = (mode & 32) ? kStoreF8 : (mode & 16) ? kStoreX2 : kStorePlain;
     const bool orc_req = (mode & 64) != 0;
+    const bool res_nhwc = (mode & 128) != 0;  // mode | 128: residual / skip NHWC even with an RC output
     mode &= 15;
     OS_REQUIRE(mode >= 0 && mode <= 3, "debug_conv: bad mode");
     OS_REQUIRE((mode != 1 && mode != 2) || r, "debug_conv: mode needs r");
@@ -1144,9 +1156,10 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
     }
     out.ensure(rows_out * coutp * bpc);
     f32o.ensure(rows_out * Cout * 4);
-    const int in_rc = nz_eligible(H, W, cinp * sm, coutp, k, stride, mode) ? 1 : 0;
+    const int in_rc = (nz_eligible(H, W, cinp * sm, coutp, k, stride, mode) ||
+                       (orc_req && s2_eligible(H, W, cinp * sm, coutp, k, stride, mode))) ? 1 : 0;
     const int out_rc = orc_req && ow >= 128 && ow % 128 == 0 ? 1 : 0;
-    const int res_rc = out_rc && mode != 2 ? 1 : 0;
+    const int res_rc = res_nhwc ? 0 : out_rc;
     if (bf) {
       launch_f32_to_t<__nv_bfloat16>(f32in.as<float>(), xin.as<__nv_bfloat16>(), rows_in, Cin, cinp, split,
                                      in_rc ? W : 0, s);

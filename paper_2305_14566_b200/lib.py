@@ -216,7 +216,7 @@ class Omniseg:
                                                   _ptr(out_g), _ptr(out_F)))
         return out_p, out_F, out_g
 
-    def conv(self, x, w, b, stride=1, r=None, mode=0, split=False, rc=False):
+    def conv(self, x, w, b, stride=1, r=None, mode=0, split=False, rc=False, res_nhwc=False):
         """x: float32 [B][H][W][Cin]; w: [Cout][k][k][Cin]; returns float32 output.
         split: False (plain 16-bit storage), True / "x2" (hi + lo 16-bit), "f8" (fp16 + e4m3 lo).
         rc: residual and output in the row-chunked layout (where the width allows; the input is
@@ -233,6 +233,6 @@ class Omniseg:
         y = np.zeros((B, Ho, Wo, Cout), np.float32)
         rr = None if r is None else np.ascontiguousarray(r, np.float32)
         _check(load().omniseg_debug_conv(self.h, _ptr(x), B, H, W, Cin, _ptr(w), _ptr(b), Cout, k, stride,
-                                         _ptr(rr), mode | (32 if split == "f8" else 16 if split else 0) | (64 if rc else 0),
+                                         _ptr(rr), mode | (32 if split == "f8" else 16 if split else 0) | (64 if rc else 0) | (128 if res_nhwc else 0),
                                          _ptr(y)))
         return y

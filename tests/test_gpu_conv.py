@@ -115,8 +115,11 @@ def _e5m2_lo_weights(w):
 RC_CASES = [
     (1, 128, 128, 32, 32, 3, 1, 1),   # nz, row-chunked residual + output
     (2, 128, 128, 64, 64, 3, 1, 0),
-    (1, 256, 256, 32, 64, 3, 2, 0),   # stride-2 per-tap, row-chunked output (the down convs)
-    (1, 64, 64, 64, 32, 1, 1, 2),     # up-add, row-chunked output, NHWC skip
+    (1, 256, 256, 32, 64, 3, 2, 0),   # stride-2 over a row-chunked input (conv3s2_rc_kernel), RC output
+    (2, 256, 256, 64, 128, 3, 2, 0),  # the level-1 down conv shape (BN = 128, R = 2)
+    (1, 256, 128, 32, 32, 3, 2, 0),   # ragged-ish: 2 column blocks, BN = 32
+    (1, 64, 64, 64, 32, 1, 1, 2),     # up-add, row-chunked output and skip
+    (1, 128, 128, 128, 64, 1, 1, 2),  # the level-1 up-conv shape (two 32-channel epilogue chunks)
     (1, 128, 128, 32, 32, 1, 1, 0),   # 1x1 per-tap (the stem), row-chunked output
 ]
 
@@ -129,7 +132,16 @@ def test_conv_parity_row_chunked(h, B, H, W, Cin, Cout, k, stride, mode, split):
     _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=True)
 
 
-def _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=False):
+@pytest.mark.parametrize("split", [False, "x2", "f8"])
+@pytest.mark.parametrize("B,H,W,Cin,Cout,k,stride,mode", [(1, 128, 128, 128, 64, 1, 1, 2), (1, 128, 128, 64, 32, 1, 1, 2),
+                                                          (1, 128, 128, 64, 64, 3, 1, 1)])
+def test_conv_parity_rc_out_nhwc_res(h, B, H, W, Cin, Cout, k, stride, mode, split):
+    """Row-chunked output with an NHWC residual / skip (the up-conv of a level whose skip is
+    NHWC, the b-conv writing E_l)."""
+    _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=True, res_nhwc=True)
+
+
+def _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=False, res_nhwc=False):
     rng = np.random.default_rng(B * 1000 + H + Cin + Cout + k + stride + mode)
     x = rng.standard_normal((B, H, W, Cin)) if split else _f16(rng.standard_normal((B, H, W, Cin)))
     w = _f16(rng.standard_normal((Cout, k, k, Cin)) * np.sqrt(2.0 / (k * k * Cin)))
@@ -159,7 +171,7 @@ def _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=False):
             ref = rs + np.stack([nn.up2(p) for p in pre])
         else:
             ref = pre if rs is None else pre + rs
-        got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split, rc=rc)
+        got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split, rc=rc, res_nhwc=res_nhwc)
         ref_abs = _ref(np.abs(x), np.abs(w), np.abs(b), stride, None if r is None else np.abs(r),
                        3 if mode != 2 else 2)
         bound = 2.0 ** -18 * np.abs(ref_abs) + 2.0 ** -14 * np.abs(ref) + 2.0 ** -15
@@ -168,7 +180,7 @@ def _run(h, B, H, W, Cin, Cout, k, stride, mode, split, rc=False):
         assert (err <= bound).all(), f"max err {err.max():.3g} at {np.unravel_index(err.argmax(), err.shape)}"
         return
     ref = _ref(x, w, b, stride, r, mode)
-    got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split, rc=rc)
+    got = h.conv(x, w, b, stride=stride, r=r, mode=mode, split=split, rc=rc, res_nhwc=res_nhwc)
     err = np.abs(got - ref)
     if split:
         # fp32 accumulation over K terms: |err| <= K eps32 sum|terms| (worst case); use the
