@@ -1,7 +1,7 @@
 """Benchmark: slide-wise Omni-Seg prediction on B200 (BASELINE.json metric
 "slide megapixels/sec (all classes) at 1/2/4/8 B200; sec per synthetic biopsy WSI").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--dtype fp16x2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--dtype fp16f8]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
     python bench.py --impl reference ...      # the oracle arm (CPU, bounded sample)
 
@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4")
-    ap.add_argument("--dtype", default=None, help="fp16x2 (parity-gated default), fp16, bf16")
+    ap.add_argument("--dtype", default=None,
+                    help="fp16f8 (default: fp16 + e4m3 residual, parity-gated), fp16x2 (gated), fp16, bf16")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

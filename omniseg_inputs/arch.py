@@ -26,7 +26,7 @@ THETA_LEN = 8 * 8 + 8 + 8 * 8 + 8 + 1 * 8 + 1   # W1 b1 W2 b2 W3 b3 = 153
 
 
 def arch_dict(levels=5, base=32, ncls=6, scale_codes=SCALE_CODES_4, slide_mag=40,
-              dtype="fp16x2", batch=64):
+              dtype="fp16f8", batch=64):
     return dict(levels=int(levels), base=int(base), head=HEAD_WIDTH, ncls=int(ncls),
                 scale_codes=tuple(int(s) for s in scale_codes), slide_mag=int(slide_mag),
                 dtype=str(dtype), batch=int(batch))

@@ -1,5 +1,5 @@
 """Per-layer conv timing (CUDA events per launch) on a bench workload.
-    python scripts/layer_profile.py [cfg2] [fp16x2] [steps]"""
+    python scripts/layer_profile.py [cfg2] [fp16f8] [steps]"""
 import os
 import sys
 
@@ -10,7 +10,7 @@ from omniseg_inputs import arch_string, geometry, render, workload  # noqa: E402
 from paper_2305_14566_b200 import Omniseg  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-dt = sys.argv[2] if len(sys.argv) > 2 else "fp16x2"
+dt = sys.argv[2] if len(sys.argv) > 2 else "fp16f8"
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 w = workload(int(cfg[3:]))
 w.arch["dtype"] = dt

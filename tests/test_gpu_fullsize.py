@@ -1,5 +1,5 @@
 """Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py times
-(fp16x2, batch 64, device-resident slide and outputs):
+(fp16f8, batch 64, device-resident slide and outputs):
 
 * front end bit-exact at full size: Otsu t, g_pad, the level-8 foreground mask and the
   kept-tile list, against the oracle's detection (evaluated row-chunked, identical to the

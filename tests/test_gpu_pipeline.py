@@ -71,7 +71,8 @@ def _cfg1_ref():
 
 @pytest.fixture(scope="module")
 def cfg1(gpu_lib):
-    """The gated precision mode (fp16x2: fp32-grade activations, R9)."""
+    """The x2 precision mode (fp16x2: fp32-grade activations, R9), gated; the default
+    fp16f8 is gated by test_cfg1_f8_gated and the full-size tests."""
     w = workload(1)
     w.arch["dtype"] = "fp16x2"
     slide, ref = _cfg1_ref()
