@@ -40,6 +40,18 @@ bool nz_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mod
 // The stride-2 kernel over a row-chunked input (conv3s2_rc_kernel) applies to this shape.
 bool s2_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode);
 void set_conv_batch(ConvPlan& p, int B);
+
+// Fused window gather + stem (stem_tc_kernel): the stem conv's output maps come from its
+// ConvPlan (a 1x1 conv over the unfused im2col input); windows are read from the RGBX levels.
+struct StemPlan {
+  ConvPlan conv;   // output maps, bias, weights, storage kind
+  StemArgs args;
+  int grid = 0;
+};
+bool stem_fusable(int P, int Cout);
+StemPlan make_stem_plan(const ConvPlan& stem_conv, const void* w, int P);
+void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32_t* const L[4], int S, int Hp, int Wp,
+              cudaStream_t s);
 void run_conv(const ConvPlan& p, cudaStream_t s);
 int num_sms();
 

@@ -40,18 +40,20 @@ CUtensorMapSwizzle swz(int bytes) {
   return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
 }
 
-template <typename T, int BN, int BK, bool UP>
+template <typename T, int BN, int BK, int MODE>
 struct Cfg {
-  static constexpr int kStageBytes = ConvSmem<BN, BK, 1, UP>::kStage;
-  static constexpr int kStages0 = (UP ? kStageBudgetTapUp : kStageBudgetTap) / kStageBytes;
+  static constexpr int kStageBytes = ConvSmem<BN, BK, 1, MODE>::kStage;
+  static constexpr int kStages0 = (MODE == kUpAdd ? kStageBudgetTapUp : kStageBudgetTap) / kStageBytes;
   static constexpr int STAGES = kStages0 > 8 ? 8 : (kStages0 < 2 ? 2 : kStages0);
-  using Smem = ConvSmem<BN, BK, STAGES, UP>;
+  using Smem = ConvSmem<BN, BK, STAGES, MODE>;
 };
 
 template <typename T, int BN, int BK>
 void launch_tpl(const ConvPlan& p, cudaStream_t s) {
-  using C = Cfg<T, BN, BK, false>;
-  using CU = Cfg<T, BN, BK, true>;
+  using C0 = Cfg<T, BN, BK, kReluBias>;
+  using C1 = Cfg<T, BN, BK, kResidualRelu>;
+  using CU = Cfg<T, BN, BK, kUpAdd>;
+  using C3 = Cfg<T, BN, BK, kBias>;
   auto launch_mode = [&](auto kern, int smem) {
     // all instantiations share one function-pointer type: remember each kernel separately
     static std::mutex mu;
@@ -61,14 +63,15 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, p.mode == kUpAdd ? 384 : 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
+    kern<<<p.grid, tap_epi_warps(BN, p.mode) == 8 ? 384 : 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
   };
-  constexpr int sm = C::Smem::kTotal, smu = CU::Smem::kTotal;
   switch (p.mode) {
-    case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kReluBias>, sm); break;
-    case kResidualRelu: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kResidualRelu>, sm); break;
-    case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, CU::STAGES, kUpAdd>, smu); break;
-    default: launch_mode(conv_tc_kernel<T, BN, BK, C::STAGES, kBias>, sm); break;
+    case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C0::STAGES, kReluBias>, C0::Smem::kTotal); break;
+    case kResidualRelu:
+      launch_mode(conv_tc_kernel<T, BN, BK, C1::STAGES, kResidualRelu>, C1::Smem::kTotal);
+      break;
+    case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, CU::STAGES, kUpAdd>, CU::Smem::kTotal); break;
+    default: launch_mode(conv_tc_kernel<T, BN, BK, C3::STAGES, kBias>, C3::Smem::kTotal); break;
   }
 }
 
@@ -99,18 +102,14 @@ void launch_rows(const ConvPlan& p, cudaStream_t s) {
 template <typename T, int BN, bool DYF>
 void launch_nz(const ConvPlan& p, cudaStream_t s) {
   constexpr int R = NzCfg::R(BN);
-  constexpr int ST = NzCfg::STAGES(BN, 4, false);   // plain epilogue (4 warps)
-  constexpr int STR = NzCfg::STAGES(BN, 8, false);  // residual epilogue (8 warps)
-  constexpr int STH = NzCfg::STAGES(BN, 8, true);   // fused head (8 warps, residual slots only)
+  constexpr int ST = NzCfg::STAGES(BN, 0);   // output-only epilogue
+  constexpr int STR = NzCfg::STAGES(BN, 1);  // residual epilogue
+  constexpr int STH = NzCfg::STAGES(BN, 2);  // fused head (residual slots only)
   static_assert(ST >= 2 && STR >= 2 && STH >= 2, "no-swizzle tile does not fit shared memory");
-  int smem = NzSmem<BN, R, ST, DYF, 4, false>::kTotal, threads = 256;
-  if (p.mode == kResidualRelu) {
-    smem = NzSmem<BN, R, STR, DYF, 8, false>::kTotal;
-    threads = 384;
-  } else if (p.mode == kHeadFused) {
-    smem = NzSmem<BN, R, STH, DYF, 8, true>::kTotal;
-    threads = 384;
-  }
+  int smem = NzSmem<BN, R, ST, DYF, 8, 0>::kTotal;
+  const int threads = 384;
+  if (p.mode == kResidualRelu) smem = NzSmem<BN, R, STR, DYF, 8, 1>::kTotal;
+  else if (p.mode == kHeadFused) smem = NzSmem<BN, R, STH, DYF, 8, 2>::kTotal;
   auto go = [&](auto kern) {
     static std::mutex mu;
     static std::unordered_set<const void*> done;
@@ -370,7 +369,8 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     // output / residual maps for the TMA epilogue: [B][Ho][Wo][C], one warp box = CH channels
     // x (bw x bh) pixels, 64-B (CH=32) / 32-B (CH=16) swizzle; x2 stores [C hi | C lo] per
     // pixel (lo at channel Cout), F8 a fp16 hi map + an e4m3 lo map (CH-byte rows, 32-B / no swizzle)
-    const int CH = p.bn < 32 ? p.bn : 32;
+    const bool tap = p.nz_R == 0 && p.rows_R == 0 && p.s2_R == 0;  // per-tap kernel (conv_tc_kernel)
+    const int CH = tap ? tap_epi_ch(p.bn, mode) : (p.bn < 32 ? p.bn : 32);
     const bool f8o = split_out == kStoreF8;
     const int Cst = split_out == kStoreX2 ? 2 * Cout : Cout;
     const uint64_t opx = f8o ? 3ull * Cout : 2ull * Cst;
@@ -459,6 +459,64 @@ void set_conv_batch(ConvPlan& p, int B) {
   a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
   p.flops = 2.0 * (double)B * a.Ho * a.Wo * a.Cout * (double)a.ksize * a.ksize * a.Cin;
+}
+
+constexpr int kStemR = 4, kStemNA = 8;
+
+bool stem_fusable(int P, int Cout) {
+  int bn = 256;
+  while (Cout % bn) bn >>= 1;
+  return P % 128 == 0 && P % kStemR == 0 && Cout == bn && (bn == 16 || bn == 32 || bn == 64);
+}
+
+StemPlan make_stem_plan(const ConvPlan& stem_conv, const void* w, int P) {
+  StemPlan p;
+  p.conv = stem_conv;
+  StemArgs& a = p.args;
+  a = StemArgs{};
+  a.bias = stem_conv.args.bias;
+  a.w = w;
+  a.P = P;
+  a.tiles_x = P / 128;
+  a.tiles_y = P / kStemR;
+  a.split = stem_conv.args.split;
+  a.out_rc = stem_conv.args.out_rc;
+  a.Cout = stem_conv.args.Cout;
+  return p;
+}
+
+template <typename T, int BN>
+void launch_stem(const StemPlan& p, cudaStream_t s) {
+  using S = StemSmem<BN, kStemR, kStemNA>;
+  auto kern = stem_tc_kernel<T, BN, kStemR, kStemNA>;
+  static std::once_flag once;
+  std::call_once(once, [&] { OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal)); });
+  kern<<<p.grid, 512, S::kTotal, s>>>(p.conv.tmO, p.args, p.conv.lo);
+}
+
+void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32_t* const L[4], int S, int Hp, int Wp,
+              cudaStream_t s) {
+  StemArgs& a = p.args;
+  a.tiles = tiles;
+  for (int i = 0; i < 4; ++i) a.L[i] = L[i];
+  a.first = first;
+  a.S = S;
+  a.Hp = Hp;
+  a.Wp = Wp;
+  a.num_work = n * a.tiles_x * a.tiles_y;
+  if (a.num_work <= 0) return;
+  p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
+  const int bn = p.conv.bn;
+  if (p.conv.bf16) {
+    if (bn == 16) launch_stem<__nv_bfloat16, 16>(p, s);
+    else if (bn == 32) launch_stem<__nv_bfloat16, 32>(p, s);
+    else launch_stem<__nv_bfloat16, 64>(p, s);
+  } else {
+    if (bn == 16) launch_stem<__half, 16>(p, s);
+    else if (bn == 32) launch_stem<__half, 32>(p, s);
+    else launch_stem<__half, 64>(p, s);
+  }
+  OS_CUDA(cudaGetLastError());
 }
 
 void run_conv(const ConvPlan& p0, cudaStream_t s) {

@@ -236,13 +236,36 @@ struct EpiTile {
 };
 
 struct EpiState {
-  uint8_t* buf;         // this warp's 6 buffers (out hi, out lo, 2 x residual hi/lo)
+  uint8_t* buf;         // this warp's 6 kBuf-sized buffers (EpiTile::kWarpBytes)
   uint64_t* rbar;       // this warp's 2 residual mbarriers (double-buffered prefetch)
   uint32_t rphase[2];
   int res_base = 2;     // buffer index of residual slot 0 (0 when the warp has no out buffers)
   int res_rc = 0;       // residual / output tensors in the row-chunked layout (see ConvArgs)
   int out_rc = 0;
+  // byte offsets of the out / residual slots (epi_layout); a slot is [hi kBuf][lo]
+  int out_off[2] = {0, 0}, res_off[2] = {0, 0};
+  int oslot = 0;
 };
+
+// Slot layout in the warp's 6 kBuf: a slot holds hi (kBuf) + lo (x2: kBuf, F8: kBuf/2, plain:
+// none). Plain / F8 slots take 1.5 kBuf, so there is room for TWO output slots (double-
+// buffered TMA stores: the next chunk's STS does not wait for the previous store) beside the
+// two residual slots; x2 keeps one output slot.
+template <int CH>
+__device__ __forceinline__ void epi_layout(EpiState& es, int split) {
+  constexpr int kB = EpiTile<CH>::kBuf;
+  if (split == kStoreX2) {
+    es.out_off[0] = es.out_off[1] = 0;
+    es.res_off[0] = es.res_base * kB;
+    es.res_off[1] = (es.res_base + 2) * kB;
+  } else {
+    es.out_off[0] = 0;
+    es.out_off[1] = kB + kB / 2;
+    const int rb = es.res_base ? 3 * kB : 0;
+    es.res_off[0] = rb;
+    es.res_off[1] = rb + kB + kB / 2;
+  }
+}
 
 // smem image offsets of one warp box (32 pixels x CH channels). NHWC boxes are 64-B (CH = 32)
 // / 32-B (CH = 16) swizzled pixel rows; row-chunked (RC) boxes are [16-B chunk][32 px][16 B].
@@ -264,7 +287,7 @@ __device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUte
                                               int n0, int Cout, int split, int xb, int yb, int b, uint32_t lane) {
   using E = EpiTile<CH>;
   if (lane == 0) {
-    uint8_t* hi = es.buf + (es.res_base + 2 * slot) * E::kBuf;
+    uint8_t* hi = es.buf + es.res_off[slot];
     const uint32_t tx = split == kStoreF8 ? E::kBuf + 32 * CH : (split ? 2 : 1) * E::kBuf;
     ptx::mbar_arrive_expect_tx(&es.rbar[slot], tx);
     if (es.res_rc) {
@@ -290,7 +313,7 @@ template <typename T, int CH, int MODE>
 __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t taddr, const float* bias, int n0,
                                            int split, uint32_t lane, float (&v)[CH]) {
   using E = EpiTile<CH>;
-  uint8_t* res_hi = es.buf + (es.res_base + 2 * slot) * E::kBuf;
+  uint8_t* res_hi = es.buf + es.res_off[slot];
   uint8_t* res_lo = res_hi + E::kBuf;
   constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
   uint32_t u[32];
@@ -340,12 +363,21 @@ template <typename T, int CH, int MODE>
 __device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensorMap* tmO, const CUtensorMap* tmO2,
                                           uint32_t taddr, const float* bias, int n0, int Cout, int split, int xb,
                                           int yb, int b, uint32_t lane) {
-  uint8_t* out_hi = es.buf;
-  uint8_t* out_lo = es.buf + EpiTile<CH>::kBuf;
+  uint8_t* out_hi = es.buf + es.out_off[es.oslot];
+  uint8_t* out_lo = out_hi + EpiTile<CH>::kBuf;
+  const bool dbl = es.out_off[1] != es.out_off[0];
+  es.oslot ^= dbl ? 1 : 0;
   const int rc = es.out_rc;
   float v[CH];
   epi_values<T, CH, MODE>(es, slot, taddr, bias, n0, split, lane, v);
-  if (lane == 0) ptx::bulk_wait_read0();  // previous stores of this warp done reading smem
+  // the store that last read this slot is done reading smem (one store may stay in flight
+  // when the output is double-buffered)
+  if (lane == 0) {
+    if (dbl)
+      ptx::bulk_wait_read1();
+    else
+      ptx::bulk_wait_read0();
+  }
   __syncwarp();
   if (split == kStoreF8) {
 #pragma unroll
@@ -490,8 +522,116 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
   }
 }
 
-template <int BN, int BK, int STAGES, bool UP = false>
+// The fused head for TWO pixels per thread (rows r0, r1 of the warp's column): every shared
+// weight load feeds both, and the FMAs run as packed f32x2 (__ffma2_rn, sm_100) -- the same
+// fp32 arithmetic per pixel, half the FMA and load instructions of epi_head. v0 / v1: the D0
+// values (epi_values) of the two pixels; (x, y0) / (x, y1): their window coordinates.
+template <typename T, int CH>
+__device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v1)[CH], int x, int y0, int y1, int b,
+                                          const HeadArgs& ha, const float* s_w, const float* s_b, const float* s_th,
+                                          int lf, int oy, int ox) {
+  float2 F[kHead];
+#pragma unroll
+  for (int o = 0; o < kHead; ++o) {
+    float2 a = make_float2(s_b[o], s_b[o]);
+#pragma unroll
+    for (int j = 0; j < CH; j += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(s_w + o * CH + j);
+      a = __ffma2_rn(make_float2(w4.x, w4.x), make_float2(v0[j], v1[j]), a);
+      a = __ffma2_rn(make_float2(w4.y, w4.y), make_float2(v0[j + 1], v1[j + 1]), a);
+      a = __ffma2_rn(make_float2(w4.z, w4.z), make_float2(v0[j + 2], v1[j + 2]), a);
+      a = __ffma2_rn(make_float2(w4.w, w4.w), make_float2(v0[j + 3], v1[j + 3]), a);
+    }
+    F[o] = a;
+  }
+  if (ha.out_F) {
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      ha.out_F[(((int64_t)b * ha.P + y0) * ha.P + x) * kHead + o] = F[o].x;
+      ha.out_F[(((int64_t)b * ha.P + y1) * ha.P + x) * kHead + o] = F[o].y;
+    }
+  }
+  const int f = 1 << lf;
+  for (int t = 0; t < ha.ntasks; ++t) {
+    if (ha.tiles && ha.tt.log2f[t] != lf) continue;
+    const float* th = s_th + t * 156;
+    float2 h1[kHead], h2[kHead];
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + o * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + o * 8 + 4);
+      float2 a = make_float2(th[64 + o], th[64 + o]);
+      a = __ffma2_rn(make_float2(a4.x, a4.x), F[0], a);
+      a = __ffma2_rn(make_float2(a4.y, a4.y), F[1], a);
+      a = __ffma2_rn(make_float2(a4.z, a4.z), F[2], a);
+      a = __ffma2_rn(make_float2(a4.w, a4.w), F[3], a);
+      a = __ffma2_rn(make_float2(b4.x, b4.x), F[4], a);
+      a = __ffma2_rn(make_float2(b4.y, b4.y), F[5], a);
+      a = __ffma2_rn(make_float2(b4.z, b4.z), F[6], a);
+      a = __ffma2_rn(make_float2(b4.w, b4.w), F[7], a);
+      h1[o] = make_float2(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
+    }
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + 72 + o * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + 72 + o * 8 + 4);
+      float2 a = make_float2(th[136 + o], th[136 + o]);
+      a = __ffma2_rn(make_float2(a4.x, a4.x), h1[0], a);
+      a = __ffma2_rn(make_float2(a4.y, a4.y), h1[1], a);
+      a = __ffma2_rn(make_float2(a4.z, a4.z), h1[2], a);
+      a = __ffma2_rn(make_float2(a4.w, a4.w), h1[3], a);
+      a = __ffma2_rn(make_float2(b4.x, b4.x), h1[4], a);
+      a = __ffma2_rn(make_float2(b4.y, b4.y), h1[5], a);
+      a = __ffma2_rn(make_float2(b4.z, b4.z), h1[6], a);
+      a = __ffma2_rn(make_float2(b4.w, b4.w), h1[7], a);
+      h2[o] = make_float2(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
+    }
+    const float4 c4 = *reinterpret_cast<const float4*>(th + 144);
+    const float4 d4 = *reinterpret_cast<const float4*>(th + 148);
+    float2 z = make_float2(th[152], th[152]);
+    z = __ffma2_rn(make_float2(c4.x, c4.x), h2[0], z);
+    z = __ffma2_rn(make_float2(c4.y, c4.y), h2[1], z);
+    z = __ffma2_rn(make_float2(c4.z, c4.z), h2[2], z);
+    z = __ffma2_rn(make_float2(c4.w, c4.w), h2[3], z);
+    z = __ffma2_rn(make_float2(d4.x, d4.x), h2[4], z);
+    z = __ffma2_rn(make_float2(d4.y, d4.y), h2[5], z);
+    z = __ffma2_rn(make_float2(d4.z, d4.z), h2[6], z);
+    z = __ffma2_rn(make_float2(d4.w, d4.w), h2[7], z);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float zz = k ? z.y : z.x;
+      const int y = k ? y1 : y0;
+      const float p = 1.0f / (1.0f + expf(-zz));
+      if (ha.out_p) {
+        ha.out_p[(((int64_t)b * ha.ntasks + t) * ha.P + y) * ha.P + x] = p;
+      } else {
+        const int cy = oy + y - ha.pad / f, cx = ox + x - ha.pad / f;
+        const int Wt = ha.tt.Wt[t];
+        if (cy >= 0 && cy < ha.tt.Ht[t] && cx >= 0 && cx < Wt && cy >= ha.tt.row0[t] && cy < ha.tt.row1[t]) {
+          const uint32_t qv = __float2uint_rn(p * 1048576.0f);
+          atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, (1u << 28) + qv);
+        }
+      }
+    }
+  }
+}
+
+// Per-tap kernel epilogue shape: the output-only modes (kReluBias, kBias) with BN >= 32 run 8
+// epilogue warps that split the channels (a pair per TMEM lane quadrant; chunks of tap_epi_ch
+// channels); the up-add runs 8 warps split by output row; the residual mode 4 warps.
+__host__ __device__ constexpr bool tap_split8(int bn, int mode) {
+  return (mode == kReluBias || mode == kBias) && bn >= 32;
+}
+__host__ __device__ constexpr int tap_epi_ch(int bn, int mode) {
+  return tap_split8(bn, mode) ? (bn >= 64 ? 32 : bn / 2) : (bn < 32 ? bn : 32);
+}
+__host__ __device__ constexpr int tap_epi_warps(int bn, int mode) {
+  return (mode == kUpAdd || tap_split8(bn, mode)) ? 8 : 4;
+}
+
+template <int BN, int BK, int STAGES, int MODE = kReluBias>
 struct ConvSmem {
+  static constexpr bool UP = MODE == kUpAdd;
   static constexpr int kA = 128 * BK * 2;
   static constexpr int kB = ((BN * BK * 2 + 1023) / 1024) * 1024;
   static constexpr int kStage = kA + kB;
@@ -502,7 +642,9 @@ struct ConvSmem {
   // up-add: 8 epilogue warps x 2 slots x (skip hi, skip lo) 64-pixel buffers, the output
   // computed in place over the skip
   static constexpr int kUpBytes = 8 * 4 * 64 * kCH * 2;
-  static constexpr int kEpiBytes = UP ? kUpBytes : EpiTile<kCH>::kBytes;
+  static constexpr int kEpiBytes = UP ? kUpBytes
+                                  : tap_split8(BN, MODE) ? 8 * 3 * EpiTile<tap_epi_ch(BN, MODE)>::kBuf
+                                                         : EpiTile<kCH>::kBytes;
   static constexpr int kTotal = kEpiOff + kEpiBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                                           : (2 * BN <= 256) ? 256 : 512;
@@ -513,11 +655,11 @@ struct ConvSmem {
 };
 
 template <typename T, int BN, int BK, int STAGES, int MODE>
-__global__ void __launch_bounds__(MODE == kUpAdd ? 384 : 256, 1)
+__global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                    const ConvArgs args, const __grid_constant__ LoMaps lo) {
-  using S = ConvSmem<BN, BK, STAGES, MODE == kUpAdd>;
+  using S = ConvSmem<BN, BK, STAGES, MODE>;
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
@@ -526,7 +668,7 @@ __global__ void __launch_bounds__(MODE == kUpAdd ? 384 : 256, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   // epilogue warps: 8 for the up-add (a pair per TMEM lane quadrant, one per output row), else 4
-  constexpr int EW = MODE == kUpAdd ? 8 : 4;
+  constexpr int EW = tap_epi_warps(BN, MODE);
   uint64_t* rbar = tempty + 2;  // two residual / skip barriers per epilogue warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * EW);
 
@@ -648,8 +790,10 @@ __global__ void __launch_bounds__(MODE == kUpAdd ? 384 : 256, 1)
     const int ew = warp - 4, half = ew >> 2;
     const int row = q * 32 + lane;        // M row = pixel within the tile
     const int py = row / args.wb, px = row - (row / args.wb) * args.wb;
-    constexpr int CH = BN < 32 ? BN : 32;
+    constexpr int CH = tap_epi_ch(BN, MODE);
+    constexpr bool kSplit8 = tap_split8(BN, MODE);  // the warp pair of a quadrant splits the channels
     EpiState es{smem + S::kEpiOff + ew * (S::kEpiBytes / EW), &rbar[2 * ew], {0, 0}, 2, args.res_rc, args.out_rc};
+    epi_layout<CH>(es, args.split);
     const int bw = args.wb < 32 ? args.wb : 32;
     const int box_dx = (q * 32) % args.wb, box_dy = (q * 32) / args.wb;
     (void)bw;
@@ -707,7 +851,7 @@ __global__ void __launch_bounds__(MODE == kUpAdd ? 384 : 256, 1)
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN; c += CH) {
+      for (int c = kSplit8 ? half * CH : 0; c < BN; c += kSplit8 ? 2 * CH : CH) {
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
         const int n0 = nt * BN + c;
         const int slot = (c / CH) & 1;
@@ -1064,6 +1208,7 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     constexpr int CH = BN < 32 ? BN : 32;
     EpiState es{smem + S::kEpiOff + q * EpiTile<CH>::kWarpBytes, &rbar[2 * q], {0, 0}, 2, args.res_rc, args.out_rc};
+    epi_layout<CH>(es, args.split);
     const int box_dx = (q * 32) % WB, box_dy = (q * 32) / WB;
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
@@ -1121,8 +1266,11 @@ __global__ void __launch_bounds__(256, 1)
 // so the operand of block r, tap (dy, dx) starts at row r+dy, pixel 7+dx of the box (LBO =
 // the chunk plane): all 9 taps of all R blocks come from one load (~(R+2)/R input reads per
 // output). Weights: 9 per-tap SW32 boxes per chunk, shared by the R blocks.
-template <int BN, int R, int STAGES, bool DYF = false, int EW = 4, bool HEAD = false>
+// EK: epilogue kind -- 0 output only (two compact output slots, 3 kBuf per warp), 1 output +
+// residual (6 kBuf), 2 fused head (residual slots only, 4 kBuf).
+template <int BN, int R, int STAGES, bool DYF = false, int EW = 8, int EK = 0>
 struct NzSmem {
+  static constexpr bool HEAD = EK == 2;
   static constexpr int kPx = 144;                                   // 18 units of 8 pixels
   static constexpr int kChunkStride = kPx * 16;                      // LBO of the A operand
   static constexpr int kRowStride = 2 * kChunkStride;                // two chunks (K = 32 B) per row
@@ -1135,8 +1283,7 @@ struct NzSmem {
   static constexpr int kBars = (2 * STAGES + 24) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
-  static constexpr int kWarpEpi = HEAD ? 4 * EpiTile<(BN < 32 ? BN : 32)>::kBuf   // residual slots only
-                                       : EpiTile<(BN < 32 ? BN : 32)>::kWarpBytes;
+  static constexpr int kWarpEpi = (EK == 2 ? 4 : EK == 1 ? 6 : 3) * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
   static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 : 0;
@@ -1151,12 +1298,13 @@ struct NzCfg {
   static constexpr int stage_bytes(int bn) {
     return (((R(bn) + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + 9 * (((bn * 32 + 1023) / 1024) * 1024);
   }
-  // ring depth from what the epilogue (ew warps; head: residual slots only) leaves of 227 KB
-  static constexpr int STAGES(int bn, int ew = 4, bool head = false) {
-    return budget(bn, ew, head) / stage_bytes(bn) > 6 ? 6 : budget(bn, ew, head) / stage_bytes(bn);
+  // ring depth from what the 8 epilogue warps (kind ek, see NzSmem) leave of 227 KB
+  static constexpr int STAGES(int bn, int ek) {
+    return budget(bn, ek) / stage_bytes(bn) > 6 ? 6 : budget(bn, ek) / stage_bytes(bn);
   }
-  static constexpr int budget(int bn, int ew, bool head) {
-    return 227 * 1024 - 3 * 1024 - ew * (head ? 4 : 6) * 32 * (bn < 32 ? bn : 32) * 2 - (head ? 7680 : 0);
+  static constexpr int budget(int bn, int ek) {
+    return 227 * 1024 - 3 * 1024 - 8 * (ek == 2 ? 4 : ek == 1 ? 6 : 3) * 32 * (bn < 32 ? bn : 32) * 2 -
+           (ek == 2 ? 7680 : 0);
   }
 };
 
@@ -1209,14 +1357,17 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
 // (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
 // tensor-core operand traffic than one MMA per (tap, row).
 template <typename T, int BN, int R, int STAGES, int MODE, bool DYF>
-__global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) ? 384 : 256, 1)
+__global__ void __launch_bounds__(384, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                     const ConvArgs args, const __grid_constant__ HeadArgs hargs, const __grid_constant__ LoMaps lo) {
   // epilogue warps: 8 (2 per TMEM lane quadrant, alternating rows) for the residual and
   // fused-head epilogues, whose per-row work exceeds the MMA time of thin layers; 4 otherwise
-  constexpr int EW = (MODE == kHeadFused || MODE == kResidualRelu) ? 8 : 4;
-  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused>;
+  // 8 epilogue warps (2 per TMEM lane quadrant, alternating rows): a single warp per SM
+  // sub-partition leaves the epilogue latency-bound (measured: it, not the loads or MMAs, set
+  // the pace of the thin layers)
+  constexpr int EW = 8;
+  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? 2 : MODE == kResidualRelu ? 1 : 0>;
   static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
@@ -1346,6 +1497,7 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
     constexpr int CH = BN < 32 ? BN : 32;
     EpiState es{smem + S::kEpiOff + ew * S::kWarpEpi, &rbar[2 * ew], {0, 0}, MODE == kHeadFused ? 0 : 2, args.res_rc,
                 args.out_rc};
+    epi_layout<CH>(es, args.split);
     float* s_th = reinterpret_cast<float*>(smem + S::kHeadOff);
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;
@@ -1402,6 +1554,32 @@ __global__ void __launch_bounds__((MODE == kHeadFused || MODE == kResidualRelu) 
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, tyg * R + half, b + args.b_res, lane);
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
+      if constexpr (MODE == kHeadFused && NC == 1 && RM % 2 == 0) {
+        // two rows (pixels (xb + lane, r0) and (xb + lane, r1)) per pass: both residual slots
+        // are consumed by epi_values before the head math, so the next pair's residual loads
+        // are issued right away and overlap it
+#pragma unroll 1
+        for (int i = 0; i < RM; i += 2) {
+          const int r0 = i * NH + half, r1 = (i + 1) * NH + half;
+          epi_res_issue<CH>(es, 1, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res, lane);
+          const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN;
+          float v0[CH], v1[CH];
+          epi_values<T, CH, kHeadFused>(es, 0, tq + (DYF ? (R - 1 - r0) : r0) * BN, args.bias, 0, args.split, lane, v0);
+          epi_values<T, CH, kHeadFused>(es, 1, tq + (DYF ? (R - 1 - r1) : r1) * BN, args.bias, 0, args.split, lane, v1);
+          if (i + 2 < RM)
+            epi_res_issue<CH>(es, 0, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + (i + 2) * NH + half,
+                              b + args.b_res, lane);
+          if (!args.split) {
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+              v0[j] = float(T(v0[j]));
+              v1[j] = float(T(v1[j]));
+            }
+          }
+          epi_head2<T, CH>(v0, v1, xb + (int)lane, tyg * R + r0, tyg * R + r1, b + args.b_head, hargs, s_w, s_b, s_th,
+                           lf, oy, ox);
+        }
+      } else
 #pragma unroll 1
       for (int i = 0; i < RM * NC; ++i) {
         const int r = (i / NC) * NH + half, c = (i % NC) * CH;
@@ -1731,6 +1909,217 @@ __global__ void __launch_bounds__(256, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace osg
+
+namespace osg {
+
+// ---------------------------------------------------------------------------------------
+// Fused window gather + stem conv (A5 + the first A6 layer). For each kept window of the
+// batch, the 3x3x3 stem is a K = 27 (padded to 32) GEMM over an im2col operand that four
+// converter warps build directly in shared memory from the RGBX level image of the window's
+// scale (L_f, padded frame; the window's zero 'same' padding applied by masking), so the
+// 64-B/px im2col tensor of a separate gather kernel never touches HBM. Work item = R output
+// rows x 128 pixels of one window; per row two K = 16 MMAs (M = 128, N = BN). Epilogue: the
+// 8-warp TMA epilogue of the convs (bias, ReLU, storage split, row-chunked / NHWC store).
+struct StemArgs {
+  const uint32_t* tiles;   // kept-window ids (pack_tile), batch b = tiles[first + b]
+  const uint32_t* L[4];    // RGBX u32 padded-frame levels f = 1, 2, 4, 8 (row length Wp / f)
+  const float* bias;
+  const void* w;           // [BN][32] 16-bit stem weights, K = (dy*3 + dx)*3 + c
+  int first, P, S, Hp, Wp;
+  int num_work, tiles_x, tiles_y;
+  int split, out_rc, Cout, b_out;
+};
+
+template <int BN, int R, int NA>
+struct StemSmem {
+  static constexpr int kA = 4 * 128 * 16;        // one row: [kc][128 px][16 B]
+  static constexpr int kB = 4 * BN * 16;         // [kc][BN][16 B]
+  static constexpr int kCH = tap_epi_ch(BN, kReluBias);  // the conv plans' output box width
+  static constexpr int kBOff = NA * kA;
+  static constexpr int kBarOff = ((kBOff + kB + 1023) / 1024) * 1024;
+  static constexpr int kBars = (2 * NA + 4 + 16) * 8 + 16;
+  static constexpr int kEpiOff = ((kBarOff + kBars + 1023) / 1024) * 1024;
+  static constexpr int kTotal = kEpiOff + 8 * 3 * EpiTile<kCH>::kBuf + 1024;
+  static constexpr uint32_t kTmemCols = (2 * R * BN <= 32) ? 32 : (2 * R * BN <= 64) ? 64 : (2 * R * BN <= 128) ? 128
+                                        : (2 * R * BN <= 256) ? 256 : 512;
+};
+
+template <typename T, int BN, int R, int NA>
+__global__ void __launch_bounds__(512, 1)
+    stem_tc_kernel(const __grid_constant__ CUtensorMap tmO, const __grid_constant__ StemArgs args,
+                   const __grid_constant__ LoMaps lo) {
+  using S = StemSmem<BN, R, NA>;
+  constexpr int CH = S::kCH;
+  static_assert(S::kTotal <= 227 * 1024, "shared memory");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* afull = reinterpret_cast<uint64_t*>(smem + S::kBarOff);
+  uint64_t* aempty = afull + NA;
+  uint64_t* tfull = aempty + NA;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;  // unused by the output-only epilogue (EpiState needs the slots)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 16);
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < NA; ++i) {
+      ptx::mbar_init(&afull[i], 128);
+      ptx::mbar_init(&aempty[i], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 256);
+    }
+    for (int a = 0; a < 16; ++a) ptx::mbar_init(&rbar[a], 1);
+    ptx::fence_barrier_init();
+  }
+  // weights -> smem B operand (no-swizzle K-major: [kc][n][8 x 16-bit])
+  if (tid < 128) {
+    const uint4* wsrc = static_cast<const uint4*>(args.w);
+    for (int i = tid; i < BN * 4; i += 128) {
+      const int n = i / 4, kc = i % 4;
+      *reinterpret_cast<uint4*>(smem + S::kBOff + kc * BN * 16 + n * 16) = wsrc[n * 4 + kc];
+    }
+    ptx::fence_proxy_async();
+  }
+  if (warp == 5) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 4) {
+    // ------------------------------------------ im2col converters: thread = output pixel
+    const int px = tid;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
+      const int tx = w % args.tiles_x;
+      int m = w / args.tiles_x;
+      const int tyg = m % args.tiles_y;
+      const int b = m / args.tiles_y;
+      const uint32_t id = __ldg(args.tiles + args.first + b);
+      const int lf = id >> 30, f = 1 << lf;
+      const int Ex = args.Wp / f, Ey = args.Hp / f;
+      const int oy = min((int)((id >> 15) & 0x7FFF) * args.S, Ey - args.P);
+      const int ox = min((int)(id & 0x7FFF) * args.S, Ex - args.P);
+      const uint32_t* L = args.L[lf];
+      const int x = tx * 128 + px;  // window column
+      // the (R+2) x 3 RGBX neighbourhood of this pixel's R output rows, all loads in flight at
+      // once (a load-use chain per row left the converters latency-bound)
+      const int y0 = tyg * R;
+      uint32_t win[R + 2][3];
+#pragma unroll
+      for (int i = 0; i < R + 2; ++i) {
+        const int yy = y0 + i - 1;
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const int xx = x + dx - 1;
+          win[i][dx] = (yy >= 0 && yy < args.P && xx >= 0 && xx < args.P)
+                           ? __ldg(L + (int64_t)(oy + yy) * Ex + (ox + xx))
+                           : 0u;  // the window's zero padding
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ptx::mbar_wait(&aempty[stage], phase ^ 1);
+        uint8_t* a = smem + stage * S::kA;
+        float v[32];
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) {
+            const uint32_t q = win[r + dy][dx];
+            const int k = (dy * 3 + dx) * 3;
+            v[k] = float(q & 255);
+            v[k + 1] = float((q >> 8) & 255);
+            v[k + 2] = float((q >> 16) & 255);
+          }
+#pragma unroll
+        for (int k = 27; k < 32; ++k) v[k] = 0.f;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[e] = StoreT<T>::pack(v[8 * kc + 2 * e], v[8 * kc + 2 * e + 1]);
+          *reinterpret_cast<uint4*>(a + kc * 2048 + px * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+        ptx::mbar_arrive(&afull[stage]);
+        if (++stage == NA) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------ MMA issuer (warp-collective)
+    constexpr bool kBf = std::is_same<T, __nv_bfloat16>::value;
+    constexpr uint32_t idesc = ptx::idesc_f16(128, BN, kBf);
+    const uint32_t sb = ptx::smem_u32(smem + S::kBOff);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+      const int acc = local & 1;
+      ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+      ptx::tc_fence_after();
+      for (int r = 0; r < R; ++r) {
+        ptx::mbar_wait(&afull[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + stage * S::kA);
+        const uint32_t d = tmem_base + acc * R * BN + r * BN;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t da = ptx::smem_desc_noswz(sa + ks * 2 * 2048, 2048, 128);
+          const uint64_t db = ptx::smem_desc_noswz(sb + ks * 2 * BN * 16, BN * 16, 128);
+          ptx::mma_f16_w(d, da, db, idesc, ks);
+        }
+        ptx::mma_commit_w(&aempty[stage]);
+        if (++stage == NA) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ptx::mma_commit_w(&tfull[acc]);
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------ epilogue (8 warps, rows alternate per pair)
+    const int q = warp & 3, ew = warp - 8, half = ew >> 2;
+    EpiState es{smem + S::kEpiOff + ew * 3 * EpiTile<CH>::kBuf, &rbar[2 * ew], {0, 0}, 0, 0, args.out_rc};
+    epi_layout<CH>(es, args.split);
+    int local = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int tx = w % args.tiles_x;
+      int m = w / args.tiles_x;
+      const int tyg = m % args.tiles_y;
+      const int b = m / args.tiles_y;
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
+      const int xb = tx * 128 + q * 32;
+#pragma unroll 1
+      for (int i = 0; i < (R / 2) * (BN / CH); ++i) {
+        const int r = (i / (BN / CH)) * 2 + half, c = (i % (BN / CH)) * CH;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
+        epi_chunk<T, CH, kReluBias>(es, 0, &tmO, &lo.O, taddr, args.bias, c, args.Cout, args.split, xb,
+                                    tyg * R + r, b + args.b_out, lane);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
   }

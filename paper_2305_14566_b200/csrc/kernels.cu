@@ -30,8 +30,10 @@ __device__ __forceinline__ int luma_u8(int r, int g, int b) { return (77 * r + 1
 // Area-mean levels f = 2, 4, 8 of the padded slide, each directly from 40x and rounded
 // half up (R3; §2.2, §3.1), plus the level-8 luma (77R+150G+29B)>>8 (R4).
 // One thread per level-8 pixel = one 8x8 block of the padded frame; padding is virtual.
-__global__ void pyramid_kernel(FrontParams p, const DevState* st, uint32_t* L2, uint32_t* L4, uint32_t* L8,
-                               uint8_t* luma8) {
+// L1 (optional): the padded 40x frame itself as RGBX u32 (pad colour outside the slide), the
+// level the fused stem reads for f = 1 windows.
+__global__ void pyramid_kernel(FrontParams p, const DevState* st, uint32_t* L1, uint32_t* L2, uint32_t* L4,
+                               uint32_t* L8, uint8_t* luma8) {
   const int x8 = blockIdx.x * blockDim.x + threadIdx.x;
   const int y8 = p.r8_0 + blockIdx.y;
   if (x8 >= p.W8 || y8 >= p.r8_1) return;
@@ -47,6 +49,7 @@ __global__ void pyramid_kernel(FrontParams p, const DevState* st, uint32_t* L2, 
     const int64_t sy = (int64_t)y8 * 8 + yy - p.pad;
     const bool row_in = sy >= 0 && sy < p.H;
     const uint8_t* rowp = row_in ? p.slide + (sy - p.slide_row0) * p.W * 3 : nullptr;
+    uint32_t rgbx[8];
 #pragma unroll
     for (int xx = 0; xx < 8; ++xx) {
       const int64_t sx = sx0 + xx;
@@ -57,9 +60,15 @@ __global__ void pyramid_kernel(FrontParams p, const DevState* st, uint32_t* L2, 
         g = __ldg(q + 1);
         b = __ldg(q + 2);
       }
+      rgbx[xx] = uint32_t(r) | (uint32_t(g) << 8) | (uint32_t(b) << 16);
       s2[yy >> 1][xx >> 1][0] += r;
       s2[yy >> 1][xx >> 1][1] += g;
       s2[yy >> 1][xx >> 1][2] += b;
+    }
+    if (L1) {
+      uint4* d = reinterpret_cast<uint4*>(L1 + ((int64_t)y8 * 8 + yy) * p.Wp + (int64_t)x8 * 8);
+      d[0] = make_uint4(rgbx[0], rgbx[1], rgbx[2], rgbx[3]);
+      d[1] = make_uint4(rgbx[4], rgbx[5], rgbx[6], rgbx[7]);
     }
   }
   int s4[2][2][3], s8[3] = {0, 0, 0};
@@ -700,11 +709,11 @@ __global__ void t_to_f32_kernel(const T* in, float* out, int64_t rows, int cout,
 void launch_pad_colour(const uint8_t* slide, int64_t W, DevState* st, cudaStream_t s) {
   pad_colour_kernel<<<1, 32, 0, s>>>(slide, W, st);
 }
-void launch_pyramid(const FrontParams& p, const DevState* st, uint32_t* L2, uint32_t* L4, uint32_t* L8,
+void launch_pyramid(const FrontParams& p, const DevState* st, uint32_t* L1, uint32_t* L2, uint32_t* L4, uint32_t* L8,
                     uint8_t* luma8, cudaStream_t s) {
   if (p.r8_1 <= p.r8_0) return;
   dim3 grid((p.W8 + 127) / 128, p.r8_1 - p.r8_0);
-  pyramid_kernel<<<grid, 128, 0, s>>>(p, st, L2, L4, L8, luma8);
+  pyramid_kernel<<<grid, 128, 0, s>>>(p, st, L1, L2, L4, L8, luma8);
 }
 void launch_median(const uint8_t* g, uint8_t* out, int H8, int W8, int r0, int r1, cudaStream_t s) {
   if (r1 <= r0) return;

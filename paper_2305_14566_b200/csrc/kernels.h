@@ -18,7 +18,7 @@ struct DevState {
 
 
 void launch_pad_colour(const uint8_t* slide, int64_t W, DevState* st, cudaStream_t s);
-void launch_pyramid(const FrontParams& p, const DevState* st, uint32_t* L2, uint32_t* L4, uint32_t* L8,
+void launch_pyramid(const FrontParams& p, const DevState* st, uint32_t* L1, uint32_t* L2, uint32_t* L4, uint32_t* L8,
                     uint8_t* luma8, cudaStream_t s);
 void launch_median(const uint8_t* g, uint8_t* out, int H8, int W8, int r0, int r1, cudaStream_t s);
 void launch_hist(const uint8_t* gm, int W8, int r0, int r1, int c0, int c1, unsigned long long* hist, cudaStream_t s);

@@ -204,9 +204,11 @@ struct omniseg {
   std::vector<ConvPlan> enc_plans, dec_plans;
   std::vector<const Layer*> enc_layers, dec_layers;
   ConvPlan head_plan{};   // dec0.b with the dynamic head + stitch fused into its epilogue
+  StemPlan stem_plan{};   // window gather + stem fused (stem_tc_kernel)
+  bool stem_fused = false;
   bool head_fusable = false;
   // front end / canvases
-  DevBuf slide, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
+  DevBuf slide, L1, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
   std::vector<uint32_t> h_tiles;
   int64_t n_tiles = 0;
   int H8 = 0, W8 = 0, otsu_t = -1, g_pad = -1;
@@ -476,6 +478,9 @@ void ensure_workspace(omniseg* h, int P) {
     dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000, rc[l], 0, rc[l]);
     dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], 0);
   }
+  // fused window gather + stem
+  h->stem_fused = stem_fusable(P, h->stem.coutp) && h->stem.cinp == 32;
+  if (h->stem_fused) h->stem_plan = make_stem_plan(h->enc_plans[0], h->stem.w.p, P);
   // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
   h->head_fusable = false;
   if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr && rc[0]) {
@@ -536,7 +541,8 @@ double conv_alg_flops(const ConvPlan& p, const Layer& ly, int n) {
   return 2.0 * M * ly.cout * K;
 }
 
-void run_conv_prof(omniseg* h, const ConvPlan& p, const Layer& ly, int layer_idx, int n) {
+template <typename F>
+void run_prof(omniseg* h, const ConvPlan& p, const Layer& ly, int layer_idx, int n, F&& launch) {
   if (h->profile) {
     if ((int)h->pev.size() < 2 * (h->pn + 1)) {
       for (int i = 0; i < 64; ++i) {
@@ -546,7 +552,7 @@ void run_conv_prof(omniseg* h, const ConvPlan& p, const Layer& ly, int layer_idx
       }
     }
     OS_CUDA(cudaEventRecord(h->pev[2 * h->pn], h->stream));
-    run_conv(p, h->stream);
+    launch();
     OS_CUDA(cudaEventRecord(h->pev[2 * h->pn + 1], h->stream));
     if ((int)h->player.size() <= h->pn) {
       h->player.resize(h->pn + 1);
@@ -556,8 +562,11 @@ void run_conv_prof(omniseg* h, const ConvPlan& p, const Layer& ly, int layer_idx
     h->pflops[h->pn] = conv_alg_flops(p, ly, n);
     h->pn++;
   } else {
-    run_conv(p, h->stream);
+    launch();
   }
+}
+void run_conv_prof(omniseg* h, const ConvPlan& p, const Layer& ly, int layer_idx, int n) {
+  run_prof(h, p, ly, layer_idx, n, [&] { run_conv(p, h->stream); });
 }
 
 // Resolve the event pairs of the finished call into the accumulators.
@@ -603,13 +612,13 @@ void fill_head(HeadArgs& ha, omniseg* h, int ntasks, int P, int S, int Hp, int W
 }
 
 template <typename T>
-void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int first, const HeadTaskTable& tt,
+void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int first, bool stem_done, const HeadTaskTable& tt,
                         int ntasks, int S, int Hp, int Wp, int pad, float* out_p, float* out_F, float* out_g) {
   const int L = h->arch.levels;
   cudaStream_t s = h->stream;
   const size_t ne = h->enc_plans.size();
-  // ---------------- encoder
-  for (size_t i = 0; i < ne; ++i) {
+  // ---------------- encoder (the stem already ran fused with the window gather when stem_done)
+  for (size_t i = stem_done ? 1 : 0; i < ne; ++i) {
     set_conv_batch(h->enc_plans[i], n);
     run_conv_prof(h, h->enc_plans[i], *h->enc_layers[i], (int)i, n);
     h->conv_launches++;
@@ -687,6 +696,8 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   }
   bool needf[4] = {false, false, false, false};
   for (int i = 0; i < tk.n; ++i) needf[tk.log2f[i]] = true;
+  const bool l1_needed = needf[0] && h->stem_fused && getenv("OMNISEG_NO_STEM_FUSION") == nullptr;
+  if (l1_needed) h->L1.ensure((size_t)Hp * Wp * 4);
   if (needf[1]) h->L2.ensure((size_t)(Hp / 2) * (Wp / 2) * 4);
   if (needf[2]) h->L4.ensure((size_t)(Hp / 4) * (Wp / 4) * 4);
   if (needf[3]) h->L8.ensure((size_t)H8 * W8 * 4);
@@ -717,7 +728,8 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   fp.r8_1 = l1;
   fp.own8_0 = (int)(row0 / 8);
   fp.own8_1 = (int)(row1 / 8);
-  launch_pyramid(fp, st, needf[1] ? h->L2.as<uint32_t>() : nullptr, needf[2] ? h->L4.as<uint32_t>() : nullptr,
+  launch_pyramid(fp, st, l1_needed ? h->L1.as<uint32_t>() : nullptr, needf[1] ? h->L2.as<uint32_t>() : nullptr,
+                 needf[2] ? h->L4.as<uint32_t>() : nullptr,
                  needf[3] ? h->L8.as<uint32_t>() : nullptr, h->luma8.as<uint8_t>(), s);
   // the median reads luma rows [m0-3, m1+3) with edge replication only at the frame border
   launch_median(h->luma8.as<uint8_t>(), h->gm.as<uint8_t>(), H8, W8, m0, m1, s);
@@ -792,12 +804,22 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   // ---- hot loop over batches of kept tiles
   const int B = h->arch.batch;
   double t_gather = 0;
+  const bool fused = h->stem_fused && getenv("OMNISEG_NO_STEM_FUSION") == nullptr;
+  const uint32_t* Lv[4] = {h->L1.as<uint32_t>(), h->L2.as<uint32_t>(), h->L4.as<uint32_t>(), h->L8.as<uint32_t>()};
   for (int64_t first = 0; first < h->n_tiles; first += B) {
     const int n = (int)std::min<int64_t>(B, h->n_tiles - first);
-    launch_gather<T>(h->tiles.as<uint32_t>(), (int)first, n, P, S, fp, st, h->L2.as<uint32_t>(),
-                     h->L4.as<uint32_t>(), h->L8.as<uint32_t>(), h->X0.as<T>(), s);
-    h->launches++;
-    run_trunk_and_head<T>(h, n, P, h->tiles.as<uint32_t>(), (int)first, tt, tk.n, S, Hp, Wp, pad, nullptr, nullptr,
+    if (fused) {
+      // window gather + stem in one kernel (A5 + the first conv of A6)
+      run_prof(h, h->enc_plans[0], *h->enc_layers[0], 0, n, [&] {
+        run_stem(h->stem_plan, h->tiles.as<uint32_t>(), (int)first, n, Lv, S, Hp, Wp, s);
+      });
+      h->conv_launches++;
+    } else {
+      launch_gather<T>(h->tiles.as<uint32_t>(), (int)first, n, P, S, fp, st, h->L2.as<uint32_t>(),
+                       h->L4.as<uint32_t>(), h->L8.as<uint32_t>(), h->X0.as<T>(), s);
+      h->launches++;
+    }
+    run_trunk_and_head<T>(h, n, P, h->tiles.as<uint32_t>(), (int)first, fused, tt, tk.n, S, Hp, Wp, pad, nullptr, nullptr,
                           nullptr);
   }
   (void)t_gather;
@@ -1095,11 +1117,11 @@ int omniseg_debug_predict_tiles(omniseg_t* h, const uint8_t* tiles_u8, int n, in
     HeadTaskTable tt{};
     if (h->arch.bf16) {
       launch_gather_raw<__nv_bfloat16>(src, n, P, h->X0.as<__nv_bfloat16>(), s);
-      run_trunk_and_head<__nv_bfloat16>(h, n, P, nullptr, 0, tt, n_tasks, P, P, P, 0, dp.as<float>(),
+      run_trunk_and_head<__nv_bfloat16>(h, n, P, nullptr, 0, false, tt, n_tasks, P, P, P, 0, dp.as<float>(),
                                         out_F ? dF.as<float>() : nullptr, out_g ? dg.as<float>() : nullptr);
     } else {
       launch_gather_raw<__half>(src, n, P, h->X0.as<__half>(), s);
-      run_trunk_and_head<__half>(h, n, P, nullptr, 0, tt, n_tasks, P, P, P, 0, dp.as<float>(),
+      run_trunk_and_head<__half>(h, n, P, nullptr, 0, false, tt, n_tasks, P, P, P, 0, dp.as<float>(),
                                  out_F ? dF.as<float>() : nullptr, out_g ? dg.as<float>() : nullptr);
     }
     OS_CUDA(cudaMemcpyAsync(out_p, dp.p, (size_t)n * n_tasks * P * P * 4, cudaMemcpyDefault, s));
