@@ -40,6 +40,10 @@ bool nz_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mod
 // The stride-2 kernel over a row-chunked input (conv3s2_rc_kernel) applies to this shape.
 bool s2_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode);
 void set_conv_batch(ConvPlan& p, int B);
+// nz / stride-2 plans read their weights as per-K-step smem images: the caller allocates
+// conv_wimage_bytes(p) bytes (0: not needed) and builds them once (stream-ordered).
+size_t conv_wimage_bytes(const ConvPlan& p);
+void build_conv_wimage(ConvPlan& p, const void* w, const void* w_lo, void* dst, cudaStream_t s);
 
 // Fused window gather + stem (stem_tc_kernel): the stem conv's output maps come from its
 // ConvPlan (a 1x1 conv over the unfused im2col input); windows are read from the RGBX levels.

@@ -137,7 +137,7 @@ void launch_s2(const ConvPlan& p, cudaStream_t s) {
   auto kern = conv3s2_rc_kernel<T, BN, R, ST>;
   static std::once_flag once;
   std::call_once(once, [&] { OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); });
-  kern<<<p.grid, 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.args, p.lo);
+  kern<<<p.grid, 384, smem, s>>>(p.tmA, p.tmB, p.tmO, p.args, p.lo);
 }
 
 template <typename T>
@@ -155,6 +155,7 @@ void dispatch(const ConvPlan& p, cudaStream_t s) {
     if (p.bn == 16) return dyf ? launch_nz<T, 16, true>(p, s) : launch_nz<T, 16, false>(p, s);
     if (p.bn == 32) return dyf ? launch_nz<T, 32, true>(p, s) : launch_nz<T, 32, false>(p, s);
     if (p.bn == 64) return dyf ? launch_nz<T, 64, true>(p, s) : launch_nz<T, 64, false>(p, s);
+    if (p.bn == 128) return launch_nz<T, 128, false>(p, s);  // 3 x 128 > 256: no dy stacking
     throw Error(-1, "unsupported no-swizzle conv shape");
   }
   if (p.rows_R > 0) {
@@ -203,8 +204,8 @@ bool s2_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mod
 bool nz_eligible(int Hin, int Win, int Cin, int Cout, int k, int stride, int mode) {
   int bn = 256;
   while (Cout % bn) bn >>= 1;
-  return k == 3 && stride == 1 && mode != kUpAdd && bn <= 64 && Cout == bn && Cin % 16 == 0 && Win >= 128 &&
-         Win % 128 == 0 && Hin % NzCfg::R(bn) == 0;
+  return k == 3 && stride == 1 && mode != kUpAdd && bn <= 128 && Cout == bn && Cin % 16 == 0 && Win >= 128 &&
+         Win % 128 == 0 && Hin % NzCfg::R(bn) == 0 && (bn <= 64 || mode != kHeadFused);
 }
 
 ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int Cin, const void* w,
@@ -329,6 +330,9 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.res = res;
   a.out = out;
   a.split = split_out;
+  // per-tap kernel: 128-channel lo chunks when the K chunk is 64 (one SW128 row like the hi chunks)
+  a.lo2 = (f8in && p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bk == 64 && Cin % 128 == 0) ? 1 : 0;
+  if (a.lo2) a.kch_lo = Cin / 128;
   if (p.nz_R == 0 && p.s2_R == 0) {
     cuuint64_t dims[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)B_in};
     cuuint64_t strides[3] = {in_px, (cuuint64_t)Win * in_px, (cuuint64_t)Hin * Win * in_px};
@@ -340,8 +344,9 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(A) failed: " + std::to_string((int)r));
     if (f8in) {
-      r = encode_fn()(&p.lo.A, d8, 4, const_cast<void*>(in_lo), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      swz(p.bk), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      cuuint32_t bl[4] = {box[0] * (a.lo2 ? 2u : 1u), box[1], box[2], box[3]};
+      r = encode_fn()(&p.lo.A, d8, 4, const_cast<void*>(in_lo), dims, strides, bl, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swz(p.bk * (a.lo2 ? 2 : 1)), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(A lo) failed: " + std::to_string((int)r));
     }
   }
@@ -357,7 +362,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
     if (f8in) {
       // lo weights: e5m2 bytes [Cout][taps*Cin]; a lo chunk is bk (nz: 32) bytes wide
-      const int bkl = (p.nz_R > 0 || p.s2_R > 0) ? 32 : p.bk;
+      const int bkl = (p.nz_R > 0 || p.s2_R > 0) ? 32 : p.bk * (a.lo2 ? 2 : 1);
       cuuint64_t s1[1] = {(cuuint64_t)taps * Cin};
       cuuint32_t b1[2] = {(cuuint32_t)bkl, (cuuint32_t)p.bn};
       r = encode_fn()(&p.lo.B, d8, 2, const_cast<void*>(w_lo), dims, s1, b1, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -461,6 +466,59 @@ void set_conv_batch(ConvPlan& p, int B) {
   p.flops = 2.0 * (double)B * a.Ho * a.Wo * a.Cout * (double)a.ksize * a.ksize * a.Cin;
 }
 
+// ---- per-K-step weight images of the nz / stride-2 kernels (ConvArgs::wimg)
+namespace {
+struct SlotMap {
+  int tap[9];
+};
+// one thread per (n tile, K step, slot, row n, 16-B half j)
+__global__ void wimage_kernel(const uint8_t* w16, const uint8_t* wlo, uint8_t* dst, int ntn, int BN, int taps_cin,
+                              int Cin, int khi, int klo, SlotMap sm) {
+  const int nks = khi + klo;
+  const int64_t total = (int64_t)ntn * nks * 9 * BN * 2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int j = (int)(i & 1);
+  int64_t r = i >> 1;
+  const int n = (int)(r % BN);
+  r /= BN;
+  const int slot = (int)(r % 9);
+  r /= 9;
+  const int ks = (int)(r % nks);
+  const int nt = (int)(r / nks);
+  const int co = nt * BN + n, tap = sm.tap[slot];
+  const uint8_t* src = ks < khi ? w16 + ((int64_t)co * taps_cin + (int64_t)tap * Cin + 16 * ks + 8 * j) * 2
+                                : wlo + (int64_t)co * taps_cin + (int64_t)tap * Cin + 32 * (ks - khi) + 16 * j;
+  uint8_t* d = dst + (((int64_t)nt * nks + ks) * 9 + slot) * BN * 32 + n * 32 + 16 * (j ^ ((n >> 2) & 1));
+  *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(src);
+}
+}  // namespace
+
+size_t conv_wimage_bytes(const ConvPlan& p) {
+  if (p.nz_R == 0 && p.s2_R == 0) return 0;
+  return (size_t)p.args.n_tiles_n * (p.args.kchunks + p.args.kch_lo) * 9 * p.bn * 32;
+}
+
+void build_conv_wimage(ConvPlan& p, const void* w, const void* w_lo, void* dst, cudaStream_t s) {
+  const size_t bytes = conv_wimage_bytes(p);
+  if (!bytes) return;
+  SlotMap sm;
+  for (int tap = 0; tap < 9; ++tap) {
+    const int dy = tap / 3, dx = tap % 3;
+    int slot;
+    if (p.s2_R > 0) slot = dx * 3 + (dy == 0 ? 0 : dy == 2 ? 1 : 2);  // [dx][dy0, dy2, dy1]
+    else if (getenv("OMNISEG_NO_DYF") == nullptr && p.bn <= 64) slot = dx * 3 + dy;  // dy-fused: [dx][dy]
+    else slot = tap;
+    sm.tap[slot] = tap;
+  }
+  const int64_t total = (int64_t)bytes / 16;
+  wimage_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+      static_cast<const uint8_t*>(w), static_cast<const uint8_t*>(w_lo), static_cast<uint8_t*>(dst),
+      p.args.n_tiles_n, p.bn, 9 * p.args.Cin, p.args.Cin, p.args.kchunks, p.args.kch_lo, sm);
+  OS_CUDA(cudaGetLastError());
+  p.args.wimg = static_cast<const uint8_t*>(dst);
+}
+
 constexpr int kStemR = 4, kStemNA = 8;
 
 bool stem_fusable(int P, int Cout) {
@@ -521,9 +579,10 @@ void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32
 
 void run_conv(const ConvPlan& p0, cudaStream_t s) {
   if (p0.args.num_work <= 0) return;
+  OS_REQUIRE((p0.nz_R == 0 && p0.s2_R == 0) || p0.args.wimg != nullptr, "conv plan: weight image not built");
   ConvPlan p = p0;
   static unsigned long long* dbuf = nullptr;
-  if ((p.args.dbg & 8) && p.nz_R > 0) {  // experiment: MMA-warp cycle counters
+  if ((p.args.dbg & 8) && (p.nz_R > 0 || p.s2_R > 0)) {  // experiment: MMA-warp cycle counters
     if (!dbuf) OS_CUDA(cudaMalloc(&dbuf, 148 * 4 * 8));
     p.args.dbg_out = dbuf;
   } else {
@@ -545,8 +604,8 @@ void run_conv(const ConvPlan& p0, cudaStream_t s) {
       fu += h[4 * i + 2];
       n += h[4 * i + 3];
     }
-    fprintf(stderr, "[nz BN=%d Cin=%d mode=%d] per item: total %.0f, wait tempty %.0f, wait full %.0f cycles (%.0f items/CTA)\n",
-            p.bn, p.args.Cin, p.mode, a / n, te / n, fu / n, n / p.grid);
+    fprintf(stderr, "[%s BN=%d Cin=%d mode=%d] per item: total %.0f, wait tempty %.0f, wait full %.0f cycles (%.0f items/CTA)\n",
+            p.s2_R ? "s2" : "nz", p.bn, p.args.Cin, p.mode, a / n, te / n, fu / n, n / p.grid);
   }
 }
 

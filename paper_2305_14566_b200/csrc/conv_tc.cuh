@@ -60,6 +60,7 @@ struct ConvArgs {
   void* out;              // [B][Ho][Wo][Cout] (mode 2: [B][2Ho][2Wo][Cout])
   int split;              // StoreKind of res/out
   int kch_lo;             // F8 input: number of lo K chunks (after the kchunks hi chunks), else 0
+  int lo2;                // per-tap kernel: a lo chunk holds 2 BK channels (128-B rows, SW128)
   // batch-index offsets of the tensors (a launch over images [0, B) of the work space reads
   // input image b + b_in, residual b + b_res, writes b + b_out, head tile b + b_head)
   int b_in, b_res, b_out, b_head;
@@ -69,6 +70,10 @@ struct ConvArgs {
   int dbg;  // experiments only (OMNISEG_DBG, conv3_nz_kernel): 1 skip epilogue math/stores, 2 skip MMAs, 4 skip loads,
             // 8 record MMA-warp cycle counters into dbg_out[blockIdx.x][4]
   unsigned long long* dbg_out;
+  // nz / stride-2 kernels: the weights pre-arranged as the per-K-step smem image
+  // [n tile][K step][9 tap slots][BN rows][32 B, SW32 swizzled] (build_conv_wimage), loaded with
+  // one bulk copy per K step instead of 9 TMA boxes of 32-byte rows
+  const uint8_t* wimg;
 };
 
 template <typename T>
@@ -728,10 +733,12 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
             ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0 + dy, b + args.b_in);
             ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
           } else {
-            const int kl = kc - args.kchunks;
-            ptx::mbar_arrive_expect_tx(&full[stage], kTxLo);
-            ptx::tma_load_4d(sa, &lo.A, &full[stage], kl * BK, x0 + dx, y0 + dy, b + args.b_in);
-            ptx::tma_load_2d(sb, &lo.B, &full[stage], tap * args.Cin + kl * BK, nt * BN);
+            // lo chunk: BK e4m3 channels (BK-byte rows), or 2 BK (lo2: 128-byte rows, as many TMA
+            // rows as a hi chunk for twice the MMAs of a BK-wide lo chunk)
+            const int kl = kc - args.kchunks, kw = args.lo2 ? 2 * BK : BK;
+            ptx::mbar_arrive_expect_tx(&full[stage], args.lo2 ? 2 * kTxLo : kTxLo);
+            ptx::tma_load_4d(sa, &lo.A, &full[stage], kl * kw, x0 + dx, y0 + dy, b + args.b_in);
+            ptx::tma_load_2d(sb, &lo.B, &full[stage], tap * args.Cin + kl * kw, nt * BN);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -765,6 +772,14 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
               const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBO, S::kLayout);
               const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBO, S::kLayout);
               ptx::mma_f16_w(d_tmem, da, db, idesc, (it | k) != 0);
+            }
+          } else if (BK == 64 && args.lo2) {
+            // F8 lo chunk of 2 BK = 128 channels: 128-byte rows (SW128), 32 K per MMA
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t da = ptx::smem_desc(sa + k * 32, 1024, 2u);
+              const uint64_t db = ptx::smem_desc(sb + k * 32, 1024, 2u);
+              ptx::mma_f8_w(d_tmem, da, db, idesc8, 1u);
             }
           } else if constexpr (BK >= 32) {
             // F8 lo chunk: BK bytes per row (SW64 / SW32), 32 K per MMA
@@ -1278,8 +1293,8 @@ struct NzSmem {
   static constexpr int kA = ((kABytes + 1023) / 1024) * 1024;
   // one tap's BN x 16-channel weight tile (SW32); the dy-stacked variant packs the three dy
   // tiles of one dx back to back, so they must be exactly BN*32 bytes apart
-  static constexpr int kBt = DYF ? BN * 32 : ((BN * 32 + 1023) / 1024) * 1024;
-  static constexpr int kStage = kA + 9 * kBt;
+  static constexpr int kBt = BN * 32;  // tap slots back to back (one bulk copy per K step)
+  static constexpr int kStage = kA + ((9 * kBt + 1023) / 1024) * 1024;
   static constexpr int kBars = (2 * STAGES + 24) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
@@ -1296,7 +1311,7 @@ struct NzCfg {
   // rows (the (R+2)-row input box must leave room for >= 2 ring stages)
   static constexpr int R(int bn) { return 256 / bn < 8 ? 256 / bn : 8; }
   static constexpr int stage_bytes(int bn) {
-    return (((R(bn) + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + 9 * (((bn * 32 + 1023) / 1024) * 1024);
+    return (((R(bn) + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + ((9 * bn * 32 + 1023) / 1024) * 1024;
   }
   // ring depth from what the 8 epilogue warps (kind ek, see NzSmem) leave of 227 KB
   static constexpr int STAGES(int bn, int ek) {
@@ -1433,12 +1448,9 @@ __global__ void __launch_bounds__(384, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
           // chunks 2kc, 2kc+1 of the RC input: hi chunks first, then (F8) the lo chunks
           ptx::tma_load_5d(sa, &tmA, &full[stage], 0, u0, 2 * kc, y0, b + args.b_in);
-#pragma unroll
-          for (int tap = 0; tap < 9; ++tap) {
-            const int slot = DYF ? (tap % 3) * 3 + tap / 3 : tap;  // DYF: [dx][dy] order
-            ptx::tma_load_2d(sa + S::kA + slot * S::kBt, hi ? &tmB : &lo.B, &full[stage],
-                             tap * args.Cin + kk * (hi ? 16 : 32), nt * BN);
-          }
+          (void)hi;
+          (void)kk;
+          ptx::bulk_load(sa + S::kA, args.wimg + ((size_t)nt * kiters + kc) * 9 * BN * 32, 9 * BN * 32, &full[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1655,7 +1667,7 @@ struct S2Smem {
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   static constexpr int kCH = BN < 32 ? BN : 32;
   static constexpr int kEpiBuf = 16 * kCH * 2;                 // 16 output pixels x CH 16-bit channels
-  static constexpr int kTotal = kEpiOff + 4 * 2 * kEpiBuf + 1024;
+  static constexpr int kTotal = kEpiOff + 8 * 4 * kEpiBuf + 1024;  // 8 warps x 2 x (hi, lo)
   static constexpr uint32_t kTmemCols = (2 * R * BN <= 256) ? 256 : 512;
 };
 
@@ -1664,11 +1676,8 @@ struct S2Cfg {
   static constexpr int stage_bytes(int bn) {
     return (((2 * R(bn) + 1) * 2 * 144 * 16 + 1023) / 1024) * 1024 + ((9 * bn * 32 + 1023) / 1024) * 1024;
   }
-  static constexpr int STAGES(int bn) {
-    return (227 * 1024 - 3 * 1024 - 8 * 16 * (bn < 32 ? bn : 32) * 2) / stage_bytes(bn) > 4
-               ? 4
-               : (227 * 1024 - 3 * 1024 - 8 * 16 * (bn < 32 ? bn : 32) * 2) / stage_bytes(bn);
-  }
+  static constexpr int budget(int bn) { return 227 * 1024 - 3 * 1024 - 32 * 16 * (bn < 32 ? bn : 32) * 2; }
+  static constexpr int STAGES(int bn) { return budget(bn) / stage_bytes(bn) > 4 ? 4 : budget(bn) / stage_bytes(bn); }
 };
 
 template <int BN, int R, bool F8, bool BF, typename S>
@@ -1708,7 +1717,7 @@ __device__ __forceinline__ void s2_mma_chunk(uint32_t sa, uint32_t d_base) {
 }
 
 template <typename T, int BN, int R, int STAGES>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     conv3s2_rc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, const ConvArgs args,
                       const __grid_constant__ LoMaps lo) {
@@ -1735,7 +1744,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 128);
+      ptx::mbar_init(&tempty[a], 256);
     }
     ptx::fence_barrier_init();
   }
@@ -1767,13 +1776,9 @@ __global__ void __launch_bounds__(256, 1)
           const int kk = hi ? kc : kc - args.kchunks;
           ptx::mbar_arrive_expect_tx(&full[stage], kTx);
           ptx::tma_load_5d(sa, &tmA, &full[stage], 0, u0, 2 * kc, y0, b + args.b_in);
-#pragma unroll
-          for (int tap = 0; tap < 9; ++tap) {
-            const int dy = tap / 3, dx = tap % 3;
-            const int slot = dx * 3 + (dy == 0 ? 0 : dy == 2 ? 1 : 2);
-            ptx::tma_load_2d(sa + S::kA + slot * S::kBt, hi ? &tmB : &lo.B, &full[stage],
-                             tap * args.Cin + kk * (hi ? 16 : 32), nt * BN);
-          }
+          (void)hi;
+          (void)kk;
+          ptx::bulk_load(sa + S::kA, args.wimg + ((size_t)nt * kiters + kc) * 9 * BN * 32, 9 * BN * 32, &full[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1786,13 +1791,18 @@ __global__ void __launch_bounds__(256, 1)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
+    unsigned long long c_te = 0, c_full = 0, t_start = clock64();
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
+      unsigned long long t0 = clock64();
       ptx::mbar_wait(&tempty[acc], (local >> 1) & 1);  // the epilogue zeroes and arrives up front
+      c_te += clock64() - t0;
       ptx::tc_fence_after();
       const uint32_t d_base = tmem_base + acc * R * BN;
       for (int kc = 0; kc < kiters; ++kc) {
+        t0 = clock64();
         ptx::mbar_wait(&full[stage], phase);
+        c_full += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
         if (kc >= args.kchunks)
@@ -1807,18 +1817,34 @@ __global__ void __launch_bounds__(256, 1)
       }
       ptx::mma_commit_w(&tfull[acc]);
     }
+    if ((args.dbg & 8) && lane == 0) {
+      args.dbg_out[blockIdx.x * 4 + 0] = clock64() - t_start;
+      args.dbg_out[blockIdx.x * 4 + 1] = c_te;
+      args.dbg_out[blockIdx.x * 4 + 2] = c_full;
+      args.dbg_out[blockIdx.x * 4 + 3] = local;
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue: even TMEM lanes are outputs
-    const int q = warp & 3;
-    uint8_t* o_hi = smem + S::kEpiOff + q * 2 * S::kEpiBuf;
-    uint8_t* o_lo = o_hi + S::kEpiBuf;
+    // 8 warps: a pair per TMEM lane quadrant, alternating output rows. Each output pixel's
+    // CH = 32 channels are shared by its lane pair: the even lane (which holds the pixel in
+    // TMEM) keeps channels 0-15, the odd lane takes 16-31 through a shuffle, so all 32 lanes
+    // convert and store. Output staging double-buffered (two (hi, lo) sets per warp).
+    const int q = warp & 3, ew = warp - 4, half = ew >> 2;
+    uint8_t* obase = smem + S::kEpiOff + ew * 4 * S::kEpiBuf;
+    int oslot = 0;
     const int px = (int)lane >> 1;  // output pixel within the warp's 16
-    const bool even = (lane & 1) == 0;
+    const bool odd = (lane & 1) != 0;
+    constexpr bool kPair = CH == 32;  // lane-pair channel split
+    constexpr int CW = kPair ? 16 : CH;  // channels converted by one lane
+    const int cb = (kPair && odd) ? 16 : 0;
     const int rc = args.out_rc;
     // NHWC box images: 16 rows of CH*2 bytes, 64-B (CH = 32) / 32-B swizzle; RC: [chunk][16 px][16 B]
     auto o16 = [&](int j16) { return rc ? (uint32_t)(j16 * 256 + px * 16) : EpiTile<CH>::off(px, j16); };
     auto o8 = [&](int j8) { return rc ? (uint32_t)(j8 * 256 + px * 16) : lo_off<CH>(px, j8); };
-    for (int c = 0; c < 2 * R * BN; c += 16) ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + c);
+    {
+      const int c0 = half * (R * BN), c1 = c0 + R * BN;  // the pair splits the zeroing of both buffers
+      for (int c = c0; c < c1; c += 16) ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + c);
+    }
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
     ptx::mbar_arrive(&tempty[0]);
@@ -1836,8 +1862,8 @@ __global__ void __launch_bounds__(256, 1)
       ptx::tc_fence_after();
       const int xo = tx * 64 + q * 16;
 #pragma unroll 1
-      for (int i = 0; i < R * (BN / CH); ++i) {
-        const int r = i / (BN / CH), c = (i % (BN / CH)) * CH;
+      for (int i = 0; i < (R / 2) * (BN / CH); ++i) {
+        const int r = (i / (BN / CH)) * 2 + half, c = (i % (BN / CH)) * CH;
         const int n0 = nt * BN + c;
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (R - 1 - r) * BN + c;
         uint32_t u[32];
@@ -1847,34 +1873,45 @@ __global__ void __launch_bounds__(256, 1)
           ptx::tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
         }
         ptx::tmem_ld_wait();
-        float v[CH];
+        float v[CW];
 #pragma unroll
-        for (int j = 0; j < CH; ++j) v[j] = fmaxf(__uint_as_float(u[j]) + __ldg(args.bias + n0 + j), 0.0f);
-        if (lane == 0) ptx::bulk_wait_read0();
+        for (int j = 0; j < CW; ++j) {
+          float x0 = fmaxf(__uint_as_float(u[j]) + __ldg(args.bias + n0 + j), 0.0f);
+          if constexpr (kPair) {
+            const float x1 = fmaxf(__uint_as_float(u[16 + j]) + __ldg(args.bias + n0 + 16 + j), 0.0f);
+            const float from_even = __shfl_sync(0xffffffffu, x1, (int)lane ^ 1);
+            x0 = odd ? from_even : x0;
+          }
+          v[j] = x0;
+        }
+        uint8_t* o_hi = obase + oslot * 2 * S::kEpiBuf;
+        uint8_t* o_lo = o_hi + S::kEpiBuf;
+        oslot ^= 1;
+        if (lane == 0) ptx::bulk_wait_read1();  // the store that last used this slot has read it
         __syncwarp();
-        if (even) {
-          if (args.split == kStoreF8) {
+        if (!kPair && odd) {
+          // without the pair split only the even lanes hold output pixels
+        } else if (args.split == kStoreF8) {
 #pragma unroll
-            for (int j = 0; j < CH / 16; ++j) {
-              uint4 h0, h1, l4;
-              split_f8_16(v + 16 * j, h0, h1, l4);
-              *reinterpret_cast<uint4*>(o_hi + o16(2 * j)) = h0;
-              *reinterpret_cast<uint4*>(o_hi + o16(2 * j + 1)) = h1;
-              *reinterpret_cast<uint4*>(o_lo + o8(j)) = l4;
+          for (int j = 0; j < CW / 16; ++j) {
+            uint4 h0, h1, l4;
+            split_f8_16(v + 16 * j, h0, h1, l4);
+            *reinterpret_cast<uint4*>(o_hi + o16(cb / 8 + 2 * j)) = h0;
+            *reinterpret_cast<uint4*>(o_hi + o16(cb / 8 + 2 * j + 1)) = h1;
+            *reinterpret_cast<uint4*>(o_lo + o8(cb / 16 + j)) = l4;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < CW / 8; ++j) {
+            uint32_t o[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              o[e] = StoreT<T>::pack(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+              const float2 hv = StoreT<T>::unpack(o[e]);
+              l[e] = StoreT<T>::pack(v[8 * j + 2 * e] - hv.x, v[8 * j + 2 * e + 1] - hv.y);
             }
-          } else {
-#pragma unroll
-            for (int j = 0; j < CH / 8; ++j) {
-              uint32_t o[4], l[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                o[e] = StoreT<T>::pack(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
-                const float2 hv = StoreT<T>::unpack(o[e]);
-                l[e] = StoreT<T>::pack(v[8 * j + 2 * e] - hv.x, v[8 * j + 2 * e + 1] - hv.y);
-              }
-              *reinterpret_cast<uint4*>(o_hi + o16(j)) = make_uint4(o[0], o[1], o[2], o[3]);
-              if (args.split) *reinterpret_cast<uint4*>(o_lo + o16(j)) = make_uint4(l[0], l[1], l[2], l[3]);
-            }
+            *reinterpret_cast<uint4*>(o_hi + o16(cb / 8 + j)) = make_uint4(o[0], o[1], o[2], o[3]);
+            if (args.split) *reinterpret_cast<uint4*>(o_lo + o16(cb / 8 + j)) = make_uint4(l[0], l[1], l[2], l[3]);
           }
         }
         ptx::fence_proxy_async();
@@ -1897,9 +1934,11 @@ __global__ void __launch_bounds__(256, 1)
           ptx::bulk_commit();
         }
       }
-      for (int r = 0; r < R; ++r)
+      for (int j = 0; j < R / 2; ++j) {
+        const int r = j * 2 + half;
         for (int c = 0; c < BN; c += 16)
           ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (R - 1 - r) * BN + c);
+      }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);

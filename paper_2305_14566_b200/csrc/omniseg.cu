@@ -165,6 +165,7 @@ int pad16(int c) { return (c + 15) / 16 * 16; }
 struct Layer {
   DevBuf w;      // [coutp][k*k][cinp] 16-bit
   DevBuf wlo;    // f8 inputs: [coutp][k*k][cinp] e5m2 bytes of W * 2^-6 (the lo term's weights)
+  mutable DevBuf wimg;  // per-K-step smem image of the weights for nz / stride-2 plans
   DevBuf b;      // [coutp] fp32
   int in_kind = 0;  // StoreKind of the layer's input
   int cin = 0, cout = 0, cinp = 0, coutp = 0, k = 3, stride = 1;
@@ -441,8 +442,14 @@ void ensure_workspace(omniseg* h, int P) {
   // out_level: U-Net level of the output (and residual / skip) tensor
   auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int out_level,
                   int in_rc, int res_rc, int out_rc) {
-    return make_conv_plan(bf, in, B, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride, mode,
-                          res, out, ar.sp(out_level), -1, -1, -1, ly.in_kind, ly.wlo.p, in_rc, res_rc, out_rc);
+    ConvPlan p = make_conv_plan(bf, in, B, Hin, Hin, ly.cinp, ly.w.p, ly.b.as<float>(), ly.coutp, ly.k, ly.stride,
+                                mode, res, out, ar.sp(out_level), -1, -1, -1, ly.in_kind, ly.wlo.p, in_rc, res_rc,
+                                out_rc);
+    if (const size_t wb = conv_wimage_bytes(p)) {
+      ly.wimg.ensure(wb);
+      build_conv_wimage(p, ly.w.p, ly.wlo.p, ly.wimg.p, h->stream);
+    }
+    return p;
   };
   auto enc = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int ol, int irc,
                  int rrc, int orc) {
@@ -1195,6 +1202,10 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
     }
     ConvPlan p = make_conv_plan(bf, xin.p, B, H, W, cinp * sm, L.w.p, L.b.as<float>(), coutp, k, stride, mode,
                                 r ? rin.p : nullptr, out.p, split, -1, -1, -1, split, L.wlo.p, in_rc, res_rc, out_rc);
+    if (const size_t wb = conv_wimage_bytes(p)) {
+      L.wimg.ensure(wb);
+      build_conv_wimage(p, L.w.p, L.wlo.p, L.wimg.p, s);
+    }
     run_conv(p, s);
     if (bf)
       launch_t_to_f32<__nv_bfloat16>(out.as<__nv_bfloat16>(), f32o.as<float>(), rows_out, Cout, coutp, split,
