@@ -16,6 +16,7 @@ struct ConvPlan {
   int rows_R = 0;        // > 0: the multi-row 3x3 kernel (conv3_rows_kernel) with R blocks
   int nz_R = 0;          // > 0: the no-swizzle multi-row 3x3 kernel (conv3_nz_kernel)
   int s2_R = 0;          // > 0: the stride-2 row-chunked-input kernel (conv3s2_rc_kernel)
+  int cl = 1;            // per-tap kernel cluster size (2: CTA pairs multicasting the weight tiles)
   int hb = 1;
   bool bf16;
   HeadArgs head{};       // kHead mode (fused dynamic head + stitch), set by the caller per launch

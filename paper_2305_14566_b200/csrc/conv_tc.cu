@@ -54,7 +54,7 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
   using C1 = Cfg<T, BN, BK, kResidualRelu>;
   using CU = Cfg<T, BN, BK, kUpAdd>;
   using C3 = Cfg<T, BN, BK, kBias>;
-  auto launch_mode = [&](auto kern, int smem) {
+  auto launch_mode = [&](auto kern, int smem, int cl) {
     // all instantiations share one function-pointer type: remember each kernel separately
     static std::mutex mu;
     static std::unordered_set<const void*> done;
@@ -63,15 +63,45 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
       if (done.insert(reinterpret_cast<const void*>(kern)).second)
         OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    kern<<<p.grid, tap_epi_warps(BN, p.mode) == 8 ? 384 : 256, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
+    const int threads = tap_epi_warps(BN, p.mode) == 8 ? 384 : 256;
+    if (cl == 1) {
+      kern<<<p.grid, threads, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo);
+      return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    OS_CUDA(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo));
   };
+  if constexpr (BN == 256) {
+    if (p.cl == 2) {
+      switch (p.mode) {
+        case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C0::STAGES, kReluBias, 2>, C0::Smem::kTotal, 2); break;
+        case kResidualRelu:
+          launch_mode(conv_tc_kernel<T, BN, BK, C1::STAGES, kResidualRelu, 2>, C1::Smem::kTotal, 2);
+          break;
+        case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, CU::STAGES, kUpAdd, 2>, CU::Smem::kTotal, 2); break;
+        default: launch_mode(conv_tc_kernel<T, BN, BK, C3::STAGES, kBias, 2>, C3::Smem::kTotal, 2); break;
+      }
+      return;
+    }
+  }
   switch (p.mode) {
-    case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C0::STAGES, kReluBias>, C0::Smem::kTotal); break;
+    case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C0::STAGES, kReluBias>, C0::Smem::kTotal, 1); break;
     case kResidualRelu:
-      launch_mode(conv_tc_kernel<T, BN, BK, C1::STAGES, kResidualRelu>, C1::Smem::kTotal);
+      launch_mode(conv_tc_kernel<T, BN, BK, C1::STAGES, kResidualRelu>, C1::Smem::kTotal, 1);
       break;
-    case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, CU::STAGES, kUpAdd>, CU::Smem::kTotal); break;
-    default: launch_mode(conv_tc_kernel<T, BN, BK, C3::STAGES, kBias>, C3::Smem::kTotal); break;
+    case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, CU::STAGES, kUpAdd>, CU::Smem::kTotal, 1); break;
+    default: launch_mode(conv_tc_kernel<T, BN, BK, C3::STAGES, kBias>, C3::Smem::kTotal, 1); break;
   }
 }
 
@@ -330,6 +360,10 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.res = res;
   a.out = out;
   a.split = split_out;
+  // per-tap 256-channel layers: CTA pairs sharing (multicasting) the weight tiles
+  if (p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bn == 256 && (a.tiles_x * a.tiles_y) % 2 == 0 &&
+      getenv("OMNISEG_CLUSTER") != nullptr)  // opt-in: measured no faster (these layers are tensor-bound)
+    p.cl = 2;
   // per-tap kernel: 128-channel lo chunks when the K chunk is 64 (one SW128 row like the hi chunks)
   a.lo2 = (f8in && p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bk == 64 && Cin % 128 == 0) ? 1 : 0;
   if (a.lo2) a.kch_lo = Cin / 128;
@@ -354,7 +388,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     const int taps = k * k;
     cuuint64_t dims[2] = {(cuuint64_t)taps * Cin, (cuuint64_t)Cout};
     cuuint64_t strides[1] = {(cuuint64_t)taps * Cin * 2};
-    cuuint32_t box[2] = {(cuuint32_t)p.bk, (cuuint32_t)p.bn};
+    cuuint32_t box[2] = {(cuuint32_t)p.bk, (cuuint32_t)(p.bn / p.cl)};  // CL = 2: each CTA loads half
     cuuint32_t es[2] = {1, 1};
     CUresult r = encode_fn()(&p.tmB, dt, 2, const_cast<void*>(w), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz(p.bk * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -364,7 +398,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
       // lo weights: e5m2 bytes [Cout][taps*Cin]; a lo chunk is bk (nz: 32) bytes wide
       const int bkl = (p.nz_R > 0 || p.s2_R > 0) ? 32 : p.bk * (a.lo2 ? 2 : 1);
       cuuint64_t s1[1] = {(cuuint64_t)taps * Cin};
-      cuuint32_t b1[2] = {(cuuint32_t)bkl, (cuuint32_t)p.bn};
+      cuuint32_t b1[2] = {(cuuint32_t)bkl, (cuuint32_t)(p.bn / p.cl)};
       r = encode_fn()(&p.lo.B, d8, 2, const_cast<void*>(w_lo), dims, s1, b1, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       swz(bkl), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(B lo) failed: " + std::to_string((int)r));
@@ -453,6 +487,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   }
   p.stages = (p.rows_R > 0 || p.nz_R > 0 || p.s2_R > 0) ? 0 : stages_for(p.bn, p.bk);
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
+  if (p.cl == 2) p.grid &= ~1;  // whole clusters (num_work is even)
   p.flops = 2.0 * (double)B * Ho * Wo * Cout * (double)k * k * Cin;
   p.hb = a.hb;
   return p;
@@ -463,6 +498,7 @@ void set_conv_batch(ConvPlan& p, int B) {
   ConvArgs& a = p.args;
   a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
+  if (p.cl == 2) p.grid &= ~1;
   p.flops = 2.0 * (double)B * a.Ho * a.Wo * a.Cout * (double)a.ksize * a.ksize * a.Cin;
 }
 
@@ -582,7 +618,7 @@ void run_conv(const ConvPlan& p0, cudaStream_t s) {
   OS_REQUIRE((p0.nz_R == 0 && p0.s2_R == 0) || p0.args.wimg != nullptr, "conv plan: weight image not built");
   ConvPlan p = p0;
   static unsigned long long* dbuf = nullptr;
-  if ((p.args.dbg & 8) && (p.nz_R > 0 || p.s2_R > 0)) {  // experiment: MMA-warp cycle counters
+  if ((p.args.dbg & 8) && p.rows_R == 0) {  // experiment: MMA-warp cycle counters
     if (!dbuf) OS_CUDA(cudaMalloc(&dbuf, 148 * 4 * 8));
     p.args.dbg_out = dbuf;
   } else {
@@ -604,8 +640,8 @@ void run_conv(const ConvPlan& p0, cudaStream_t s) {
       fu += h[4 * i + 2];
       n += h[4 * i + 3];
     }
-    fprintf(stderr, "[%s BN=%d Cin=%d mode=%d] per item: total %.0f, wait tempty %.0f, wait full %.0f cycles (%.0f items/CTA)\n",
-            p.s2_R ? "s2" : "nz", p.bn, p.args.Cin, p.mode, a / n, te / n, fu / n, n / p.grid);
+    fprintf(stderr, "[%s BN=%d Cin=%d Wo=%d mode=%d] per item: total %.0f, wait tempty %.0f, wait full %.0f cycles (%.0f items/CTA)\n",
+            p.s2_R ? "s2" : p.nz_R ? "nz" : "tap", p.bn, p.args.Cin, p.args.Wo, p.mode, a / n, te / n, fu / n, n / p.grid);
   }
 }
 

@@ -659,7 +659,12 @@ struct ConvSmem {
   static constexpr uint32_t kSBOLo = 8 * BK;
 };
 
-template <typename T, int BN, int BK, int STAGES, int MODE>
+// CL = 2: a cluster of two CTAs processes work items in pairs (two M tiles, the same N tile
+// and K sequence); each CTA loads half of every B (weight) tile and multicasts it to both, and
+// each MMA warp's stage release is multicast to both CTAs' empty barriers -- half the L2 ->
+// SM weight traffic, which bounds the 256-channel layers (measured: their MMA warp waited on
+// loads a third of the time).
+template <typename T, int BN, int BK, int STAGES, int MODE, int CL = 1>
 __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
@@ -679,13 +684,26 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
+  static_assert(CL == 1 || CL == 2, "cluster size");
+  const uint32_t crank = CL == 2 ? ptx::cluster_ctarank() : 0;
+  // work item w -> (n tile, m tile); CL = 2: pairs (2p, 2p + 1) share the n tile
+  auto decode = [&](int w, int& nt, int& m) {
+    if constexpr (CL == 2) {
+      const int pp = w >> 1;
+      nt = pp % args.n_tiles_n;
+      m = 2 * (pp / args.n_tiles_n) + (w & 1);
+    } else {
+      nt = w % args.n_tiles_n;
+      m = w / args.n_tiles_n;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], CL);  // CL = 2: released by both CTAs' MMA warps
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -696,7 +714,10 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2)
+    ptx::cluster_sync();  // both CTAs' barriers initialised before any multicast
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -713,8 +734,8 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
-        const int nt = w % args.n_tiles_n;
-        int m = w / args.n_tiles_n;
+        int nt, m;
+        decode(w, nt, m);
         const int tx = m % args.tiles_x;
         m /= args.tiles_x;
         const int ty = m % args.tiles_y;
@@ -731,14 +752,22 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
           if (kc < args.kchunks) {
             ptx::mbar_arrive_expect_tx(&full[stage], kTx);
             ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0 + dy, b + args.b_in);
-            ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
+            if constexpr (CL == 2)
+              ptx::tma_load_2d_mc(sb + crank * (BN / 2) * BK * 2, &tmB, &full[stage], tap * args.Cin + kc * BK,
+                                  nt * BN + crank * (BN / 2), 0x3);
+            else
+              ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
           } else {
             // lo chunk: BK e4m3 channels (BK-byte rows), or 2 BK (lo2: 128-byte rows, as many TMA
             // rows as a hi chunk for twice the MMAs of a BK-wide lo chunk)
             const int kl = kc - args.kchunks, kw = args.lo2 ? 2 * BK : BK;
             ptx::mbar_arrive_expect_tx(&full[stage], args.lo2 ? 2 * kTxLo : kTxLo);
             ptx::tma_load_4d(sa, &lo.A, &full[stage], kl * kw, x0 + dx, y0 + dy, b + args.b_in);
-            ptx::tma_load_2d(sb, &lo.B, &full[stage], tap * args.Cin + kl * kw, nt * BN);
+            if constexpr (CL == 2)
+              ptx::tma_load_2d_mc(sb + crank * (BN / 2) * kw, &lo.B, &full[stage], tap * args.Cin + kl * kw,
+                                  nt * BN + crank * (BN / 2), 0x3);
+            else
+              ptx::tma_load_2d(sb, &lo.B, &full[stage], tap * args.Cin + kl * kw, nt * BN);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -755,14 +784,19 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
+      unsigned long long c_te = 0, c_full = 0, t_start = clock64();
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
+        unsigned long long t0 = clock64();
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        c_te += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int it = 0; it < kiters; ++it) {
+          t0 = clock64();
           ptx::mbar_wait(&full[stage], phase);
+          c_full += clock64() - t0;
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
           const uint32_t sb = sa + S::kA;
@@ -790,13 +824,22 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
               ptx::mma_f8_w(d_tmem, da, db, idesc8, 1u);
             }
           }
-          ptx::mma_commit_w(&empty[stage]);
+          if constexpr (CL == 2)
+            ptx::mma_commit_mc_w(&empty[stage], 0x3);
+          else
+            ptx::mma_commit_w(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
         ptx::mma_commit_w(&tfull[acc]);
+      }
+      if ((args.dbg & 8) && lane == 0) {
+        args.dbg_out[blockIdx.x * 4 + 0] = clock64() - t_start;
+        args.dbg_out[blockIdx.x * 4 + 1] = c_te;
+        args.dbg_out[blockIdx.x * 4 + 2] = c_full;
+        args.dbg_out[blockIdx.x * 4 + 3] = local;
       }
     }
   } else if (warp >= 4) {
@@ -819,8 +862,8 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
       if (lane != 0) return;
       constexpr int kUB = 64 * CH * 2;
       const bool f8 = args.split == kStoreF8;
-      const int nt2 = w2 % args.n_tiles_n;
-      int m2 = w2 / args.n_tiles_n;
+      int nt2, m2;
+      decode(w2, nt2, m2);
       const int tx2 = m2 % args.tiles_x;
       m2 /= args.tiles_x;
       const int ty2 = m2 % args.tiles_y;
@@ -852,8 +895,8 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int nt = w % args.n_tiles_n;
-      int m = w / args.n_tiles_n;
+      int nt, m;
+      decode(w, nt, m);
       const int tx = m % args.tiles_x;
       m /= args.tiles_x;
       const int ty = m % args.tiles_y;
@@ -1018,7 +1061,10 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
     if (lane == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2)
+    ptx::cluster_sync();  // no CTA leaves while its peer may still multicast into it
+  else
+    __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
@@ -1979,7 +2025,7 @@ template <int BN, int R, int NA>
 struct StemSmem {
   static constexpr int kA = 4 * 128 * 16;        // one row: [kc][128 px][16 B]
   static constexpr int kB = 4 * BN * 16;         // [kc][BN][16 B]
-  static constexpr int kCH = tap_epi_ch(BN, kReluBias);  // the conv plans' output box width
+  static constexpr int kCH = BN < 32 ? BN : 32;  // output box width (make_stem_plan's maps)
   static constexpr int kBOff = NA * kA;
   static constexpr int kBarOff = ((kBOff + kB + 1023) / 1024) * 1024;
   static constexpr int kBars = (2 * NA + 4 + 16) * 8 + 16;
@@ -2039,7 +2085,10 @@ __global__ void __launch_bounds__(512, 1)
     const int px = tid;
     int stage = 0;
     uint32_t phase = 0;
-    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
+    // the (R+2) x 3 RGBX neighbourhood of this pixel's R output rows; the NEXT work item's
+    // loads are issued before this item is converted (software pipelining: a load-use chain
+    // per item left the converters latency-bound)
+    auto fetch = [&](int w, uint32_t (&win)[R + 2][3]) {
       const int tx = w % args.tiles_x;
       int m = w / args.tiles_x;
       const int tyg = m % args.tiles_y;
@@ -2051,10 +2100,7 @@ __global__ void __launch_bounds__(512, 1)
       const int ox = min((int)(id & 0x7FFF) * args.S, Ex - args.P);
       const uint32_t* L = args.L[lf];
       const int x = tx * 128 + px;  // window column
-      // the (R+2) x 3 RGBX neighbourhood of this pixel's R output rows, all loads in flight at
-      // once (a load-use chain per row left the converters latency-bound)
       const int y0 = tyg * R;
-      uint32_t win[R + 2][3];
 #pragma unroll
       for (int i = 0; i < R + 2; ++i) {
         const int yy = y0 + i - 1;
@@ -2066,6 +2112,16 @@ __global__ void __launch_bounds__(512, 1)
                            : 0u;  // the window's zero padding
         }
       }
+    };
+    uint32_t nxt[R + 2][3];
+    if ((int)blockIdx.x < args.num_work) fetch(blockIdx.x, nxt);
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
+      uint32_t win[R + 2][3];
+#pragma unroll
+      for (int i = 0; i < R + 2; ++i)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) win[i][dx] = nxt[i][dx];
+      if (w + (int)gridDim.x < args.num_work) fetch(w + gridDim.x, nxt);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         ptx::mbar_wait(&aempty[stage], phase ^ 1);

@@ -467,7 +467,7 @@ void ensure_workspace(omniseg* h, int P) {
   h->erc.assign(L, 0);
   for (int l = 0; l + 1 < L; ++l)
     h->erc[l] = h->rc[l] && s2_eligible(P >> l, P >> l, h->down[l].cinp, h->down[l].coutp, 3, 2, kReluBias) &&
-                h->down[l].coutp <= 64 &&  // the stride-2 kernel's 2x MMA work only pays off for thin N
+                h->down[l].coutp <= (getenv("OMNISEG_S2_WIDE") ? 128 : 64) &&  // 2x MMA work: thin N only
                 getenv("OMNISEG_NO_S2") == nullptr;
   const auto& rc = h->rc;
   const auto& erc = h->erc;
@@ -487,7 +487,16 @@ void ensure_workspace(omniseg* h, int P) {
   }
   // fused window gather + stem
   h->stem_fused = stem_fusable(P, h->stem.coutp) && h->stem.cinp == 32;
-  if (h->stem_fused) h->stem_plan = make_stem_plan(h->enc_plans[0], h->stem.w.p, P);
+  if (h->stem_fused) {
+    // the stem kernel's epilogue stores 32-channel boxes (the per-tap output-only plan splits
+    // the channels over 16-wide warp pairs): its output maps come from a residual-mode plan
+    // of the same conv (no residual given), whose epilogue box is min(C, 32) channels wide
+    ConvPlan mp = make_conv_plan(bf, h->X0.p, B, P, P, h->stem.cinp, h->stem.w.p, h->stem.b.as<float>(),
+                                 h->stem.coutp, 1, 1, kResidualRelu, nullptr, h->lv[0].A.p, ar.sp(0), -1, -1, -1,
+                                 kStorePlain, nullptr, 0, 0, rc[0]);
+    mp.args.split = h->enc_plans[0].args.split;
+    h->stem_plan = make_stem_plan(mp, h->stem.w.p, P);
+  }
   // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
   h->head_fusable = false;
   if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr && rc[0]) {
