@@ -299,10 +299,19 @@ def main():
     pk, pk_kind = peaks()
     achieved = prof["flops"] / (prof["ms"] / 1e3) / 1e12 if prof["ms"] > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    roof = {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 implicit GEMM, all trunk convs)",
+    # DRAM traffic per conv launch from the committed ncu capture of the same launch shapes
+    # (batch-64 launches of the cfg2 profile run: dram__bytes_read.sum + dram__bytes_write.sum)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "r01k_summary.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = tj.get("conv_dram_bytes_per_launch")
+        traffic_src = "profiles/r01k_summary.json (ncu, %d conv launches)" % tj.get("conv_launches", 0)
+    roof = {"bound": "tensor", "kernel": "tcgen05 conv family (stem_tc / conv3_nz / conv3s2_rc / conv_tc kernels)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
             "peak_kind": f"{pk_kind} bf16 sustained (fp16 kind::f16 nominal ratio 1.0)",
-            "traffic": None, "conv_share_of_step": (prof["ms"] / steps) / ms if ms else None,
+            "traffic": traffic, "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
+            "conv_share_of_step": (prof["ms"] / steps) / ms if ms else None,
             "alg_flops_per_launch": prof["flops"] / max(prof["launches"], 1),
             "avg_launch_ms": prof["ms"] / max(prof["launches"], 1)}
     cpu = None
