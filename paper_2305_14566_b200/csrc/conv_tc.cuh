@@ -746,7 +746,10 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
           const int tap = it / kct;
           const int kc = it - tap * kct;
           const int dy = tap / args.ksize, dx = tap - (tap / args.ksize) * args.ksize;
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if constexpr (MODE == kUpAdd)  // epilogue-bound: let the epilogue warps have the issue slots
+            ptx::mbar_wait_backoff(&empty[stage], phase ^ 1);
+          else
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
           uint8_t* sb = sa + S::kA;
           if (kc < args.kchunks) {
@@ -789,7 +792,7 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         unsigned long long t0 = clock64();
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::mbar_wait_backoff(&tempty[acc], acc_phase ^ 1);
         c_te += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -1479,7 +1482,10 @@ __global__ void __launch_bounds__(384, 1)
         const int u0 = tx * 16 - 1;  // first 8-pixel unit of the box (pixels [x0 - 8, x0 + 136))
         const int y0 = tyg * R - 1;
         for (int kc = 0; kc < kiters; ++kc) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if constexpr (MODE == kHeadFused)  // epilogue-bound: leave the issue slots to the head math
+            ptx::mbar_wait_backoff(&empty[stage], phase ^ 1);
+          else
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
           const bool hi = kc < args.kchunks;
           const int kk = hi ? kc : kc - args.kchunks;
@@ -1515,7 +1521,7 @@ __global__ void __launch_bounds__(384, 1)
         const int acc = local & 1;
         // DYF: the epilogue zeroes every buffer and arrives once up front (real phases)
         unsigned long long t0 = clock64();
-        ptx::mbar_wait(&tempty[acc], DYF ? ((local >> 1) & 1) : (((local >> 1) & 1) ^ 1));
+        ptx::mbar_wait_backoff(&tempty[acc], DYF ? ((local >> 1) & 1) : (((local >> 1) & 1) ^ 1));
         c_te += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + acc * R * BN;
@@ -1841,7 +1847,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
       unsigned long long t0 = clock64();
-      ptx::mbar_wait(&tempty[acc], (local >> 1) & 1);  // the epilogue zeroes and arrives up front
+      ptx::mbar_wait_backoff(&tempty[acc], (local >> 1) & 1);  // the epilogue zeroes and arrives up front
       c_te += clock64() - t0;
       ptx::tc_fence_after();
       const uint32_t d_base = tmem_base + acc * R * BN;
