@@ -189,6 +189,8 @@ struct omniseg {
   DevBuf Wpre, bpre, Wc, bc;
   int nin = 0;
   cudaStream_t own_stream = nullptr, stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // progressive D2H of finished canvas rows (host outputs)
+  cudaEvent_t copy_ev = nullptr;
 
   // workspace (per patch size / batch capacity)
   int ws_P = 0, ws_B = 0;
@@ -246,6 +248,8 @@ struct omniseg {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (copy_ev) cudaEventDestroy(copy_ev);
   }
 };
 
@@ -817,30 +821,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
     tt.log2f[t] = tk.log2f[t];
   }
   upload_tasks(h, tk);
-  // ---- hot loop over batches of kept tiles
-  const int B = h->arch.batch;
-  double t_gather = 0;
-  const bool fused = h->stem_fused && getenv("OMNISEG_NO_STEM_FUSION") == nullptr;
-  const uint32_t* Lv[4] = {h->L1.as<uint32_t>(), h->L2.as<uint32_t>(), h->L4.as<uint32_t>(), h->L8.as<uint32_t>()};
-  for (int64_t first = 0; first < h->n_tiles; first += B) {
-    const int n = (int)std::min<int64_t>(B, h->n_tiles - first);
-    if (fused) {
-      // window gather + stem in one kernel (A5 + the first conv of A6)
-      run_prof(h, h->enc_plans[0], *h->enc_layers[0], 0, n, [&] {
-        run_stem(h->stem_plan, h->tiles.as<uint32_t>(), (int)first, n, Lv, S, Hp, Wp, s);
-      });
-      h->conv_launches++;
-    } else {
-      launch_gather<T>(h->tiles.as<uint32_t>(), (int)first, n, P, S, fp, st, h->L2.as<uint32_t>(),
-                       h->L4.as<uint32_t>(), h->L8.as<uint32_t>(), h->X0.as<T>(), s);
-      h->launches++;
-    }
-    run_trunk_and_head<T>(h, n, P, h->tiles.as<uint32_t>(), (int)first, fused, tt, tk.n, S, Hp, Wp, pad, nullptr, nullptr,
-                          nullptr);
-  }
-  (void)t_gather;
-  record(h, 3);
-  // ---- finalize into the caller's buffers (device) or staging + D2H (host)
+  // ---- outputs: the caller's device buffers, or device staging + D2H for host buffers
   const bool prob_dev = is_device_ptr(out_prob), mask_dev = is_device_ptr(out_mask);
   float* dprob = nullptr;
   uint8_t* dmask = nullptr;
@@ -860,19 +841,89 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   }
   h->area.ensure(kMaxTasks * 8);
   OS_CUDA(cudaMemsetAsync(h->area.p, 0, kMaxTasks * 8, s));
-  for (int t = 0; t < tk.n; ++t) {
-    const int64_t n = (r1[t] - r0[t]) * tk.Wt[t];
-    launch_finalize(tt.canvas[t], n, dprob ? dprob + off[t] : nullptr, dmask ? dmask + off[t] : nullptr,
+  // Host outputs are finalised and copied back PROGRESSIVELY: windows are ordered (scale
+  // descending, row, column), so once the batch loop has passed a window row of scale f, the
+  // canvas rows above the next pending window of that scale can no longer change. Those rows
+  // are finalised on the compute stream and their D2H runs on a copy stream under the
+  // remaining trunk work (bit-identical to finalising at the end).
+  const bool host_out = (out_prob && !prob_dev) || (out_mask && !mask_dev);
+  std::vector<int64_t> done(r0);
+  auto finalize_rows = [&](int t, int64_t ra, int64_t rb) {
+    if (rb <= ra) return;
+    const int64_t base = off[t] + (ra - r0[t]) * tk.Wt[t], n = (rb - ra) * tk.Wt[t];
+    launch_finalize(tt.canvas[t] + base - off[t], n, dprob ? dprob + base : nullptr, dmask ? dmask + base : nullptr,
                     h->area.as<unsigned long long>() + t, s);
     h->launches++;
+    if (host_out) {
+      if (!h->copy_stream) OS_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+      if (!h->copy_ev) OS_CUDA(cudaEventCreateWithFlags(&h->copy_ev, cudaEventDisableTiming));
+      OS_CUDA(cudaEventRecord(h->copy_ev, s));
+      OS_CUDA(cudaStreamWaitEvent(h->copy_stream, h->copy_ev, 0));
+      if (out_prob && !prob_dev)
+        OS_CUDA(cudaMemcpyAsync(out_prob + base, dprob + base, (size_t)n * 4, cudaMemcpyDeviceToHost, h->copy_stream));
+      if (out_mask && !mask_dev)
+        OS_CUDA(cudaMemcpyAsync(out_mask + base, dmask + base, (size_t)n, cudaMemcpyDeviceToHost, h->copy_stream));
+    }
+    done[t] = rb;
+  };
+  // per-scale ranges of the (host copy of the) kept-window list
+  int64_t sb[4] = {0, 0, 0, 0}, se[4] = {0, 0, 0, 0};
+  if (host_out && h->n_tiles > 0) {
+    h->h_tiles.resize(h->n_tiles);
+    OS_CUDA(cudaMemcpyAsync(h->h_tiles.data(), h->tiles.p, h->n_tiles * 4, cudaMemcpyDeviceToHost, s));
+    OS_CUDA(cudaStreamSynchronize(s));
+    for (int l = 0; l < 4; ++l) sb[l] = se[l] = -1;
+    for (int64_t i = 0; i < h->n_tiles; ++i) {
+      const int l = h->h_tiles[i] >> 30;
+      if (sb[l] < 0) sb[l] = i;
+      se[l] = i + 1;
+    }
   }
+  auto progress = [&](int64_t k) {  // windows [0, k) are done
+    for (int t = 0; t < tk.n; ++t) {
+      const int l = tk.log2f[t], f = 1 << l;
+      int64_t safe;
+      if (sb[l] < 0 || k >= se[l]) safe = r1[t];
+      else if (k <= sb[l]) safe = r0[t];
+      else {
+        const int ty = (h->h_tiles[k] >> 15) & 0x7FFF;
+        const int64_t oy = std::min<int64_t>((int64_t)ty * S, Hp / f - P);
+        safe = std::max(r0[t], std::min(r1[t], oy - pad / f));
+      }
+      if (safe - done[t] >= 256 || (safe == r1[t] && safe > done[t])) finalize_rows(t, done[t], safe);
+    }
+  };
+  // ---- hot loop over batches of kept tiles
+  const int B = h->arch.batch;
+  const bool fused = h->stem_fused && getenv("OMNISEG_NO_STEM_FUSION") == nullptr;
+  const uint32_t* Lv[4] = {h->L1.as<uint32_t>(), h->L2.as<uint32_t>(), h->L4.as<uint32_t>(), h->L8.as<uint32_t>()};
+  for (int64_t first = 0; first < h->n_tiles; first += B) {
+    const int n = (int)std::min<int64_t>(B, h->n_tiles - first);
+    if (fused) {
+      // window gather + stem in one kernel (A5 + the first conv of A6)
+      run_prof(h, h->enc_plans[0], *h->enc_layers[0], 0, n, [&] {
+        run_stem(h->stem_plan, h->tiles.as<uint32_t>(), (int)first, n, Lv, S, Hp, Wp, s);
+      });
+      h->conv_launches++;
+    } else {
+      launch_gather<T>(h->tiles.as<uint32_t>(), (int)first, n, P, S, fp, st, h->L2.as<uint32_t>(),
+                       h->L4.as<uint32_t>(), h->L8.as<uint32_t>(), h->X0.as<T>(), s);
+      h->launches++;
+    }
+    run_trunk_and_head<T>(h, n, P, h->tiles.as<uint32_t>(), (int)first, fused, tt, tk.n, S, Hp, Wp, pad, nullptr, nullptr,
+                          nullptr);
+    if (host_out) progress(first + n);
+  }
+  record(h, 3);
+  // ---- finalize the remaining rows
+  for (int t = 0; t < tk.n; ++t) finalize_rows(t, done[t], r1[t]);
   if (h->comm)
     g_nccl.check(g_nccl.allReduce(h->area.p, h->area.p, tk.n, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(area)");
   record(h, 4);
-  if (out_prob && !prob_dev)
-    OS_CUDA(cudaMemcpyAsync(out_prob, dprob, (size_t)canvas_px * 4, cudaMemcpyDeviceToHost, s));
-  if (out_mask && !mask_dev)
-    OS_CUDA(cudaMemcpyAsync(out_mask, dmask, (size_t)canvas_px, cudaMemcpyDeviceToHost, s));
+  if (host_out) {  // the compute stream waits for the progressive copies
+    OS_CUDA(cudaEventRecord(h->copy_ev, h->copy_stream));
+    OS_CUDA(cudaStreamWaitEvent(s, h->copy_ev, 0));
+  }
   if (out_area) OS_CUDA(cudaMemcpyAsync(out_area, h->area.p, tk.n * 8, cudaMemcpyDefault, s));
   record(h, 5);
   OS_CUDA(cudaStreamSynchronize(s));
