@@ -29,7 +29,7 @@ def parse_arch(s: str) -> dict:
         d[k.strip()] = v.strip()
     return dict(levels=int(d["levels"]), base=int(d["base"]), ncls=int(d["ncls"]),
                 scale_codes=[int(x) for x in d["scale_codes"].split(",")],
-                slide_mag=int(d["slide_mag"]))
+                slide_mag=int(d["slide_mag"]), fusion=d.get("fusion", "mean"))
 
 
 def unpack_weights(arch: dict, blob: np.ndarray) -> dict:

@@ -42,10 +42,17 @@ def canvas_shape(H, W, f):
 
 
 def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, stride: int,
-                  scales, classes, progress=None):
+                  scales, classes, progress=None, fusion=None):
     """Plain CPU pipeline. Returns dict with per-task prob (float64),
-    mask (u8), area (int), the kept tile list, fg mask and Otsu t."""
+    mask (u8), area (int), the kept tile list, fg mask and Otsu t.
+    fusion: "mean" (overlap-weighted mean of p, DESIGN R11) or "vote" (hard majority vote,
+    SURVEY N1: each window votes p >= 1/2, "majority of the testing results", "1 of
+    2" / "4 of 8" -- both "at least half"); default: the arch string's `fusion` key, else mean."""
     arch = nn.parse_arch(arch_s)
+    if fusion is None:
+        fusion = arch.get("fusion", "mean")
+    if fusion not in ("mean", "vote"):
+        raise ValueError("fusion must be mean or vote")
     net = nn.unpack_weights(arch, blob)
     H, W, _ = slide.shape
     tf = task_factors(arch, scales)
@@ -60,7 +67,8 @@ def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, st
         tasks = [(t, classes[t], s) for t, (ft, s) in enumerate(tf) if ft == f]
         p = nn.predict_tile(net, arch, tile, [(c, s) for _, c, s in tasks])
         for k, (t, _c, _s) in enumerate(tasks):
-            stitch_add(sums[t], cnts[t], p[k], oy - pad // f, ox - pad // f)
+            val = vote_of(p[k]) if fusion == "vote" else p[k]
+            stitch_add(sums[t], cnts[t], val, oy - pad // f, ox - pad // f)
         if progress:
             progress(i, len(fr["kept"]))
     probs, masks, areas = [], [], []
@@ -72,6 +80,11 @@ def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, st
     return dict(prob=probs, mask=masks, area=areas, kept=fr["kept"], grids=fr["grids"],
                 fg=fr["det"]["fg"], t=fr["det"]["t"], hist=fr["det"]["hist"],
                 g_pad=fr["det"]["g_pad"], cnt=cnts)
+
+
+def vote_of(p):
+    """A window's binary vote per pixel: p >= 1/2 (P:97 thresholds)."""
+    return (np.asarray(p) >= 0.5).astype(np.float64)
 
 
 def stitch_add(acc_sum, acc_cnt, p, y0, x0):

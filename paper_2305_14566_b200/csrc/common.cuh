@@ -58,7 +58,16 @@ struct HeadTaskTable {
   int Ht[kMaxTasks], Wt[kMaxTasks];
   int row0[kMaxTasks], row1[kMaxTasks];
   int log2f[kMaxTasks];
+  int vote;  // fusion rule: 0 mean of p (R11), 1 hard majority vote
 };
+
+// Canvas accumulator update of one window-task pixel (R12). Mean fusion: count << 28 plus
+// round(p 2^20); vote fusion ("majority of the testing results", P:97 votes): count << 16
+// plus the window's binary decision p >= 1/2, taken as z >= 0 (sigma(z) >= 1/2 exactly, the
+// fp64 oracle's decision without fp32 rounding of p).
+__device__ __forceinline__ uint32_t stitch_value(float p, float z, int vote) {
+  return vote ? (1u << 16) + (z >= 0.f ? 1u : 0u) : (1u << 28) + __float2uint_rn(p * 1048576.0f);
+}
 
 // Everything the dynamic head + stitch needs (fused into the last decoder conv).
 struct HeadArgs {

@@ -520,8 +520,7 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
       const int cy = oy + y - ha.pad / f, cx = ox + x - ha.pad / f;
       const int Wt = ha.tt.Wt[t];
       if (cy >= 0 && cy < ha.tt.Ht[t] && cx >= 0 && cx < Wt && cy >= ha.tt.row0[t] && cy < ha.tt.row1[t]) {
-        const uint32_t qv = __float2uint_rn(p * 1048576.0f);
-        atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, (1u << 28) + qv);
+        atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, stitch_value(p, z, ha.tt.vote));
       }
     }
   }
@@ -613,8 +612,7 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
         const int cy = oy + y - ha.pad / f, cx = ox + x - ha.pad / f;
         const int Wt = ha.tt.Wt[t];
         if (cy >= 0 && cy < ha.tt.Ht[t] && cx >= 0 && cx < Wt && cy >= ha.tt.row0[t] && cy < ha.tt.row1[t]) {
-          const uint32_t qv = __float2uint_rn(p * 1048576.0f);
-          atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, (1u << 28) + qv);
+          atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, stitch_value(p, zz, ha.tt.vote));
         }
       }
     }

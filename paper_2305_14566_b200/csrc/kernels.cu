@@ -625,8 +625,7 @@ __global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, 
         const int cy = oy + y - pad / f, cx = ox + x - pad / f;
         const int Wt = tt.Wt[t];
         if (cy >= 0 && cy < tt.Ht[t] && cx >= 0 && cx < Wt && cy >= tt.row0[t] && cy < tt.row1[t]) {
-          const uint32_t qv = __float2uint_rn(p * 1048576.0f);
-          atomicAdd(tt.canvas[t] + (int64_t)(cy - tt.row0[t]) * Wt + cx, (1u << 28) + qv);
+          atomicAdd(tt.canvas[t] + (int64_t)(cy - tt.row0[t]) * Wt + cx, stitch_value(p, z, tt.vote));
         }
       }
     }
@@ -636,17 +635,21 @@ __global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, 
 // ------------------------------------------------------------------ K10 finalize
 // cnt = acc >> 28, sum = acc & (2^28 - 1): prob = sum 2^-20 / cnt (0 if cnt = 0),
 // mask = 2 sum >= cnt 2^20 (exactly prob >= 1/2 on the fixed-point values, R12), area.
+// vote: the accumulator is count << 16 | votes (hard majority vote): prob = vote
+// fraction, mask = 2 votes >= count; else count << 28 | sum(round(p 2^20)) (R12).
 __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask,
-                                unsigned long long* area) {
+                                unsigned long long* area, int vote) {
   __shared__ unsigned long long s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
   unsigned long long local = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t a = acc[i];
-    const uint32_t cnt = a >> 28, sum = a & 0x0FFFFFFFu;
-    const bool m = cnt > 0 && 2ull * sum >= ((unsigned long long)cnt << 20);
-    if (prob) prob[i] = cnt ? (float(sum) * (1.0f / 1048576.0f)) / float(cnt) : 0.f;
+    const int sh = vote ? 16 : 28;
+    const uint32_t cnt = a >> sh, sum = a & ((1u << sh) - 1u);
+    const int fb = vote ? 0 : 20;  // fixed-point bits of the per-window value
+    const bool m = cnt > 0 && 2ull * sum >= ((unsigned long long)cnt << fb);
+    if (prob) prob[i] = cnt ? (float(sum) * (vote ? 1.0f : 1.0f / 1048576.0f)) / float(cnt) : 0.f;
     if (mask) mask[i] = m ? 1 : 0;
     local += m;
   }
@@ -772,11 +775,11 @@ void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const fl
   head_stitch_kernel<T><<<grid, 128, 0, s>>>(D0, C0p, C0, split, P, Wpre, bpre, theta, ntasks, tiles, first, tt, S, Hp, Wp,
                                              pad, out_p, out_F);
 }
-void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area,
+void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area, int vote,
                      cudaStream_t s) {
   if (n <= 0) return;
   int blocks = (int)std::min<int64_t>(8 * 148, (n + 255) / 256);
-  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area);
+  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area, vote);
 }
 template <typename T>
 void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, int rc_w, cudaStream_t s) {

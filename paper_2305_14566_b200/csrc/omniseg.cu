@@ -99,6 +99,7 @@ struct Arch {
   int split = kStorePlain;  // StoreKind of the activations: fp16/bf16 plain, x2 (hi + lo 16-bit), f8 (fp16 + e4m3 lo)
   int xlevels = -1;         // split storage only for tensors at U-Net levels < xlevels (-1: all levels)
   int xa = 1;               // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
+  int vote = 0;             // fusion rule: 0 mean of p (R11), 1 hard majority vote
   int sp(int level) const { return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain; }
   // bytes per channel of a tensor stored with kind k
   static int bpc(int k) { return k == kStoreX2 ? 4 : k == kStoreF8 ? 3 : 2; }
@@ -135,6 +136,10 @@ Arch parse_arch(const char* s) {
     else if (k == "device") a.device = toi(v);
     else if (k == "xlevels") a.xlevels = toi(v);
     else if (k == "xa") a.xa = toi(v);
+    else if (k == "fusion") {
+      OS_REQUIRE(v == "mean" || v == "vote", "arch: fusion must be mean or vote");
+      a.vote = v == "vote";
+    }
     else if (k == "dtype") {
       OS_REQUIRE(v == "fp16" || v == "bf16" || v == "fp16x2" || v == "bf16x2" || v == "fp16f8",
                  "arch: dtype must be fp16, bf16, fp16x2, bf16x2 or fp16f8");
@@ -802,6 +807,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   record(h, 2);
   // ---- canvases (owned rows only)
   HeadTaskTable tt{};
+  tt.vote = h->arch.vote;
   int64_t canvas_px = 0;
   std::vector<int64_t> off(tk.n);
   std::vector<int64_t> r0(tk.n), r1(tk.n);
@@ -852,7 +858,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
     if (rb <= ra) return;
     const int64_t base = off[t] + (ra - r0[t]) * tk.Wt[t], n = (rb - ra) * tk.Wt[t];
     launch_finalize(tt.canvas[t] + base - off[t], n, dprob ? dprob + base : nullptr, dmask ? dmask + base : nullptr,
-                    h->area.as<unsigned long long>() + t, s);
+                    h->area.as<unsigned long long>() + t, h->arch.vote, s);
     h->launches++;
     if (host_out) {
       if (!h->copy_stream) OS_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
@@ -949,14 +955,17 @@ int fail(const Error& e) {
   return e.code;
 }
 
-void validate_common(int64_t H, int64_t W, int pad, int P, int S) {
+void validate_common(int64_t H, int64_t W, int pad, int P, int S, bool vote) {
   OS_REQUIRE(H >= 2 && W >= 2, "H and W must be >= 2");
   OS_REQUIRE(pad >= 0 && pad % 8 == 0, "pad must be a non-negative multiple of 8");
   OS_REQUIRE(S >= 8 && S <= P && S % 8 == 0, "stride must satisfy 8 <= stride <= patch, stride % 8 == 0");
   OS_REQUIRE(P % 8 == 0, "patch must be a multiple of 8");
   OS_REQUIRE((H / 8) * (W / 8) < (int64_t(1) << 28), "slide too large for the exact Otsu (interior >= 2^28 px)");
   const int per_axis = (P + S - 1) / S + 1;
-  OS_REQUIRE(per_axis * per_axis <= 15, "coverage count could exceed 15: need (ceil(P/S)+1)^2 <= 15");
+  if (vote)
+    OS_REQUIRE(per_axis * per_axis <= 65535, "vote fusion: coverage count could exceed 16 bits");
+  else
+    OS_REQUIRE(per_axis * per_axis <= 15, "coverage count could exceed 15: need (ceil(P/S)+1)^2 <= 15");
 }
 
 }  // namespace
@@ -1032,7 +1041,7 @@ int omniseg_segment_slide(omniseg_t* h, const uint8_t* rgb_u8, int64_t H, int64_
     OS_REQUIRE(h != nullptr, "handle is NULL");
     OS_REQUIRE(rgb_u8 != nullptr, "rgb_u8 is NULL");
     OS_CUDA(cudaSetDevice(h->device));
-    validate_common(H, W, pad, patch, stride);
+    validate_common(H, W, pad, patch, stride, h->arch.vote != 0);
     Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
     const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
     if (h->arch.bf16)
@@ -1077,7 +1086,7 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
   try {
     OS_REQUIRE(h != nullptr, "handle is NULL");
     OS_CUDA(cudaSetDevice(h->device));
-    validate_common(H, W, pad, patch, stride);
+    validate_common(H, W, pad, patch, stride, h->arch.vote != 0);
     Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
     const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
     OS_REQUIRE(row0 >= 0 && row0 < row1 && row1 <= Hp, "band: need 0 <= row0 < row1 <= Hp");

@@ -94,6 +94,26 @@ def test_cfg1_f8_gated(gpu_lib):
     print(f"fp16f8: max |dp| {dmax:.4g}, mask agreement {agree:.5f}")
 
 
+def test_cfg1_vote_fusion(gpu_lib):
+    """Hard majority-vote fusion (arch fusion=vote) against the oracle's vote mode:
+    every window votes p >= 1/2; the canvas holds the vote fraction, the mask is 'at least
+    half'. A window's vote can differ only where its p is within rounding of 1/2, so vote
+    fractions and masks must agree on >= 99.9% of pixels."""
+    w = workload(1)
+    w.arch["fusion"] = "vote"
+    slide, _ = _cfg1_ref()
+    ref = op.segment_slide(slide, w.weights(), arch_string(w.arch), w.pad, w.patch, w.stride, w.scales, w.classes)
+    h, prob, mask, area = run_gpu(w, slide)
+    H, W = slide.shape[:2]
+    p = prob.reshape(H, W).astype(np.float64)
+    m = mask.reshape(H, W)
+    same = np.abs(p - ref["prob"][0]) <= 1e-6
+    agree = (m == ref["mask"][0]).mean()
+    print(f"vote: fraction-equal {same.mean():.5f}, mask agreement {agree:.5f}")
+    assert same.mean() >= 0.999 and agree >= 0.999
+    assert int(area[0]) == int(m.sum())
+
+
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
 def test_cfg1_16bit_storage_numerics_report(gpu_lib, dtype):
     """Plain 16-bit activation storage (BASELINE configs' 'bf16 activations', and fp16):

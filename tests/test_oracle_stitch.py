@@ -97,3 +97,49 @@ def test_covering_tiles_matches_count_canvas():
     for _ in range(50):
         y, x = int(rng.integers(0, H)), int(rng.integers(0, W))
         assert len(op.covering_tiles(fr["kept"], 1, w.pad, w.patch, y, x)) == cnt[y, x]
+
+
+# ---------------------------------------------------------------- hard-vote fusion
+def test_vote_of_threshold_is_at_least_half():
+    """the paper's thresholds (1 of 2, 4 of 8) are 'at least half' -- a window votes
+    positive iff p >= 1/2, ties included."""
+    p = np.array([0.0, 0.4999999, 0.5, 0.5000001, 1.0])
+    assert op.vote_of(p).tolist() == [0, 0, 1, 1, 1]
+
+
+def test_vote_fusion_matches_brute_force_majority():
+    """Vote fraction and mask against an explicit per-pixel count of covering windows and
+    positive votes (brute force over tiles), including exact ties (2 of 4 -> positive)."""
+    rng = np.random.default_rng(5)
+    H, W, P = 40, 44, 16
+    tiles = [(int(rng.integers(-8, 36)), int(rng.integers(-8, 40))) for _ in range(30)]
+    ps = [rng.random((P, P)) for _ in tiles]
+    s, c = np.zeros((H, W)), np.zeros((H, W), np.int64)
+    for (y, x), p in zip(tiles, ps):
+        op.stitch_add(s, c, op.vote_of(p), y, x)
+    prob, mask = op.finalize(s, c)
+    for yy in range(H):
+        for xx in range(W):
+            votes = cov = 0
+            for (y, x), p in zip(tiles, ps):
+                if y <= yy < y + P and x <= xx < x + P:
+                    cov += 1
+                    votes += int(p[yy - y, xx - x] >= 0.5)
+            assert c[yy, xx] == cov
+            assert prob[yy, xx] == (votes / cov if cov else 0.0)
+            assert mask[yy, xx] == int(cov > 0 and 2 * votes >= cov)
+
+
+def test_vote_equals_thresholded_mean_where_one_window_covers():
+    """End to end (cfg1): where exactly one kept window covers a pixel, the vote fraction is
+    that window's decision, i.e. the mean-fusion probability thresholded at 1/2."""
+    w = workload(1)
+    slide = make_slide(w.slide).numpy()
+    a = arch_string(w.arch)
+    rm = op.segment_slide(slide, w.weights(), a, w.pad, w.patch, w.stride, w.scales, w.classes)
+    rv = op.segment_slide(slide, w.weights(), a, w.pad, w.patch, w.stride, w.scales, w.classes, fusion="vote")
+    one = rm["cnt"][0] == 1
+    assert one.sum() > 1000
+    assert (rv["prob"][0][one] == (rm["prob"][0][one] >= 0.5)).all()
+    k = rv["prob"][0] * rm["cnt"][0]  # vote fractions are (integer votes) / cnt
+    assert np.allclose(k, np.round(k), atol=1e-9)
