@@ -43,6 +43,10 @@ def arch_string(a: dict) -> str:
         s += ";xa=%d" % a["xa"]
     if a.get("fusion") is not None:
         s += ";fusion=%s" % a["fusion"]
+    if a.get("fgmin") is not None:
+        s += ";fgmin=%d" % a["fgmin"]
+    if a.get("maskfg") is not None:
+        s += ";maskfg=%d" % a["maskfg"]
     return s
 
 

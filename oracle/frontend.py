@@ -101,7 +101,7 @@ def otsu_threshold(hist) -> int:
     return best_t
 
 
-def detection(padded: np.ndarray, H: int, W: int, pad: int, k: int = 7, guard: int = 16):
+def detection(padded: np.ndarray, H: int, W: int, pad: int, k: int = 7, guard: int = 16, min_area: int = 0):
     """Tissue detection at 5x = level 8. [SURVEY O4-O5]
 
     Returns dict(g8 = luma of level 8, gm = median-blurred luma, hist (interior),
@@ -122,7 +122,26 @@ def detection(padded: np.ndarray, H: int, W: int, pad: int, k: int = 7, guard: i
     pc = padded[0, 0]
     g_pad = int(luma(pc[None, None, :])[0, 0])
     fg = interior & (gm.astype(np.int64) <= t) & (gm.astype(np.int64) <= g_pad - guard)
+    if min_area > 0:  # SURVEY N2 (arch fgmin): components below min_area level-8 pixels dropped
+        fg = drop_small_components(fg, min_area)
     return dict(g8=g8, gm=gm, hist=hist, t=t, g_pad=g_pad, fg=fg.astype(np.uint8))
+
+
+def drop_small_components(fg: np.ndarray, min_area: int) -> np.ndarray:
+    """Tiny-noise removal ("the foreground contour was set to a certain threshold to
+    remove tiny noises"; S:124-127 detect_foreground: 4-connected components, drop those
+    below min_component_area). Labelling by scipy.ndimage.label with the
+    4-neighbour cross (a library primitive, pinned against a brute-force flood fill in
+    tests/test_oracle_frontend.py); keep components with >= min_area pixels."""
+    from scipy import ndimage
+    fg = np.asarray(fg).astype(bool)
+    if min_area <= 0 or not fg.any():
+        return fg.astype(np.uint8)
+    lab, _ = ndimage.label(fg, structure=[[0, 1, 0], [1, 1, 1], [0, 1, 0]])
+    sizes = np.bincount(lab.ravel())
+    keep = sizes >= min_area
+    keep[0] = False
+    return keep[lab].astype(np.uint8)
 
 
 def origins(E: int, P: int, S: int):

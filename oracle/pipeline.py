@@ -24,12 +24,13 @@ def task_factors(arch: dict, scales):
     return out
 
 
-def front_end(slide: np.ndarray, pad: int, patch: int, stride: int, factors):
-    """O1-O6: pad colour, padded frame, level-8 detection, tile plan."""
+def front_end(slide: np.ndarray, pad: int, patch: int, stride: int, factors, min_area: int = 0):
+    """O1-O6: pad colour, padded frame, level-8 detection (+ the optional tiny-component
+    removal), tile plan."""
     H, W, _ = slide.shape
     padded = fe.pad_slide(slide, pad)
     Hp, Wp = padded.shape[:2]
-    det = fe.detection(padded, H, W, pad)
+    det = fe.detection(padded, H, W, pad, min_area=min_area)
     kept, grids = fe.tile_plan(det["fg"], Hp, Wp, factors, patch, stride)
     return dict(padded=padded, Hp=Hp, Wp=Wp, det=det, kept=kept, grids=grids,
                 pc=fe.pad_colour(slide))
@@ -56,7 +57,7 @@ def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, st
     net = nn.unpack_weights(arch, blob)
     H, W, _ = slide.shape
     tf = task_factors(arch, scales)
-    fr = front_end(slide, pad, patch, stride, [f for f, _ in tf])
+    fr = front_end(slide, pad, patch, stride, [f for f, _ in tf], min_area=arch.get("fgmin", 0))
     levels = {f: fe.level(fr["padded"], f) for f in set(f for f, _ in tf)}
     sums, cnts = [], []
     for (f, _s) in tf:
@@ -74,6 +75,8 @@ def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, st
     probs, masks, areas = [], [], []
     for t in range(len(tf)):
         prob, mask = finalize(sums[t], cnts[t])
+        if arch.get("maskfg", 0):
+            mask = mask_by_foreground(mask, fr["det"]["fg"], tf[t][0], pad)
         probs.append(prob)
         masks.append(mask)
         areas.append(int(mask.sum()))
@@ -107,6 +110,17 @@ def finalize(acc_sum, acc_cnt):
     (the paper's 1-of-2 and 4-of-8 votes are both 'at least half'; DESIGN R11)."""
     prob = np.where(acc_cnt > 0, acc_sum / np.maximum(acc_cnt, 1), 0.0)
     return prob, (prob >= 0.5).astype(np.uint8)
+
+
+def mask_by_foreground(mask, fg8, f, pad):
+    """P:87 §2.3 "the foreground contour generated during tissue detection was utilized again to
+    filter out noises from the prediction"; S:350 filter_by_foreground: map AND mask with the
+    mask nearest-neighbour rescaled. Canvas pixel (cy, cx) of a task at level f
+    is padded-40x pixel (cy f + pad, cx f + pad), i.e. level-8 pixel ((cy f + pad) // 8, ...)."""
+    Ht, Wt = mask.shape
+    ys = (np.arange(Ht) * f + pad) // 8
+    xs = (np.arange(Wt) * f + pad) // 8
+    return (mask.astype(bool) & fg8[np.ix_(ys, xs)].astype(bool)).astype(np.uint8)
 
 
 def covering_tiles(kept, f, pad, patch, cy, cx):

@@ -637,8 +637,10 @@ __global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, 
 // mask = 2 sum >= cnt 2^20 (exactly prob >= 1/2 on the fixed-point values, R12), area.
 // vote: the accumulator is count << 16 | votes (hard majority vote): prob = vote
 // fraction, mask = 2 votes >= count; else count << 28 | sum(round(p 2^20)) (R12).
+// fg8 (optional, SURVEY N2 / P:87): the mask is ANDed with the level-8 foreground, nearest-
+// neighbour: canvas pixel (cy, cx) -> level-8 pixel ((cy f + pad) / 8, (cx f + pad) / 8).
 __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask,
-                                unsigned long long* area, int vote) {
+                                unsigned long long* area, int vote, FgMaskArgs fm) {
   __shared__ unsigned long long s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
@@ -648,7 +650,11 @@ __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uin
     const int sh = vote ? 16 : 28;
     const uint32_t cnt = a >> sh, sum = a & ((1u << sh) - 1u);
     const int fb = vote ? 0 : 20;  // fixed-point bits of the per-window value
-    const bool m = cnt > 0 && 2ull * sum >= ((unsigned long long)cnt << fb);
+    bool m = cnt > 0 && 2ull * sum >= ((unsigned long long)cnt << fb);
+    if (fm.fg8 && m) {
+      const int64_t cy = fm.cy0 + i / fm.Wt, cx = i % fm.Wt;
+      m = fm.fg8[((cy * fm.f + fm.pad) >> 3) * (int64_t)fm.W8 + ((cx * fm.f + fm.pad) >> 3)] != 0;
+    }
     if (prob) prob[i] = cnt ? (float(sum) * (vote ? 1.0f : 1.0f / 1048576.0f)) / float(cnt) : 0.f;
     if (mask) mask[i] = m ? 1 : 0;
     local += m;
@@ -658,6 +664,59 @@ __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uin
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(&s, local);
   __syncthreads();
   if (threadIdx.x == 0 && s) atomicAdd(area, s);
+}
+
+// ------------------------------------------------------------------ N2: tiny-component removal
+// 4-connected components of the level-8 foreground rows [r0, r1) by union-find (union by the
+// smaller index with atomicMin, so every root is its component's smallest index: the result
+// is independent of the thread schedule), component sizes by atomics on the roots, then every
+// pixel of a component with fewer than min_area pixels is cleared ("remove
+// tiny noises").
+__device__ __forceinline__ int uf_find(const int* l, int x) {
+  int p = l[x];
+  while (p != x) {
+    x = p;
+    p = l[x];
+  }
+  return x;
+}
+__device__ __forceinline__ void uf_unite(int* l, int a, int b) {
+  for (;;) {
+    a = uf_find(l, a);
+    b = uf_find(l, b);
+    if (a == b) return;
+    if (a < b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    // link the larger root a under b; retry if a stopped being a root meanwhile
+    const int old = atomicMin(l + a, b);
+    if (old == a) return;
+    a = old;
+  }
+}
+__global__ void cc_init_kernel(const uint8_t* fg, int* lab, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) lab[i] = fg[i] ? (int)i : -1;
+}
+__global__ void cc_merge_kernel(const uint8_t* fg, int* lab, int W, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !fg[i]) return;
+  const int x = (int)(i % W);
+  if (x > 0 && fg[i - 1]) uf_unite(lab, (int)i, (int)(i - 1));
+  if (i >= W && fg[i - W]) uf_unite(lab, (int)i, (int)(i - W));
+}
+__global__ void cc_count_kernel(const uint8_t* fg, int* lab, int* size, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !fg[i]) return;
+  const int r = uf_find(lab, (int)i);
+  lab[i] = r;
+  atomicAdd(size + r, 1);
+}
+__global__ void cc_filter_kernel(uint8_t* fg, const int* lab, const int* size, int min_area, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && fg[i] && size[lab[i]] < min_area) fg[i] = 0;
 }
 
 // ------------------------------------------------------------------ conversions (debug / weights)
@@ -776,10 +835,21 @@ void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const fl
                                              pad, out_p, out_F);
 }
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area, int vote,
-                     cudaStream_t s) {
+                     const FgMaskArgs& fm, cudaStream_t s) {
   if (n <= 0) return;
   int blocks = (int)std::min<int64_t>(8 * 148, (n + 255) / 256);
-  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area, vote);
+  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area, vote, fm);
+}
+void launch_fg_components(uint8_t* fg, int W, int r0, int r1, int min_area, int* lab, int* size, cudaStream_t s) {
+  const int64_t n = (int64_t)(r1 - r0) * W;
+  if (n <= 0 || min_area <= 0) return;
+  uint8_t* f = fg + (int64_t)r0 * W;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  OS_CUDA(cudaMemsetAsync(size, 0, n * sizeof(int), s));
+  cc_init_kernel<<<g, 256, 0, s>>>(f, lab, n);
+  cc_merge_kernel<<<g, 256, 0, s>>>(f, lab, W, n);
+  cc_count_kernel<<<g, 256, 0, s>>>(f, lab, size, n);
+  cc_filter_kernel<<<g, 256, 0, s>>>(f, lab, size, min_area, n);
 }
 template <typename T>
 void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, int rc_w, cudaStream_t s) {

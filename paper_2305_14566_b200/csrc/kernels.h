@@ -42,8 +42,17 @@ template <typename T>
 void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
                  const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
                  int Hp, int Wp, int pad, float* out_p, float* out_F, cudaStream_t s);
+// Optional foreground filter of the finalized mask: canvas row of element 0 = cy0.
+struct FgMaskArgs {
+  const uint8_t* fg8 = nullptr;  // level-8 foreground (full grid, row stride W8); NULL: off
+  int W8 = 0, f = 1, pad = 0, Wt = 1;
+  int64_t cy0 = 0;
+};
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area, int vote,
-                     cudaStream_t s);
+                     const FgMaskArgs& fm, cudaStream_t s);
+// Tiny-component removal on level-8 foreground rows [r0, r1) (lab, size: scratch of
+// (r1 - r0) W ints each).
+void launch_fg_components(uint8_t* fg, int W, int r0, int r1, int min_area, int* lab, int* size, cudaStream_t s);
 template <typename T>
 void launch_f32_to_t(const float* in, T* out, int64_t rows, int cin, int cpad, int split, int rc_w, cudaStream_t s);
 template <typename T>

@@ -100,6 +100,8 @@ struct Arch {
   int xlevels = -1;         // split storage only for tensors at U-Net levels < xlevels (-1: all levels)
   int xa = 1;               // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
   int vote = 0;             // fusion rule: 0 mean of p (R11), 1 hard majority vote
+  int fgmin = 0;            // drop foreground components below fgmin level-8 pixels
+  int maskfg = 0;           // AND the output masks with the foreground
   int sp(int level) const { return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain; }
   // bytes per channel of a tensor stored with kind k
   static int bpc(int k) { return k == kStoreX2 ? 4 : k == kStoreF8 ? 3 : 2; }
@@ -136,6 +138,8 @@ Arch parse_arch(const char* s) {
     else if (k == "device") a.device = toi(v);
     else if (k == "xlevels") a.xlevels = toi(v);
     else if (k == "xa") a.xa = toi(v);
+    else if (k == "fgmin") a.fgmin = toi(v);
+    else if (k == "maskfg") a.maskfg = toi(v);
     else if (k == "fusion") {
       OS_REQUIRE(v == "mean" || v == "vote", "arch: fusion must be mean or vote");
       a.vote = v == "vote";
@@ -216,6 +220,7 @@ struct omniseg {
   bool stem_fused = false;
   bool head_fusable = false;
   // front end / canvases
+  DevBuf cc_lab, cc_size;  // SURVEY N2 component-labelling scratch
   DevBuf slide, L1, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
   std::vector<uint32_t> h_tiles;
   int64_t n_tiles = 0;
@@ -769,6 +774,13 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   OS_CUDA(cudaMemcpyAsync(h->last_hist, h->hist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
   launch_otsu(h->hist.as<unsigned long long>(), st, s);
   launch_fg(h->gm.as<uint8_t>(), h->fg.as<uint8_t>(), W8, m0, m1, ir0, ir1, ic0, ic1, st, s);
+  if (h->arch.fgmin > 0) {
+    // tiny-component removal needs whole components: single-slide calls only (see the band check)
+    const size_t nfg = (size_t)(m1 - m0) * W8;
+    h->cc_lab.ensure(nfg * 4);
+    h->cc_size.ensure(nfg * 4);
+    launch_fg_components(h->fg.as<uint8_t>(), W8, m0, m1, h->arch.fgmin, h->cc_lab.as<int>(), h->cc_size.as<int>(), s);
+  }
   // candidate grids (canonical order: factor descending, row, col)
   std::vector<ScaleGrid> grids(tk.nf);
   int total = 0;
@@ -857,8 +869,17 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   auto finalize_rows = [&](int t, int64_t ra, int64_t rb) {
     if (rb <= ra) return;
     const int64_t base = off[t] + (ra - r0[t]) * tk.Wt[t], n = (rb - ra) * tk.Wt[t];
+    FgMaskArgs fm;
+    if (h->arch.maskfg) {
+      fm.fg8 = h->fg.as<uint8_t>();
+      fm.W8 = W8;
+      fm.f = tk.f[t];
+      fm.pad = pad;
+      fm.Wt = (int)tk.Wt[t];
+      fm.cy0 = ra;
+    }
     launch_finalize(tt.canvas[t] + base - off[t], n, dprob ? dprob + base : nullptr, dmask ? dmask + base : nullptr,
-                    h->area.as<unsigned long long>() + t, h->arch.vote, s);
+                    h->area.as<unsigned long long>() + t, h->arch.vote, fm, s);
     h->launches++;
     if (host_out) {
       if (!h->copy_stream) OS_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
@@ -1086,6 +1107,7 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
   try {
     OS_REQUIRE(h != nullptr, "handle is NULL");
     OS_CUDA(cudaSetDevice(h->device));
+    OS_REQUIRE(h->arch.fgmin == 0, "band calls do not support fgmin (component removal needs whole components)");
     validate_common(H, W, pad, patch, stride, h->arch.vote != 0);
     Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
     const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;

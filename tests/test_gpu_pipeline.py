@@ -114,6 +114,26 @@ def test_cfg1_vote_fusion(gpu_lib):
     assert int(area[0]) == int(m.sum())
 
 
+def test_cfg1_component_removal_and_fg_mask(gpu_lib):
+    """SURVEY N2 (arch fgmin / maskfg): the level-8 foreground loses its components below
+    fgmin pixels (GPU union-find vs the oracle's labelling, bit-exact), the window plan follows
+    (bit-exact), and the output masks are ANDed with the foreground."""
+    w = workload(1)
+    w.arch["fgmin"] = 700      # cfg1's foreground components: 621, 741, 2043 level-8 px
+    w.arch["maskfg"] = 1
+    slide, _ = _cfg1_ref()
+    ref = op.segment_slide(slide, w.weights(), arch_string(w.arch), w.pad, w.patch, w.stride, w.scales, w.classes)
+    h, prob, mask, area = run_gpu(w, slide)
+    H, W = slide.shape[:2]
+    Hp, Wp = fe.padded_extent(H, W, w.pad)
+    fg, t, gpad = h.fgmask()
+    assert t == ref["t"] and (fg == ref["fg"]).all()
+    assert int(ref["fg"].sum()) == 741 + 2043
+    assert unpack_tiles(h.tiles(), Hp, Wp, w.patch, w.stride) == ref["kept"]
+    check_prob_mask(prob.reshape(H, W), mask.reshape(H, W), ref["prob"][0], ref["mask"][0], "fgmin")
+    assert int(area[0]) == int(mask.sum())
+
+
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
 def test_cfg1_16bit_storage_numerics_report(gpu_lib, dtype):
     """Plain 16-bit activation storage (BASELINE configs' 'bf16 activations', and fp16):

@@ -262,3 +262,56 @@ def test_chunked_detection_equals_whole_frame():
     assert a["g_pad"] == b["g_pad"]
     L1 = fe.level(p, 4)
     assert (fe.level_window(s, w.pad, fe.pad_colour(s), 4, 40, 12, 64) == L1[40:104, 12:76]).all()
+
+
+# ---------------------------------------------------------------- tiny-component removal
+def _flood_components(mask):
+    """Brute-force 4-connected components (explicit BFS), independent of scipy."""
+    H, W = mask.shape
+    lab = -np.ones((H, W), np.int64)
+    sizes = []
+    for y in range(H):
+        for x in range(W):
+            if mask[y, x] and lab[y, x] < 0:
+                k = len(sizes)
+                stack, n = [(y, x)], 0
+                lab[y, x] = k
+                while stack:
+                    cy, cx = stack.pop()
+                    n += 1
+                    for ny, nx in ((cy - 1, cx), (cy + 1, cx), (cy, cx - 1), (cy, cx + 1)):
+                        if 0 <= ny < H and 0 <= nx < W and mask[ny, nx] and lab[ny, nx] < 0:
+                            lab[ny, nx] = k
+                            stack.append((ny, nx))
+                sizes.append(n)
+    return lab, sizes
+
+
+def test_drop_small_components_matches_flood_fill():
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        m = (rng.random((23, 31)) < 0.45).astype(np.uint8)
+        lab, sizes = _flood_components(m)
+        for min_area in (1, 2, 3, 5, 9):
+            ref = np.zeros_like(m)
+            for k, n in enumerate(sizes):
+                if n >= min_area:
+                    ref[lab == k] = 1
+            assert (fe.drop_small_components(m, min_area) == ref).all(), (trial, min_area)
+
+
+def test_drop_small_components_spec_example_and_invariants():
+    """one large dark disk + a 3-pixel speck, min area above 3 -> exactly the disk
+    survives; diagonal-only contact does not connect (4-connectivity); filtering only removes;
+    blank stays blank."""
+    m = np.zeros((64, 64), np.uint8)
+    yy, xx = np.mgrid[:64, :64]
+    m[(yy - 30) ** 2 + (xx - 30) ** 2 <= 15 ** 2] = 1
+    m[2, 60:63] = 1                                   # 3-pixel speck
+    m[50, 50] = m[51, 51] = 1                         # diagonal pair = two 1-px components
+    out = fe.drop_small_components(m, 4)
+    assert out[2, 60:63].sum() == 0 and out[50, 50] == 0 and out[51, 51] == 0
+    assert (out[(yy - 30) ** 2 + (xx - 30) ** 2 <= 15 ** 2] == 1).all()
+    assert (out <= m).all()
+    assert fe.drop_small_components(np.zeros((8, 8), np.uint8), 5).sum() == 0
+    assert (fe.drop_small_components(m, 0) == m).all()
