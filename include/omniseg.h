@@ -116,6 +116,21 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
 int omniseg_band_rows(int64_t H, int64_t row0, int64_t row1, int pad, int f,
                       int64_t* r0_t, int64_t* r1_t);
 
+/* 40x merge + colour overlay + 10x overlay (§2.3 "stained with different colors
+ * on WSIs ... a final downsampled prediction of the 10x WSI ... by directly resizing the final
+ * prediction of the 40x image"). rgb_u8: the H x W x 3 slide; masks: the per-task masks
+ * exactly as omniseg_segment_slide returns them (tasks concatenated, each ceil(H/f) x ceil(W/f)
+ * u8 0/1) for the same scales[] / classes[]. Each task mask is upsampled nearest-neighbour to
+ * 40x; where several classes are positive the lowest class code wins (TUFT > CAP > PT > DT >
+ * PTC > VES, codes 0..5); a positive pixel becomes round(0.4 colour + 0.6 base) per channel with
+ * the fixed palette TUFT (255,0,0), CAP (255,128,0), PT (0,255,0), DT (0,128,255), PTC
+ * (255,0,255), VES (128,0,128) (the paper gives no values), others keep the slide pixel.
+ * out40: H x W x 3 (or NULL); out10: ceil(H/4) x ceil(W/4) x 3 factor-4 area mean of the 40x
+ * overlay, round half up, partial edge blocks averaging their pixels (or NULL). Host or device
+ * pointers; synchronous. -1 on bad arguments (class code >= 6, no output). */
+int omniseg_render_overlay(omniseg_t* h, const uint8_t* rgb_u8, int64_t H, int64_t W, const uint8_t* masks,
+                           const int* scales, const int* classes, int n_tasks, uint8_t* out40, uint8_t* out10);
+
 /* Introspection (valid after the last segment call on this handle). */
 /* Kept tiles in canonical order (scale descending, then row, then column), packed
  * (log2 f) << 30 | ty << 15 | tx  (grid indices; origin = min(i*S, E-P), R3). */

@@ -666,6 +666,64 @@ __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uin
   if (threadIdx.x == 0 && s) atomicAdd(area, s);
 }
 
+// ------------------------------------------------------------------ N3: 40x merge + overlay + 10x
+// ("all of the merged results of the various tissue types were stained with different
+// colors on WSIs ... a final downsampled prediction of the 10x WSI ... by directly resizing the
+// final prediction of the 40x image"). Per 40x pixel: every task's mask sampled
+// nearest-neighbour at (y / f, x / f); the lowest class code present wins (TUFT > CAP > PT >
+// DT > PTC > VES); out = round(0.4 colour + 0.6 base) = (4 c + 6 b + 5) / 10 (never a tie).
+__constant__ uint8_t c_palette[6][3] = {{255, 0, 0}, {255, 128, 0}, {0, 255, 0},
+                                        {0, 128, 255}, {255, 0, 255}, {128, 0, 128}};
+__global__ void overlay40_kernel(const uint8_t* slide, int64_t H, int64_t W, RenderTasks rt, uint8_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= H * W) return;
+  const int64_t y = i / W, x = i - (i / W) * W;
+  int best = 99;
+  for (int t = 0; t < rt.n; ++t) {
+    const int f = rt.f[t];
+    if (rt.cls[t] < best && rt.m[t][(y / f) * rt.Wt[t] + x / f]) best = rt.cls[t];
+  }
+  const uint8_t* b = slide + i * 3;
+  uint8_t* o = out + i * 3;
+  if (best == 99) {
+    o[0] = b[0];
+    o[1] = b[1];
+    o[2] = b[2];
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o[c] = (uint8_t)((4 * c_palette[best][c] + 6 * b[c] + 5) / 10);
+  }
+}
+// factor-4 area mean per channel, round half up; partial edge blocks average their pixels
+__global__ void down4_kernel(const uint8_t* in, int64_t H, int64_t W, uint8_t* out) {
+  const int64_t Ho = (H + 3) / 4, Wo = (W + 3) / 4;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Ho * Wo) return;
+  const int64_t by = i / Wo, bx = i - (i / Wo) * Wo;
+  int s0 = 0, s1 = 0, s2 = 0, n = 0;
+  for (int64_t y = 4 * by; y < min(H, 4 * by + 4); ++y)
+    for (int64_t x = 4 * bx; x < min(W, 4 * bx + 4); ++x) {
+      const uint8_t* p = in + (y * W + x) * 3;
+      s0 += p[0];
+      s1 += p[1];
+      s2 += p[2];
+      ++n;
+    }
+  uint8_t* o = out + i * 3;
+  o[0] = (uint8_t)((s0 + n / 2) / n);
+  o[1] = (uint8_t)((s1 + n / 2) / n);
+  o[2] = (uint8_t)((s2 + n / 2) / n);
+}
+void launch_overlay(const uint8_t* slide, int64_t H, int64_t W, const RenderTasks& rt, uint8_t* out40, uint8_t* out10,
+                    cudaStream_t s) {
+  const int64_t n = H * W;
+  overlay40_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(slide, H, W, rt, out40);
+  if (out10) {
+    const int64_t n10 = ((H + 3) / 4) * ((W + 3) / 4);
+    down4_kernel<<<(unsigned)((n10 + 255) / 256), 256, 0, s>>>(out40, H, W, out10);
+  }
+}
+
 // ------------------------------------------------------------------ N2: tiny-component removal
 // 4-connected components of the level-8 foreground rows [r0, r1) by union-find (union by the
 // smaller index with atomicMin, so every root is its component's smallest index: the result

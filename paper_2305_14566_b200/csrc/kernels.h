@@ -42,6 +42,14 @@ template <typename T>
 void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
                  const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
                  int Hp, int Wp, int pad, float* out_p, float* out_F, cudaStream_t s);
+// N3 render: per task its mask (task-scale canvas, row stride Wt), level factor, class code.
+struct RenderTasks {
+  const uint8_t* m[kMaxTasks];
+  int f[kMaxTasks], Wt[kMaxTasks], cls[kMaxTasks];
+  int n;
+};
+void launch_overlay(const uint8_t* slide, int64_t H, int64_t W, const RenderTasks& rt, uint8_t* out40, uint8_t* out10,
+                    cudaStream_t s);
 // Optional foreground filter of the finalized mask: canvas row of element 0 = cy0.
 struct FgMaskArgs {
   const uint8_t* fg8 = nullptr;  // level-8 foreground (full grid, row stride W8); NULL: off

@@ -221,6 +221,7 @@ struct omniseg {
   bool head_fusable = false;
   // front end / canvases
   DevBuf cc_lab, cc_size;  // SURVEY N2 component-labelling scratch
+  DevBuf r_slide, r_mask, r_40, r_10;  // SURVEY N3 render staging (host inputs / outputs)
   DevBuf slide, L1, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
   std::vector<uint32_t> h_tiles;
   int64_t n_tiles = 0;
@@ -1124,6 +1125,69 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
                              out_area);
     else
       segment<__half>(h, rgb_band, H, W, row0, row1, b0, b1, pad, patch, stride, tk, out_prob, out_mask, out_area);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(Error(-2, e.what()));
+  }
+}
+
+int omniseg_render_overlay(omniseg_t* h, const uint8_t* rgb_u8, int64_t H, int64_t W, const uint8_t* masks,
+                           const int* scales, const int* classes, int n_tasks, uint8_t* out40, uint8_t* out10) {
+  try {
+    OS_REQUIRE(h && rgb_u8 && masks, "render_overlay: NULL argument");
+    OS_REQUIRE(out40 || out10, "render_overlay: no output requested");
+    OS_REQUIRE(H >= 1 && W >= 1, "render_overlay: bad size");
+    OS_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    const Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
+    for (int t = 0; t < tk.n; ++t) OS_REQUIRE(tk.cls[t] < 6, "render_overlay: palette has 6 classes");
+    int64_t mtot = 0;
+    std::vector<int64_t> moff(tk.n);
+    for (int t = 0; t < tk.n; ++t) {
+      moff[t] = mtot;
+      mtot += tk.Ht[t] * tk.Wt[t];
+    }
+    const uint8_t* dslide = rgb_u8;
+    if (!is_device_ptr(rgb_u8)) {
+      h->r_slide.ensure((size_t)H * W * 3);
+      OS_CUDA(cudaMemcpyAsync(h->r_slide.p, rgb_u8, (size_t)H * W * 3, cudaMemcpyHostToDevice, s));
+      dslide = h->r_slide.as<uint8_t>();
+    }
+    const uint8_t* dmask = masks;
+    if (!is_device_ptr(masks)) {
+      h->r_mask.ensure((size_t)mtot);
+      OS_CUDA(cudaMemcpyAsync(h->r_mask.p, masks, (size_t)mtot, cudaMemcpyHostToDevice, s));
+      dmask = h->r_mask.as<uint8_t>();
+    }
+    RenderTasks rt{};
+    rt.n = tk.n;
+    for (int t = 0; t < tk.n; ++t) {
+      rt.m[t] = dmask + moff[t];
+      rt.f[t] = tk.f[t];
+      rt.Wt[t] = (int)tk.Wt[t];
+      rt.cls[t] = tk.cls[t];
+    }
+    uint8_t* d40 = out40;
+    if (!out40 || !is_device_ptr(out40)) {
+      h->r_40.ensure((size_t)H * W * 3);
+      d40 = h->r_40.as<uint8_t>();
+    }
+    const int64_t n10 = ((H + 3) / 4) * ((W + 3) / 4) * 3;
+    uint8_t* d10 = nullptr;
+    if (out10) {
+      d10 = out10;
+      if (!is_device_ptr(out10)) {
+        h->r_10.ensure((size_t)n10);
+        d10 = h->r_10.as<uint8_t>();
+      }
+    }
+    launch_overlay(dslide, H, W, rt, d40, d10, s);
+    OS_CUDA(cudaGetLastError());
+    if (out40 && d40 != out40) OS_CUDA(cudaMemcpyAsync(out40, d40, (size_t)H * W * 3, cudaMemcpyDeviceToHost, s));
+    if (out10 && d10 != out10) OS_CUDA(cudaMemcpyAsync(out10, d10, (size_t)n10, cudaMemcpyDeviceToHost, s));
+    OS_CUDA(cudaStreamSynchronize(s));
     return 0;
   } catch (const Error& e) {
     return fail(e);

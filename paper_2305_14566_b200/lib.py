@@ -16,7 +16,8 @@ _lib = None
 
 # Every symbol include/omniseg.h and include/omniseg_debug.h declare.
 SYMBOLS = ("omniseg_create", "omniseg_segment_slide", "omniseg_output_size", "omniseg_comm_init",
-           "omniseg_segment_band", "omniseg_band_rows", "omniseg_get_tiles", "omniseg_get_fgmask",
+           "omniseg_segment_band", "omniseg_band_rows", "omniseg_render_overlay", "omniseg_get_tiles",
+           "omniseg_get_fgmask",
            "omniseg_get_timings", "omniseg_set_stream", "omniseg_last_error", "omniseg_destroy",
            "omniseg_debug_predict_tiles", "omniseg_debug_conv", "omniseg_debug_set_profile",
            "omniseg_debug_get_profile", "omniseg_debug_band_globals", "omniseg_debug_get_detection")
@@ -50,6 +51,8 @@ def load(path: str = LIB_PATH):
     L.omniseg_segment_band.restype = i32
     L.omniseg_band_rows.argtypes = [i64, i64, i64, i32, i32, C.POINTER(i64), C.POINTER(i64)]
     L.omniseg_band_rows.restype = i32
+    L.omniseg_render_overlay.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, vp, vp]
+    L.omniseg_render_overlay.restype = i32
     L.omniseg_get_tiles.argtypes = [vp, vp, i64, C.POINTER(i64)]
     L.omniseg_get_tiles.restype = i32
     L.omniseg_get_fgmask.argtypes = [vp, vp, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)]
@@ -142,6 +145,11 @@ class Omniseg:
         _check(load().omniseg_segment_slide(self.h, _ptr(rgb), H, W, pad, patch, stride, _ints(scales),
                                             _ints(classes), len(scales), _ptr(out_prob), _ptr(out_mask),
                                             _ptr(out_area)))
+
+    def render_overlay(self, rgb, H, W, masks, scales, classes, out40=None, out10=None):
+        """40x merge + colour overlay (+ 10x) of segment_slide masks (include/omniseg.h)."""
+        _check(load().omniseg_render_overlay(self.h, _ptr(rgb), H, W, _ptr(masks), _ints(scales), _ints(classes),
+                                             len(scales), _ptr(out40), _ptr(out10)))
 
     def comm_init(self, uid_bytes: bytes, world: int, rank: int):
         buf = C.create_string_buffer(bytes(uid_bytes), 128)

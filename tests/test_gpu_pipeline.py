@@ -134,6 +134,38 @@ def test_cfg1_component_removal_and_fg_mask(gpu_lib):
     assert int(area[0]) == int(mask.sum())
 
 
+def test_overlay_render_bit_exact(gpu_lib):
+    """SURVEY N3 (omniseg_render_overlay): the 40x overlay and the 10x downsample of the masks a
+    segment call produced, bit-exact against oracle/render.py on the same masks -- including
+    several tasks of different scales and classes overlapping (precedence) and a ragged 10x edge."""
+    from oracle import render as rd
+    w = workload(1)
+    slide, _ = _cfg1_ref()
+    slide = slide[:1021, :1018].copy()           # ragged: neither side a multiple of 4
+    H, W = slide.shape[:2]
+    a = dict(w.arch, ncls=6, scale_codes=(5, 10, 40), slide_mag=40)
+    from omniseg_inputs import make_weights
+    from paper_2305_14566_b200 import Omniseg
+    h = Omniseg(arch_string(a), make_weights(a, 1))
+    scales, classes = (40, 10, 5, 40), (2, 0, 5, 4)
+    sizes = [h.output_size(H, W, s) for s in scales]
+    mask = np.zeros(sum(sizes), np.uint8)
+    h.segment_slide(slide, H, W, 64, 128, 64, scales, classes, None, mask, None)
+    rng = np.random.default_rng(0)
+    mask |= (rng.random(mask.shape) < 0.05).astype(np.uint8)   # more overlap between classes
+    out40 = np.zeros((H, W, 3), np.uint8)
+    out10 = np.zeros(((H + 3) // 4, (W + 3) // 4, 3), np.uint8)
+    h.render_overlay(slide, H, W, mask, scales, classes, out40, out10)
+    factors = [40 // s for s in scales]
+    ms, o = [], 0
+    for n, f in zip(sizes, factors):
+        ms.append(mask[o:o + n].reshape((H + f - 1) // f, (W + f - 1) // f))
+        o += n
+    ref40 = rd.overlay_40x(slide, rd.merge_40x(ms, factors, H, W), classes)
+    assert (out40 == ref40).all()
+    assert (out10 == rd.downsample_4(ref40)).all()
+
+
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
 def test_cfg1_16bit_storage_numerics_report(gpu_lib, dtype):
     """Plain 16-bit activation storage (BASELINE configs' 'bf16 activations', and fp16):
