@@ -45,7 +45,7 @@ void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const fl
 // N3 render: per task its mask (task-scale canvas, row stride Wt), level factor, class code.
 struct RenderTasks {
   const uint8_t* m[kMaxTasks];
-  int f[kMaxTasks], Wt[kMaxTasks], cls[kMaxTasks];
+  int f[kMaxTasks], lf[kMaxTasks], Wt[kMaxTasks], cls[kMaxTasks];
   int n;
 };
 void launch_overlay(const uint8_t* slide, int64_t H, int64_t W, const RenderTasks& rt, uint8_t* out40, uint8_t* out10,

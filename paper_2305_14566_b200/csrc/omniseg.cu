@@ -1166,6 +1166,7 @@ int omniseg_render_overlay(omniseg_t* h, const uint8_t* rgb_u8, int64_t H, int64
     for (int t = 0; t < tk.n; ++t) {
       rt.m[t] = dmask + moff[t];
       rt.f[t] = tk.f[t];
+      rt.lf[t] = tk.log2f[t];
       rt.Wt[t] = (int)tk.Wt[t];
       rt.cls[t] = tk.cls[t];
     }
