@@ -117,11 +117,16 @@ __device__ __forceinline__ void split_f8_16(const float* v, uint4& h0, uint4& h1
   uint32_t h[8], l[4];
 #pragma unroll
   for (int e = 0; e < 8; ++e) h[e] = StoreT<__half>::pack(v[2 * e], v[2 * e + 1]);
+  // (v - hi) 2^6 as one packed FMA per pair: fma(v, 2^6, -hi 2^6) rounds 2^6 (v - hi), which is
+  // exact (v - hi is exact by Sterbenz, the scaling by a power of two too): bit-identical
+  const float2 s64 = make_float2(kLoScale, kLoScale), m64 = make_float2(-kLoScale, -kLoScale);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const float2 a = StoreT<__half>::unpack(h[2 * e]), b = StoreT<__half>::unpack(h[2 * e + 1]);
-    l[e] = f8_pack4((v[4 * e] - a.x) * kLoScale, (v[4 * e + 1] - a.y) * kLoScale, (v[4 * e + 2] - b.x) * kLoScale,
-                    (v[4 * e + 3] - b.y) * kLoScale);
+    const float2 a = __ffma2_rn(make_float2(v[4 * e], v[4 * e + 1]), s64,
+                                __fmul2_rn(StoreT<__half>::unpack(h[2 * e]), m64));
+    const float2 b = __ffma2_rn(make_float2(v[4 * e + 2], v[4 * e + 3]), s64,
+                                __fmul2_rn(StoreT<__half>::unpack(h[2 * e + 1]), m64));
+    l[e] = f8_pack4(a.x, a.y, b.x, b.y);
   }
   h0 = make_uint4(h[0], h[1], h[2], h[3]);
   h1 = make_uint4(h[4], h[5], h[6], h[7]);
@@ -129,14 +134,18 @@ __device__ __forceinline__ void split_f8_16(const float* v, uint4& h0, uint4& h1
 }
 // v[0..16) += the 16 lo values of one uint4 of e4m3
 __device__ __forceinline__ void add_f8_16(float* v, const uint4& q) {
+  // v += lo 2^-6 as packed FMAs (the scaling by a power of two is exact: bit-identical)
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  const float2 inv = make_float2(kLoInv, kLoInv);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const float2 a = f8_unpack2(w[e]), b = f8_unpack2(w[e] >> 16);
-    v[4 * e] += a.x;
-    v[4 * e + 1] += a.y;
-    v[4 * e + 2] += b.x;
-    v[4 * e + 3] += b.y;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)((w[e] >> (16 * k)) & 0xFFFFu), __NV_E4M3);
+      const float2 r = __ffma2_rn(__half22float2(__half2(hr)), inv, make_float2(v[4 * e + 2 * k], v[4 * e + 2 * k + 1]));
+      v[4 * e + 2 * k] = r.x;
+      v[4 * e + 2 * k + 1] = r.y;
+    }
   }
 }
 // smem image of one F8 lo box row of CH bytes: 32-B swizzle (CH = 32) / none (CH = 16)
