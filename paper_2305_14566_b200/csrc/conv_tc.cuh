@@ -338,7 +338,12 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
   }
   ptx::tmem_ld_wait();
 #pragma unroll
-  for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(bias + n0 + j);
+  for (int j = 0; j < CH; j += 2) {  // + bias, packed
+    const float2 r = __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
+                                make_float2(__ldg(bias + n0 + j), __ldg(bias + n0 + j + 1)));
+    v[j] = r.x;
+    v[j + 1] = r.y;
+  }
   if constexpr (kRes) {
     const int rc = es.res_rc;
     ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
@@ -358,9 +363,9 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
         const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float2 f = StoreT<T>::unpack(rr[e]);
-          v[8 * j + 2 * e] += f.x;
-          v[8 * j + 2 * e + 1] += f.y;
+          const float2 f = __fadd2_rn(StoreT<T>::unpack(rr[e]), make_float2(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]));
+          v[8 * j + 2 * e] = f.x;
+          v[8 * j + 2 * e + 1] = f.y;
         }
       }
     }
