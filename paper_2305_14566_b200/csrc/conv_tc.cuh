@@ -460,21 +460,23 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
 #pragma unroll
     for (int j = 0; j < CH; ++j) v[j] = float(T(v[j]));
   }
-  // precls with the weights padded to CH columns (zeros beyond C0): fully unrolled, v stays
-  // in registers, one float4 shared load per 4 FMAs
+  // precls, weights TRANSPOSED in smem (s_w[j * 8 + o], zero rows beyond C0): input-outer
+  // order so the 8 accumulators are independent FMA chains (two float4 loads per input)
   float F[kHead];
 #pragma unroll
-  for (int o = 0; o < kHead; ++o) {
-    float a = s_b[o];
+  for (int o = 0; o < kHead; ++o) F[o] = s_b[o];
 #pragma unroll
-    for (int j = 0; j < CH; j += 4) {
-      const float4 w4 = *reinterpret_cast<const float4*>(s_w + o * CH + j);
-      a = fmaf(w4.x, v[j], a);
-      a = fmaf(w4.y, v[j + 1], a);
-      a = fmaf(w4.z, v[j + 2], a);
-      a = fmaf(w4.w, v[j + 3], a);
-    }
-    F[o] = a;
+  for (int j = 0; j < CH; ++j) {
+    const float4 w0 = *reinterpret_cast<const float4*>(s_w + j * 8);
+    const float4 w1 = *reinterpret_cast<const float4*>(s_w + j * 8 + 4);
+    F[0] = fmaf(w0.x, v[j], F[0]);
+    F[1] = fmaf(w0.y, v[j], F[1]);
+    F[2] = fmaf(w0.z, v[j], F[2]);
+    F[3] = fmaf(w0.w, v[j], F[3]);
+    F[4] = fmaf(w1.x, v[j], F[4]);
+    F[5] = fmaf(w1.y, v[j], F[5]);
+    F[6] = fmaf(w1.z, v[j], F[6]);
+    F[7] = fmaf(w1.w, v[j], F[7]);
   }
   const int y = yb, x = xb + (int)lane;  // hb = 1: the warp's 32 pixels of one row
   if (ha.out_F) {
@@ -484,38 +486,44 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
   const int f = 1 << lf;
   for (int t = 0; t < ha.ntasks; ++t) {
     if (ha.tiles && ha.tt.log2f[t] != lf) continue;
+    // theta in smem with W1 / W2 transposed: [i * 8 + o] (see the theta load)
     const float* th = s_th + t * 156;
     float h1[kHead], h2[kHead];
 #pragma unroll
-    for (int o = 0; o < kHead; ++o) {
-      const float4 a4 = *reinterpret_cast<const float4*>(th + o * 8);
-      const float4 b4 = *reinterpret_cast<const float4*>(th + o * 8 + 4);
-      float a = th[64 + o];
-      a = fmaf(a4.x, F[0], a);
-      a = fmaf(a4.y, F[1], a);
-      a = fmaf(a4.z, F[2], a);
-      a = fmaf(a4.w, F[3], a);
-      a = fmaf(b4.x, F[4], a);
-      a = fmaf(b4.y, F[5], a);
-      a = fmaf(b4.z, F[6], a);
-      a = fmaf(b4.w, F[7], a);
-      h1[o] = fmaxf(a, 0.f);
+    for (int o = 0; o < kHead; ++o) h1[o] = th[64 + o];
+#pragma unroll
+    for (int i = 0; i < kHead; ++i) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + i * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + i * 8 + 4);
+      h1[0] = fmaf(a4.x, F[i], h1[0]);
+      h1[1] = fmaf(a4.y, F[i], h1[1]);
+      h1[2] = fmaf(a4.z, F[i], h1[2]);
+      h1[3] = fmaf(a4.w, F[i], h1[3]);
+      h1[4] = fmaf(b4.x, F[i], h1[4]);
+      h1[5] = fmaf(b4.y, F[i], h1[5]);
+      h1[6] = fmaf(b4.z, F[i], h1[6]);
+      h1[7] = fmaf(b4.w, F[i], h1[7]);
     }
 #pragma unroll
     for (int o = 0; o < kHead; ++o) {
-      const float4 a4 = *reinterpret_cast<const float4*>(th + 72 + o * 8);
-      const float4 b4 = *reinterpret_cast<const float4*>(th + 72 + o * 8 + 4);
-      float a = th[136 + o];
-      a = fmaf(a4.x, h1[0], a);
-      a = fmaf(a4.y, h1[1], a);
-      a = fmaf(a4.z, h1[2], a);
-      a = fmaf(a4.w, h1[3], a);
-      a = fmaf(b4.x, h1[4], a);
-      a = fmaf(b4.y, h1[5], a);
-      a = fmaf(b4.z, h1[6], a);
-      a = fmaf(b4.w, h1[7], a);
-      h2[o] = fmaxf(a, 0.f);
+      h1[o] = fmaxf(h1[o], 0.f);
+      h2[o] = th[136 + o];
     }
+#pragma unroll
+    for (int i = 0; i < kHead; ++i) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + 72 + i * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + 72 + i * 8 + 4);
+      h2[0] = fmaf(a4.x, h1[i], h2[0]);
+      h2[1] = fmaf(a4.y, h1[i], h2[1]);
+      h2[2] = fmaf(a4.z, h1[i], h2[2]);
+      h2[3] = fmaf(a4.w, h1[i], h2[3]);
+      h2[4] = fmaf(b4.x, h1[i], h2[4]);
+      h2[5] = fmaf(b4.y, h1[i], h2[5]);
+      h2[6] = fmaf(b4.z, h1[i], h2[6]);
+      h2[7] = fmaf(b4.w, h1[i], h2[7]);
+    }
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) h2[o] = fmaxf(h2[o], 0.f);
     const float4 c4 = *reinterpret_cast<const float4*>(th + 144);
     const float4 d4 = *reinterpret_cast<const float4*>(th + 148);
     float z = th[152];
@@ -548,19 +556,23 @@ template <typename T, int CH>
 __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v1)[CH], int x, int y0, int y1, int b,
                                           const HeadArgs& ha, const float* s_w, const float* s_b, const float* s_th,
                                           int lf, int oy, int ox) {
+  // precls with transposed weights (s_w[j * 8 + o]): input-outer, 8 independent packed chains
   float2 F[kHead];
 #pragma unroll
-  for (int o = 0; o < kHead; ++o) {
-    float2 a = make_float2(s_b[o], s_b[o]);
+  for (int o = 0; o < kHead; ++o) F[o] = make_float2(s_b[o], s_b[o]);
 #pragma unroll
-    for (int j = 0; j < CH; j += 4) {
-      const float4 w4 = *reinterpret_cast<const float4*>(s_w + o * CH + j);
-      a = __ffma2_rn(make_float2(w4.x, w4.x), make_float2(v0[j], v1[j]), a);
-      a = __ffma2_rn(make_float2(w4.y, w4.y), make_float2(v0[j + 1], v1[j + 1]), a);
-      a = __ffma2_rn(make_float2(w4.z, w4.z), make_float2(v0[j + 2], v1[j + 2]), a);
-      a = __ffma2_rn(make_float2(w4.w, w4.w), make_float2(v0[j + 3], v1[j + 3]), a);
-    }
-    F[o] = a;
+  for (int j = 0; j < CH; ++j) {
+    const float4 w0 = *reinterpret_cast<const float4*>(s_w + j * 8);
+    const float4 w1 = *reinterpret_cast<const float4*>(s_w + j * 8 + 4);
+    const float2 vj = make_float2(v0[j], v1[j]);
+    F[0] = __ffma2_rn(make_float2(w0.x, w0.x), vj, F[0]);
+    F[1] = __ffma2_rn(make_float2(w0.y, w0.y), vj, F[1]);
+    F[2] = __ffma2_rn(make_float2(w0.z, w0.z), vj, F[2]);
+    F[3] = __ffma2_rn(make_float2(w0.w, w0.w), vj, F[3]);
+    F[4] = __ffma2_rn(make_float2(w1.x, w1.x), vj, F[4]);
+    F[5] = __ffma2_rn(make_float2(w1.y, w1.y), vj, F[5]);
+    F[6] = __ffma2_rn(make_float2(w1.z, w1.z), vj, F[6]);
+    F[7] = __ffma2_rn(make_float2(w1.w, w1.w), vj, F[7]);
   }
   if (ha.out_F) {
 #pragma unroll
@@ -572,38 +584,43 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
   const int f = 1 << lf;
   for (int t = 0; t < ha.ntasks; ++t) {
     if (ha.tiles && ha.tt.log2f[t] != lf) continue;
-    const float* th = s_th + t * 156;
+    const float* th = s_th + t * 156;  // W1 / W2 transposed: [i * 8 + o]
     float2 h1[kHead], h2[kHead];
 #pragma unroll
-    for (int o = 0; o < kHead; ++o) {
-      const float4 a4 = *reinterpret_cast<const float4*>(th + o * 8);
-      const float4 b4 = *reinterpret_cast<const float4*>(th + o * 8 + 4);
-      float2 a = make_float2(th[64 + o], th[64 + o]);
-      a = __ffma2_rn(make_float2(a4.x, a4.x), F[0], a);
-      a = __ffma2_rn(make_float2(a4.y, a4.y), F[1], a);
-      a = __ffma2_rn(make_float2(a4.z, a4.z), F[2], a);
-      a = __ffma2_rn(make_float2(a4.w, a4.w), F[3], a);
-      a = __ffma2_rn(make_float2(b4.x, b4.x), F[4], a);
-      a = __ffma2_rn(make_float2(b4.y, b4.y), F[5], a);
-      a = __ffma2_rn(make_float2(b4.z, b4.z), F[6], a);
-      a = __ffma2_rn(make_float2(b4.w, b4.w), F[7], a);
-      h1[o] = make_float2(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
+    for (int o = 0; o < kHead; ++o) h1[o] = make_float2(th[64 + o], th[64 + o]);
+#pragma unroll
+    for (int i = 0; i < kHead; ++i) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + i * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + i * 8 + 4);
+      h1[0] = __ffma2_rn(make_float2(a4.x, a4.x), F[i], h1[0]);
+      h1[1] = __ffma2_rn(make_float2(a4.y, a4.y), F[i], h1[1]);
+      h1[2] = __ffma2_rn(make_float2(a4.z, a4.z), F[i], h1[2]);
+      h1[3] = __ffma2_rn(make_float2(a4.w, a4.w), F[i], h1[3]);
+      h1[4] = __ffma2_rn(make_float2(b4.x, b4.x), F[i], h1[4]);
+      h1[5] = __ffma2_rn(make_float2(b4.y, b4.y), F[i], h1[5]);
+      h1[6] = __ffma2_rn(make_float2(b4.z, b4.z), F[i], h1[6]);
+      h1[7] = __ffma2_rn(make_float2(b4.w, b4.w), F[i], h1[7]);
     }
 #pragma unroll
     for (int o = 0; o < kHead; ++o) {
-      const float4 a4 = *reinterpret_cast<const float4*>(th + 72 + o * 8);
-      const float4 b4 = *reinterpret_cast<const float4*>(th + 72 + o * 8 + 4);
-      float2 a = make_float2(th[136 + o], th[136 + o]);
-      a = __ffma2_rn(make_float2(a4.x, a4.x), h1[0], a);
-      a = __ffma2_rn(make_float2(a4.y, a4.y), h1[1], a);
-      a = __ffma2_rn(make_float2(a4.z, a4.z), h1[2], a);
-      a = __ffma2_rn(make_float2(a4.w, a4.w), h1[3], a);
-      a = __ffma2_rn(make_float2(b4.x, b4.x), h1[4], a);
-      a = __ffma2_rn(make_float2(b4.y, b4.y), h1[5], a);
-      a = __ffma2_rn(make_float2(b4.z, b4.z), h1[6], a);
-      a = __ffma2_rn(make_float2(b4.w, b4.w), h1[7], a);
-      h2[o] = make_float2(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
+      h1[o] = make_float2(fmaxf(h1[o].x, 0.f), fmaxf(h1[o].y, 0.f));
+      h2[o] = make_float2(th[136 + o], th[136 + o]);
     }
+#pragma unroll
+    for (int i = 0; i < kHead; ++i) {
+      const float4 a4 = *reinterpret_cast<const float4*>(th + 72 + i * 8);
+      const float4 b4 = *reinterpret_cast<const float4*>(th + 72 + i * 8 + 4);
+      h2[0] = __ffma2_rn(make_float2(a4.x, a4.x), h1[i], h2[0]);
+      h2[1] = __ffma2_rn(make_float2(a4.y, a4.y), h1[i], h2[1]);
+      h2[2] = __ffma2_rn(make_float2(a4.z, a4.z), h1[i], h2[2]);
+      h2[3] = __ffma2_rn(make_float2(a4.w, a4.w), h1[i], h2[3]);
+      h2[4] = __ffma2_rn(make_float2(b4.x, b4.x), h1[i], h2[4]);
+      h2[5] = __ffma2_rn(make_float2(b4.y, b4.y), h1[i], h2[5]);
+      h2[6] = __ffma2_rn(make_float2(b4.z, b4.z), h1[i], h2[6]);
+      h2[7] = __ffma2_rn(make_float2(b4.w, b4.w), h1[i], h2[7]);
+    }
+#pragma unroll
+    for (int o = 0; o < kHead; ++o) h2[o] = make_float2(fmaxf(h2[o].x, 0.f), fmaxf(h2[o].y, 0.f));
     const float4 c4 = *reinterpret_cast<const float4*>(th + 144);
     const float4 d4 = *reinterpret_cast<const float4*>(th + 148);
     float2 z = make_float2(th[152], th[152]);
@@ -1579,9 +1596,9 @@ __global__ void __launch_bounds__(384, 1)
     float* s_b = s_w + kHead * 64;
     const int et = ew * 32 + (int)lane;  // 0 .. 32*EW-1 over the epilogue warps
     if constexpr (MODE == kHeadFused) {
-      for (int i = et; i < kHead * CH; i += 32 * EW) {
+      for (int i = et; i < kHead * CH; i += 32 * EW) {  // transposed: s_w[j * 8 + o]
         const int o = i / CH, j = i - o * CH;
-        s_w[i] = j < hargs.C0 ? hargs.Wpre[o * hargs.C0 + j] : 0.f;
+        s_w[j * 8 + o] = j < hargs.C0 ? hargs.Wpre[o * hargs.C0 + j] : 0.f;
       }
       if (et < kHead) s_b[et] = hargs.bpre[et];
     }
@@ -1610,7 +1627,10 @@ __global__ void __launch_bounds__(384, 1)
         const int nth = hargs.ntasks * kTheta;
         for (int i = et; i < nth; i += 32 * EW) {
           const int t = i / kTheta;
-          s_th[t * 156 + (i - t * kTheta)] = hargs.theta[(int64_t)(b + args.b_head) * nth + i];
+          int k = i - t * kTheta;  // W1 [0, 64) and W2 [72, 136) stored transposed: [in * 8 + out]
+          if (k < 64) k = (k & 7) * 8 + (k >> 3);
+          else if (k >= 72 && k < 136) k = 72 + ((k - 72) & 7) * 8 + ((k - 72) >> 3);
+          s_th[t * 156 + k] = hargs.theta[(int64_t)(b + args.b_head) * nth + i];
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
         if (hargs.tiles) {
