@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
       const int xb = tx * args.wb + box_dx, yb = ty * args.hb + box_dy;
       if constexpr (kRes)
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, yb, b + args.b_res, lane);
-      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::mbar_wait_backoff(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
 #pragma unroll 1
       for (int c = kSplit8 ? half * CH : 0; c < BN; c += kSplit8 ? 2 * CH : CH) {
@@ -1318,7 +1318,7 @@ __global__ void __launch_bounds__(256, 1)
       const int yb0 = tyg * R * HB + box_dy;
       if constexpr (kRes)
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, yb0, b + args.b_res, lane);
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
 #pragma unroll 1
       for (int i = 0; i < R * NC; ++i) {
@@ -1648,7 +1648,7 @@ __global__ void __launch_bounds__(384, 1)
       // the first residual chunk does not depend on the accumulator: issue it before waiting
       if constexpr (kRes)
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, tyg * R + half, b + args.b_res, lane);
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
       if constexpr (MODE == kHeadFused && NC == 1 && RM % 2 == 0) {
         // two rows (pixels (xb + lane, r0) and (xb + lane, r1)) per pass: both residual slots
@@ -1942,7 +1942,7 @@ __global__ void __launch_bounds__(384, 1)
       m /= args.tiles_x;
       const int tyg = m % args.tiles_y;
       const int b = m / args.tiles_y;
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
       const int xo = tx * 64 + q * 16;
 #pragma unroll 1
@@ -2235,7 +2235,7 @@ __global__ void __launch_bounds__(512, 1)
       int m = w / args.tiles_x;
       const int tyg = m % args.tiles_y;
       const int b = m / args.tiles_y;
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
       const int xb = tx * 128 + q * 32;
 #pragma unroll 1
