@@ -600,6 +600,10 @@ void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32
   a.num_work = n * a.tiles_x * a.tiles_y;
   if (a.num_work <= 0) return;
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
+  static unsigned long long* sdbg = nullptr;
+  const bool dbg = getenv("OMNISEG_DBG") && (atoi(getenv("OMNISEG_DBG")) & 8);
+  if (dbg && !sdbg) OS_CUDA(cudaMalloc(&sdbg, 148 * 4 * 8));
+  a.dbg_out = dbg ? sdbg : nullptr;
   const int bn = p.conv.bn;
   if (p.conv.bf16) {
     if (bn == 16) launch_stem<__nv_bfloat16, 16>(p, s);
@@ -611,6 +615,15 @@ void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32
     else launch_stem<__half, 64>(p, s);
   }
   OS_CUDA(cudaGetLastError());
+  if (dbg) {
+    unsigned long long hb[148 * 4];
+    OS_CUDA(cudaStreamSynchronize(s));
+    OS_CUDA(cudaMemcpy(hb, sdbg, sizeof(hb), cudaMemcpyDeviceToHost));
+    double t = 0, te = 0, fu = 0, nn = 0;
+    for (int i = 0; i < p.grid; ++i) t += hb[4 * i], te += hb[4 * i + 1], fu += hb[4 * i + 2], nn += hb[4 * i + 3];
+    fprintf(stderr, "[stem] per item: total %.0f, wait tempty %.0f, wait afull %.0f cycles (%.0f items/CTA)\n", t / nn,
+            te / nn, fu / nn, nn / p.grid);
+  }
 }
 
 void run_conv(const ConvPlan& p0, cudaStream_t s) {

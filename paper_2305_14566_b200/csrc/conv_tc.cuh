@@ -378,17 +378,30 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
 }
 
 // One CH-wide chunk: values -> 16-bit (hi, + lo in x2 / F8) -> STS -> TMA store.
+template <typename T, int CH>
+__device__ __forceinline__ void epi_store(EpiState& es, const CUtensorMap* tmO, const CUtensorMap* tmO2,
+                                          const float (&v)[CH], int n0, int Cout, int split, int xb, int yb, int b,
+                                          uint32_t lane);
+
 template <typename T, int CH, int MODE>
 __device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensorMap* tmO, const CUtensorMap* tmO2,
                                           uint32_t taddr, const float* bias, int n0, int Cout, int split, int xb,
                                           int yb, int b, uint32_t lane) {
+  float v[CH];
+  epi_values<T, CH, MODE>(es, slot, taddr, bias, n0, split, lane, v);
+  epi_store<T, CH>(es, tmO, tmO2, v, n0, Cout, split, xb, yb, b, lane);
+}
+
+// The store half of epi_chunk: v (final values) -> storage kind -> STS -> TMA store.
+template <typename T, int CH>
+__device__ __forceinline__ void epi_store(EpiState& es, const CUtensorMap* tmO, const CUtensorMap* tmO2,
+                                          const float (&v)[CH], int n0, int Cout, int split, int xb, int yb, int b,
+                                          uint32_t lane) {
   uint8_t* out_hi = es.buf + es.out_off[es.oslot];
   uint8_t* out_lo = out_hi + EpiTile<CH>::kBuf;
   const bool dbl = es.out_off[1] != es.out_off[0];
   es.oslot ^= dbl ? 1 : 0;
   const int rc = es.out_rc;
-  float v[CH];
-  epi_values<T, CH, MODE>(es, slot, taddr, bias, n0, split, lane, v);
   // the store that last read this slot is done reading smem (one store may stay in flight
   // when the output is double-buffered)
   if (lane == 0) {
@@ -2057,6 +2070,7 @@ struct StemArgs {
   int first, P, S, Hp, Wp;
   int num_work, tiles_x, tiles_y;
   int split, out_rc, Cout, b_out;
+  unsigned long long* dbg_out;  // experiments (OMNISEG_DBG & 8): MMA-warp cycle counters
 };
 
 template <int BN, int R, int NA>
@@ -2200,12 +2214,17 @@ __global__ void __launch_bounds__(512, 1)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
+    unsigned long long c_te = 0, c_full = 0, t_start = clock64();
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
+      unsigned long long t0 = clock64();
       ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+      c_te += clock64() - t0;
       ptx::tc_fence_after();
       for (int r = 0; r < R; ++r) {
+        t0 = clock64();
         ptx::mbar_wait(&afull[stage], phase);
+        c_full += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + stage * S::kA);
         const uint32_t d = tmem_base + acc * R * BN + r * BN;
@@ -2223,11 +2242,20 @@ __global__ void __launch_bounds__(512, 1)
       }
       ptx::mma_commit_w(&tfull[acc]);
     }
+    if (args.dbg_out && lane == 0) {
+      args.dbg_out[blockIdx.x * 4 + 0] = clock64() - t_start;
+      args.dbg_out[blockIdx.x * 4 + 1] = c_te;
+      args.dbg_out[blockIdx.x * 4 + 2] = c_full;
+      args.dbg_out[blockIdx.x * 4 + 3] = local;
+    }
   } else if (warp >= 8) {
     // ------------------------------------------ epilogue (8 warps, rows alternate per pair)
     const int q = warp & 3, ew = warp - 8, half = ew >> 2;
     EpiState es{smem + S::kEpiOff + ew * 3 * EpiTile<CH>::kBuf, &rbar[2 * ew], {0, 0}, 0, 0, args.out_rc};
     epi_layout<CH>(es, args.split);
+    float bias_r[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) bias_r[j] = __ldg(args.bias + j);
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -2238,12 +2266,37 @@ __global__ void __launch_bounds__(512, 1)
       ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
       const int xb = tx * 128 + q * 32;
+      if constexpr (BN == CH && CH == 32) {
+        // one 32-channel chunk per row: bias held in registers, the next row's accumulator
+        // loaded from TMEM while this row is converted and stored
+        constexpr int NI = R / 2;
+        uint32_t u[2][32];
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN;
+        ptx::tmem_ld_32x32b_x32(tb + half * BN, u[0]);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          if (i + 1 < NI) ptx::tmem_ld_32x32b_x32(tb + ((i + 1) * 2 + half) * BN, u[(i + 1) & 1]);
+          float v[CH];
+#pragma unroll
+          for (int j = 0; j < CH; j += 2) {
+            const float2 t2 = __fadd2_rn(make_float2(__uint_as_float(u[i & 1][j]), __uint_as_float(u[i & 1][j + 1])),
+                                         make_float2(bias_r[j], bias_r[j + 1]));
+            v[j] = fmaxf(t2.x, 0.f);
+            v[j + 1] = fmaxf(t2.y, 0.f);
+          }
+          epi_store<T, CH>(es, &tmO, &lo.O, v, 0, args.Cout, args.split, xb, tyg * R + i * 2 + half, b + args.b_out,
+                           lane);
+          ptx::tmem_ld_wait();
+        }
+      } else {
 #pragma unroll 1
-      for (int i = 0; i < (R / 2) * (BN / CH); ++i) {
-        const int r = (i / (BN / CH)) * 2 + half, c = (i % (BN / CH)) * CH;
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
-        epi_chunk<T, CH, kReluBias>(es, 0, &tmO, &lo.O, taddr, args.bias, c, args.Cout, args.split, xb,
-                                    tyg * R + r, b + args.b_out, lane);
+        for (int i = 0; i < (R / 2) * (BN / CH); ++i) {
+          const int r = (i / (BN / CH)) * 2 + half, c = (i % (BN / CH)) * CH;
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
+          epi_chunk<T, CH, kReluBias>(es, 0, &tmO, &lo.O, taddr, args.bias, c, args.Cout, args.split, xb,
+                                      tyg * R + r, b + args.b_out, lane);
+        }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
