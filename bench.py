@@ -37,7 +37,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--workload", default="cfg4",
+                    help="cfg1..cfg5 (BASELINE.json configs), or a SURVEY §8(f) geometry on cfg4's slide: "
+                         "cfg4_paper (N1: vote fusion, 40x S=256, 10x/5x S=64), "
+                         "cfg4_n4 (N4: Oracle-pipeline geometry, 256 windows, S=128, pad 2048, vote)")
     ap.add_argument("--dtype", default=None,
                     help="fp16f8 (default: fp16 + e4m3 residual, parity-gated), fp16x2 (gated), fp16, bf16")
     ap.add_argument("--batch", type=int, default=None)
@@ -100,6 +103,35 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# SURVEY §8(f) workloads on cfg4's slide. `groups`: (stride, magnifications) per
+# omniseg_segment_slide call -- the API takes one stride per call, so the paper's per-scale
+# strides (40x 256, 10x/5x 64) are two calls per step.
+PRESETS = {
+    "cfg4_paper": dict(base=4, fusion="vote", groups=((256, (40,)), (64, (10, 5)))),
+    "cfg4_n4": dict(base=4, fusion="vote", patch=256, stride=128, pad=2048),
+}
+
+
+def resolve_workload(name):
+    """-> (Workload, [(stride, [task indices])]) for a --workload name."""
+    from omniseg_inputs import workload
+    pr = PRESETS.get(name)
+    if pr is None:
+        w = workload(int(name.replace("cfg", "")))
+        return w, [(w.stride, list(range(len(w.scales))))]
+    w = workload(pr["base"])
+    w.name = name
+    w.arch["fusion"] = pr["fusion"]
+    for k in ("patch", "stride", "pad"):
+        if k in pr:
+            setattr(w, k, pr[k])
+    if "groups" not in pr:
+        return w, [(w.stride, list(range(len(w.scales))))]
+    groups = [(S, [i for i, s in enumerate(w.scales) if s in mags]) for S, mags in pr["groups"]]
+    assert sorted(i for _, g in groups for i in g) == list(range(len(w.scales)))
+    return w, groups
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -143,8 +175,11 @@ def run_reference(a):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from omniseg_inputs import geometry, render, workload
-    w = workload(int(a.workload.replace("cfg", "")))
+    from omniseg_inputs import geometry, render
+    if a.workload in PRESETS:
+        print(json.dumps({"impl": "reference", "unavailable": f"{a.workload}: the oracle arm is timed on cfg1..cfg5"}))
+        return 0
+    w, _ = resolve_workload(a.workload)
     g = geometry(w.slide)
     rows = lambda r0, r1: render(g, r0, r1).numpy()  # noqa: E731
     n_kept = tile_estimate(w)
@@ -195,12 +230,14 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from omniseg_inputs import arch_string, geometry, render, workload
+    from omniseg_inputs import arch_string, geometry, render
     from paper_2305_14566_b200 import Omniseg
     from paper_2305_14566_b200 import dist as D
     from paper_2305_14566_b200 import lib as L
 
-    w = workload(int(a.workload.replace("cfg", "")))
+    w, groups = resolve_workload(a.workload)
+    if world > 1 and len(groups) > 1:
+        raise SystemExit(f"{a.workload}: per-scale strides run at N=1 only (bands follow one stride)")
     if a.dtype:
         w.arch["dtype"] = a.dtype
     if a.batch:
@@ -223,22 +260,34 @@ def main():
     h = Omniseg(arch_string(w.arch), w.weights())
     stream = torch.cuda.current_stream(dev)
     h.set_stream(stream.cuda_stream)
-    # outputs (owned canvas rows of every task)
-    ncan = 0
-    for s in w.scales:
-        f = w.arch["slide_mag"] // s
-        r0t, r1t = L.band_rows(H, row0, row1, w.pad, f)
-        ncan += (r1t - r0t) * ((W + f - 1) // f)
+    # outputs (owned canvas rows of every task), laid out group by group
+    ncan, gsl = 0, []
+    for S, idx in groups:
+        n0 = ncan
+        for i in idx:
+            f = w.arch["slide_mag"] // w.scales[i]
+            r0t, r1t = L.band_rows(H, row0, row1, w.pad, f)
+            ncan += (r1t - r0t) * ((W + f - 1) // f)
+        gsl.append((S, [w.scales[i] for i in idx], [w.classes[i] for i in idx], n0, ncan, idx))
     prob = torch.empty(max(ncan, 1), dtype=torch.float32, device=dev)
     mask = torch.empty(max(ncan, 1), dtype=torch.uint8, device=dev)
     area = torch.zeros(len(w.scales), dtype=torch.int64, device=dev)
     D.init_comm(h, world, rank)
+    tiles_per_step = [0]
 
     def step(src, p_out, m_out, a_out):
         if world > 1:
             h.segment_band(src, H, W, row0, row1, w.pad, w.patch, w.stride, w.scales, w.classes, p_out, m_out, a_out)
-        else:
-            h.segment_slide(src, H, W, w.pad, w.patch, w.stride, w.scales, w.classes, p_out, m_out, a_out)
+            return
+        nt = 0
+        for S, sc, cl, n0, n1, idx in gsl:
+            if len(gsl) == 1:
+                h.segment_slide(src, H, W, w.pad, w.patch, S, sc, cl, p_out, m_out, a_out)
+            else:
+                h.segment_slide(src, H, W, w.pad, w.patch, S, sc, cl, p_out[n0:n1], m_out[n0:n1],
+                                a_out[idx[0]:idx[-1] + 1])
+            nt += len(h.tiles()) if len(gsl) > 1 else 0
+        tiles_per_step[0] = nt
 
     def barrier():
         if world > 1:
@@ -247,7 +296,7 @@ def main():
 
     for _ in range(max(1, a.warmup if not a.profile_only else 1)):
         step(slide, prob, mask, area)
-    n_tiles = len(h.tiles())
+    n_tiles = tiles_per_step[0] if len(gsl) > 1 else len(h.tiles())
     steps = 1 if a.profile_only else a.steps
     clocks = Clocks(local)
     h.set_profile(True)
@@ -315,7 +364,10 @@ def main():
             "alg_flops_per_launch": prof["flops"] / max(prof["launches"], 1),
             "avg_launch_ms": prof["ms"] / max(prof["launches"], 1)}
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
+    if a.workload in PRESETS:
+        cpu = {"value": None, "unit": "Mpx/s", "cores": 0, "kind": "oracle",
+               "sample": "not run: the oracle baseline is timed on cfg1..cfg5 (bench.py --workload cfg4)"}
+    elif rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
         try:
             t_fe, t_tile = oracle_sample(w, lambda r0, r1: render(g, r0, r1).numpy())
             n_or = tile_estimate(w)
@@ -331,7 +383,9 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": "Mpx/s", "n_gpus": world, "steps": steps,
                "warmup": a.warmup, "ms_per_step": ms, "sec_per_wsi": ms / 1e3, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": w.arch["dtype"], "data": "synthetic",
-               "config": {"workload": w.name, "H": H, "W": W, "patch": w.patch, "stride": w.stride, "pad": w.pad,
+               "config": {"workload": w.name, "H": H, "W": W, "patch": w.patch,
+                          "stride": w.stride if len(gsl) == 1 else {"x".join(map(str, g[1])): g[0] for g in gsl},
+                          "pad": w.pad, "fusion": w.arch.get("fusion", "mean"),
                           "tasks": len(w.scales), "kept_tiles": n_tiles, "batch": w.arch["batch"],
                           "parallelism": f"row-bands x{world}" if world > 1 else "single GPU",
                           "l2": "inputs larger than L2 (slide %.1f GB, canvases %.1f GB)"

@@ -114,6 +114,42 @@ def test_cfg1_vote_fusion(gpu_lib):
     assert int(area[0]) == int(m.sum())
 
 
+def _vote_case(**geom):
+    w = workload(1)
+    w.arch["fusion"] = "vote"
+    for k, v in geom.items():
+        setattr(w, k, v)
+    slide, _ = _cfg1_ref()
+    ref = op.segment_slide(slide, w.weights(), arch_string(w.arch), w.pad, w.patch, w.stride, w.scales, w.classes)
+    h, prob, mask, area = run_gpu(w, slide)
+    H, W = slide.shape[:2]
+    Hp, Wp = fe.padded_extent(H, W, w.pad)
+    assert unpack_tiles(h.tiles(), Hp, Wp, w.patch, w.stride) == ref["kept"]
+    p = prob.reshape(H, W).astype(np.float64)
+    m = mask.reshape(H, W)
+    same = (np.abs(p - ref["prob"][0]) <= 1e-6).mean()
+    agree = (m == ref["mask"][0]).mean()
+    assert same >= 0.999 and agree >= 0.999, (same, agree)
+    assert int(area[0]) == int(m.sum())
+    return ref, same, agree
+
+
+def test_cfg1_vote_dense_stride64(gpu_lib):
+    """SURVEY N1's dense geometry (S = 64 at 10x/5x, 'at least half' of the covering
+    windows): stride P/4, so an interior pixel is covered by up to 16 kept windows -- beyond the
+    mean mode's 15-window count field, inside the vote mode's 16-bit one."""
+    ref, same, agree = _vote_case(stride=64)
+    assert ref["cnt"][0].max() == 16
+    print(f"vote S=64: {len(ref['kept'])} tiles, fraction-equal {same:.5f}, mask agreement {agree:.5f}")
+
+
+def test_cfg1_oracle_pipeline_geometry_n4(gpu_lib):
+    """SURVEY N4 (the original pipeline's 2048-px padding and 256^2 windows),
+    half-window stride and majority vote: tile plan bit-exact, votes as above."""
+    ref, same, agree = _vote_case(pad=2048, patch=256, stride=128)
+    print(f"N4 geometry: {len(ref['kept'])} tiles, fraction-equal {same:.5f}, mask agreement {agree:.5f}")
+
+
 def test_cfg1_component_removal_and_fg_mask(gpu_lib):
     """SURVEY N2 (arch fgmin / maskfg): the level-8 foreground loses its components below
     fgmin pixels (GPU union-find vs the oracle's labelling, bit-exact), the window plan follows
