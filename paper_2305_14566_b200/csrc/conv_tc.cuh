@@ -595,12 +595,7 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
     }
   }
   const int f = 1 << lf;
-#ifdef OMNISEG_EXP_NOTASK
-  const int ntk = F[0].x == 12345.f ? ha.ntasks : 0;
-#else
-  const int ntk = ha.ntasks;
-#endif
-  for (int t = 0; t < ntk; ++t) {
+  for (int t = 0; t < ha.ntasks; ++t) {
     if (ha.tiles && ha.tt.log2f[t] != lf) continue;
     const float* th = s_th + t * 156;  // W1 / W2 transposed: [i * 8 + o]
     float2 h1[kHead], h2[kHead];
@@ -661,9 +656,6 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
         const int cy = oy + y - ha.pad / f, cx = ox + x - ha.pad / f;
         const int Wt = ha.tt.Wt[t];
         if (cy >= 0 && cy < ha.tt.Ht[t] && cx >= 0 && cx < Wt && cy >= ha.tt.row0[t] && cy < ha.tt.row1[t]) {
-#ifdef OMNISEG_EXP_NOSTITCH
-          if (__float_as_uint(p) == 0x7fc00001u)
-#endif
           atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, stitch_value(p, zz, ha.tt.vote));
         }
       }
