@@ -41,6 +41,8 @@ def arch_string(a: dict) -> str:
         s += ";xlevels=%d" % a["xlevels"]
     if a.get("xa") is not None:
         s += ";xa=%d" % a["xa"]
+    if a.get("xal") is not None:
+        s += ";xal=%d" % a["xal"]
     if a.get("fusion") is not None:
         s += ";fusion=%s" % a["fusion"]
     if a.get("fgmin") is not None:

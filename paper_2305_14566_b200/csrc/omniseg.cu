@@ -99,6 +99,8 @@ struct Arch {
   int split = kStorePlain;  // StoreKind of the activations: fp16/bf16 plain, x2 (hi + lo 16-bit), f8 (fp16 + e4m3 lo)
   int xlevels = -1;         // split storage only for tensors at U-Net levels < xlevels (-1: all levels)
   int xa = 1;               // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
+  int xal = 64;             // with xa = 1: conv_a outputs keep the split kind only at levels < xal
+  int xa_level(int l) const { return xa && l < xal ? l : 1000; }  // level passed to sp() for conv_a outputs
   int vote = 0;             // fusion rule: 0 mean of p (R11), 1 hard majority vote
   int fgmin = 0;            // drop foreground components below fgmin level-8 pixels
   int maskfg = 0;           // AND the output masks with the foreground
@@ -138,6 +140,7 @@ Arch parse_arch(const char* s) {
     else if (k == "device") a.device = toi(v);
     else if (k == "xlevels") a.xlevels = toi(v);
     else if (k == "xa") a.xa = toi(v);
+    else if (k == "xal") a.xal = toi(v);
     else if (k == "fgmin") a.fgmin = toi(v);
     else if (k == "maskfg") a.maskfg = toi(v);
     else if (k == "fusion") {
@@ -378,13 +381,13 @@ void load_weights(omniseg* h, const float* blob) {
   h->dec_b.resize(L);
   for (int l = 0; l < L; ++l) {
     conv(h->enc_a[l], h->C[l], 3, h->C[l], 1, l);
-    conv(h->enc_b[l], h->C[l], 3, h->C[l], 1, a.xa ? l : 1000);
+    conv(h->enc_b[l], h->C[l], 3, h->C[l], 1, a.xa_level(l));
     if (l < L - 1) conv(h->down[l], h->C[l + 1], 3, h->C[l], 2, l);
   }
   for (int l = L - 2; l >= 0; --l) {
     conv(h->up[l], h->C[l], 1, h->C[l + 1], 1, l + 1);
     conv(h->dec_a[l], h->C[l], 3, h->C[l], 1, l);
-    conv(h->dec_b[l], h->C[l], 3, h->C[l], 1, a.xa ? l : 1000);
+    conv(h->dec_b[l], h->C[l], 3, h->C[l], 1, a.xa_level(l));
   }
   {
     const float* w = take((size_t)kHead * h->C[0]);
@@ -489,7 +492,7 @@ void ensure_workspace(omniseg* h, int P) {
   enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias, 0, 0, 0, rc[0]);
   for (int l = 0; l < L; ++l) {
     LevelBufs& q = h->lv[l];
-    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000, rc[l], 0, rc[l]);
+    enc(h->enc_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa_level(l), rc[l], 0, rc[l]);
     enc(h->enc_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], erc[l]);
     if (l < L - 1)
       enc(h->down[l], q.E.p, q.P, nullptr, h->lv[l + 1].A.p, kReluBias, l + 1, erc[l], 0, rc[l + 1]);
@@ -497,7 +500,7 @@ void ensure_workspace(omniseg* h, int P) {
   for (int l = L - 2; l >= 0; --l) {
     LevelBufs& q = h->lv[l];
     dec(h->up[l], h->lv[l + 1].E.p, q.P / 2, q.E.p, q.A.p, kUpAdd, l, 0, erc[l], rc[l]);
-    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa ? l : 1000, rc[l], 0, rc[l]);
+    dec(h->dec_a[l], q.A.p, q.P, nullptr, q.Bt.p, kReluBias, ar.xa_level(l), rc[l], 0, rc[l]);
     dec(h->dec_b[l], q.Bt.p, q.P, q.A.p, q.E.p, kResidualRelu, l, rc[l], rc[l], 0);
   }
   // fused window gather + stem

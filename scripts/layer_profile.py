@@ -14,6 +14,9 @@ dt = sys.argv[2] if len(sys.argv) > 2 else "fp16f8"
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 w = workload(int(cfg[3:]))
 w.arch["dtype"] = dt
+for kv in sys.argv[4:]:  # extra arch keys, e.g. xa=0
+    k, v = kv.split("=")
+    w.arch[k] = int(v) if v.lstrip("-").isdigit() else v
 slide = render(geometry(w.slide), device="cuda")
 h = Omniseg(arch_string(w.arch), w.weights())
 n = sum(h.output_size(w.H, w.W, s) for s in w.scales)

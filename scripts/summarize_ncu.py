@@ -92,4 +92,5 @@ def main():
     print(summary)
 
 
-main()
+if __name__ == "__main__":
+    main()
