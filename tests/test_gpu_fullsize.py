@@ -104,3 +104,72 @@ def test_synthetic_slide_cpu_gpu_identical(gpu_lib):
             a = render(g, r0, r0 + 256, c0, c0 + 512).numpy()
             b = render(g, r0, r0 + 256, c0, c0 + 512, device="cuda").cpu().numpy()
             assert (a == b).all(), (cfg, r0, c0)
+
+
+def test_fullsize_paper_geometry_vote_sampled(gpu_lib):
+    """SURVEY N1 at full size, in bench.py's `cfg4_paper` launch configuration (cfg4 slide,
+    vote fusion, 40x windows at S = 256 and 10x / 5x windows at S = 64, one call per stride):
+    each call's tile plan bit-exact against the oracle's; on sampled pixels (chosen where few
+    kept windows cover them, so the fp64 oracle stays cheap) the vote fraction equals the
+    oracle's count of windows with p >= 1/2, except where a window's oracle p is within 1e-2
+    of 1/2 (its vote may flip under fp16f8 rounding)."""
+    import importlib.util
+    import os
+    from paper_2305_14566_b200 import Omniseg
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    w, groups = bench.resolve_workload("cfg4_paper")
+    H, W, P, pad = w.H, w.W, w.patch, w.pad
+    slide_d = render(geometry(w.slide), device="cuda", chunk_rows=2048)
+    slide = slide_d.cpu().numpy()
+    det = fe.detection_chunked(slide, pad)
+    arch = nn.parse_arch(arch_string(w.arch))
+    assert arch["fusion"] == "vote"
+    net = nn.unpack_weights(arch, w.weights())
+    h = Omniseg(arch_string(w.arch), w.weights())
+    rng = np.random.default_rng(41)
+    checked = 0
+    for S, idx in groups:
+        scales = [w.scales[i] for i in idx]
+        classes = [w.classes[i] for i in idx]
+        tf = op.task_factors(arch, scales)
+        sizes = [h.output_size(H, W, s) for s in scales]
+        prob = torch.empty(sum(sizes), dtype=torch.float32, device="cuda")
+        mask = torch.empty(sum(sizes), dtype=torch.uint8, device="cuda")
+        h.segment_slide(slide_d, H, W, pad, P, S, scales, classes, prob, mask, None)
+        torch.cuda.synchronize()
+        prob, mask = prob.cpu().numpy(), mask.cpu().numpy()
+        kept, _ = fe.tile_plan(det["fg"], det["Hp"], det["Wp"], [f for f, _ in tf], P, S)
+        assert _unpack(h.tiles(), det["Hp"], det["Wp"], P, S) == kept
+        offs = np.concatenate([[0], np.cumsum(sizes)])
+        cache = {}
+        for ti, (f, s_idx) in enumerate(tf):
+            Ht, Wt = (H + f - 1) // f, (W + f - 1) // f
+            pt = prob[offs[ti]:offs[ti + 1]].reshape(Ht, Wt)
+            mt = mask[offs[ti]:offs[ti + 1]].reshape(Ht, Wt)
+            cov = np.argwhere(pt > 0)
+            cand = [tuple(cov[i]) for i in rng.choice(len(cov), min(400, len(cov)), replace=False)]
+            cand = sorted(cand, key=lambda c: len(op.covering_tiles(kept, f, pad, P, int(c[0]), int(c[1]))))
+            done = 0
+            for (cy, cx) in cand:
+                tl = op.covering_tiles(kept, f, pad, P, int(cy), int(cx))
+                need = [k for k in tl if k not in cache]
+                if done >= 3 or len(cache) + len(need) > 24:
+                    break
+                for (ff, oy, ox) in need:
+                    win = fe.level_window(slide, pad, det["pc"], ff, oy, ox, P)
+                    tasks = [(c, s) for c, (f2, s) in zip(classes, tf) if f2 == ff]
+                    Fr, Er = nn.trunk(net, arch, win)
+                    g = nn.gap(Er)
+                    cache[(ff, oy, ox)] = {(c, s): nn.head(Fr, nn.controller(net, arch, g, c, s)) for c, s in tasks}
+                ps = np.array([cache[k][(classes[ti], s_idx)][cy + pad // f - k[1], cx + pad // f - k[2]] for k in tl])
+                votes = int((ps >= 0.5).sum())
+                frac_ref = votes / len(tl)
+                if np.abs(ps - 0.5).min() > 1e-2:
+                    assert abs(float(pt[cy, cx]) - frac_ref) <= 1e-6, (S, ti, cy, cx, pt[cy, cx], frac_ref)
+                    assert int(mt[cy, cx]) == int(2 * votes >= len(tl))
+                done += 1
+                checked += 1
+    assert checked >= 6
