@@ -351,11 +351,11 @@ def main():
     # DRAM traffic per conv launch from the committed ncu capture of the same launch shapes
     # (batch-64 launches of the cfg2 profile run: dram__bytes_read.sum + dram__bytes_write.sum)
     traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "r01k_summary.json")
+    tpath = os.path.join(ROOT, "profiles", "r01o_cfg2_summary.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         traffic = tj.get("conv_dram_bytes_per_launch")
-        traffic_src = "profiles/r01k_summary.json (ncu, %d conv launches)" % tj.get("conv_launches", 0)
+        traffic_src = "profiles/r01o_cfg2_summary.json (ncu, %d conv launches)" % tj.get("conv_launches", 0)
     roof = {"bound": "tensor", "kernel": "tcgen05 conv family (stem_tc / conv3_nz / conv3s2_rc / conv_tc kernels)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
             "peak_kind": f"{pk_kind} bf16 sustained (fp16 kind::f16 nominal ratio 1.0)",

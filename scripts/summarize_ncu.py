@@ -49,7 +49,8 @@ def main():
         a[0] += 1
         a[1] += t
         a[2] += byt
-    ours = {k: v for k, v in agg.items() if "osg::" in k}
+    # namespace-qualified names, or (captures filtered with -k regex:osg::) every kernel listed
+    ours = {k: v for k, v in agg.items() if "osg::" in k} or dict(agg)
     tot = sum(v[1] for v in ours.values())
     conv = {k: v for k, v in ours.items() if any(s in k for s in ("conv", "stem_tc"))}
     conv_launch = sum(v[0] for v in conv.values())
@@ -65,22 +66,26 @@ def main():
     }
     # full capture
     full = []
-    h = None
+    h, u = None, None
     for r in csv.reader(open(fpath)):
         if "Kernel Name" in r and h is None:
             h = r
+            continue
+        if h and u is None and len(r) == len(h) and r[0] == "":
+            u = dict(zip(h, r))  # the units row
             continue
         if h and len(r) == len(h) and r[0] not in ("", "ID") and not r[0].startswith("("):
             d = dict(zip(h, r))
             if not d.get("Kernel Name"):
                 continue
             g = lambda k: num(d.get(k, "nan"))  # noqa: E731
-            full.append((d["Kernel Name"].split("(")[0].replace("void ", ""), g("gpu__time_duration.sum"),
-                         g("dram__bytes_read.sum"), g("dram__bytes_write.sum"),
+            gu = lambda k: g(k) * {**scale, **bscale}.get((u or {}).get(k, ""), 1.0)  # noqa: E731
+            full.append((d["Kernel Name"].split("(")[0].replace("void ", ""), gu("gpu__time_duration.sum"),
+                         gu("dram__bytes_read.sum") / 1e9, gu("dram__bytes_write.sum") / 1e9,
                          g("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                          g("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                          g("lts__throughput.avg.pct_of_peak_sustained_elapsed")))
-    flines = ["| kernel (one batch, launch order) | duration | DRAM read | DRAM write | tensor pipe active % | DRAM % | L2 % |",
+    flines = ["| kernel (one batch, launch order) | ms | DRAM read GB | DRAM write GB | tensor pipe active % | DRAM % | L2 % |",
               "|---|---|---|---|---|---|---|"]
     for f in full:
         flines.append("| `%s` | %.3f | %.3f | %.3f | %.1f | %.1f | %.1f |" % f)
