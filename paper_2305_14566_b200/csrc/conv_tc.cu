@@ -585,7 +585,7 @@ void launch_stem(const StemPlan& p, cudaStream_t s) {
   auto kern = stem_tc_kernel<T, BN, kStemR, kStemNA>;
   static std::once_flag once;
   std::call_once(once, [&] { OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal)); });
-  kern<<<p.grid, 512, S::kTotal, s>>>(p.conv.tmO, p.args, p.conv.lo);
+  kern<<<p.grid, S::kThreads, S::kTotal, s>>>(p.conv.tmO, p.args, p.conv.lo);
 }
 
 void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32_t* const L[4], int S, int Hp, int Wp,

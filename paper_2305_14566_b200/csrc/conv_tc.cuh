@@ -2080,15 +2080,18 @@ struct StemSmem {
   static constexpr int kCH = BN < 32 ? BN : 32;  // output box width (make_stem_plan's maps)
   static constexpr int kBOff = NA * kA;
   static constexpr int kBarOff = ((kBOff + kB + 1023) / 1024) * 1024;
-  static constexpr int kBars = (2 * NA + 4 + 16) * 8 + 16;
+  // epilogue warps: 16 for 32 channels (one output row each per 4-row item), else 8
+  static constexpr int kEW = (BN == 32 && R == 4) ? 16 : 8;
+  static constexpr int kThreads = 256 + 32 * kEW;
+  static constexpr int kBars = (2 * NA + 4 + 2 * kEW) * 8 + 16;
   static constexpr int kEpiOff = ((kBarOff + kBars + 1023) / 1024) * 1024;
-  static constexpr int kTotal = kEpiOff + 8 * 3 * EpiTile<kCH>::kBuf + 1024;
+  static constexpr int kTotal = kEpiOff + kEW * 3 * EpiTile<kCH>::kBuf + 1024;
   static constexpr uint32_t kTmemCols = (2 * R * BN <= 32) ? 32 : (2 * R * BN <= 64) ? 64 : (2 * R * BN <= 128) ? 128
                                         : (2 * R * BN <= 256) ? 256 : 512;
 };
 
 template <typename T, int BN, int R, int NA>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
     stem_tc_kernel(const __grid_constant__ CUtensorMap tmO, const __grid_constant__ StemArgs args,
                    const __grid_constant__ LoMaps lo) {
   using S = StemSmem<BN, R, NA>;
@@ -2101,7 +2104,7 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* tfull = aempty + NA;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;  // unused by the output-only epilogue (EpiState needs the slots)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * S::kEW);
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   const int tid = threadIdx.x;
@@ -2112,9 +2115,9 @@ __global__ void __launch_bounds__(512, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 256);
+      ptx::mbar_init(&tempty[a], 32 * S::kEW);
     }
-    for (int a = 0; a < 16; ++a) ptx::mbar_init(&rbar[a], 1);
+    for (int a = 0; a < 2 * S::kEW; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
   // weights -> smem B operand (no-swizzle K-major: [kc][n][8 x 16-bit])
@@ -2249,13 +2252,16 @@ __global__ void __launch_bounds__(512, 1)
       args.dbg_out[blockIdx.x * 4 + 3] = local;
     }
   } else if (warp >= 8) {
-    // ------------------------------------------ epilogue (8 warps, rows alternate per pair)
+    // ------------------------------------------ epilogue (kEW warps: 8 -> rows alternate per
+    // pair of warps on a TMEM lane quadrant; 16 -> one row per warp)
     const int q = warp & 3, ew = warp - 8, half = ew >> 2;
     EpiState es{smem + S::kEpiOff + ew * 3 * EpiTile<CH>::kBuf, &rbar[2 * ew], {0, 0}, 0, 0, args.out_rc};
     epi_layout<CH>(es, args.split);
-    float bias_r[CH];
+    float bias_r[S::kEW == 16 ? 1 : CH];  // 16 warps: the bias is read (L1-resident) per row
+    if constexpr (S::kEW != 16) {
 #pragma unroll
-    for (int j = 0; j < CH; ++j) bias_r[j] = __ldg(args.bias + j);
+      for (int j = 0; j < CH; ++j) bias_r[j] = __ldg(args.bias + j);
+    }
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -2266,7 +2272,29 @@ __global__ void __launch_bounds__(512, 1)
       ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
       const int xb = tx * 128 + q * 32;
-      if constexpr (BN == CH && CH == 32) {
+      if constexpr (S::kEW == 16) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + half * BN, u);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);  // the accumulator row is in registers
+        float v[CH];
+        const float4* b4 = reinterpret_cast<const float4*>(args.bias);
+#pragma unroll
+        for (int j = 0; j < CH; j += 4) {
+          const float4 bb = __ldg(b4 + j / 4);
+          const float2 t0 = __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
+                                       make_float2(bb.x, bb.y));
+          const float2 t1 = __fadd2_rn(make_float2(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])),
+                                       make_float2(bb.z, bb.w));
+          v[j] = fmaxf(t0.x, 0.f);
+          v[j + 1] = fmaxf(t0.y, 0.f);
+          v[j + 2] = fmaxf(t1.x, 0.f);
+          v[j + 3] = fmaxf(t1.y, 0.f);
+        }
+        epi_store<T, CH>(es, &tmO, &lo.O, v, 0, args.Cout, args.split, xb, tyg * R + half, b + args.b_out, lane);
+        continue;
+      } else if constexpr (BN == CH && CH == 32) {
         // one 32-channel chunk per row: bias held in registers, the next row's accumulator
         // loaded from TMEM while this row is converted and stored
         constexpr int NI = R / 2;
