@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -62,3 +63,20 @@ def test_no_oracle_import_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 s = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", s).replace("oracle_", ""), f
+
+
+@pytest.mark.parametrize("arch, msg", [
+    ("levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=0", "batch"),
+    ("levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=x", "bad integer"),
+    ("levels=5;base=32;nonsense", "key=value"),
+    ("levels=5;base=1024;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=64", "base must"),
+    ("levels=5;base=32;head=4;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=64", "head must be 8"),
+    ("levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;color=1", "unknown key"),
+])
+def test_create_rejects_bad_arch_strings_before_touching_the_device(arch, msg):
+    """omniseg_create parses and validates the arch string first: a bad one returns NULL with
+    a message (no GPU needed to see it)."""
+    from paper_2305_14566_b200 import Omniseg, lib
+    lib.load(lib.LIB_PATH) if os.path.exists(lib.LIB_PATH) else pytest.skip("library not built")
+    with pytest.raises(lib.OmnisegError, match=msg):
+        Omniseg(arch, np.zeros(4, np.float32))

@@ -291,3 +291,37 @@ def test_predict_tiles_cfg2_net(gpu_lib):
         d = np.abs(p[0, k] - pr)
         print(f"task {k}: max |dp| {d.max():.4g}  p99.99 {np.quantile(d, 0.9999):.4g}")
         assert d.max() <= 5e-2
+
+
+def test_invalid_calls_fail_cleanly_and_the_handle_recovers(gpu_lib):
+    """Boundary error behaviour (include/omniseg.h): every invalid call returns a nonzero code
+    with a message and leaves the handle usable -- the next valid call gives the same result
+    as a fresh handle."""
+    from paper_2305_14566_b200 import Omniseg, lib
+    w = workload(1)
+    slide, _ = _cfg1_ref()
+    H, W = slide.shape[:2]
+    h = Omniseg(arch_string(w.arch), w.weights())
+    n = h.output_size(H, W, w.scales[0])
+    prob = np.zeros(n, np.float32)
+    mask = np.zeros(n, np.uint8)
+    bad = [
+        (dict(patch=250), "multiple"),              # patch not a multiple of 16 / 8
+        (dict(stride=0), "stride"),                 # stride out of range
+        (dict(stride=w.patch * 2), "stride"),       # stride > patch
+        (dict(pad=3), "pad"),                       # pad not a multiple of 8
+        (dict(scales=(7,)), "scale"),               # scale not in scale_codes
+        (dict(classes=(99,)), "class"),             # class index out of range
+        (dict(H=1), "H and W"),                     # degenerate slide
+    ]
+    for over, msg in bad:
+        a = dict(H=H, W=W, pad=w.pad, patch=w.patch, stride=w.stride, scales=w.scales, classes=w.classes)
+        a.update(over)
+        with pytest.raises(lib.OmnisegError, match=msg):
+            h.segment_slide(slide, a["H"], a["W"], a["pad"], a["patch"], a["stride"], a["scales"], a["classes"],
+                            prob, mask, None)
+    with pytest.raises(lib.OmnisegError):
+        h.segment_slide(None, H, W, w.pad, w.patch, w.stride, w.scales, w.classes, prob, mask, None)
+    h.segment_slide(slide, H, W, w.pad, w.patch, w.stride, w.scales, w.classes, prob, mask, None)
+    _, p2, m2, _ = run_gpu(w, slide)
+    assert (prob == p2).all() and (mask == m2).all()
