@@ -325,3 +325,102 @@ def test_invalid_calls_fail_cleanly_and_the_handle_recovers(gpu_lib):
     h.segment_slide(slide, H, W, w.pad, w.patch, w.stride, w.scales, w.classes, prob, mask, None)
     _, p2, m2, _ = run_gpu(w, slide)
     assert (prob == p2).all() and (mask == m2).all()
+
+
+def _shift_identity_net(levels, base, bc=None):
+    """Weights of the single-tap identity network (see test_shift_identity_network_bit_exact);
+    bc: optional controller bias (= theta, the controller weights being zero)."""
+    from omniseg_inputs.arch import arch_dict, blob_layout, param_count
+    a = arch_dict(levels=levels, base=base, ncls=1, scale_codes=(1,), slide_mag=1, batch=16)
+    arch = nn.parse_arch(arch_string(a))
+    net = nn.unpack_weights(arch, np.zeros(param_count(a)))
+
+    def tap(name, kh, kw, scale=1.0):
+        w = np.zeros_like(net[name][0])
+        for c in range(3):
+            w[c, kh, kw, c] = scale
+        net[name] = (w, net[name][1])
+
+    for name, kh, kw, s in (("stem", 0, 1, 1.0), ("enc0.a", 1, 1, 1.0), ("enc0.b", 1, 1, 0.5), ("down0", 1, 2, 1.0),
+                            ("precls", 0, 0, 1.0)):
+        tap(name, kh, kw, s)
+    for l in range(1, levels - 1):
+        tap(f"down{l}", 1, 1)
+    for l in range(levels - 1):
+        tap(f"up{l}", 0, 0)
+    if bc is not None:
+        net["ctrl"] = (net["ctrl"][0], np.asarray(bc, np.float64))
+    blob = np.concatenate([net[n.rsplit(".", 1)[0]][0 if n.endswith(".w") else 1].ravel()
+                           for n, _ in blob_layout(a)]).astype(np.float32)
+    assert blob.size == param_count(a)
+    return a, net, blob
+
+
+@pytest.mark.parametrize("levels, base, P", [(3, 8, 256), (5, 32, 512)])
+def test_shift_identity_network_bit_exact(gpu_lib, levels, base, P):
+    """The single-tap identity network of tests/test_oracle_net.py, generalised to L levels
+    (stem tap (0, 1): y = x shifted down one row; enc0 = RB with conv_a = I, conv_b = I/2, so
+    E0 = 1.5 y; down0 tap (1, 2), deeper downs centre taps; identity up-convs and precls):
+        F[i, j, c] = 1.5 (y[i, j] + sum_{l=1}^{L-1} y[2^l (i >> l), 2^l (j >> l) + 1]),  c < 3,
+    through the CUDA trunk (the bench network's kernels at levels=5, base=32, P=512): every
+    value is exact in the fp16 + e4m3 storage and in fp32 accumulation, so F must match
+    BIT-EXACTLY -- this pins the kernels' spatial layout (tap orientation, padding, the
+    stride-2 sample, up x2, skips) independently of rounding. theta = 0 (zero controller)
+    gives p = sigmoid(0) = 1/2 exactly."""
+    from paper_2305_14566_b200 import Omniseg
+    a, net, blob = _shift_identity_net(levels, base)
+    arch = nn.parse_arch(arch_string(a))
+    tiles = random_tiles(2, P, 21).numpy()
+    h = Omniseg(arch_string(a), blob)
+    p, F, _ = h.predict_tiles(tiles, [(0, 0)], with_F=True)
+    i = np.arange(P)[:, None]
+    j = np.arange(P)[None, :]
+    for t in range(2):
+        y = np.zeros((P, P, 3))
+        y[1:] = tiles[t][:-1]
+        exp = y.copy()
+        for l in range(1, levels):
+            exp += y[(i >> l) << l, ((j >> l) << l) + 1]
+        exp *= 1.5
+        if levels == 3:
+            Fr, _ = nn.trunk(net, arch, tiles[t])
+            assert (Fr[:, :, :3] == exp).all()  # the oracle meets the closed form
+        assert (F[t, :, :, :3] == exp).all(), np.abs(F[t, :, :, :3] - exp).max()
+        assert (F[t, :, :, 3:] == 0).all()
+    assert (p == 0.5).all()
+
+
+@pytest.mark.parametrize("levels, base, P, S, pad", [(3, 8, 256, 128, 128), (5, 32, 512, 256, 256)])
+def test_shift_identity_network_slide_parity(gpu_lib, levels, base, P, S, pad):
+    """The identity network end to end through omniseg_segment_slide (fused gather + stem,
+    trunk, fused head + stitch, finalize) on the cfg1 slide, with theta = bc chosen so that
+    z = F_0 / 256 - 2 (W1 = W2 = I, W3 = e_0 / 256, b3 = -2): F is exact on both sides, so
+    the stitched probabilities may differ only by the fp32 sigmoid and the 2^-20 fixed point
+    -- |dp| <= 2e-6 instead of the 1e-2 gate for random networks -- and the masks agree
+    except where the oracle's mean is within 2e-6 of 1/2. Pins the window gather, the
+    stem's window-relative padding and the stitch geometry; (5, 32, 512) runs the bench
+    network's kernels (32-channel fused stem, no-swizzle / stride-2 / per-tap convs, fused
+    head + stitch)."""
+    theta = np.zeros(153)
+    theta[0:64] = np.eye(8).ravel()
+    theta[72:136] = np.eye(8).ravel()
+    theta[144] = 1.0 / 256
+    theta[152] = -2.0
+    a, net, blob = _shift_identity_net(levels, base, bc=theta)
+    w = workload(1)
+    slide, _ = _cfg1_ref()
+    H, W = slide.shape[:2]
+    ref = op.segment_slide(slide, blob, arch_string(a), pad, P, S, w.scales, w.classes)
+    from paper_2305_14566_b200 import Omniseg
+    h = Omniseg(arch_string(a), blob)
+    prob = np.zeros(H * W, np.float32)
+    mask = np.zeros(H * W, np.uint8)
+    h.segment_slide(slide, H, W, pad, P, S, w.scales, w.classes, prob, mask, None)
+    p_ref = ref["prob"][0]
+    d = np.abs(prob.reshape(H, W).astype(np.float64) - p_ref)
+    assert d.max() <= 2e-6, d.max()
+    covered = ref["cnt"][0] > 0
+    pc = p_ref[covered]
+    assert covered.mean() > 0.3 and pc.min() < 0.3 and pc.max() > 0.7 and pc.std() > 0.02  # informative
+    dis = mask.reshape(H, W) != ref["mask"][0]
+    assert (np.abs(p_ref[dis] - 0.5) <= 2e-6).all()

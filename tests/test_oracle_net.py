@@ -182,3 +182,46 @@ def test_sigmoid_matches_library():
     z = np.linspace(-30, 30, 1001)
     np.testing.assert_allclose(nn.sigmoid(z), scipy.special.expit(z), rtol=1e-14, atol=1e-300)
     assert nn.sigmoid(0.0) == 0.5 and math.isclose(nn.sigmoid(math.log(3)), 0.75)
+
+
+def test_shift_identity_network_closed_form():
+    """A network of single-tap identity convolutions with known offsets: the whole trunk
+    reduces to a per-pixel formula, which pins the spatial bookkeeping end to end --
+    cross-correlation orientation (not a flipped kernel), zero 'same' padding, the pixel a
+    stride-2 conv samples, nearest up x2, the skip order, the residual form and the
+    [C_out][kh][kw][C_in] layout. With y[i, j] = x[i-1, j] (0 on row 0; stem tap kh=0, kw=1),
+    enc0 = RB with conv_a = I, conv_b = I/2 (so E0 = 1.5 y), down0 tap (kh=1, kw=2) and
+    down1 centre tap, identity up-convs and identity-free decoder RBs:
+        F[i, j, c] = 1.5 (y[i, j] + y[2(i//2), 2(j//2) + 1] + y[4(i//4), 4(j//4) + 1])
+    for c < 3 (channel c of the input), and GAP(E2) = 1.5 mean_{i,j} y[4i, 4j+1]."""
+    a = arch_dict(levels=3, base=8, ncls=1, scale_codes=(1,), slide_mag=1)
+    arch = nn.parse_arch(arch_string(a))
+    net = nn.unpack_weights(arch, np.zeros(param_count(a)))
+
+    def tap(name, kh, kw, scale=1.0):
+        w, b = net[name]
+        w = np.zeros_like(w)
+        for c in range(3):
+            w[c, kh, kw, c] = scale
+        net[name] = (w, b)
+
+    tap("stem", 0, 1)
+    tap("enc0.a", 1, 1)
+    tap("enc0.b", 1, 1, 0.5)
+    tap("down0", 1, 2)
+    tap("down1", 1, 1)
+    tap("up1", 0, 0)
+    tap("up0", 0, 0)
+    tap("precls", 0, 0)
+    P = 16
+    x = np.random.default_rng(7).integers(0, 256, (P, P, 3)).astype(np.uint8)
+    y = np.zeros((P, P, 3))
+    y[1:] = x[:-1]
+    F, E = nn.trunk(net, arch, x)
+    exp = np.zeros((P, P, 3))
+    for i in range(P):
+        for j in range(P):
+            exp[i, j] = 1.5 * (y[i, j] + y[2 * (i // 2), 2 * (j // 2) + 1] + y[4 * (i // 4), 4 * (j // 4) + 1])
+    assert (F[:, :, :3] == exp).all()
+    assert (F[:, :, 3:] == 0).all()
+    np.testing.assert_allclose(nn.gap(E)[:3], 1.5 * y[0::4, 1::4].mean(axis=(0, 1)), rtol=1e-14)
