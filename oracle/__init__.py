@@ -9,8 +9,9 @@ CUDA path (paper_2305_14566_b200) and never imports it.
 Pins (tests/test_oracle_*.py, -m "not gpu"): brute-force convolution, SciPy
 median filter, textbook Otsu with exact rationals, SPEC worked examples
 (tests/golden/), tile-grid closed forms, stitch closed forms, special-weight
-closed forms of the network and head. Parity unpinned: the end-to-end output
-of a random network has no closed form; it is pinned only through its parts
-(DESIGN.md §5).
+closed forms of the network and head (constant network, hand-set theta, the
+shift-identity network whose trunk reduces to a per-pixel formula). Parity
+unpinned: the end-to-end output of a random network has no closed form; it is
+pinned through its parts and those special networks.
 """
 from . import frontend, net, pipeline  # noqa: F401
