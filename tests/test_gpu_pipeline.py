@@ -327,11 +327,12 @@ def test_invalid_calls_fail_cleanly_and_the_handle_recovers(gpu_lib):
     assert (prob == p2).all() and (mask == m2).all()
 
 
-def _shift_identity_net(levels, base, bc=None):
+def _shift_identity_net(levels, base, bc=None, dtype="fp16f8"):
     """Weights of the single-tap identity network (see test_shift_identity_network_bit_exact);
     bc: optional controller bias (= theta, the controller weights being zero)."""
     from omniseg_inputs.arch import arch_dict, blob_layout, param_count
     a = arch_dict(levels=levels, base=base, ncls=1, scale_codes=(1,), slide_mag=1, batch=16)
+    a["dtype"] = dtype
     arch = nn.parse_arch(arch_string(a))
     net = nn.unpack_weights(arch, np.zeros(param_count(a)))
 
@@ -356,8 +357,9 @@ def _shift_identity_net(levels, base, bc=None):
     return a, net, blob
 
 
-@pytest.mark.parametrize("levels, base, P", [(3, 8, 256), (5, 32, 512)])
-def test_shift_identity_network_bit_exact(gpu_lib, levels, base, P):
+@pytest.mark.parametrize("levels, base, P, dtype", [(3, 8, 256, "fp16f8"), (5, 32, 512, "fp16f8"),
+                                                   (5, 32, 512, "fp16x2")])
+def test_shift_identity_network_bit_exact(gpu_lib, levels, base, P, dtype):
     """The single-tap identity network of tests/test_oracle_net.py, generalised to L levels
     (stem tap (0, 1): y = x shifted down one row; enc0 = RB with conv_a = I, conv_b = I/2, so
     E0 = 1.5 y; down0 tap (1, 2), deeper downs centre taps; identity up-convs and precls):
@@ -368,7 +370,7 @@ def test_shift_identity_network_bit_exact(gpu_lib, levels, base, P):
     stride-2 sample, up x2, skips) independently of rounding. theta = 0 (zero controller)
     gives p = sigmoid(0) = 1/2 exactly."""
     from paper_2305_14566_b200 import Omniseg
-    a, net, blob = _shift_identity_net(levels, base)
+    a, net, blob = _shift_identity_net(levels, base, dtype=dtype)
     arch = nn.parse_arch(arch_string(a))
     tiles = random_tiles(2, P, 21).numpy()
     h = Omniseg(arch_string(a), blob)
