@@ -426,3 +426,33 @@ def test_shift_identity_network_slide_parity(gpu_lib, levels, base, P, S, pad):
     assert covered.mean() > 0.3 and pc.min() < 0.3 and pc.max() > 0.7 and pc.std() > 0.02  # informative
     dis = mask.reshape(H, W) != ref["mask"][0]
     assert (np.abs(p_ref[dis] - 0.5) <= 2e-6).all()
+
+
+def test_shift_identity_network_vote_exact(gpu_lib):
+    """Vote fusion with the identity network and z = F_0 / 256 - 2: z is exact in
+    fp32 on the GPU (F exact, a power-of-two scale), so every window's vote equals the
+    oracle's and the vote fractions and masks must agree EXACTLY, dense stride included
+    (S = 64: up to 16 covering windows)."""
+    theta = np.zeros(153)
+    theta[0:64] = np.eye(8).ravel()
+    theta[72:136] = np.eye(8).ravel()
+    theta[144] = 1.0 / 256
+    theta[152] = -2.0
+    a, net, blob = _shift_identity_net(3, 8, bc=theta)
+    a["fusion"] = "vote"
+    w = workload(1)
+    slide, _ = _cfg1_ref()
+    H, W = slide.shape[:2]
+    ref = op.segment_slide(slide, blob, arch_string(a), w.pad, w.patch, 64, w.scales, w.classes)
+    from paper_2305_14566_b200 import Omniseg
+    h = Omniseg(arch_string(a), blob)
+    prob = np.zeros(H * W, np.float32)
+    mask = np.zeros(H * W, np.uint8)
+    area = np.zeros(1, np.uint64)
+    h.segment_slide(slide, H, W, w.pad, w.patch, 64, w.scales, w.classes, prob, mask, area)
+    assert ref["cnt"][0].max() == 16
+    d = np.abs(prob.reshape(H, W).astype(np.float64) - ref["prob"][0])
+    assert d.max() <= 1e-7, d.max()
+    assert (mask.reshape(H, W) == ref["mask"][0]).all()
+    assert int(area[0]) == int(ref["mask"][0].sum())
+    assert 0.05 < ref["mask"][0].mean() < 0.95
