@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4",
-                    help="cfg1..cfg5 (BASELINE.json configs), or a SURVEY §8(f) geometry on cfg4's slide: "
+                    help="cfg1..cfg5 (BASELINE.json configs; cfg5_fg5/25/60/95: the foreground sweep), "
+                         "or a SURVEY §8(f) geometry on cfg4's slide: "
                          "cfg4_paper (N1: vote fusion, 40x S=256, 10x/5x S=64), "
                          "cfg4_n4 (N4: Oracle-pipeline geometry, 256 windows, S=128, pad 2048, vote)")
     ap.add_argument("--dtype", default=None,
@@ -116,6 +117,9 @@ def resolve_workload(name):
     """-> (Workload, [(stride, [task indices])]) for a --workload name."""
     from omniseg_inputs import workload
     pr = PRESETS.get(name)
+    if pr is None and name.startswith("cfg5_fg"):  # BASELINE configs[4] sweep point: cfg5_fg5/25/60/95
+        w = workload(5, fg_fraction=int(name[7:]) / 100)
+        return w, [(w.stride, list(range(len(w.scales))))]
     if pr is None:
         w = workload(int(name.replace("cfg", "")))
         return w, [(w.stride, list(range(len(w.scales))))]
