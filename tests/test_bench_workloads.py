@@ -36,3 +36,11 @@ def test_oracle_pipeline_geometry_n4():
     w, groups = _bench().resolve_workload("cfg4_n4")
     assert (w.patch, w.stride, w.pad) == (256, 128, 2048)
     assert w.arch["fusion"] == "vote" and len(groups) == 1
+
+
+def test_foreground_sweep_names():
+    b = _bench()
+    for f in (5, 25, 60, 95):
+        w, groups = b.resolve_workload(f"cfg5_fg{f}")
+        assert w.name == f"cfg5_sweep_fg{f}" and (w.H, w.W) == (40000, 40000)
+        assert groups == [(256, list(range(6)))]
