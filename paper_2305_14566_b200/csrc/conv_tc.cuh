@@ -2075,8 +2075,11 @@ struct StemArgs {
 
 template <int BN, int R, int NA>
 struct StemSmem {
-  static constexpr int kA = 4 * 128 * 16;        // one row: [kc][128 px][16 B]
-  static constexpr int kB = 4 * BN * 16;         // [kc][BN][16 B]
+  // K = 48: the 3x3 window's 9 pixels x RGBX (k = (dy*3 + dx)*4 + c, X and k >= 36 weighted 0),
+  // so one RGBX word of the level image becomes two fp16 pairs by byte permutes
+  static constexpr int kKC = 6;                  // 16-byte K chunks
+  static constexpr int kA = kKC * 128 * 16;      // one row: [kc][128 px][16 B]
+  static constexpr int kB = kKC * BN * 16;       // [kc][BN][16 B]
   static constexpr int kCH = BN < 32 ? BN : 32;  // output box width (make_stem_plan's maps)
   static constexpr int kBOff = NA * kA;
   static constexpr int kBarOff = ((kBOff + kB + 1023) / 1024) * 1024;
@@ -2123,9 +2126,9 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
   // weights -> smem B operand (no-swizzle K-major: [kc][n][8 x 16-bit])
   if (tid < 128) {
     const uint4* wsrc = static_cast<const uint4*>(args.w);
-    for (int i = tid; i < BN * 4; i += 128) {
-      const int n = i / 4, kc = i % 4;
-      *reinterpret_cast<uint4*>(smem + S::kBOff + kc * BN * 16 + n * 16) = wsrc[n * 4 + kc];
+    for (int i = tid; i < BN * S::kKC; i += 128) {
+      const int n = i / S::kKC, kc = i % S::kKC;
+      *reinterpret_cast<uint4*>(smem + S::kBOff + kc * BN * 16 + n * 16) = wsrc[n * S::kKC + kc];
     }
     ptx::fence_proxy_async();
   }
@@ -2181,26 +2184,28 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
       for (int r = 0; r < R; ++r) {
         ptx::mbar_wait(&aempty[stage], phase ^ 1);
         uint8_t* a = smem + stage * S::kA;
-        float v[32];
+        uint32_t o[24];  // 48 16-bit K values: pixel p -> o[2p] = (R, G), o[2p+1] = (B, X)
 #pragma unroll
         for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx) {
             const uint32_t q = win[r + dy][dx];
-            const int k = (dy * 3 + dx) * 3;
-            v[k] = float(q & 255);
-            v[k + 1] = float((q >> 8) & 255);
-            v[k + 2] = float((q >> 16) & 255);
+            const int p2 = (dy * 3 + dx) * 2;
+            if constexpr (std::is_same<T, __half>::value) {
+              // byte b -> fp16 bits 0x6400 | b = 1024 + b (exact), minus 1024 in one packed op
+              o[p2] = ptx::hsub2_u32(__byte_perm(q, 0x64646464u, 0x4140), 0x64006400u);
+              o[p2 + 1] = ptx::hsub2_u32(__byte_perm(q, 0x64646464u, 0x4342), 0x64006400u);
+            } else {
+              o[p2] = StoreT<T>::pack(float(q & 255), float((q >> 8) & 255));
+              o[p2 + 1] = StoreT<T>::pack(float((q >> 16) & 255), float(q >> 24));
+            }
           }
 #pragma unroll
-        for (int k = 27; k < 32; ++k) v[k] = 0.f;
+        for (int k = 18; k < 24; ++k) o[k] = 0u;
 #pragma unroll
-        for (int kc = 0; kc < 4; ++kc) {
-          uint32_t o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) o[e] = StoreT<T>::pack(v[8 * kc + 2 * e], v[8 * kc + 2 * e + 1]);
-          *reinterpret_cast<uint4*>(a + kc * 2048 + px * 16) = make_uint4(o[0], o[1], o[2], o[3]);
-        }
+        for (int kc = 0; kc < S::kKC; ++kc)
+          *reinterpret_cast<uint4*>(a + kc * 2048 + px * 16) =
+              make_uint4(o[4 * kc], o[4 * kc + 1], o[4 * kc + 2], o[4 * kc + 3]);
         ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
         ptx::mbar_arrive(&afull[stage]);
         if (++stage == NA) {
@@ -2232,7 +2237,7 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
         const uint32_t sa = ptx::smem_u32(smem + stage * S::kA);
         const uint32_t d = tmem_base + acc * R * BN + r * BN;
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
+        for (int ks = 0; ks < S::kKC / 2; ++ks) {
           const uint64_t da = ptx::smem_desc_noswz(sa + ks * 2 * 2048, 2048, 128);
           const uint64_t db = ptx::smem_desc_noswz(sb + ks * 2 * BN * 16, BN * 16, 128);
           ptx::mma_f16_w(d, da, db, idesc, ks);

@@ -182,6 +182,7 @@ struct Layer {
   int in_kind = 0;  // StoreKind of the layer's input
   int cin = 0, cout = 0, cinp = 0, coutp = 0, k = 3, stride = 1;
   int alg_k = 0; // algorithmic K if not k*k*cin (the stem: 27)
+  DevBuf wpx;    // stem only: [coutp][48] weights of the fused stem's pixel-major RGBX im2col
 };
 
 struct LevelBufs {
@@ -328,6 +329,13 @@ void upload_stem(Layer& L, const float* w, const float* b, int cout, int coutp) 
     for (int j = 0; j < 27; ++j) w32[(size_t)o * 32 + j] = w[(size_t)o * 27 + j];
   upload_conv<T>(L, w32.data(), b, 32, cout, 1, 1, 32, coutp);
   L.alg_k = 27;
+  // fused stem (stem_tc_kernel): column (dy*3 + dx)*4 + c, c < 3; the X byte and 36..47 weigh 0
+  std::vector<T> w48((size_t)coutp * 48, to16<T>(0.f));
+  for (int o = 0; o < cout; ++o)
+    for (int p = 0; p < 9; ++p)
+      for (int c = 0; c < 3; ++c) w48[(size_t)o * 48 + p * 4 + c] = to16<T>(w[(size_t)o * 27 + p * 3 + c]);
+  L.wpx.ensure(w48.size() * sizeof(T));
+  OS_CUDA(cudaMemcpy(L.wpx.p, w48.data(), w48.size() * sizeof(T), cudaMemcpyHostToDevice));
 }
 
 size_t param_count(const Arch& a) {
@@ -513,7 +521,7 @@ void ensure_workspace(omniseg* h, int P) {
                                  h->stem.coutp, 1, 1, kResidualRelu, nullptr, h->lv[0].A.p, ar.sp(0), -1, -1, -1,
                                  kStorePlain, nullptr, 0, 0, rc[0]);
     mp.args.split = h->enc_plans[0].args.split;
-    h->stem_plan = make_stem_plan(mp, h->stem.w.p, P);
+    h->stem_plan = make_stem_plan(mp, h->stem.wpx.p, P);
   }
   // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
   h->head_fusable = false;
