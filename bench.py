@@ -373,13 +373,14 @@ def main():
                "sample": "not run: the oracle baseline is timed on cfg1..cfg5 (bench.py --workload cfg4)"}
     elif rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
         try:
-            t_fe, t_tile = oracle_sample(w, lambda r0, r1: render(g, r0, r1).numpy())
+            strip, nt = 1024, 2  # ~10 s of CPU work
+            t_fe, t_tile = oracle_sample(w, lambda r0, r1: render(g, r0, r1).numpy(), n_tiles=nt, strip=strip)
             n_or = tile_estimate(w)
-            T = t_fe * H / 512 + t_tile * n_or
+            T = t_fe * H / strip + t_tile * n_or
             cpu = {"value": H * W / 1e6 / T, "unit": "Mpx/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-                   "sample": f"oracle (fp64 numpy) front end on a 512-row strip ({t_fe:.2f} s) + one 512^2 window "
-                             f"through trunk+head+stitch ({t_tile:.2f} s), extrapolated to {H} rows and "
-                             f"{n_or} kept tiles (oracle tile plan)"}
+                   "sample": f"oracle (fp64 numpy) front end on a {strip}-row strip ({t_fe:.2f} s) + {nt} 512^2 "
+                             f"windows through trunk+head+stitch ({t_tile:.2f} s each), extrapolated to {H} rows "
+                             f"and {n_or} kept tiles (oracle tile plan)"}
         except Exception as e:  # the baseline must never break the bench line
             cpu = {"value": None, "unit": "Mpx/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"failed: {e}"}
