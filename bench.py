@@ -108,7 +108,9 @@ class Clocks:
 # omniseg_segment_slide call -- the API takes one stride per call, so the paper's per-scale
 # strides (40x 256, 10x/5x 64) are two calls per step.
 PRESETS = {
-    "cfg4_paper": dict(base=4, fusion="vote", groups=((256, (40,)), (64, (10, 5)))),
+    # vthr: the paper's literal vote-count thresholds per scale code 5/10/20/40 ("set to 4" at
+    # 10x/5x, "set to 1" at 40x; 20x has none -> majority), against the 2-D coverage, min(thr, cov)
+    "cfg4_paper": dict(base=4, fusion="vote", vthr=(4, 4, 0, 1), groups=((256, (40,)), (64, (10, 5)))),
     "cfg4_n4": dict(base=4, fusion="vote", patch=256, stride=128, pad=2048),
 }
 
@@ -126,6 +128,8 @@ def resolve_workload(name):
     w = workload(pr["base"])
     w.name = name
     w.arch["fusion"] = pr["fusion"]
+    if "vthr" in pr:
+        w.arch["vthr"] = pr["vthr"]
     for k in ("patch", "stride", "pad"):
         if k in pr:
             setattr(w, k, pr[k])

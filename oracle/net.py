@@ -30,7 +30,8 @@ def parse_arch(s: str) -> dict:
     return dict(levels=int(d["levels"]), base=int(d["base"]), ncls=int(d["ncls"]),
                 scale_codes=[int(x) for x in d["scale_codes"].split(",")],
                 slide_mag=int(d["slide_mag"]), fusion=d.get("fusion", "mean"),
-                fgmin=int(d.get("fgmin", 0)), maskfg=int(d.get("maskfg", 0)))
+                fgmin=int(d.get("fgmin", 0)), maskfg=int(d.get("maskfg", 0)),
+                vthr=[int(x) for x in d["vthr"].split(",")] if "vthr" in d else None)
 
 
 def unpack_weights(arch: dict, blob: np.ndarray) -> dict:

@@ -43,12 +43,15 @@ def canvas_shape(H, W, f):
 
 
 def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, stride: int,
-                  scales, classes, progress=None, fusion=None):
+                  scales, classes, progress=None, fusion=None, keep_windows=False):
     """Plain CPU pipeline. Returns dict with per-task prob (float64),
     mask (u8), area (int), the kept tile list, fg mask and Otsu t.
     fusion: "mean" (overlap-weighted mean of p, DESIGN R11) or "vote" (hard majority vote,
     SURVEY N1: each window votes p >= 1/2, "majority of the testing results", "1 of
-    2" / "4 of 8" -- both "at least half"); default: the arch string's `fusion` key, else mean."""
+    2" / "4 of 8" -- both "at least half"); default: the arch string's `fusion` key, else mean.
+    With the arch key vthr (one vote count per scale code) the vote mask is the paper's literal
+    count threshold instead (finalize_vote_count). keep_windows: also return every kept window's
+    per-task probability maps, {(f, oy, ox): {task index: p}} (for tests that inspect votes)."""
     arch = nn.parse_arch(arch_s)
     if fusion is None:
         fusion = arch.get("fusion", "mean")
@@ -59,7 +62,7 @@ def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, st
     tf = task_factors(arch, scales)
     fr = front_end(slide, pad, patch, stride, [f for f, _ in tf], min_area=arch.get("fgmin", 0))
     levels = {f: fe.level(fr["padded"], f) for f in set(f for f, _ in tf)}
-    sums, cnts = [], []
+    sums, cnts, windows = [], [], {}
     for (f, _s) in tf:
         sums.append(np.zeros(canvas_shape(H, W, f)))
         cnts.append(np.zeros(canvas_shape(H, W, f), np.int64))
@@ -67,14 +70,23 @@ def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, st
         tile = levels[f][oy:oy + patch, ox:ox + patch]
         tasks = [(t, classes[t], s) for t, (ft, s) in enumerate(tf) if ft == f]
         p = nn.predict_tile(net, arch, tile, [(c, s) for _, c, s in tasks])
+        if keep_windows:
+            windows[(f, oy, ox)] = {t: p[k] for k, (t, _c, _s) in enumerate(tasks)}
         for k, (t, _c, _s) in enumerate(tasks):
             val = vote_of(p[k]) if fusion == "vote" else p[k]
             stitch_add(sums[t], cnts[t], val, oy - pad // f, ox - pad // f)
         if progress:
             progress(i, len(fr["kept"]))
+    vthr = arch.get("vthr")
+    if vthr is not None and len(vthr) != len(arch["scale_codes"]):
+        raise ValueError("vthr needs one threshold per scale code")
     probs, masks, areas = [], [], []
     for t in range(len(tf)):
-        prob, mask = finalize(sums[t], cnts[t])
+        thr = vthr[tf[t][1]] if (fusion == "vote" and vthr) else 0
+        if thr > 0:
+            prob, mask = finalize_vote_count(sums[t], cnts[t], thr)
+        else:
+            prob, mask = finalize(sums[t], cnts[t])
         if arch.get("maskfg", 0):
             mask = mask_by_foreground(mask, fr["det"]["fg"], tf[t][0], pad)
         probs.append(prob)
@@ -82,7 +94,7 @@ def segment_slide(slide: np.ndarray, blob, arch_s: str, pad: int, patch: int, st
         areas.append(int(mask.sum()))
     return dict(prob=probs, mask=masks, area=areas, kept=fr["kept"], grids=fr["grids"],
                 fg=fr["det"]["fg"], t=fr["det"]["t"], hist=fr["det"]["hist"],
-                g_pad=fr["det"]["g_pad"], cnt=cnts)
+                g_pad=fr["det"]["g_pad"], cnt=cnts, windows=windows if keep_windows else None)
 
 
 def vote_of(p):
@@ -110,6 +122,16 @@ def finalize(acc_sum, acc_cnt):
     (the paper's 1-of-2 and 4-of-8 votes are both 'at least half'; DESIGN R11)."""
     prob = np.where(acc_cnt > 0, acc_sum / np.maximum(acc_cnt, 1), 0.0)
     return prob, (prob >= 0.5).astype(np.uint8)
+
+
+def finalize_vote_count(votes, cnt, thr):
+    """Hard vote with the paper's literal vote-count threshold (arch key vthr; "the major
+    vote threshold was set to 1" at 40x, "set to 4" at 10x / 5x; S:266-268, S:310-311 read
+    against the 2-D coverage): mask = votes >= min(thr, coverage), coverage > 0 (min() keeps
+    edge pixels covered by fewer windows than thr decidable). prob = vote fraction."""
+    prob = np.where(cnt > 0, votes / np.maximum(cnt, 1), 0.0)
+    mask = (cnt > 0) & (votes >= np.minimum(thr, cnt))
+    return prob, mask.astype(np.uint8)
 
 
 def mask_by_foreground(mask, fg8, f, pad):

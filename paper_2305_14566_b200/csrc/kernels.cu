@@ -636,11 +636,13 @@ __global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, 
 // cnt = acc >> 28, sum = acc & (2^28 - 1): prob = sum 2^-20 / cnt (0 if cnt = 0),
 // mask = 2 sum >= cnt 2^20 (exactly prob >= 1/2 on the fixed-point values, R12), area.
 // vote: the accumulator is count << 16 | votes (hard majority vote): prob = vote
-// fraction, mask = 2 votes >= count; else count << 28 | sum(round(p 2^20)) (R12).
+// fraction, mask = 2 votes >= count, or with a literal count threshold vthr > 0 (arch key
+// vthr; "major vote threshold was set to 1" / "4"): votes >= min(vthr, count);
+// else count << 28 | sum(round(p 2^20)) (R12).
 // fg8 (optional, SURVEY N2 / P:87): the mask is ANDed with the level-8 foreground, nearest-
 // neighbour: canvas pixel (cy, cx) -> level-8 pixel ((cy f + pad) / 8, (cx f + pad) / 8).
 __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask,
-                                unsigned long long* area, int vote, FgMaskArgs fm) {
+                                unsigned long long* area, int vote, int vthr, FgMaskArgs fm) {
   __shared__ unsigned long long s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
@@ -650,7 +652,7 @@ __global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uin
     const int sh = vote ? 16 : 28;
     const uint32_t cnt = a >> sh, sum = a & ((1u << sh) - 1u);
     const int fb = vote ? 0 : 20;  // fixed-point bits of the per-window value
-    bool m = cnt > 0 && 2ull * sum >= ((unsigned long long)cnt << fb);
+    bool m = cnt > 0 && (vthr > 0 ? sum >= min((uint32_t)vthr, cnt) : 2ull * sum >= ((unsigned long long)cnt << fb));
     if (fm.fg8 && m) {
       const int64_t cy = fm.cy0 + i / fm.Wt, cx = i % fm.Wt;
       m = fm.fg8[((cy * fm.f + fm.pad) >> 3) * (int64_t)fm.W8 + ((cx * fm.f + fm.pad) >> 3)] != 0;
@@ -916,10 +918,10 @@ void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const fl
                                              pad, out_p, out_F);
 }
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area, int vote,
-                     const FgMaskArgs& fm, cudaStream_t s) {
+                     int vthr, const FgMaskArgs& fm, cudaStream_t s) {
   if (n <= 0) return;
   int blocks = (int)std::min<int64_t>(8 * 148, (n + 255) / 256);
-  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area, vote, fm);
+  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area, vote, vote ? vthr : 0, fm);
 }
 void launch_fg_components(uint8_t* fg, int W, int r0, int r1, int min_area, int* lab, int* size, cudaStream_t s) {
   const int64_t n = (int64_t)(r1 - r0) * W;

@@ -56,8 +56,10 @@ struct FgMaskArgs {
   int W8 = 0, f = 1, pad = 0, Wt = 1;
   int64_t cy0 = 0;
 };
+// vote: 0 mean fusion, 1 hard vote; vthr (vote only): 0 = majority ("at least half"), else the
+// literal vote-count threshold min(vthr, coverage) (arch key vthr).
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area, int vote,
-                     const FgMaskArgs& fm, cudaStream_t s);
+                     int vthr, const FgMaskArgs& fm, cudaStream_t s);
 // Tiny-component removal on level-8 foreground rows [r0, r1) (lab, size: scratch of
 // (r1 - r0) W ints each).
 void launch_fg_components(uint8_t* fg, int W, int r0, int r1, int min_area, int* lab, int* size, cudaStream_t s);

@@ -104,6 +104,7 @@ struct Arch {
   int vote = 0;             // fusion rule: 0 mean of p (R11), 1 hard majority vote
   int fgmin = 0;            // drop foreground components below fgmin level-8 pixels
   int maskfg = 0;           // AND the output masks with the foreground
+  std::vector<int> vthr;    // vote fusion: literal vote-count threshold per scale code; empty = majority
   int sp(int level) const { return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain; }
   // bytes per channel of a tensor stored with kind k
   static int bpc(int k) { return k == kStoreX2 ? 4 : k == kStoreF8 ? 3 : 2; }
@@ -143,6 +144,15 @@ Arch parse_arch(const char* s) {
     else if (k == "xal") a.xal = toi(v);
     else if (k == "fgmin") a.fgmin = toi(v);
     else if (k == "maskfg") a.maskfg = toi(v);
+    else if (k == "vthr") {
+      a.vthr.clear();
+      std::stringstream s2(v);
+      std::string x;
+      while (std::getline(s2, x, ',')) {
+        a.vthr.push_back(toi(x));
+        OS_REQUIRE(a.vthr.back() >= 0, "arch: vthr entries must be >= 0");
+      }
+    }
     else if (k == "fusion") {
       OS_REQUIRE(v == "mean" || v == "vote", "arch: fusion must be mean or vote");
       a.vote = v == "vote";
@@ -169,6 +179,7 @@ Arch parse_arch(const char* s) {
   OS_REQUIRE(!a.scale_codes.empty() && a.scale_codes.size() <= 8, "arch: 1..8 scale codes");
   OS_REQUIRE(a.batch >= 1 && a.batch <= 4096, "arch: batch out of range");
   OS_REQUIRE(a.slide_mag >= 1, "arch: slide_mag must be positive");
+  OS_REQUIRE(a.vthr.empty() || a.vthr.size() == a.scale_codes.size(), "arch: vthr needs one entry per scale code");
   return a;
 }
 
@@ -891,7 +902,8 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
       fm.cy0 = ra;
     }
     launch_finalize(tt.canvas[t] + base - off[t], n, dprob ? dprob + base : nullptr, dmask ? dmask + base : nullptr,
-                    h->area.as<unsigned long long>() + t, h->arch.vote, fm, s);
+                    h->area.as<unsigned long long>() + t, h->arch.vote, h->arch.vthr.empty() ? 0 : h->arch.vthr[tk.scl[t]],
+                    fm, s);
     h->launches++;
     if (host_out) {
       if (!h->copy_stream) OS_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));

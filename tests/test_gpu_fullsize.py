@@ -28,8 +28,43 @@ def _unpack(ids, Hp, Wp, P, S):
     return out
 
 
+def _region_check(kept, f, pad, P, S, Ht, Wt, rng, pt_tasks, masks, want):
+    """Pick up to `want` kept windows K of scale f; each K's sub-square [S/2, S) x [S/2, S)
+    (window-relative) lies in K and the windows one stride up / left only (S = P/2), so a
+    handful of windows covers every pixel of it. Yields (region slices, covering windows)."""
+    ks = [k for k in kept if k[0] == f]
+    order = rng.permutation(len(ks))
+    # prefer windows whose region holds positive mask pixels of the first task (informative)
+    def region(k):
+        y0, x0 = k[1] - pad // f + S // 2, k[2] - pad // f + S // 2
+        return max(0, y0), min(Ht, y0 + S // 2), max(0, x0), min(Wt, x0 + S // 2)
+    scored = []
+    for i in order[:400]:
+        y0, y1, x0, x1 = region(ks[i])
+        if y1 - y0 < 16 or x1 - x0 < 16:
+            continue
+        scored.append((-int(masks[0][y0:y1, x0:x1].sum() > 0), int(i)))
+    scored.sort()
+    out = []
+    for _, i in scored:
+        y0, y1, x0, x1 = region(ks[i])
+        py0, py1, px0, px1 = y0 + pad // f, y1 + pad // f, x0 + pad // f, x1 + pad // f
+        cov = [k for k in ks if k[1] < py1 and k[1] + P > py0 and k[2] < px1 and k[2] + P > px0]
+        if len(cov) > 6:
+            continue
+        out.append(((y0, y1, x0, x1), cov))
+        if len(out) == want:
+            break
+    return out
+
+
 @pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_fullsize_front_end_and_sampled_probabilities(gpu_lib, cfg):
+    """Full-size bit-exact front end, then, for EVERY task (every scale: 5x f = 8, 10x f = 4,
+    40x f = 1 on cfg3/cfg4), element-wise probability/mask checks over whole sub-squares of
+    kept windows whose covering windows the fp64 oracle computes (two regions per scale,
+    <= 6 oracle windows each): |dp| <= 1e-2, masks equal except where the oracle p is within
+    1e-2 of 1/2; >= 500 checked pixels per task (printed)."""
     from paper_2305_14566_b200 import Omniseg
     w = workload(cfg)
     H, W, P, S, pad = w.H, w.W, w.patch, w.stride, w.pad
@@ -52,47 +87,46 @@ def test_fullsize_front_end_and_sampled_probabilities(gpu_lib, cfg):
     kept, _ = fe.tile_plan(det["fg"], det["Hp"], det["Wp"], [f for f, _ in tf], P, S)
     got = _unpack(h.tiles(), det["Hp"], det["Wp"], P, S)
     assert got == kept
-    # ---- sampled probabilities
+    # ---- element-wise regions, per scale (tasks of one scale share the windows)
     net = nn.unpack_weights(arch, w.weights())
     rng = np.random.default_rng(cfg)
     offs = np.concatenate([[0], np.cumsum(sizes)])
-    cache, checked, budget = {}, 0, 10
-    for ti, (f, s_idx) in enumerate(tf):
+    checked = [0] * len(tf)
+    worst = [0.0] * len(tf)
+    for f in sorted(set(f for f, _ in tf), reverse=True):
+        tids = [ti for ti, (ft, _) in enumerate(tf) if ft == f]
         Ht, Wt = (H + f - 1) // f, (W + f - 1) // f
-        pt = prob[offs[ti]:offs[ti + 1]].reshape(Ht, Wt)
-        mt = mask[offs[ti]:offs[ti + 1]].reshape(Ht, Wt)
-        cand = []
-        pos = np.argwhere(mt == 1)
-        if len(pos):
-            cand += [tuple(pos[i]) for i in rng.choice(len(pos), min(2, len(pos)), replace=False)]
-        cov = np.argwhere(pt > 0)
-        if len(cov):
-            cand += [tuple(cov[i]) for i in rng.choice(len(cov), min(2, len(cov)), replace=False)]
-        for (cy, cx) in cand:
-            tiles = op.covering_tiles(kept, f, pad, P, int(cy), int(cx))
-            need = [k for k in tiles if k not in cache]
-            if len(cache) + len(need) > budget:
-                continue
-            for (ff, oy, ox) in need:
-                win = fe.level_window(slide, pad, det["pc"], ff, oy, ox, P)
-                tasks = [(c, s) for c, (f2, s) in zip(w.classes, tf) if f2 == ff]
-                Fr, Er = nn.trunk(net, arch, win)
-                g = nn.gap(Er)
-                cache[(ff, oy, ox)] = {(c, s): nn.head(Fr, nn.controller(net, arch, g, c, s)) for c, s in tasks}
-            # the chosen pixel and its 24x24 neighbourhood wherever the covering windows are cached
-            for yy in range(max(0, cy - 12), min(Ht, cy + 12)):
-                for xx in range(max(0, cx - 12), min(Wt, cx + 12)):
-                    tl = op.covering_tiles(kept, f, pad, P, yy, xx)
-                    if any(k not in cache for k in tl):
-                        continue
-                    ps = [cache[(ff, oy, ox)][(w.classes[ti], s_idx)][yy + pad // f - oy, xx + pad // f - ox]
-                          for (ff, oy, ox) in tl]
-                    p_ref = float(np.mean(ps)) if ps else 0.0
-                    assert abs(float(pt[yy, xx]) - p_ref) <= 1e-2, (ti, yy, xx, pt[yy, xx], p_ref)
-                    if abs(p_ref - 0.5) > 1e-2:
-                        assert int(mt[yy, xx]) == int(p_ref >= 0.5)
-                    checked += 1
-    assert checked >= 500
+        pts = [prob[offs[ti]:offs[ti + 1]].reshape(Ht, Wt) for ti in tids]
+        mts = [mask[offs[ti]:offs[ti + 1]].reshape(Ht, Wt) for ti in tids]
+        cache = {}
+        for (y0, y1, x0, x1), cov in _region_check(kept, f, pad, P, S, Ht, Wt, rng, pts, mts, 2):
+            for k in cov:
+                if k not in cache:
+                    win = fe.level_window(slide, pad, det["pc"], f, k[1], k[2], P)
+                    Fr, Er = nn.trunk(net, arch, win)
+                    g = nn.gap(Er)
+                    cache[k] = {ti: nn.head(Fr, nn.controller(net, arch, g, w.classes[ti], tf[ti][1])) for ti in tids}
+            for j, ti in enumerate(tids):
+                acc = np.zeros((y1 - y0, x1 - x0))
+                cnt = np.zeros((y1 - y0, x1 - x0), np.int64)
+                for k in cov:
+                    oy, ox = k[1] - pad // f, k[2] - pad // f   # window origin in canvas coordinates
+                    a0, a1 = max(y0, oy), min(y1, oy + P)
+                    b0, b1 = max(x0, ox), min(x1, ox + P)
+                    acc[a0 - y0:a1 - y0, b0 - x0:b1 - x0] += cache[k][ti][a0 - oy:a1 - oy, b0 - ox:b1 - ox]
+                    cnt[a0 - y0:a1 - y0, b0 - x0:b1 - x0] += 1
+                assert (cnt > 0).all()
+                p_ref = acc / cnt
+                p_gpu = pts[j][y0:y1, x0:x1].astype(np.float64)
+                m_gpu = mts[j][y0:y1, x0:x1]
+                d = np.abs(p_gpu - p_ref)
+                assert d.max() <= 1e-2, (cfg, ti, f, d.max())
+                dis = m_gpu != (p_ref >= 0.5)
+                assert (np.abs(p_ref[dis] - 0.5) <= 1e-2).all(), (cfg, ti, "mask flip away from 1/2")
+                checked[ti] += d.size
+                worst[ti] = max(worst[ti], float(d.max()))
+    print(f"cfg{cfg}: checked px per task {checked}, max |dp| per task {[f'{v:.2e}' for v in worst]}")
+    assert min(checked) >= 500, checked
 
 
 def test_synthetic_slide_cpu_gpu_identical(gpu_lib):
@@ -169,7 +203,9 @@ def test_fullsize_paper_geometry_vote_sampled(gpu_lib):
                 frac_ref = votes / len(tl)
                 if np.abs(ps - 0.5).min() > 1e-2:
                     assert abs(float(pt[cy, cx]) - frac_ref) <= 1e-6, (S, ti, cy, cx, pt[cy, cx], frac_ref)
-                    assert int(mt[cy, cx]) == int(2 * votes >= len(tl))
+                    thr = arch["vthr"][s_idx] if arch.get("vthr") else 0
+                    exp_m = votes >= min(thr, len(tl)) if thr else 2 * votes >= len(tl)
+                    assert int(mt[cy, cx]) == int(exp_m)
                 done += 1
                 checked += 1
     assert checked >= 6

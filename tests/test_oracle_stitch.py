@@ -143,3 +143,76 @@ def test_vote_equals_thresholded_mean_where_one_window_covers():
     assert (rv["prob"][0][one] == (rm["prob"][0][one] >= 0.5)).all()
     k = rv["prob"][0] * rm["cnt"][0]  # vote fractions are (integer votes) / cnt
     assert np.allclose(k, np.round(k), atol=1e-9)
+
+
+# ---------------------------------------------------------------- literal vote-count threshold (arch vthr)
+def _vote_sim(tiles, ps, H, W, P, thr):
+    """Brute force: explicit per-pixel counters over every tile (S:311 'brute-force simulator')."""
+    votes = np.zeros((H, W), np.int64)
+    cov = np.zeros((H, W), np.int64)
+    for (y, x), p in zip(tiles, ps):
+        for yy in range(max(0, y), min(H, y + P)):
+            for xx in range(max(0, x), min(W, x + P)):
+                cov[yy, xx] += 1
+                votes[yy, xx] += int(p[yy - y, xx - x] >= 0.5)
+    mask = np.zeros((H, W), np.uint8)
+    for yy in range(H):
+        for xx in range(W):
+            c = cov[yy, xx]
+            mask[yy, xx] = int(c > 0 and votes[yy, xx] >= min(thr, c))
+    return votes, cov, mask
+
+
+def test_vote_count_threshold_brute_force_and_monotone():
+    """P:97 literal thresholds ('set to 1' at 40x, 'set to 4' at 10x/5x) applied to the 2-D
+    coverage with the clamp min(thr, coverage): against the per-pixel brute force
+    on random windows; raising the threshold never turns a 0 pixel into a 1."""
+    rng = np.random.default_rng(11)
+    H, W, P = 36, 40, 12
+    tiles = [(int(rng.integers(-6, 32)), int(rng.integers(-6, 36))) for _ in range(40)]
+    ps = [rng.random((P, P)) for _ in tiles]
+    s, c = np.zeros((H, W)), np.zeros((H, W), np.int64)
+    for (y, x), p in zip(tiles, ps):
+        op.stitch_add(s, c, op.vote_of(p), y, x)
+    prev = None
+    for thr in (1, 2, 4, 8, 64):
+        votes, cov, mask = _vote_sim(tiles, ps, H, W, P, thr)
+        prob, m = op.finalize_vote_count(s, c, thr)
+        assert (c == cov).all() and (s == votes).all()
+        assert (m == mask).all(), thr
+        assert (prob == np.where(cov > 0, votes / np.maximum(cov, 1), 0)).all()
+        if prev is not None:
+            assert not (m & ~prev).any()
+        prev = m.astype(bool)
+
+
+def test_vote_count_threshold_spec_40x_example():
+    """40x configuration (extent 4096, window 512, stride 256 -> 225 tiles, threshold 1),
+    predictor positive only in tiles whose origin x = 0: a pixel covered by such a tile gets
+    >= 1 vote -> 1; pixels covered only by other tiles -> 0."""
+    E, P, S = 4096, 512, 256
+    org = fe.origins(E, P, S)
+    assert len(org) ** 2 == 225
+    s, c = np.zeros((E, E)), np.zeros((E, E), np.int64)
+    for oy in org:
+        for ox in org:
+            op.stitch_add(s, c, np.full((P, P), 1.0 if ox == 0 else 0.0), oy, ox)
+    _, m = op.finalize_vote_count(s, c, 1)
+    exp = np.zeros((E, E), np.uint8)
+    exp[:, :P] = 1
+    assert (m == exp).all()
+    assert (c[P:E - P, P:E - P] == 4).all()       # interior 2-D coverage (window / stride)^2
+
+
+def test_vote_count_threshold_end_to_end_per_scale():
+    """segment_slide with vthr: each task uses its scale code's threshold; thr = 1 makes a
+    pixel positive iff any covering window votes positive."""
+    w = workload(1)
+    slide = make_slide(w.slide).numpy()
+    w.arch["fusion"] = "vote"
+    rm = op.segment_slide(slide, w.weights(), arch_string(w.arch), w.pad, w.patch, w.stride, w.scales, w.classes)
+    w.arch["vthr"] = (1,)
+    r1 = op.segment_slide(slide, w.weights(), arch_string(w.arch), w.pad, w.patch, w.stride, w.scales, w.classes)
+    assert (r1["prob"][0] == rm["prob"][0]).all()
+    assert (r1["mask"][0] == (rm["prob"][0] > 0)).all()
+    assert r1["mask"][0].sum() >= rm["mask"][0].sum()
