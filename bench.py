@@ -253,8 +253,9 @@ def main():
     H, W = w.H, w.W
     Hp = (H + 2 * w.pad + 127) // 128 * 128
     fmax = max(w.arch["slide_mag"] // s for s in w.scales)
+    cuts = D.band_cuts(Hp, world, w.stride)
     if world > 1:
-        row0, row1 = D.band_partition(Hp, world, w.stride)[rank]
+        row0, row1 = cuts[rank], cuts[rank + 1]
         b0, b1 = D.band_slide_rows(H, w.pad, w.patch, fmax, row0, row1)
     else:
         row0, row1, b0, b1 = 0, Hp, 0, H
@@ -279,13 +280,19 @@ def main():
         gsl.append((S, [w.scales[i] for i in idx], [w.classes[i] for i in idx], n0, ncan, idx))
     prob = torch.empty(max(ncan, 1), dtype=torch.float32, device=dev)
     mask = torch.empty(max(ncan, 1), dtype=torch.uint8, device=dev)
+    # N > 1, device-resident: the bands are gathered into full-slide outputs on rank 0 (NCCL)
+    nfull = sum(((H + f - 1) // f) * ((W + f - 1) // f) for f in (w.arch["slide_mag"] // s for s in w.scales))
+    full_prob = torch.empty(nfull if (world > 1 and rank == 0) else 1, dtype=torch.float32, device=dev)
+    full_mask = torch.empty(nfull if (world > 1 and rank == 0) else 1, dtype=torch.uint8, device=dev)
     area = torch.zeros(len(w.scales), dtype=torch.int64, device=dev)
     D.init_comm(h, world, rank)
     tiles_per_step = [0]
 
-    def step(src, p_out, m_out, a_out):
+    def step(src, p_out, m_out, a_out, gather=True):
         if world > 1:
             h.segment_band(src, H, W, row0, row1, w.pad, w.patch, w.stride, w.scales, w.classes, p_out, m_out, a_out)
+            if gather:   # device-resident outputs: the band gather to rank 0 (host outputs stay per rank)
+                h.gather_bands(0, H, W, w.pad, cuts, w.scales, p_out, m_out, full_prob, full_mask)
             return
         nt = 0
         for S, sc, cl, n0, n1, idx in gsl:
@@ -336,13 +343,13 @@ def main():
         hprob = torch.empty(prob.shape, dtype=torch.float32, pin_memory=True)
         hmask = torch.empty(mask.shape, dtype=torch.uint8, pin_memory=True)
         harea = torch.zeros(area.shape, dtype=torch.int64, pin_memory=True)
-        step(hslide, hprob, hmask, harea)
+        step(hslide, hprob, hmask, harea, gather=False)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
-            step(hslide, hprob, hmask, harea)
+            step(hslide, hprob, hmask, harea, gather=False)
         e1.record(stream)
         barrier()
         ems = torch.tensor([e0.elapsed_time(e1) / steps], device=dev)
@@ -396,7 +403,8 @@ def main():
                           "stride": w.stride if len(gsl) == 1 else {"x".join(map(str, g[1])): g[0] for g in gsl},
                           "pad": w.pad, "fusion": w.arch.get("fusion", "mean"),
                           "tasks": len(w.scales), "kept_tiles": n_tiles, "batch": w.arch["batch"],
-                          "parallelism": f"row-bands x{world}" if world > 1 else "single GPU",
+                          "parallelism": (f"row-bands x{world} + NCCL band gather to rank 0" if world > 1
+                                          else "single GPU"),
                           "l2": "inputs larger than L2 (slide %.1f GB, canvases %.1f GB)"
                                 % (slide.numel() / 1e9, ncan * 5 / 1e9),
                           "slide_gen_s": round(gen_s, 1)},

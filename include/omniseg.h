@@ -111,6 +111,26 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
                          const int* scales, const int* classes, int n_tasks,
                          float* out_prob, uint8_t* out_mask, uint64_t* out_area);
 
+/* An EMPTY band (row0 == row1 > 0: more ranks than 8*stride row units) computes nothing but
+ * joins the same collectives (pad-colour broadcast, histogram and area all-reduces), so a
+ * world larger than the slide's row-unit count still completes; out_area gets the global areas.
+ *
+ * Band gather (the north_star NCCL step, SURVEY §8(e) collective 2): after
+ * omniseg_segment_band on every rank, gather every rank's owned canvas rows into full-slide
+ * outputs on rank `root` (device-resident), one ncclSend/ncclRecv pair per (rank, task) in one
+ * NCCL group (the root's own band too, as a self pair).
+ *   cuts      : world+1 band boundaries of the PADDED 40x frame (cuts[r] = row0 of rank r,
+ *               cuts[world] = Hp), as passed to each rank's segment_band.
+ *   scales    : the n_tasks magnifications of the segment_band calls (classes are not needed).
+ *   band_prob / band_mask: this rank's segment_band outputs (device; NULL = not gathered).
+ *   out_prob / out_mask  : root only: device buffers laid out as omniseg_segment_slide's
+ *               outputs (tasks concatenated, ceil(H/f) x ceil(W/f) each); ignored elsewhere.
+ * Collective: every rank of the communicator must call it with the same cuts / scales.
+ * Errors: EINVAL without a communicator or for host buffers; ENCCL on NCCL failure. */
+int omniseg_gather_bands(omniseg_t* h, int root, int64_t H, int64_t W, int pad, const int64_t* cuts,
+                         const int* scales, int n_tasks, const float* band_prob, const uint8_t* band_mask,
+                         float* out_prob, uint8_t* out_mask);
+
 /* Owned canvas rows of band [row0,row1) for a task at factor f: [r0_t, r1_t) with
  * r0_t = clamp(ceil((row0 - pad)/f), 0, Ht) (likewise r1_t). Pure arithmetic helper. */
 int omniseg_band_rows(int64_t H, int64_t row0, int64_t row1, int pad, int f,

@@ -72,6 +72,10 @@ struct Nccl {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
   void load() {
     if (so) return;
@@ -82,7 +86,12 @@ struct Nccl {
     broadcast = (decltype(broadcast))dlsym(so, "ncclBroadcast");
     commDestroy = (decltype(commDestroy))dlsym(so, "ncclCommDestroy");
     errStr = (decltype(errStr))dlsym(so, "ncclGetErrorString");
-    if (!commInitRank || !allReduce || !broadcast || !commDestroy || !errStr)
+    send = (decltype(send))dlsym(so, "ncclSend");
+    recv = (decltype(recv))dlsym(so, "ncclRecv");
+    groupStart = (decltype(groupStart))dlsym(so, "ncclGroupStart");
+    groupEnd = (decltype(groupEnd))dlsym(so, "ncclGroupEnd");
+    if (!commInitRank || !allReduce || !broadcast || !commDestroy || !errStr || !send || !recv || !groupStart ||
+        !groupEnd)
       throw Error(-4, "libnccl.so.2 lacks required symbols");
   }
   void check(ncclResult_t r, const char* what) {
@@ -906,8 +915,6 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
                     fm, s);
     h->launches++;
     if (host_out) {
-      if (!h->copy_stream) OS_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-      if (!h->copy_ev) OS_CUDA(cudaEventCreateWithFlags(&h->copy_ev, cudaEventDisableTiming));
       OS_CUDA(cudaEventRecord(h->copy_ev, s));
       OS_CUDA(cudaStreamWaitEvent(h->copy_stream, h->copy_ev, 0));
       if (out_prob && !prob_dev)
@@ -995,6 +1002,43 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   h->timings[10] = h->conv_launches + h->launches;
 }
 
+// A rank whose band owns no rows (more ranks than 8*stride row units, dist.band_partition):
+// no compute, but the same collective sequence as segment() -- receive the pad colour, add a
+// zero histogram, add zero areas -- so the other ranks' NCCL calls complete.
+void segment_empty(omniseg* h, int64_t H, int64_t W, int pad, const Tasks& tk, uint64_t* out_area) {
+  cudaStream_t s = h->stream;
+  h->conv_launches = 0;
+  h->launches = 0;
+  const int Hp = (int)((H + 2 * pad + 127) / 128 * 128), Wp = (int)((W + 2 * pad + 127) / 128 * 128);
+  h->H8 = Hp / 8;
+  h->W8 = Wp / 8;
+  h->fg_r0 = h->fg_r1 = 0;
+  h->n_tiles = 0;
+  h->state.ensure(sizeof(DevState));
+  DevState* st = h->state.as<DevState>();
+  OS_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  if (h->inject) OS_CUDA(cudaMemcpyAsync(st, h->inj_pc, 4, cudaMemcpyHostToDevice, s));
+  if (h->comm) g_nccl.check(g_nccl.broadcast(st, st, 4, ncclUint8, 0, h->comm, s), "ncclBroadcast(pad colour)");
+  h->hist.ensure(256 * 8);
+  OS_CUDA(cudaMemsetAsync(h->hist.p, 0, 256 * 8, s));
+  if (h->comm)
+    g_nccl.check(g_nccl.allReduce(h->hist.p, h->hist.p, 256, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(hist)");
+  if (h->inject) OS_CUDA(cudaMemcpyAsync(h->hist.p, h->inj_hist, 256 * 8, cudaMemcpyHostToDevice, s));
+  OS_CUDA(cudaMemcpyAsync(h->last_hist, h->hist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
+  launch_otsu(h->hist.as<unsigned long long>(), st, s);
+  h->area.ensure(kMaxTasks * 8);
+  OS_CUDA(cudaMemsetAsync(h->area.p, 0, kMaxTasks * 8, s));
+  if (h->comm)
+    g_nccl.check(g_nccl.allReduce(h->area.p, h->area.p, tk.n, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(area)");
+  if (out_area) OS_CUDA(cudaMemcpyAsync(out_area, h->area.p, tk.n * 8, cudaMemcpyDefault, s));
+  DevState hst;
+  OS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  OS_CUDA(cudaStreamSynchronize(s));
+  h->otsu_t = hst.otsu_t;
+  h->g_pad = hst.g_pad;
+  for (double& v : h->timings) v = 0;
+}
+
 int fail(const Error& e) {
   g_last_error = e.what();
   return e.code;
@@ -1046,6 +1090,8 @@ omniseg_t* omniseg_create(const char* arch, const void* weights, size_t nbytes) 
     else
       load_weights<__half>(h.get(), blob.data());
     OS_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    OS_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    OS_CUDA(cudaEventCreateWithFlags(&h->copy_ev, cudaEventDisableTiming));
     h->stream = h->own_stream;
     for (auto& e : h->ev) OS_CUDA(cudaEventCreate(&e));
     return h.release();
@@ -1106,11 +1152,6 @@ int omniseg_comm_init(omniseg_t* h, const void* id, int world, int rank) {
     OS_REQUIRE(h && id, "comm_init: NULL argument");
     OS_REQUIRE(world >= 1 && rank >= 0 && rank < world, "comm_init: bad world/rank");
     OS_CUDA(cudaSetDevice(h->device));
-    if (world == 1 && getenv("OMNISEG_FORCE_NCCL") == nullptr) {
-      h->world = 1;
-      h->rank = 0;
-      return 0;
-    }
     g_nccl.load();
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
@@ -1135,7 +1176,12 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
     validate_common(H, W, pad, patch, stride, h->arch.vote != 0);
     Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
     const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
-    OS_REQUIRE(row0 >= 0 && row0 < row1 && row1 <= Hp, "band: need 0 <= row0 < row1 <= Hp");
+    OS_REQUIRE(row0 >= 0 && row0 <= row1 && row1 <= Hp, "band: need 0 <= row0 <= row1 <= Hp");
+    if (row0 == row1) {  // an empty band: collectives only
+      OS_REQUIRE(row0 > 0, "band 0 must not be empty (it holds the pad colour, the broadcast root)");
+      segment_empty(h, H, W, pad, tk, out_area);
+      return 0;
+    }
     OS_REQUIRE(row0 % (8 * stride) == 0 && (row1 == Hp || row1 % (8 * stride) == 0),
                "band: row0/row1 must be multiples of 8*stride (row1 may be Hp)");
     const int64_t halo = (int64_t)patch * tk.fmax + 64;
@@ -1148,6 +1194,69 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
                              out_area);
     else
       segment<__half>(h, rgb_band, H, W, row0, row1, b0, b1, pad, patch, stride, tk, out_prob, out_mask, out_area);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(Error(-2, e.what()));
+  }
+}
+
+int omniseg_gather_bands(omniseg_t* h, int root, int64_t H, int64_t W, int pad, const int64_t* cuts,
+                         const int* scales, int n_tasks, const float* band_prob, const uint8_t* band_mask,
+                         float* out_prob, uint8_t* out_mask) {
+  try {
+    OS_REQUIRE(h && cuts && scales, "gather_bands: NULL argument");
+    OS_REQUIRE(h->comm != nullptr, "gather_bands: needs omniseg_comm_init");
+    OS_REQUIRE(root >= 0 && root < h->world, "gather_bands: bad root");
+    OS_CUDA(cudaSetDevice(h->device));
+    std::vector<int> classes(n_tasks, 0);
+    const Tasks tk = make_tasks(h, scales, classes.data(), n_tasks, H, W);
+    const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
+    OS_REQUIRE(cuts[0] == 0 && cuts[h->world] == Hp, "gather_bands: cuts must run from 0 to Hp");
+    for (int r = 0; r < h->world; ++r) OS_REQUIRE(cuts[r] <= cuts[r + 1], "gather_bands: cuts must be ascending");
+    const bool me_root = h->rank == root;
+    if (band_prob || band_mask) {
+      OS_REQUIRE(!band_prob || is_device_ptr(band_prob), "gather_bands: band_prob must be device memory");
+      OS_REQUIRE(!band_mask || is_device_ptr(band_mask), "gather_bands: band_mask must be device memory");
+    }
+    if (me_root) {
+      OS_REQUIRE((!band_prob || (out_prob && is_device_ptr(out_prob))) &&
+                     (!band_mask || (out_mask && is_device_ptr(out_mask))),
+                 "gather_bands: the root needs device out_prob / out_mask for every band output given");
+    }
+    cudaStream_t s = h->stream;
+    // per task: offset of the task in the full output and in each rank's band output
+    std::vector<int64_t> full_off(tk.n);
+    int64_t acc = 0;
+    for (int t = 0; t < tk.n; ++t) {
+      full_off[t] = acc;
+      acc += tk.Ht[t] * tk.Wt[t];
+    }
+    g_nccl.check(g_nccl.groupStart(), "ncclGroupStart");
+    for (int r = 0; r < h->world; ++r) {
+      if (!me_root && r != h->rank) continue;
+      int64_t boff = 0;
+      for (int t = 0; t < tk.n; ++t) {
+        int64_t r0, r1;
+        omniseg_band_rows(H, cuts[r], cuts[r + 1], pad, tk.f[t], &r0, &r1);
+        const int64_t n = (r1 - r0) * tk.Wt[t];
+        if (n > 0) {
+          const int64_t dst = full_off[t] + r0 * tk.Wt[t];
+          if (r == h->rank) {  // my band: send to the root (a self send/recv pair on the root)
+            if (band_prob) g_nccl.check(g_nccl.send(band_prob + boff, n, ncclFloat32, root, h->comm, s), "ncclSend");
+            if (band_mask) g_nccl.check(g_nccl.send(band_mask + boff, n, ncclUint8, root, h->comm, s), "ncclSend");
+          }
+          if (me_root) {
+            if (band_prob) g_nccl.check(g_nccl.recv(out_prob + dst, n, ncclFloat32, r, h->comm, s), "ncclRecv");
+            if (band_mask) g_nccl.check(g_nccl.recv(out_mask + dst, n, ncclUint8, r, h->comm, s), "ncclRecv");
+          }
+        }
+        boff += n;
+      }
+    }
+    g_nccl.check(g_nccl.groupEnd(), "ncclGroupEnd");
+    OS_CUDA(cudaStreamSynchronize(s));
     return 0;
   } catch (const Error& e) {
     return fail(e);

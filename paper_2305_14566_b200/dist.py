@@ -13,14 +13,24 @@ def padded_extent(H: int, W: int, pad: int):
     return r(H + 2 * pad), r(W + 2 * pad)
 
 
-def band_partition(Hp: int, world: int, stride: int):
-    """Owned rows of the padded 40x frame per rank: contiguous bands whose boundaries are
-    multiples of 8*stride (so every scale's tile rows and the level-8 grid align), the
-    last band ending at Hp. Units are split as evenly as possible."""
+def band_cuts(Hp: int, world: int, stride: int):
+    """world+1 band boundaries of the padded 40x frame: contiguous bands whose boundaries are
+    multiples of 8*stride (so every scale's tile rows and the level-8 grid align), the last
+    band ending at Hp; the nb = ceil(Hp / (8 stride)) row units are split as evenly as
+    possible over min(world, nb) ranks -- rank 0 always holds row 0 (the pad colour, the
+    broadcast root) and ranks beyond nb get EMPTY bands (Hp, Hp), which join the collectives
+    without compute (omniseg.h)."""
     unit = 8 * stride
     nb = (Hp + unit - 1) // unit
-    cuts = [min(Hp, (nb * r // world) * unit) for r in range(world + 1)]
+    act = min(world, nb)
+    cuts = [min(Hp, (nb * min(r, act) // act) * unit) for r in range(world + 1)]
     cuts[-1] = Hp
+    return cuts
+
+
+def band_partition(Hp: int, world: int, stride: int):
+    """Owned rows [row0, row1) per rank (band_cuts)."""
+    cuts = band_cuts(Hp, world, stride)
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 

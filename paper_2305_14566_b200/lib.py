@@ -16,7 +16,7 @@ _lib = None
 
 # Every symbol include/omniseg.h and include/omniseg_debug.h declare.
 SYMBOLS = ("omniseg_create", "omniseg_segment_slide", "omniseg_output_size", "omniseg_comm_init",
-           "omniseg_segment_band", "omniseg_band_rows", "omniseg_render_overlay", "omniseg_get_tiles",
+           "omniseg_segment_band", "omniseg_gather_bands", "omniseg_band_rows", "omniseg_render_overlay", "omniseg_get_tiles",
            "omniseg_get_fgmask",
            "omniseg_get_timings", "omniseg_set_stream", "omniseg_last_error", "omniseg_destroy",
            "omniseg_debug_predict_tiles", "omniseg_debug_conv", "omniseg_debug_set_profile",
@@ -49,6 +49,8 @@ def load(path: str = LIB_PATH):
     L.omniseg_comm_init.restype = i32
     L.omniseg_segment_band.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, i32, vp, vp, i32, vp, vp, vp]
     L.omniseg_segment_band.restype = i32
+    L.omniseg_gather_bands.argtypes = [vp, i32, i64, i64, i32, vp, vp, i32, vp, vp, vp, vp]
+    L.omniseg_gather_bands.restype = i32
     L.omniseg_band_rows.argtypes = [i64, i64, i64, i32, i32, C.POINTER(i64), C.POINTER(i64)]
     L.omniseg_band_rows.restype = i32
     L.omniseg_render_overlay.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, vp, vp]
@@ -160,6 +162,13 @@ class Omniseg:
         _check(load().omniseg_segment_band(self.h, _ptr(rgb_band), H, W, row0, row1, pad, patch, stride,
                                            _ints(scales), _ints(classes), len(scales), _ptr(out_prob),
                                            _ptr(out_mask), _ptr(out_area)))
+
+    def gather_bands(self, root, H, W, pad, cuts, scales, band_prob=None, band_mask=None, out_prob=None,
+                     out_mask=None):
+        """NCCL gather of every rank's owned canvas rows into full outputs on `root` (omniseg.h)."""
+        cc = (C.c_int64 * len(cuts))(*[int(c) for c in cuts])
+        _check(load().omniseg_gather_bands(self.h, root, H, W, pad, cc, _ints(scales), len(scales), _ptr(band_prob),
+                                           _ptr(band_mask), _ptr(out_prob), _ptr(out_mask)))
 
     def tiles(self):
         import numpy as np

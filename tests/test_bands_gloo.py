@@ -55,11 +55,32 @@ def _worker(rank, world, port, q):
         res = _band_canvas(rank, world, a, blob, slide, fr)
         out = [None] * world
         dist.all_gather_object(out, res)
+        # band gather to rank 0 over point-to-point messages (the layout omniseg_gather_bands
+        # uses over NCCL: rank r's owned canvas rows [r0, r1) land at rows r0..r1 of the full canvas)
+        from paper_2305_14566_b200 import dist as D
+        Hp, _ = D.padded_extent(H, W, PAD)
+        cuts = D.band_cuts(Hp, world, S)
+        s_band = torch.from_numpy(np.ascontiguousarray(res[4]))
+        if rank == 0:
+            full = torch.zeros((H, W), dtype=torch.float64)
+            for r in range(world):
+                r0, r1 = D.owned_canvas_rows(H, PAD, 1, cuts[r], cuts[r + 1])
+                if r1 <= r0:
+                    continue
+                if r == 0:
+                    full[r0:r1] = s_band
+                else:
+                    buf = torch.empty((r1 - r0, W), dtype=torch.float64)
+                    dist.recv(buf, src=r)
+                    full[r0:r1] = buf
+            res = res + (full.numpy(),)
+        elif res[3] > res[2]:
+            dist.send(s_band, dst=0)
         obj = [fr["kept"] if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         assert obj[0] == fr["kept"]
         if rank == 0:
-            q.put(out)
+            q.put((out, res[7]))
     finally:
         dist.destroy_process_group()
 
@@ -81,7 +102,7 @@ def test_band_decomposition_gloo_world2():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = q.get(timeout=600)
+    out, full = q.get(timeout=600)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -100,6 +121,8 @@ def test_band_decomposition_gloo_world2():
     assert (c == ref["cnt"][0]).all()
     np.testing.assert_allclose(prob, ref["prob"][0], rtol=0, atol=1e-15)
     assert (mask == ref["mask"][0]).all()
+    # the gathered canvas sums on rank 0 are the concatenation of the owned bands
+    assert (full == s).all()
     # boundary windows are computed by both neighbours (duplication > 0, bounded)
     assert sum(o[6] for o in out) >= len(ref["kept"])
 
@@ -113,6 +136,23 @@ def test_band_partition_properties():
             assert r1 == s0 and r0 < r1 and r0 % (8 * S) == 0
         sizes = [r1 - r0 for r0, r1 in b[:-1]]
         assert max(sizes) - min(sizes) <= 8 * S
+
+
+def test_band_partition_more_ranks_than_units():
+    """with world > nb = ceil(Hp / 8S) row units (cfg1 at 4 / 8 GPUs, cfg2 at 8), the
+    first nb ranks get one unit each (rank 0 always holds row 0, the pad-colour broadcast root)
+    and the rest get EMPTY bands (Hp, Hp) that join the collectives without compute."""
+    from paper_2305_14566_b200 import dist as D
+    for Hp, S, world in [(1280, 128, 4), (1280, 128, 8), (5120, 256, 8), (2048, 256, 2)]:
+        nb = -(-Hp // (8 * S))
+        cuts = D.band_cuts(Hp, world, S)
+        b = D.band_partition(Hp, world, S)
+        assert cuts[0] == 0 and cuts[-1] == Hp and all(x <= y for x, y in zip(cuts, cuts[1:]))
+        nonempty = [(r0, r1) for r0, r1 in b if r1 > r0]
+        assert len(nonempty) == min(world, nb) and b[0][1] > 0
+        assert b[:len(nonempty)] == nonempty                     # empty bands come last
+        assert all(r0 == r1 == Hp for r0, r1 in b[len(nonempty):])
+        assert all(r0 % (8 * S) == 0 for r0, _ in nonempty)
 
 
 def test_world1_comm_init_is_noop():

@@ -48,7 +48,7 @@ def _window_rows(v, Hp):
     return oy * f, (oy + P) * f
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_bands_bit_exact(setup, world):
     from paper_2305_14566_b200 import Omniseg
     from paper_2305_14566_b200 import dist as D
@@ -84,14 +84,15 @@ def test_bands_bit_exact(setup, world):
     assert (area_sum == area).all()
 
 
-def test_nccl_plumbing_world1(setup, monkeypatch):
+def test_nccl_plumbing_world1(setup):
     """The real NCCL path (dlopen'ed libnccl, communicator from a torch-generated unique id,
     pad-colour broadcast, histogram and area all-reduces) with a communicator of size 1:
-    the single band [0, Hp) must reproduce segment_slide bit for bit."""
+    the single band [0, Hp) must reproduce segment_slide bit for bit; then the NCCL band
+    gather (ncclSend/ncclRecv group, the root's band as a self pair) assembles the
+    full-slide device outputs on rank 0, bit-identical to segment_slide's."""
     import torch
     from paper_2305_14566_b200 import Omniseg
     from paper_2305_14566_b200 import dist as D
-    monkeypatch.setenv("OMNISEG_FORCE_NCCL", "1")
     a, blob, slide, h_full, prob, mask, area, pc, hist, tiles_full = setup
     h = Omniseg(arch_string(a), blob)
     h.comm_init(torch.cuda.nccl.unique_id(), 1, 0)
@@ -101,3 +102,33 @@ def test_nccl_plumbing_world1(setup, monkeypatch):
     ba = np.zeros_like(area)
     h.segment_band(slide, H, W, 0, Hp, PAD, P, S, SCALES, CLASSES, bp, bm, ba)
     assert (bp.view(np.uint32) == prob.view(np.uint32)).all() and (bm == mask).all() and (ba == area).all()
+    # device-resident band outputs -> gather to rank 0
+    dbp = torch.empty(prob.size, dtype=torch.float32, device="cuda")
+    dbm = torch.empty(mask.size, dtype=torch.uint8, device="cuda")
+    h.segment_band(torch.from_numpy(slide).cuda(), H, W, 0, Hp, PAD, P, S, SCALES, CLASSES, dbp, dbm, None)
+    fp = torch.full((prob.size,), -1.0, dtype=torch.float32, device="cuda")
+    fm = torch.full((mask.size,), 7, dtype=torch.uint8, device="cuda")
+    h.gather_bands(0, H, W, PAD, D.band_cuts(Hp, 1, S), SCALES, dbp, dbm, fp, fm)
+    torch.cuda.synchronize()
+    assert (fp.cpu().numpy().view(np.uint32) == prob.view(np.uint32)).all()
+    assert (fm.cpu().numpy() == mask).all()
+    with pytest.raises(Exception, match="device"):
+        h.gather_bands(0, H, W, PAD, D.band_cuts(Hp, 1, S), SCALES, bp, bm, fp, fm)   # host band buffers
+
+
+def test_empty_band_joins_without_compute(setup):
+    """More ranks than row units (dist.band_cuts gives them (Hp, Hp)): segment_band computes
+    nothing, returns the (injected, i.e. all-reduced) global areas = 0 contribution, no tiles."""
+    from paper_2305_14566_b200 import Omniseg
+    from paper_2305_14566_b200 import dist as D
+    a, blob, slide, h_full, prob, mask, area, pc, hist, tiles_full = setup
+    Hp, _ = D.padded_extent(H, W, PAD)
+    cuts = D.band_cuts(Hp, 64, S)
+    assert cuts[0] == 0 and cuts[1] > 0 and cuts[-2] == Hp and cuts[-1] == Hp
+    h = Omniseg(arch_string(a), blob)
+    h.band_globals(pc, hist)
+    ba = np.ones(len(SCALES), np.uint64)
+    h.segment_band(None, H, W, Hp, Hp, PAD, P, S, SCALES, CLASSES, None, None, ba)
+    assert (ba == 0).all() and len(h.tiles()) == 0
+    _, t, gp = h.fgmask()
+    assert t == h_full.fgmask()[1]
