@@ -49,16 +49,25 @@ typedef struct omniseg omniseg_t;   /* opaque; owns device weights, workspace, s
 
 /* Create a predictor.
  *   arch   : ';'-separated key=value string, e.g.
- *            "levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16;batch=64"
+ *            "levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=64"
  *            levels/base: U-Net depth and base width (channels base*2^l); head must be 8
  *            (3-layer 8-channel dynamic head, BASELINE configs[0]); ncls classes;
  *            scale_codes: magnifications with a one-hot code each (order = code index);
  *            slide_mag: magnification of the input slide (level factor f = slide_mag/scale);
- *            dtype: activation storage, fp32 accumulation (R9): fp16 (default),
- *            bf16, or fp16x2 / bf16x2 = each activation stored as hi + lo 16-bit pair and
- *            every convolution's K loop run over both halves (exact 16-bit weights), which
- *            gives fp32-grade activations at twice the tensor work;
- *            batch: tiles per trunk launch; device: CUDA ordinal (default: current).
+ *            dtype: activation storage, fp32 accumulation (R9):
+ *              fp16f8 (default, the parity-gated product precision): each activation stored
+ *                as fp16 hi + e4m3 residual lo8 = e4m3((v - hi) * 2^6) (3 bytes / channel);
+ *                every convolution runs its K loop over the hi chunks (tcgen05 kind::f16,
+ *                exact fp16 weights) and the lo chunks (kind::f8f6f4, e5m2(W * 2^-6)) into
+ *                one fp32 accumulator (1.5x the fp16 tensor work);
+ *              fp16x2 / bf16x2: hi + lo 16-bit pairs, K loop over [W | W] (2x tensor work);
+ *              fp16 / bf16: plain 16-bit storage (reported, not parity-gated: a random
+ *                network amplifies their rounding beyond the 1e-2 gate, R9);
+ *            batch: tiles per trunk launch; device: CUDA ordinal (default: current);
+ *            fusion=mean|vote (R11 / R11b); vthr=t5,t10,... (vote fusion only: one literal
+ *            vote-count threshold per scale code, mask = votes >= min(thr, coverage); 0 =
+ *            majority); fgmin=N, maskfg=0|1 (R7b); precision knobs xlevels / xa / xal
+ *            (DESIGN.md §8).
  *   weights: flat little-endian fp32 blob in the order of DESIGN.md §3;
  *            nbytes must equal 4 * param_count(arch). Host or device; copied.
  * Returns NULL on error (see omniseg_last_error). */
@@ -77,7 +86,8 @@ omniseg_t* omniseg_create(const char* arch, const void* weights, size_t nbytes);
  *             concatenated in order: overlap-normalised probability (0 where no kept
  *             tile covers the pixel), R10-R11.
  *   out_mask: uint8[sum_t Ht*Wt] or NULL: prob >= 1/2 (decided exactly on the
- *             fixed-point accumulator, R12).
+ *             fixed-point accumulator, R12); with fusion=vote the vote fraction / majority
+ *             (or the vthr count threshold) instead.
  *   out_area: uint64[n_tasks] or NULL: number of mask pixels per task.
  * Errors: EINVAL for any violated precondition above, and when the coverage count of
  * a pixel could exceed 15 (ceil(P/S)+1)^2 > 15, which the u32 fixed-point canvas
@@ -159,9 +169,12 @@ int omniseg_get_tiles(const omniseg_t* h, uint32_t* tiles, int64_t cap, int64_t*
 int omniseg_get_fgmask(const omniseg_t* h, uint8_t* mask, int64_t cap, int64_t* h8, int64_t* w8,
                        int* otsu_t, int* g_pad);
 /* Per-stage device times of the last call, milliseconds (CUDA events on the
- * library's stream): [0] upload, [1] pyramid+detection+selection, [2] gather,
- * [3] trunk convs, [4] gap+controller, [5] head+stitch, [6] finalize, [7] download,
- * [8] total. Also the conv-kernel launch count [9] and total launches [10]. */
+ * library's stream): [0] upload, [1] pyramid+detection+selection, [3] the batch loop
+ * (window gather fused into the stem kernel, trunk convs, GAP+controller, the dynamic head
+ * and stitch fused into the last decoder conv -- their per-kind split is the per-conv
+ * profile of omniseg_debug_get_profile), [6] finalize of the remaining rows + area
+ * reduction, [7] output download wait, [8] total; [2], [4], [5] are 0 (fused into [3]).
+ * Also the conv-kernel launch count [9] and total launches [10]. */
 int omniseg_get_timings(const omniseg_t* h, double* out, int cap);
 
 /* Use this CUDA stream (cudaStream_t cast to void*; NULL = the library's own). */

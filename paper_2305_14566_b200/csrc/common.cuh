@@ -26,6 +26,22 @@ struct Error : std::runtime_error {
     if (!(cond)) throw ::osg::Error(-1, std::string(msg)); \
   } while (0)
 
+// Experiment switches (DESIGN.md §8 "measured non-wins": kernel-variant toggles, MMA-warp cycle
+// counters). Compiled OUT of the product build; `scripts/build_variant.sh NAME
+// -DOMNISEG_EXPERIMENTS=1` builds a variant that reads the toggles from the environment.
+#ifndef OMNISEG_EXPERIMENTS
+#define OMNISEG_EXPERIMENTS 0
+#endif
+#define OS_EXP (OMNISEG_EXPERIMENTS != 0)
+#if OMNISEG_EXPERIMENTS
+#define OS_CLK() clock64()
+#else
+#define OS_CLK() 0ull
+#endif
+// true iff the experiment build runs with the environment variable `name` set
+bool exp_flag(const char* name);
+int exp_int(const char* name);
+
 constexpr int kMaxScales = 4;   // level factors 8, 4, 2, 1
 constexpr int kMaxTasks = 32;
 constexpr int kTheta = 153;     // W1 b1 W2 b2 W3 b3 of the 8-8-8-1 dynamic head

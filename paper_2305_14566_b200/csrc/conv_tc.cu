@@ -181,7 +181,7 @@ void dispatch(const ConvPlan& p, cudaStream_t s) {
   }
   if (p.mode == kHeadFused && p.nz_R == 0) throw Error(-1, "fused head needs the no-swizzle conv kernel");
   if (p.nz_R > 0) {
-    static const bool dyf = getenv("OMNISEG_NO_DYF") == nullptr;
+    static const bool dyf = !exp_flag("OMNISEG_NO_DYF");
     if (p.bn == 16) return dyf ? launch_nz<T, 16, true>(p, s) : launch_nz<T, 16, false>(p, s);
     if (p.bn == 32) return dyf ? launch_nz<T, 32, true>(p, s) : launch_nz<T, 32, false>(p, s);
     if (p.bn == 64) return dyf ? launch_nz<T, 64, true>(p, s) : launch_nz<T, 64, false>(p, s);
@@ -341,7 +341,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   }
   // multi-row variant for 3x3 stride-1 convs with N <= 128 (see conv3_rows_kernel)
   if (p.nz_R == 0 && k == 3 && stride == 1 && mode != kUpAdd && p.bn <= 128 && (a.hb == 1 || a.hb == 2) &&
-      Cout == p.bn && getenv("OMNISEG_NO_ROWS") == nullptr) {
+      Cout == p.bn && !exp_flag("OMNISEG_NO_ROWS")) {
     const int R = RowsCfg::R(p.bn);
     const int bk = RowsCfg::BK(p.bn, a.hb);
     if (a.tiles_y % R == 0 && Cin % bk == 0 && (!f8in || bk >= 32)) {
@@ -355,14 +355,14 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   }
   OS_REQUIRE(!f8in || p.nz_R > 0 || p.s2_R > 0 || p.bk >= 32, "F8 input needs K chunks of >= 32 channels");
   a.num_work = B * a.tiles_x * a.tiles_y * a.n_tiles_n;
-  if (const char* d = getenv("OMNISEG_DBG")) a.dbg = atoi(d);
+  a.dbg = exp_int("OMNISEG_DBG");
   a.bias = bias;
   a.res = res;
   a.out = out;
   a.split = split_out;
   // per-tap 256-channel layers: CTA pairs sharing (multicasting) the weight tiles
   if (p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bn == 256 && (a.tiles_x * a.tiles_y) % 2 == 0 &&
-      getenv("OMNISEG_CLUSTER") != nullptr)  // opt-in: measured no faster (these layers are tensor-bound)
+      exp_flag("OMNISEG_CLUSTER"))  // opt-in: measured no faster (these layers are tensor-bound)
     p.cl = 2;
   // per-tap kernel: 128-channel lo chunks when the K chunk is 64 (one SW128 row like the hi chunks)
   a.lo2 = (f8in && p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bk == 64 && Cin % 128 == 0) ? 1 : 0;
@@ -543,7 +543,7 @@ void build_conv_wimage(ConvPlan& p, const void* w, const void* w_lo, void* dst, 
     const int dy = tap / 3, dx = tap % 3;
     int slot;
     if (p.s2_R > 0) slot = dx * 3 + (dy == 0 ? 0 : dy == 2 ? 1 : 2);  // [dx][dy0, dy2, dy1]
-    else if (getenv("OMNISEG_NO_DYF") == nullptr && p.bn <= 64) slot = dx * 3 + dy;  // dy-fused: [dx][dy]
+    else if (!exp_flag("OMNISEG_NO_DYF") && p.bn <= 64) slot = dx * 3 + dy;  // dy-fused: [dx][dy]
     else slot = tap;
     sm.tap[slot] = tap;
   }
@@ -601,7 +601,7 @@ void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32
   if (a.num_work <= 0) return;
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
   static unsigned long long* sdbg = nullptr;
-  const bool dbg = getenv("OMNISEG_DBG") && (atoi(getenv("OMNISEG_DBG")) & 8);
+  const bool dbg = (exp_int("OMNISEG_DBG") & 8) != 0;
   if (dbg && !sdbg) OS_CUDA(cudaMalloc(&sdbg, 148 * 4 * 8));
   a.dbg_out = dbg ? sdbg : nullptr;
   const int bn = p.conv.bn;
@@ -624,6 +624,24 @@ void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32
     fprintf(stderr, "[stem] per item: total %.0f, wait tempty %.0f, wait afull %.0f cycles (%.0f items/CTA)\n", t / nn,
             te / nn, fu / nn, nn / p.grid);
   }
+}
+
+bool exp_flag(const char* name) {
+#if OMNISEG_EXPERIMENTS
+  return getenv(name) != nullptr;
+#else
+  (void)name;
+  return false;
+#endif
+}
+int exp_int(const char* name) {
+#if OMNISEG_EXPERIMENTS
+  const char* v = getenv(name);
+  return v ? atoi(v) : 0;
+#else
+  (void)name;
+  return 0;
+#endif
 }
 
 void run_conv(const ConvPlan& p0, cudaStream_t s) {

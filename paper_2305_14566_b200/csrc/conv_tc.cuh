@@ -829,19 +829,19 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      unsigned long long c_te = 0, c_full = 0, t_start = clock64();
+      unsigned long long c_te = 0, c_full = 0, t_start = OS_CLK();
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        unsigned long long t0 = clock64();
+        unsigned long long t0 = OS_CLK();
         ptx::mbar_wait_backoff(&tempty[acc], acc_phase ^ 1);
-        c_te += clock64() - t0;
+        c_te += OS_CLK() - t0;
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int it = 0; it < kiters; ++it) {
-          t0 = clock64();
+          t0 = OS_CLK();
           ptx::mbar_wait(&full[stage], phase);
-          c_full += clock64() - t0;
+          c_full += OS_CLK() - t0;
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
           const uint32_t sb = sa + S::kA;
@@ -880,8 +880,8 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
         }
         ptx::mma_commit_w(&tfull[acc]);
       }
-      if ((args.dbg & 8) && lane == 0) {
-        args.dbg_out[blockIdx.x * 4 + 0] = clock64() - t_start;
+      if (OS_EXP && (args.dbg & 8) && lane == 0) {
+        args.dbg_out[blockIdx.x * 4 + 0] = OS_CLK() - t_start;
         args.dbg_out[blockIdx.x * 4 + 1] = c_te;
         args.dbg_out[blockIdx.x * 4 + 2] = c_full;
         args.dbg_out[blockIdx.x * 4 + 3] = local;
@@ -1531,7 +1531,7 @@ __global__ void __launch_bounds__(384, 1)
           uint8_t* sa = smem + stage * S::kStage;
           const bool hi = kc < args.kchunks;
           const int kk = hi ? kc : kc - args.kchunks;
-          if (args.dbg & 4) {
+          if (OS_EXP && (args.dbg & 4)) {
             ptx::mbar_arrive(&full[stage]);
             if (++stage == STAGES) {
               stage = 0;
@@ -1558,22 +1558,22 @@ __global__ void __launch_bounds__(384, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      unsigned long long c_te = 0, c_full = 0, c_all = 0, t_start = clock64();
+      unsigned long long c_te = 0, c_full = 0, c_all = 0, t_start = OS_CLK();
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
         const int acc = local & 1;
         // DYF: the epilogue zeroes every buffer and arrives once up front (real phases)
-        unsigned long long t0 = clock64();
+        unsigned long long t0 = OS_CLK();
         ptx::mbar_wait_backoff(&tempty[acc], DYF ? ((local >> 1) & 1) : (((local >> 1) & 1) ^ 1));
-        c_te += clock64() - t0;
+        c_te += OS_CLK() - t0;
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + acc * R * BN;
         for (int kc = 0; kc < kiters; ++kc) {
-          t0 = clock64();
+          t0 = OS_CLK();
           ptx::mbar_wait(&full[stage], phase);
-          c_full += clock64() - t0;
+          c_full += OS_CLK() - t0;
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
-          if (args.dbg & 2) {
+          if (OS_EXP && (args.dbg & 2)) {
           } else if (kc >= args.kchunks) {  // F8 lo chunk: same smem image, kind::f8f6f4
             nz_mma_chunk<BN, R, DYF, true, kBf, S>(sa, d_base, kc);
           } else {
@@ -1587,8 +1587,8 @@ __global__ void __launch_bounds__(384, 1)
         }
         ptx::mma_commit_w(&tfull[acc]);
       }
-      c_all = clock64() - t_start;
-      if ((args.dbg & 8) && lane == 0) {
+      c_all = OS_CLK() - t_start;
+      if (OS_EXP && (args.dbg & 8) && lane == 0) {
         args.dbg_out[blockIdx.x * 4 + 0] = c_all;
         args.dbg_out[blockIdx.x * 4 + 1] = c_te;
         args.dbg_out[blockIdx.x * 4 + 2] = c_full;
@@ -1702,7 +1702,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         const uint32_t taddr =
             tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (DYF ? (R - 1 - r) : r) * BN + c;
-        if (args.dbg & 1) {
+        if (OS_EXP && (args.dbg & 1)) {
           if constexpr (kRes) {
             ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
             es.rphase[slot] ^= 1;
@@ -1888,18 +1888,18 @@ __global__ void __launch_bounds__(384, 1)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    unsigned long long c_te = 0, c_full = 0, t_start = clock64();
+    unsigned long long c_te = 0, c_full = 0, t_start = OS_CLK();
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
-      unsigned long long t0 = clock64();
+      unsigned long long t0 = OS_CLK();
       ptx::mbar_wait_backoff(&tempty[acc], (local >> 1) & 1);  // the epilogue zeroes and arrives up front
-      c_te += clock64() - t0;
+      c_te += OS_CLK() - t0;
       ptx::tc_fence_after();
       const uint32_t d_base = tmem_base + acc * R * BN;
       for (int kc = 0; kc < kiters; ++kc) {
-        t0 = clock64();
+        t0 = OS_CLK();
         ptx::mbar_wait(&full[stage], phase);
-        c_full += clock64() - t0;
+        c_full += OS_CLK() - t0;
         ptx::tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
         if (kc >= args.kchunks)
@@ -1914,8 +1914,8 @@ __global__ void __launch_bounds__(384, 1)
       }
       ptx::mma_commit_w(&tfull[acc]);
     }
-    if ((args.dbg & 8) && lane == 0) {
-      args.dbg_out[blockIdx.x * 4 + 0] = clock64() - t_start;
+    if (OS_EXP && (args.dbg & 8) && lane == 0) {
+      args.dbg_out[blockIdx.x * 4 + 0] = OS_CLK() - t_start;
       args.dbg_out[blockIdx.x * 4 + 1] = c_te;
       args.dbg_out[blockIdx.x * 4 + 2] = c_full;
       args.dbg_out[blockIdx.x * 4 + 3] = local;
@@ -2222,17 +2222,17 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    unsigned long long c_te = 0, c_full = 0, t_start = clock64();
+    unsigned long long c_te = 0, c_full = 0, t_start = OS_CLK();
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
-      unsigned long long t0 = clock64();
+      unsigned long long t0 = OS_CLK();
       ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
-      c_te += clock64() - t0;
+      c_te += OS_CLK() - t0;
       ptx::tc_fence_after();
       for (int r = 0; r < R; ++r) {
-        t0 = clock64();
+        t0 = OS_CLK();
         ptx::mbar_wait(&afull[stage], phase);
-        c_full += clock64() - t0;
+        c_full += OS_CLK() - t0;
         ptx::tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + stage * S::kA);
         const uint32_t d = tmem_base + acc * R * BN + r * BN;
@@ -2250,8 +2250,8 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
       }
       ptx::mma_commit_w(&tfull[acc]);
     }
-    if (args.dbg_out && lane == 0) {
-      args.dbg_out[blockIdx.x * 4 + 0] = clock64() - t_start;
+    if (OS_EXP && args.dbg_out && lane == 0) {
+      args.dbg_out[blockIdx.x * 4 + 0] = OS_CLK() - t_start;
       args.dbg_out[blockIdx.x * 4 + 1] = c_te;
       args.dbg_out[blockIdx.x * 4 + 2] = c_full;
       args.dbg_out[blockIdx.x * 4 + 3] = local;

@@ -105,7 +105,7 @@ struct Arch {
   int levels = 5, base = 32, head = 8, ncls = 6, slide_mag = 40, batch = 64, device = -1;
   std::vector<int> scale_codes{5, 10, 20, 40};
   bool bf16 = false;
-  int split = kStorePlain;  // StoreKind of the activations: fp16/bf16 plain, x2 (hi + lo 16-bit), f8 (fp16 + e4m3 lo)
+  int split = kStoreF8;     // StoreKind of the activations: f8 (fp16 + e4m3 lo; default), x2 (hi + lo 16-bit), plain
   int xlevels = -1;         // split storage only for tensors at U-Net levels < xlevels (-1: all levels)
   int xa = 1;               // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
   int xal = 64;             // with xa = 1: conv_a outputs keep the split kind only at levels < xal
@@ -484,7 +484,7 @@ void ensure_workspace(omniseg* h, int P) {
   for (int l = 0; l < L; ++l)
     h->rc[l] = nz_eligible(P >> l, P >> l, h->enc_a[l].cinp, h->enc_a[l].coutp, 3, 1, kReluBias) &&
                nz_eligible(P >> l, P >> l, h->enc_b[l].cinp, h->enc_b[l].coutp, 3, 1, kResidualRelu) &&
-               getenv("OMNISEG_NO_NZ") == nullptr;
+               !exp_flag("OMNISEG_NO_NZ");
   // out_level: U-Net level of the output (and residual / skip) tensor
   auto plan = [&](const Layer& ly, const void* in, int Hin, const void* res, void* out, int mode, int out_level,
                   int in_rc, int res_rc, int out_rc) {
@@ -513,8 +513,8 @@ void ensure_workspace(omniseg* h, int P) {
   h->erc.assign(L, 0);
   for (int l = 0; l + 1 < L; ++l)
     h->erc[l] = h->rc[l] && s2_eligible(P >> l, P >> l, h->down[l].cinp, h->down[l].coutp, 3, 2, kReluBias) &&
-                h->down[l].coutp <= (getenv("OMNISEG_S2_WIDE") ? 128 : 64) &&  // 2x MMA work: thin N only
-                getenv("OMNISEG_NO_S2") == nullptr;
+                h->down[l].coutp <= (exp_flag("OMNISEG_S2_WIDE") ? 128 : 64) &&  // 2x MMA work: thin N only
+                !exp_flag("OMNISEG_NO_S2");
   const auto& rc = h->rc;
   const auto& erc = h->erc;
   enc(h->stem, h->X0.p, P, nullptr, h->lv[0].A.p, kReluBias, 0, 0, 0, rc[0]);
@@ -545,7 +545,7 @@ void ensure_workspace(omniseg* h, int P) {
   }
   // fused head: only with the no-swizzle kernel and all C0 channels in one N tile
   h->head_fusable = false;
-  if (getenv("OMNISEG_NO_HEAD_FUSION") == nullptr && rc[0]) {
+  if (!exp_flag("OMNISEG_NO_HEAD_FUSION") && rc[0]) {
     LevelBufs& q = h->lv[0];
     ConvPlan hp = plan(h->dec_b[0], q.Bt.p, q.P, q.A.p, q.E.p, kHeadFused, 0, rc[0], rc[0], 0);
     if (hp.nz_R > 0 && hp.bn == h->Cp[0] && h->C[0] <= 32) {
@@ -758,7 +758,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   }
   bool needf[4] = {false, false, false, false};
   for (int i = 0; i < tk.n; ++i) needf[tk.log2f[i]] = true;
-  const bool l1_needed = needf[0] && h->stem_fused && getenv("OMNISEG_NO_STEM_FUSION") == nullptr;
+  const bool l1_needed = needf[0] && h->stem_fused && !exp_flag("OMNISEG_NO_STEM_FUSION");
   if (l1_needed) h->L1.ensure((size_t)Hp * Wp * 4);
   if (needf[1]) h->L2.ensure((size_t)(Hp / 2) * (Wp / 2) * 4);
   if (needf[2]) h->L4.ensure((size_t)(Hp / 4) * (Wp / 4) * 4);
@@ -953,7 +953,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   };
   // ---- hot loop over batches of kept tiles
   const int B = h->arch.batch;
-  const bool fused = h->stem_fused && getenv("OMNISEG_NO_STEM_FUSION") == nullptr;
+  const bool fused = h->stem_fused && !exp_flag("OMNISEG_NO_STEM_FUSION");
   const uint32_t* Lv[4] = {h->L1.as<uint32_t>(), h->L2.as<uint32_t>(), h->L4.as<uint32_t>(), h->L8.as<uint32_t>()};
   for (int64_t first = 0; first < h->n_tiles; first += B) {
     const int n = (int)std::min<int64_t>(B, h->n_tiles - first);
