@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4",
-                    help="cfg1..cfg5 (BASELINE.json configs; cfg5_fg5/25/60/95: the foreground sweep), "
+                    help="cfg1..cfg5 (BASELINE.json configs; cfg5_fg5/25/60/95[_s384|_s512]: the foreground / "
+                         "stride sweep; cfg4_24: 6 classes x 4 scales), "
                          "or a SURVEY §8(f) geometry on cfg4's slide: "
                          "cfg4_paper (N1: vote fusion, 40x S=256, 10x/5x S=64), "
                          "cfg4_n4 (N4: Oracle-pipeline geometry, 256 windows, S=128, pad 2048, vote)")
@@ -119,9 +120,24 @@ def resolve_workload(name):
     """-> (Workload, [(stride, [task indices])]) for a --workload name."""
     from omniseg_inputs import workload
     pr = PRESETS.get(name)
-    if pr is None and name.startswith("cfg5_fg"):  # BASELINE configs[4] sweep point: cfg5_fg5/25/60/95
-        w = workload(5, fg_fraction=int(name[7:]) / 100)
+    if pr is None and name.startswith("cfg5_fg"):
+        # BASELINE configs[4] sweep point: cfg5_fg5/25/60/95, optionally _s384 / _s512 (stride sweep)
+        parts = name[7:].split("_s")
+        w = workload(5, fg_fraction=int(parts[0]) / 100)
+        if len(parts) > 1:
+            w.stride = int(parts[1])
+            w.name += f"_s{w.stride}"
         return w, [(w.stride, list(range(len(w.scales))))]
+    if name == "cfg4_24":
+        # SURVEY §8(d) cfg4 variant "all 6 classes at 4 scales" (BASELINE configs[3]): 24 tasks, every
+        # class at 5x / 10x / 20x / 40x; one call per scale (6 tasks each) so every call's fused head
+        # runs only the tasks of its windows' scale
+        from omniseg_inputs.arch import SCALE_CODES_4
+        w = workload(4)
+        w.name = "cfg4_24tasks"
+        w.scales = tuple(s for s in SCALE_CODES_4 for _ in range(6))
+        w.classes = tuple(c for _ in SCALE_CODES_4 for c in range(6))
+        return w, [(w.stride, list(range(6 * k, 6 * k + 6))) for k in range(4)]
     if pr is None:
         w = workload(int(name.replace("cfg", "")))
         return w, [(w.stride, list(range(len(w.scales))))]
@@ -184,7 +200,7 @@ def run_reference(a):
     if rank != 0:
         return 0
     from omniseg_inputs import geometry, render
-    if a.workload in PRESETS:
+    if a.workload in PRESETS or a.workload == "cfg4_24":
         print(json.dumps({"impl": "reference", "unavailable": f"{a.workload}: the oracle arm is timed on cfg1..cfg5"}))
         return 0
     w, _ = resolve_workload(a.workload)
@@ -228,6 +244,57 @@ def tile_estimate(w):
 
 
 # ------------------------------------------------------------------ our arm
+def path_roofline(w, gsl, kept_ids, prof, steps, rank_windows, ms, pk, pk_kind):
+    """north_star's whole-path roofline: T_roof = max(F_alg / tensor peak,
+    B_alg / HBM bandwidth) over the algorithmic work of the step, and T_roof / T_step.
+      F_alg = sum over kept windows of the trunk's convolution FLOPs (2 M N K with the real channel
+              counts, from the live per-conv profile: per window = profiled FLOPs / windows run)
+              + the dynamic head (precls 2 C0 8 + 2 * 136 per task of the window's scale, per px);
+      B_alg = 3 H W (slide read) + 4 (Hp/f)(Wp/f) per level f > 1 written + 3 P^2 per kept window
+              (window read) + 8 P^2 per window-task (canvas read-modify-write) + 9 Ht Wt per task
+              (finalize: canvas read, prob + mask write)."""
+    H, W, P, pad = w.H, w.W, w.patch, w.pad
+    Hp, Wp = (H + 2 * pad + 127) // 128 * 128, (W + 2 * pad + 127) // 128 * 128
+    mag = w.arch["slide_mag"]
+    C0 = w.arch["base"]
+    per_window = prof["flops"] / max(steps * rank_windows, 1)
+    F = B = 0.0
+    for (S, sc, cl, n0, n1, idx), ids in zip(gsl, kept_ids):
+        lf = (np.asarray(ids, np.uint32) >> 30).astype(np.int64)
+        facs = sorted(set(mag // s for s in sc))
+        B += 3.0 * H * W + sum(4.0 * (Hp // f) * (Wp // f) for f in facs if f > 1)
+        for f in facs:
+            nk = int((lf == f.bit_length() - 1).sum())
+            ntask = sum(1 for s in sc if mag // s == f)
+            F += nk * (per_window + P * P * (2.0 * C0 * 8 + ntask * 272.0))
+            B += nk * (3.0 * P * P + ntask * 8.0 * P * P)
+        for s in sc:
+            f = mag // s
+            B += 9.0 * ((H + f - 1) // f) * ((W + f - 1) // f)
+    bw = pk.get("hbm_gbs", 6556.5) * 1e9
+    out = {"F_alg_tflop": F / 1e12, "B_alg_gb": B / 1e9, "T_step_ms": ms,
+           "bound": "tensor" if F / (pk.get("bf16_tflops_sustained", 1376.7) * 1e12) > B / bw else "hbm",
+           "peak_kind": pk_kind}
+    for kind, key in (("sustained", "bf16_tflops_sustained"), ("burst", "bf16_tflops")):
+        tf = pk.get(key)
+        if tf:
+            t_roof = max(F / (tf * 1e12), B / bw) * 1e3
+            out[f"T_roof_ms_{kind}"] = t_roof
+            out[f"frac_{kind}"] = t_roof / ms if ms else None
+    return out
+
+
+def hbm_kernels():
+    """Per-kernel DRAM throughput of the HBM-bound kernels from the committed ncu capture of the
+    cfg4 command (profiles/r02_cfg4_ncu_summary.json, scripts/summarize_ncu_r02.py)."""
+    p = os.path.join(ROOT, "profiles", "r02_cfg4_ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("hbm_kernels")
+    except (OSError, ValueError):
+        return None
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -286,32 +353,40 @@ def main():
     full_mask = torch.empty(nfull if (world > 1 and rank == 0) else 1, dtype=torch.uint8, device=dev)
     area = torch.zeros(len(w.scales), dtype=torch.int64, device=dev)
     D.init_comm(h, world, rank)
-    tiles_per_step = [0]
 
-    def step(src, p_out, m_out, a_out, gather=True):
+    def step(src, p_out, m_out, a_out, gather=True, record=None):
+        """One step; record: list receiving each call's kept-window ids (untimed warm-up only)."""
         if world > 1:
             h.segment_band(src, H, W, row0, row1, w.pad, w.patch, w.stride, w.scales, w.classes, p_out, m_out, a_out)
+            if record is not None:
+                record.append(h.tiles())
             if gather:   # device-resident outputs: the band gather to rank 0 (host outputs stay per rank)
                 h.gather_bands(0, H, W, w.pad, cuts, w.scales, p_out, m_out, full_prob, full_mask)
             return
-        nt = 0
         for S, sc, cl, n0, n1, idx in gsl:
             if len(gsl) == 1:
                 h.segment_slide(src, H, W, w.pad, w.patch, S, sc, cl, p_out, m_out, a_out)
             else:
                 h.segment_slide(src, H, W, w.pad, w.patch, S, sc, cl, p_out[n0:n1], m_out[n0:n1],
                                 a_out[idx[0]:idx[-1] + 1])
-            nt += len(h.tiles()) if len(gsl) > 1 else 0
-        tiles_per_step[0] = nt
+            if record is not None:
+                record.append(h.tiles())
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(1, a.warmup if not a.profile_only else 1)):
-        step(slide, prob, mask, area)
-    n_tiles = tiles_per_step[0] if len(gsl) > 1 else len(h.tiles())
+    nwarm = max(1, a.warmup if not a.profile_only else 1)
+    kept_ids = []
+    for i in range(nwarm):
+        step(slide, prob, mask, area, record=kept_ids if i == nwarm - 1 else None)
+    rank_windows = sum(len(k) for k in kept_ids)
+    if world > 1:   # whole-job unique windows: the union of the ranks' (overlapping) window sets
+        allk = [None] * world
+        dist.all_gather_object(allk, [k.tolist() for k in kept_ids])
+        kept_ids = [np.array(sorted(set(v for r in allk for k in r for v in k)), np.uint32)]
+    n_tiles = sum(len(k) for k in kept_ids)
     steps = 1 if a.profile_only else a.steps
     clocks = Clocks(local)
     h.set_profile(True)
@@ -366,11 +441,13 @@ def main():
     # DRAM traffic per conv launch from the committed ncu capture of the same launch shapes
     # (batch-64 launches of the cfg2 profile run: dram__bytes_read.sum + dram__bytes_write.sum)
     traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "r01o_cfg2_summary.json")
-    if os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        traffic = tj.get("conv_dram_bytes_per_launch")
-        traffic_src = "profiles/r01o_cfg2_summary.json (ncu, %d conv launches)" % tj.get("conv_launches", 0)
+    for tname in ("r02_cfg4_ncu_summary.json", "r01o_cfg2_summary.json"):
+        tpath = os.path.join(ROOT, "profiles", tname)
+        if os.path.exists(tpath):
+            tj = json.load(open(tpath))
+            traffic = tj.get("conv_dram_bytes_per_launch")
+            traffic_src = "profiles/%s (ncu, %d conv launches)" % (tname, tj.get("conv_launches", 0))
+            break
     roof = {"bound": "tensor", "kernel": "tcgen05 conv family (stem_tc / conv3_nz / conv3s2_rc / conv_tc kernels)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
             "peak_kind": f"{pk_kind} bf16 sustained (fp16 kind::f16 nominal ratio 1.0)",
@@ -378,8 +455,12 @@ def main():
             "conv_share_of_step": (prof["ms"] / steps) / ms if ms else None,
             "alg_flops_per_launch": prof["flops"] / max(prof["launches"], 1),
             "avg_launch_ms": prof["ms"] / max(prof["launches"], 1)}
+    roof["path"] = path_roofline(w, gsl, kept_ids, prof, steps, rank_windows, ms, pk, pk_kind)
+    hk = hbm_kernels()
+    if hk:
+        roof["hbm_kernels"] = hk
     cpu = None
-    if a.workload in PRESETS:
+    if a.workload in PRESETS or a.workload == "cfg4_24":
         cpu = {"value": None, "unit": "Mpx/s", "cores": 0, "kind": "oracle",
                "sample": "not run: the oracle baseline is timed on cfg1..cfg5 (bench.py --workload cfg4)"}
     elif rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
