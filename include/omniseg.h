@@ -115,6 +115,9 @@ int omniseg_comm_init(omniseg_t* h, const void* nccl_unique_id, int world, int r
  *   Otsu histogram is all-reduced over ranks (R6) so tile lists match the 1-GPU run;
  *   outputs cover only the task-canvas rows owned by this band, per task, tasks
  *   concatenated; out_area is all-reduced (global per-task areas on every rank).
+ *   With fgmin > 0 (tiny-component removal needs whole components) each rank computes the
+ *   foreground of its owned level-8 rows and the H8 x W8 grid is all-reduced (disjoint rows:
+ *   the union) before every rank labels the whole grid; this needs a communicator.
  * Canvas values are bit-identical to omniseg_segment_slide's (fixed point, R12). */
 int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64_t W,
                          int64_t row0, int64_t row1, int pad, int patch, int stride,

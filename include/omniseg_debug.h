@@ -42,6 +42,10 @@ int omniseg_debug_conv(omniseg_t* h, const float* x, int B, int H, int W, int Ci
  * deliver, so that omniseg_segment_band on one GPU without a communicator reproduces a
  * rank's result. NULL arguments switch injection off. */
 int omniseg_debug_band_globals(omniseg_t* h, const uint8_t* pc, const uint64_t* hist);
+/* Single-GPU emulation of the band foreground exchange (fgmin > 0: the ncclAllReduce of the
+ * ranks' owned level-8 foreground rows): inject the whole slide's PRE-filter level-8
+ * foreground (H8 x W8 u8, host). NULL switches injection off. */
+int omniseg_debug_band_fg(omniseg_t* h, const uint8_t* fg8, int64_t n);
 /* The pad colour and the (global) histogram used by the last segment call. */
 int omniseg_debug_get_detection(const omniseg_t* h, uint8_t* pc, uint64_t* hist);
 

@@ -270,6 +270,7 @@ struct omniseg {
   bool inject = false;
   uint8_t inj_pc[4] = {0, 0, 0, 0};
   unsigned long long inj_hist[256] = {};
+  std::vector<uint8_t> inj_fg;  // pre-filter level-8 foreground of the whole slide (band fgmin emulation)
   unsigned long long last_hist[256] = {};
 
   // NCCL
@@ -805,13 +806,37 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   if (h->inject) OS_CUDA(cudaMemcpyAsync(h->hist.p, h->inj_hist, 256 * 8, cudaMemcpyHostToDevice, s));
   OS_CUDA(cudaMemcpyAsync(h->last_hist, h->hist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
   launch_otsu(h->hist.as<unsigned long long>(), st, s);
-  launch_fg(h->gm.as<uint8_t>(), h->fg.as<uint8_t>(), W8, m0, m1, ir0, ir1, ic0, ic1, st, s);
-  if (h->arch.fgmin > 0) {
-    // tiny-component removal needs whole components: single-slide calls only (see the band check)
-    const size_t nfg = (size_t)(m1 - m0) * W8;
+  const bool partial = row0 > 0 || row1 < Hp;
+  if (h->arch.fgmin > 0 && partial) {
+    // Tiny-component removal needs whole components: a band computes the foreground
+    // of its OWNED level-8 rows only, the bands' disjoint rows are summed over the ranks
+    // (ncclAllReduce of the H8 x W8 u8 grid: the union), and every rank labels the whole grid.
+    OS_REQUIRE(h->comm || !h->inj_fg.empty(), "band fgmin needs a communicator (omniseg_comm_init)");
+    OS_CUDA(cudaMemsetAsync(h->fg.p, 0, (size_t)H8 * W8, s));
+    launch_fg(h->gm.as<uint8_t>(), h->fg.as<uint8_t>(), W8, std::max(m0, fp.own8_0), std::min(m1, fp.own8_1), ir0, ir1,
+              ic0, ic1, st, s);
+    if (h->comm)
+      g_nccl.check(g_nccl.allReduce(h->fg.p, h->fg.p, (size_t)H8 * W8, ncclUint8, ncclSum, h->comm, s),
+                   "ncclAllReduce(foreground)");
+    if (!h->inj_fg.empty()) {
+      OS_REQUIRE(h->inj_fg.size() == (size_t)H8 * W8, "injected foreground has the wrong size");
+      OS_CUDA(cudaMemcpyAsync(h->fg.p, h->inj_fg.data(), h->inj_fg.size(), cudaMemcpyHostToDevice, s));
+    }
+    h->fg_r0 = 0;
+    h->fg_r1 = H8;
+    const size_t nfg = (size_t)H8 * W8;
     h->cc_lab.ensure(nfg * 4);
     h->cc_size.ensure(nfg * 4);
-    launch_fg_components(h->fg.as<uint8_t>(), W8, m0, m1, h->arch.fgmin, h->cc_lab.as<int>(), h->cc_size.as<int>(), s);
+    launch_fg_components(h->fg.as<uint8_t>(), W8, 0, H8, h->arch.fgmin, h->cc_lab.as<int>(), h->cc_size.as<int>(), s);
+  } else {
+    launch_fg(h->gm.as<uint8_t>(), h->fg.as<uint8_t>(), W8, m0, m1, ir0, ir1, ic0, ic1, st, s);
+    if (h->arch.fgmin > 0) {
+      const size_t nfg = (size_t)(m1 - m0) * W8;
+      h->cc_lab.ensure(nfg * 4);
+      h->cc_size.ensure(nfg * 4);
+      launch_fg_components(h->fg.as<uint8_t>(), W8, m0, m1, h->arch.fgmin, h->cc_lab.as<int>(), h->cc_size.as<int>(),
+                           s);
+    }
   }
   // candidate grids (canonical order: factor descending, row, col)
   std::vector<ScaleGrid> grids(tk.nf);
@@ -1026,6 +1051,12 @@ void segment_empty(omniseg* h, int64_t H, int64_t W, int pad, const Tasks& tk, u
   if (h->inject) OS_CUDA(cudaMemcpyAsync(h->hist.p, h->inj_hist, 256 * 8, cudaMemcpyHostToDevice, s));
   OS_CUDA(cudaMemcpyAsync(h->last_hist, h->hist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
   launch_otsu(h->hist.as<unsigned long long>(), st, s);
+  if (h->arch.fgmin > 0 && h->comm) {  // the band foreground exchange of segment() (zero rows)
+    h->fg.ensure((size_t)h->H8 * h->W8);
+    OS_CUDA(cudaMemsetAsync(h->fg.p, 0, (size_t)h->H8 * h->W8, s));
+    g_nccl.check(g_nccl.allReduce(h->fg.p, h->fg.p, (size_t)h->H8 * h->W8, ncclUint8, ncclSum, h->comm, s),
+                 "ncclAllReduce(foreground)");
+  }
   h->area.ensure(kMaxTasks * 8);
   OS_CUDA(cudaMemsetAsync(h->area.p, 0, kMaxTasks * 8, s));
   if (h->comm)
@@ -1172,7 +1203,6 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
   try {
     OS_REQUIRE(h != nullptr, "handle is NULL");
     OS_CUDA(cudaSetDevice(h->device));
-    OS_REQUIRE(h->arch.fgmin == 0, "band calls do not support fgmin (component removal needs whole components)");
     validate_common(H, W, pad, patch, stride, h->arch.vote != 0);
     Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
     const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
@@ -1520,6 +1550,16 @@ int omniseg_debug_band_globals(omniseg_t* h, const uint8_t* pc, const uint64_t* 
   for (int c = 0; c < 3; ++c) h->inj_pc[c] = pc[c];
   h->inj_pc[3] = 0;
   for (int i = 0; i < 256; ++i) h->inj_hist[i] = hist[i];
+  return 0;
+}
+
+int omniseg_debug_band_fg(omniseg_t* h, const uint8_t* fg8, int64_t n) {
+  if (!h) return fail(Error(-1, "band_fg: NULL handle"));
+  if (!fg8 || n <= 0) {
+    h->inj_fg.clear();
+    return 0;
+  }
+  h->inj_fg.assign(fg8, fg8 + n);
   return 0;
 }
 

@@ -20,7 +20,7 @@ SYMBOLS = ("omniseg_create", "omniseg_segment_slide", "omniseg_output_size", "om
            "omniseg_get_fgmask",
            "omniseg_get_timings", "omniseg_set_stream", "omniseg_last_error", "omniseg_destroy",
            "omniseg_debug_predict_tiles", "omniseg_debug_conv", "omniseg_debug_set_profile",
-           "omniseg_debug_get_profile", "omniseg_debug_band_globals", "omniseg_debug_get_detection")
+           "omniseg_debug_get_profile", "omniseg_debug_band_globals", "omniseg_debug_band_fg", "omniseg_debug_get_detection")
 
 
 class OmnisegError(RuntimeError):
@@ -77,6 +77,8 @@ def load(path: str = LIB_PATH):
     L.omniseg_debug_get_profile.restype = i32
     L.omniseg_debug_band_globals.argtypes = [vp, vp, vp]
     L.omniseg_debug_band_globals.restype = i32
+    L.omniseg_debug_band_fg.argtypes = [vp, vp, i64]
+    L.omniseg_debug_band_fg.restype = i32
     L.omniseg_debug_get_detection.argtypes = [vp, vp, vp]
     L.omniseg_debug_get_detection.restype = i32
     _lib = L
@@ -201,6 +203,16 @@ class Omniseg:
         pc = np.ascontiguousarray(pc, np.uint8)
         hist = np.ascontiguousarray(hist, np.uint64)
         _check(load().omniseg_debug_band_globals(self.h, pc.ctypes.data, hist.ctypes.data))
+
+    def band_fg(self, fg8=None):
+        """Inject the whole slide's pre-filter level-8 foreground (band fgmin emulation)."""
+        import numpy as np
+        if fg8 is None:
+            _check(load().omniseg_debug_band_fg(self.h, None, 0))
+            return
+        fg8 = np.ascontiguousarray(fg8, np.uint8)
+        self._fg8 = fg8
+        _check(load().omniseg_debug_band_fg(self.h, fg8.ctypes.data, fg8.size))
 
     def detection(self):
         import numpy as np

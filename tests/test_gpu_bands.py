@@ -132,3 +132,53 @@ def test_empty_band_joins_without_compute(setup):
     assert (ba == 0).all() and len(h.tiles()) == 0
     _, t, gp = h.fgmask()
     assert t == h_full.fgmask()[1]
+
+
+def test_bands_component_removal_bit_exact(setup):
+    """SURVEY N2 on the band path (arch fgmin): the bands exchange their owned level-8
+    foreground rows (emulated here by injecting the whole slide's pre-filter foreground, as the
+    NCCL all-reduce delivers it), label the whole grid, and their owned canvas rows must be
+    bit-identical to the single-GPU fgmin run; the kept windows follow the filtered mask."""
+    import scipy.ndimage as ndi
+    from paper_2305_14566_b200 import Omniseg
+    from paper_2305_14566_b200 import dist as D
+    a, blob, slide, h_full, prob, mask, area, pc, hist, tiles_full = setup
+    fg_pre, _, _ = h_full.fgmask()
+    lab, n = ndi.label(fg_pre, structure=[[0, 1, 0], [1, 1, 1], [0, 1, 0]])
+    sizes = np.sort(np.bincount(lab.ravel())[1:])
+    assert n >= 3
+    fgmin = int(sizes[len(sizes) // 2]) + 1          # drops about half of the components
+    af = dict(a, fgmin=fgmin)
+    hf = Omniseg(arch_string(af), blob)
+    nout = prob.size
+    fprob = np.zeros(nout, np.float32)
+    fmask = np.zeros(nout, np.uint8)
+    farea = np.zeros(len(SCALES), np.uint64)
+    hf.segment_slide(slide, H, W, PAD, P, S, SCALES, CLASSES, fprob, fmask, farea)
+    fg_post, _, _ = hf.fgmask()
+    assert fg_post.sum() < fg_pre.sum()
+    Hp, _ = D.padded_extent(H, W, PAD)
+    fmax = max(a["slide_mag"] // s for s in SCALES)
+    Pf, Mf = _split(fprob, a), _split(fmask, a)
+    hb = Omniseg(arch_string(af), blob)
+    hb.band_globals(pc, hist)
+    hb.band_fg(fg_pre)
+    area_sum = np.zeros_like(farea)
+    for (row0, row1) in D.band_partition(Hp, 3, S):
+        b0, b1 = D.band_slide_rows(H, PAD, P, fmax, row0, row1)
+        own = [D.owned_canvas_rows(H, PAD, a["slide_mag"] // s, row0, row1) for s in SCALES]
+        nb = sum((r1 - r0) * ((W + f - 1) // f) for (r0, r1), f in zip(own, [a["slide_mag"] // s for s in SCALES]))
+        bp = np.zeros(max(nb, 1), np.float32)
+        bm = np.zeros(max(nb, 1), np.uint8)
+        ba = np.zeros(len(SCALES), np.uint64)
+        hb.segment_band(np.ascontiguousarray(slide[b0:b1]), H, W, row0, row1, PAD, P, S, SCALES, CLASSES, bp, bm, ba)
+        assert (hb.fgmask()[0] == fg_post).all()
+        o = 0
+        for t, ((r0, r1), s) in enumerate(zip(own, SCALES)):
+            f = a["slide_mag"] // s
+            ww = (W + f - 1) // f
+            assert (bp[o:o + (r1 - r0) * ww].view(np.uint32) == Pf[t][r0:r1].ravel().view(np.uint32)).all(), (row0, t)
+            assert (bm[o:o + (r1 - r0) * ww] == Mf[t][r0:r1].ravel()).all()
+            o += (r1 - r0) * ww
+        area_sum += ba
+    assert (area_sum == farea).all()
