@@ -423,45 +423,101 @@ __device__ __forceinline__ float act_value(const T* base, int64_t i, int c, int 
 }
 
 // ------------------------------------------------------------------ K7 GAP + controller
-// g[b][c] = mean over the bottleneck's h x w pixels (fixed summation order), fp32.
-// (x2 precision: a pixel holds [C] hi | [C] lo; the value is hi + lo.)
-// Block = 32 channels x 8 pixel slices (coalesced 64-B channel rows); each thread sums its
-// slice in pixel order, then the 8 slice sums are added in a fixed order: deterministic.
+// g[b][c] = mean over the bottleneck's h x w pixels, theta[b][t] = Wc [g_b; onehot(cls_t);
+// onehot(scl_t)] + bc (north_star controller), fp32, deterministic (fixed summation orders).
+// Stage 1 (gap_partial_kernel): grid (kGapSlices, windows); 256 threads = 4 pixel lanes x 64
+// channel groups of 8 channels, so every load is one 16-byte vector of 8 hi values (+ the 8-byte
+// e4m3 lo vector in the fp16f8 storage, or the 16-byte lo vector in x2): a slice's pixel rows
+// are read fully coalesced. The 4 pixel lanes are added in a fixed order -> part[b][slice][C].
+// Stage 2 (controller_kernel): one block per window: g = (sum of the slices in order) / hw; the
+// g-dependent part u[j] = Wc[j][:Cb] . g + bc[j] is shared by every task of the window (one
+// warp per output row j, lanes strided over the channels, fixed shuffle-tree reduction), then
+// theta[t][j] = u[j] + Wc[j][Cb + cls_t] + Wc[j][Cb + ncls + scl_t].
+constexpr int kGapSlices = 8;
 template <typename T>
-__global__ void __launch_bounds__(256) gap_kernel(const T* E, int hw, int C, int split, float* g) {
-  __shared__ float part[8][33];
-  const int b = blockIdx.y;
-  const int cl = threadIdx.x & 31, sl = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + cl;
-  float s = 0.f;
-  if (c < C) {
-    const int per = (hw + 7) / 8, i0 = sl * per, i1 = min(hw, i0 + per);
-    for (int i = i0; i < i1; ++i) s += act_value(E, (int64_t)b * hw + i, c, C, split);
-  }
-  part[sl][cl] = s;
-  __syncthreads();
-  if (sl == 0 && c < C) {
-    float t = 0.f;
+__global__ void __launch_bounds__(256) gap_partial_kernel(const T* E, int hw, int C, int split, float* part) {
+  __shared__ float red[4][512 + 8];
+  const int b = blockIdx.y, sl = blockIdx.x;
+  const int cg = threadIdx.x & 63, pl = threadIdx.x >> 6;
+  const int per = (hw + kGapSlices - 1) / kGapSlices;
+  const int i0 = sl * per, i1 = min(hw, i0 + per);
+  float acc[8];
+  for (int pass = 0; pass * 512 < C; ++pass) {  // uniform trip count: __syncthreads below
+    const int c0 = pass * 512 + cg * 8;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += part[k][cl];
-    g[(int64_t)b * C + c] = t / float(hw);
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+    for (int i = i0 + pl; i < i1 && c0 < C; i += 4) {
+      const int64_t px = (int64_t)b * hw + i;
+      if (split == 2) {
+        const uint8_t* row = reinterpret_cast<const uint8_t*>(E) + px * 3 * (int64_t)C;
+        const uint4 hv = __ldg(reinterpret_cast<const uint4*>(row + 2 * c0));
+        const uint2 lv = __ldg(reinterpret_cast<const uint2*>(row + 2 * C + c0));
+        const __half* hh = reinterpret_cast<const __half*>(&hv);
+        const uint8_t* ll = reinterpret_cast<const uint8_t*>(&lv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += __half2float(hh[k]) + f8lo(ll[k]);
+      } else {
+        const int stride = split == 1 ? 2 * C : C;
+        const uint4 hv = __ldg(reinterpret_cast<const uint4*>(E + px * stride + c0));
+        const T* hh = reinterpret_cast<const T*>(&hv);
+        if (split == 1) {
+          const uint4 lv = __ldg(reinterpret_cast<const uint4*>(E + px * stride + C + c0));
+          const T* ll = reinterpret_cast<const T*>(&lv);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] += float(hh[k]) + float(ll[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] += float(hh[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red[pl][cg * 8 + k] = acc[k];
+    __syncthreads();
+    if (pl == 0 && c0 < C) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float v = ((red[0][cg * 8 + k] + red[1][cg * 8 + k]) + red[2][cg * 8 + k]) + red[3][cg * 8 + k];
+        part[((int64_t)b * kGapSlices + sl) * C + c0 + k] = v;
+      }
+    }
+    __syncthreads();
   }
 }
 
-// theta[b][t][j] = Wc[j] . [g_b ; onehot(cls_t) ; onehot(scl_t)] + bc[j]   (north_star controller)
-__global__ void controller_kernel(const float* g, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
-                                  const int* task_cls, const int* task_scl, int ntasks, float* theta) {
-  const int b = blockIdx.y;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= ntasks * kTheta) return;
-  const int t = idx / kTheta, j = idx % kTheta;
+__global__ void __launch_bounds__(256) controller_kernel(const float* part, int hw, int C, int Cb, const float* Wc,
+                                                         const float* bc, int ncls, int nscl, const int* task_cls,
+                                                         const int* task_scl, int ntasks, float* g_out,
+                                                         float* theta) {
+  extern __shared__ float sh[];  // g [Cb] | u [kTheta]
+  float* g = sh;
+  float* u = sh + Cb;
+  const int b = blockIdx.x;
+  const float inv = 1.0f / float(hw);
+  for (int c = threadIdx.x; c < Cb; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < kGapSlices; ++k) t += part[((int64_t)b * kGapSlices + k) * C + c];
+    g[c] = t * inv;
+    if (g_out) g_out[(int64_t)b * Cb + c] = t * inv;
+  }
+  __syncthreads();
   const int nin = Cb + ncls + nscl;
-  const float* w = Wc + (int64_t)j * nin;
-  const float* gb = g + (int64_t)b * Cb;
-  float s = 0.f;
-  for (int i = 0; i < Cb; ++i) s = fmaf(w[i], gb[i], s);
-  s += w[Cb + task_cls[t]] + w[Cb + ncls + task_scl[t]] + bc[j];
-  theta[((int64_t)b * ntasks + t) * kTheta + j] = s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < kTheta; j += blockDim.x >> 5) {
+    const float* w = Wc + (int64_t)j * nin;
+    float s = 0.f;
+    for (int i = lane; i < Cb; i += 32) s = fmaf(__ldg(w + i), g[i], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) u[j] = s + bc[j];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < ntasks * kTheta; idx += blockDim.x) {
+    const int t = idx / kTheta, j = idx - t * kTheta;
+    const float* w = Wc + (int64_t)j * nin;
+    theta[((int64_t)b * ntasks + t) * kTheta + j] = u[j] + w[Cb + task_cls[t]] + w[Cb + ncls + task_scl[t]];
+  }
 }
 
 // ------------------------------------------------------------------ K8/K9 head + stitch
@@ -641,23 +697,62 @@ __global__ void __launch_bounds__(128) head_stitch_kernel(const T* D0, int C0p, 
 // else count << 28 | sum(round(p 2^20)) (R12).
 // fg8 (optional, SURVEY N2 / P:87): the mask is ANDed with the level-8 foreground, nearest-
 // neighbour: canvas pixel (cy, cx) -> level-8 pixel ((cy f + pad) / 8, (cx f + pad) / 8).
-__global__ void finalize_kernel(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask,
-                                unsigned long long* area, int vote, int vthr, FgMaskArgs fm) {
+__device__ __forceinline__ bool finalize_px(uint32_t a, int vote, int vthr, const FgMaskArgs& fm, int64_t i,
+                                            float& p) {
+  const int sh = vote ? 16 : 28;
+  const uint32_t cnt = a >> sh, sum = a & ((1u << sh) - 1u);
+  const int fb = vote ? 0 : 20;  // fixed-point bits of the per-window value
+  bool m = cnt > 0 && (vthr > 0 ? sum >= min((uint32_t)vthr, cnt) : 2ull * sum >= ((unsigned long long)cnt << fb));
+  if (fm.fg8 && m) {
+    const int64_t cy = fm.cy0 + i / fm.Wt, cx = i % fm.Wt;
+    m = fm.fg8[((cy * fm.f + fm.pad) >> 3) * (int64_t)fm.W8 + ((cx * fm.f + fm.pad) >> 3)] != 0;
+  }
+  p = cnt ? (float(sum) * (vote ? 1.0f : 1.0f / 1048576.0f)) / float(cnt) : 0.f;
+  return m;
+}
+
+// HBM-bound (9 bytes per canvas pixel): VEC moves 4 pixels per thread and iteration (16-byte
+// canvas load, 16-byte prob store, 4-byte mask store) over the aligned bulk [h0, h0 + 4 nv);
+// the unaligned head [0, h0) and the tail are done per pixel.
+template <bool VEC>
+__global__ void __launch_bounds__(256) finalize_kernel(const uint32_t* acc, int64_t n, int64_t h0, float* prob,
+                                                       uint8_t* mask, unsigned long long* area, int vote, int vthr,
+                                                       FgMaskArgs fm) {
   __shared__ unsigned long long s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
   unsigned long long local = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t a = acc[i];
-    const int sh = vote ? 16 : 28;
-    const uint32_t cnt = a >> sh, sum = a & ((1u << sh) - 1u);
-    const int fb = vote ? 0 : 20;  // fixed-point bits of the per-window value
-    bool m = cnt > 0 && (vthr > 0 ? sum >= min((uint32_t)vthr, cnt) : 2ull * sum >= ((unsigned long long)cnt << fb));
-    if (fm.fg8 && m) {
-      const int64_t cy = fm.cy0 + i / fm.Wt, cx = i % fm.Wt;
-      m = fm.fg8[((cy * fm.f + fm.pad) >> 3) * (int64_t)fm.W8 + ((cx * fm.f + fm.pad) >> 3)] != 0;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  int64_t scalar_from = 0;
+  if (VEC) {
+    const int64_t nv = (n - h0) / 4;
+    for (int64_t v = tid; v < nv; v += nth) {
+      const int64_t i = h0 + 4 * v;
+      const uint4 a = __ldcs(reinterpret_cast<const uint4*>(acc + i));
+      float p0, p1, p2, p3;
+      const bool m0 = finalize_px(a.x, vote, vthr, fm, i, p0), m1 = finalize_px(a.y, vote, vthr, fm, i + 1, p1);
+      const bool m2 = finalize_px(a.z, vote, vthr, fm, i + 2, p2), m3 = finalize_px(a.w, vote, vthr, fm, i + 3, p3);
+      if (prob) __stcs(reinterpret_cast<float4*>(prob + i), make_float4(p0, p1, p2, p3));
+      if (mask)
+        *reinterpret_cast<uint32_t*>(mask + i) = (uint32_t)m0 | ((uint32_t)m1 << 8) | ((uint32_t)m2 << 16) |
+                                                 ((uint32_t)m3 << 24);
+      local += (int)m0 + (int)m1 + (int)m2 + (int)m3;
     }
-    if (prob) prob[i] = cnt ? (float(sum) * (vote ? 1.0f : 1.0f / 1048576.0f)) / float(cnt) : 0.f;
+    // per-pixel rest: the head [0, h0) and the tail [h0 + 4 nv, n)
+    for (int64_t k = tid; k < h0 + (n - h0 - 4 * nv); k += nth) {
+      const int64_t i = k < h0 ? k : h0 + 4 * nv + (k - h0);
+      float p;
+      const bool m = finalize_px(acc[i], vote, vthr, fm, i, p);
+      if (prob) prob[i] = p;
+      if (mask) mask[i] = m ? 1 : 0;
+      local += m;
+    }
+    scalar_from = n;
+  }
+  for (int64_t i = scalar_from + tid; i < n; i += nth) {
+    float p;
+    const bool m = finalize_px(acc[i], vote, vthr, fm, i, p);
+    if (prob) prob[i] = p;
     if (mask) mask[i] = m ? 1 : 0;
     local += m;
   }
@@ -900,15 +995,15 @@ void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s)
   gather_raw_kernel<T><<<grid, 256, 0, s>>>(tiles, n, P, X);
 }
 template <typename T>
-void launch_gap(const T* E, int n, int hw, int C, int split, float* g, cudaStream_t s) {
-  dim3 grid((C + 31) / 32, n);
-  gap_kernel<T><<<grid, 256, 0, s>>>(E, hw, C, split, g);
+void launch_gap_controller(const T* E, int n, int hw, int C, int split, int Cb, const float* Wc, const float* bc,
+                           int ncls, int nscl, const int* task_cls, const int* task_scl, int ntasks, float* part,
+                           float* g, float* theta, cudaStream_t s) {
+  OS_REQUIRE(C % 8 == 0 && Cb <= C, "gap: channel count must be a multiple of 8");
+  gap_partial_kernel<T><<<dim3(kGapSlices, n), 256, 0, s>>>(E, hw, C, split, part);
+  controller_kernel<<<n, 256, (Cb + kTheta) * sizeof(float), s>>>(part, hw, C, Cb, Wc, bc, ncls, nscl, task_cls,
+                                                                   task_scl, ntasks, g, theta);
 }
-void launch_controller(const float* g, int n, int Cb, const float* Wc, const float* bc, int ncls, int nscl,
-                       const int* task_cls, const int* task_scl, int ntasks, float* theta, cudaStream_t s) {
-  dim3 grid((ntasks * kTheta + 127) / 128, n);
-  controller_kernel<<<grid, 128, 0, s>>>(g, Cb, Wc, bc, ncls, nscl, task_cls, task_scl, ntasks, theta);
-}
+size_t gap_scratch_floats(int n, int C) { return (size_t)n * kGapSlices * C; }
 template <typename T>
 void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,
                  const float* theta, int ntasks, const uint32_t* tiles, int first, const HeadTaskTable& tt, int S,
@@ -920,8 +1015,18 @@ void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const fl
 void launch_finalize(const uint32_t* acc, int64_t n, float* prob, uint8_t* mask, unsigned long long* area, int vote,
                      int vthr, const FgMaskArgs& fm, cudaStream_t s) {
   if (n <= 0) return;
-  int blocks = (int)std::min<int64_t>(8 * 148, (n + 255) / 256);
-  finalize_kernel<<<blocks, 256, 0, s>>>(acc, n, prob, mask, area, vote, vote ? vthr : 0, fm);
+  vthr = vote ? vthr : 0;
+  // head h0: pixels until the canvas is 16-byte aligned; the vector path also needs prob (16 B)
+  // and mask (4 B) aligned at the same pixel
+  const int64_t h0 = ((16 - ((uintptr_t)acc & 15)) & 15) / 4;
+  const bool vec = ((uintptr_t)acc & 3) == 0 && n >= h0 + 64 &&
+                   (!prob || (((uintptr_t)(prob + h0)) & 15) == 0) && (!mask || (((uintptr_t)(mask + h0)) & 3) == 0);
+  const int64_t work = vec ? (n - h0) / 4 : n;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(8 * 148, (work + 255) / 256));
+  if (vec)
+    finalize_kernel<true><<<blocks, 256, 0, s>>>(acc, n, h0, prob, mask, area, vote, vthr, fm);
+  else
+    finalize_kernel<false><<<blocks, 256, 0, s>>>(acc, n, 0, prob, mask, area, vote, vthr, fm);
 }
 void launch_fg_components(uint8_t* fg, int W, int r0, int r1, int min_area, int* lab, int* size, cudaStream_t s) {
   const int64_t n = (int64_t)(r1 - r0) * W;
@@ -949,7 +1054,8 @@ void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, 
   template void launch_gather<T>(const uint32_t*, int, int, int, int, const FrontParams&, const DevState*,          \
                                  const uint32_t*, const uint32_t*, const uint32_t*, T*, cudaStream_t);             \
   template void launch_gather_raw<T>(const uint8_t*, int, int, T*, cudaStream_t);                                  \
-  template void launch_gap<T>(const T*, int, int, int, int, float*, cudaStream_t);                                 \
+  template void launch_gap_controller<T>(const T*, int, int, int, int, int, const float*, const float*, int, int,    \
+                                         const int*, const int*, int, float*, float*, float*, cudaStream_t);      \
   template void launch_head<T>(const T*, int, int, int, int, int, const float*, const float*, const float*, int,        \
                                const uint32_t*, int, const HeadTaskTable&, int, int, int, int, float*, float*,     \
                                cudaStream_t);                                                                     \

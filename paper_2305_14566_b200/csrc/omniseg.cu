@@ -231,7 +231,7 @@ struct omniseg {
   std::vector<LevelBufs> lv;
   std::vector<int> rc;   // per level: A_l / Bt_l stored row-chunked (see ensure_workspace)
   std::vector<int> erc;  // per level: E_l (encoder output / skip) stored row-chunked
-  DevBuf g, theta, task_cls, task_scl;
+  DevBuf g, gpart, theta, task_cls, task_scl;
   // plans in launch order for one batch (rebuilt with the workspace)
   struct Step {
     int kind;  // 0 conv, 1 gap+controller marker
@@ -469,6 +469,7 @@ void ensure_workspace(omniseg* h, int P) {
     q.Bt.ensure(n);
   }
   h->g.ensure((size_t)B * h->C[L - 1] * 4);
+  h->gpart.ensure(gap_scratch_floats(B, h->Cp[L - 1]) * 4);
   h->theta.ensure((size_t)B * kMaxTasks * kTheta * 4);
   const bool bf = ar.bf16;
   h->enc_plans.clear();
@@ -687,10 +688,10 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
     h->conv_launches++;
   }
   const LevelBufs& bl = h->lv[L - 1];
-  launch_gap<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->arch.sp(L - 1), h->g.as<float>(), s);
-  launch_controller(h->g.as<float>(), n, h->C[L - 1], h->Wc.as<float>(), h->bc.as<float>(), h->arch.ncls,
-                    (int)h->arch.scale_codes.size(), h->task_cls.as<int>(), h->task_scl.as<int>(), ntasks,
-                    h->theta.as<float>(), s);
+  launch_gap_controller<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->arch.sp(L - 1), h->C[L - 1], h->Wc.as<float>(),
+                           h->bc.as<float>(), h->arch.ncls, (int)h->arch.scale_codes.size(), h->task_cls.as<int>(),
+                           h->task_scl.as<int>(), ntasks, h->gpart.as<float>(), h->g.as<float>(), h->theta.as<float>(),
+                           s);
   h->launches += 2;
   if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, h->g.p, (size_t)n * h->C[L - 1] * 4, cudaMemcpyDefault, s));
   // ---------------- decoder
