@@ -49,6 +49,8 @@ def arch_string(a: dict) -> str:
         s += ";fgmin=%d" % a["fgmin"]
     if a.get("maskfg") is not None:
         s += ";maskfg=%d" % a["maskfg"]
+    if a.get("headtc") is not None:
+        s += ";headtc=%d" % a["headtc"]
     if a.get("vthr") is not None:
         s += ";vthr=" + ",".join(str(int(v)) for v in a["vthr"])
     return s

@@ -95,6 +95,7 @@ struct HeadArgs {
   int first;              // index of batch tile 0 in `tiles`
   float* out_p;           // debug: [B][ntasks][P][P] probabilities instead of stitching
   float* out_F;           // debug: [B][P][P][8]
+  int no_tc;              // experiments only: force the CUDA-core head
   HeadTaskTable tt;
 };
 

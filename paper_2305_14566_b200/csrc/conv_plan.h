@@ -19,6 +19,7 @@ struct ConvPlan {
   int cl = 1;            // per-tap kernel cluster size (2: CTA pairs multicasting the weight tiles)
   int hb = 1;
   bool bf16;
+  bool head_tc = false;  // kHeadFused with the tensor-core head (R = NzCfg::RTC)
   HeadArgs head{};       // kHead mode (fused dynamic head + stitch), set by the caller per launch
   double flops;          // algorithmic FLOPs of one launch (2 * M * N * K)
 };

@@ -136,10 +136,13 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   constexpr int STR = NzCfg::STAGES(BN, 1);  // residual epilogue
   constexpr int STH = NzCfg::STAGES(BN, 2);  // fused head (residual slots only)
   static_assert(ST >= 2 && STR >= 2 && STH >= 2, "no-swizzle tile does not fit shared memory");
+  constexpr int RT = NzCfg::RTC;
+  constexpr int STT = NzCfg::STAGES(BN, 2, RT);  // tensor-core head
   int smem = NzSmem<BN, R, ST, DYF, 8, 0>::kTotal;
   const int threads = 384;
   if (p.mode == kResidualRelu) smem = NzSmem<BN, R, STR, DYF, 8, 1>::kTotal;
-  else if (p.mode == kHeadFused) smem = NzSmem<BN, R, STH, DYF, 8, 2>::kTotal;
+  else if (p.mode == kHeadFused) smem = p.head_tc ? NzSmem<BN, RT, STT, DYF, 8, 2>::kTotal : NzSmem<BN, R, STH, DYF, 8, 2>::kTotal;
+  OS_REQUIRE(p.nz_R == (p.head_tc ? RT : R), "nz plan: rows per work item mismatch");
   auto go = [&](auto kern) {
     static std::mutex mu;
     static std::unordered_set<const void*> done;
@@ -153,7 +156,15 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   switch (p.mode) {
     case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;
     case kResidualRelu: go(conv3_nz_kernel<T, BN, R, STR, kResidualRelu, DYF>); break;
-    case kHeadFused: go(conv3_nz_kernel<T, BN, R, STH, kHeadFused, DYF>); break;
+    case kHeadFused:
+      if constexpr (BN <= 32) {
+        if (p.head_tc) {
+          go(conv3_nz_kernel<T, BN, RT, STT, kHeadFused, DYF>);
+          break;
+        }
+      }
+      go(conv3_nz_kernel<T, BN, R, STH, kHeadFused, DYF>);
+      break;
     default: go(conv3_nz_kernel<T, BN, R, ST, kBias, DYF>); break;
   }
 }
@@ -252,6 +263,10 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   OS_REQUIRE(!f8in || (Cin % 32 == 0 && w_lo != nullptr && !bf16), "F8 input needs Cin % 32 == 0, fp16 and lo weights");
   OS_REQUIRE(split_out != kStoreF8 || (Cout % 32 == 0 && !bf16), "F8 output needs Cout % 32 == 0 and fp16");
   ConvPlan p{};
+  if (mode == kHeadFusedTc) {
+    mode = kHeadFused;
+    p.head_tc = !bf16 && Cout <= 32;
+  }
   p.mode = mode;
   p.bf16 = bf16;
   // K chunk = one swizzle row (128/64/32 bytes); N tile = largest power of two <= 256 dividing Cout
@@ -321,7 +336,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     a.tiles_x = Win / 128;
     a.tiles_y = Ho / R;
   } else if (in_rc) {
-    const int R = NzCfg::R(p.bn);
+    const int R = p.head_tc ? NzCfg::RTC : NzCfg::R(p.bn);
     // A: 5-D u8 view {128 B = 8 px of one chunk, W/8 units, chunk, H, B} of [B][H][chunk][W][16 B],
     // box {128, 18, 2, R+2, 1} -> smem [row][chunk][144 px][16 B]
     const uint64_t nch = in_px / 16;

@@ -29,6 +29,9 @@
 namespace osg {
 
 enum ConvMode : int { kReluBias = 0, kResidualRelu = 1, kUpAdd = 2, kBias = 3, kHeadFused = 4 };
+// plan-level request (make_conv_plan only): kHeadFused with the tensor-core head (arch headtc=1):
+// R = 4 rows per work item, the plan's mode is kHeadFused and ConvPlan::head_tc is set
+constexpr int kHeadFusedTc = 5;
 
 // Storage of an activation tensor, per pixel (R9):
 //   kStorePlain  [C] 16-bit
@@ -661,6 +664,46 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
       }
     }
   }
+}
+
+// Tensor-core dynamic head, second half (CUDA cores): h1 = ReLU(W1' D0 + b1') of one task
+// (layer 1 and precls ran on the tensor cores, epi_head_tc), then h2 = ReLU(W2 h1 + b2),
+// z = W3 h2 + b3, p = sigmoid(z) and the fixed-point stitch -- the arithmetic of epi_head.
+__device__ __forceinline__ void head_tail(const float (&h1)[kHead], const float* th, const HeadArgs& ha, int t, int x,
+                                          int y, int lf, int oy, int ox) {
+  float h2[kHead];
+#pragma unroll
+  for (int o = 0; o < kHead; ++o) h2[o] = th[136 + o];
+#pragma unroll
+  for (int i = 0; i < kHead; ++i) {
+    const float4 a4 = *reinterpret_cast<const float4*>(th + 72 + i * 8);
+    const float4 b4 = *reinterpret_cast<const float4*>(th + 72 + i * 8 + 4);
+    h2[0] = fmaf(a4.x, h1[i], h2[0]);
+    h2[1] = fmaf(a4.y, h1[i], h2[1]);
+    h2[2] = fmaf(a4.z, h1[i], h2[2]);
+    h2[3] = fmaf(a4.w, h1[i], h2[3]);
+    h2[4] = fmaf(b4.x, h1[i], h2[4]);
+    h2[5] = fmaf(b4.y, h1[i], h2[5]);
+    h2[6] = fmaf(b4.z, h1[i], h2[6]);
+    h2[7] = fmaf(b4.w, h1[i], h2[7]);
+  }
+  const float4 c4 = *reinterpret_cast<const float4*>(th + 144);
+  const float4 d4 = *reinterpret_cast<const float4*>(th + 148);
+  float z = th[152];
+  z = fmaf(c4.x, fmaxf(h2[0], 0.f), z);
+  z = fmaf(c4.y, fmaxf(h2[1], 0.f), z);
+  z = fmaf(c4.z, fmaxf(h2[2], 0.f), z);
+  z = fmaf(c4.w, fmaxf(h2[3], 0.f), z);
+  z = fmaf(d4.x, fmaxf(h2[4], 0.f), z);
+  z = fmaf(d4.y, fmaxf(h2[5], 0.f), z);
+  z = fmaf(d4.z, fmaxf(h2[6], 0.f), z);
+  z = fmaf(d4.w, fmaxf(h2[7], 0.f), z);
+  const float p = 1.0f / (1.0f + expf(-z));
+  const int f = 1 << lf;
+  const int cy = oy + y - ha.pad / f, cx = ox + x - ha.pad / f;
+  const int Wt = ha.tt.Wt[t];
+  if (cy >= 0 && cy < ha.tt.Ht[t] && cx >= 0 && cx < Wt && cy >= ha.tt.row0[t] && cy < ha.tt.row1[t])
+    atomicAdd(ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * Wt + cx, stitch_value(p, z, ha.tt.vote));
 }
 
 // Per-tap kernel epilogue shape: the output-only modes (kReluBias, kBias) with BN >= 32 run 8
@@ -1393,24 +1436,40 @@ struct NzSmem {
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
   static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 : 0;
-  static constexpr int kTotal = kHeadOff + kHeadBytes + 1024;
-  static constexpr uint32_t kTmemCols = (2 * R * BN <= 256) ? 256 : 512;
+  // tensor-core dynamic head (fp16 activations, see epi_head_tc): per epilogue half the D0 row
+  // as UMMA A operands (128 px x BN channels, fp16 hi and lo, no-swizzle K-major), the item's B
+  // operand W1' = W1 Wpre (BN x BN, hi and lo), b1' and one MMA-completion mbarrier per half
+  // (2 halves x 2 rows in flight x hi / lo A tiles; layer-1 results in TMEM columns past the
+  // two accumulator buffers)
+  static constexpr int kTcA = 128 * BN * 2;                          // one A tile (hi or lo)
+  static constexpr int kTcB = BN * BN * 2;                           // one B tile
+  static constexpr int kTcOff = ((kHeadOff + kHeadBytes + 1023) / 1024) * 1024;
+  static constexpr bool kTc = EK == 2 && BN <= 32 && R == 4;  // = NzCfg::tc(BN, EK, R)
+  static constexpr int kTcBytes = kTc ? 8 * kTcA + 2 * kTcB + BN * 4 + 64 : 0;
+  static constexpr int kTotal = kTcOff + kTcBytes + 1024;
+  static constexpr uint32_t kTmemCols = kTc || 2 * R * BN > 256 ? 512 : 256;
 };
 
 struct NzCfg {
   // R output rows per work item: 2 R BN = 512 TMEM columns (two accumulator buffers), at most 8
-  // rows (the (R+2)-row input box must leave room for >= 2 ring stages)
+  // rows (the (R+2)-row input box must leave room for >= 2 ring stages). The optional tensor-core
+  // head (arch headtc=1, BN <= 32) runs R = 4: half the accumulator columns stay free for its
+  // layer-1 results and the smaller input box leaves shared memory for its A tiles.
   static constexpr int R(int bn) { return 256 / bn < 8 ? 256 / bn : 8; }
-  static constexpr int stage_bytes(int bn) {
-    return (((R(bn) + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + ((9 * bn * 32 + 1023) / 1024) * 1024;
+  static constexpr int RTC = 4;
+  static constexpr bool tc(int bn, int ek, int r) { return ek == 2 && bn <= 32 && r == RTC; }
+  static constexpr int stage_bytes(int bn, int r) {
+    return (((r + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + ((9 * bn * 32 + 1023) / 1024) * 1024;
   }
   // ring depth from what the 8 epilogue warps (kind ek, see NzSmem) leave of 227 KB
-  static constexpr int STAGES(int bn, int ek) {
-    return budget(bn, ek) / stage_bytes(bn) > 6 ? 6 : budget(bn, ek) / stage_bytes(bn);
+  static constexpr int STAGES(int bn, int ek, int r) {
+    return budget(bn, ek, r) / stage_bytes(bn, r) > 6 ? 6 : budget(bn, ek, r) / stage_bytes(bn, r);
   }
-  static constexpr int budget(int bn, int ek) {
+  static constexpr int STAGES(int bn, int ek) { return STAGES(bn, ek, R(bn)); }
+  static constexpr int tc_bytes(int bn) { return 8 * 128 * bn * 2 + 2 * bn * bn * 2 + bn * 4 + 64; }
+  static constexpr int budget(int bn, int ek, int r) {
     return 227 * 1024 - 3 * 1024 - 8 * (ek == 2 ? 4 : ek == 1 ? 6 : 3) * 32 * (bn < 32 ? bn : 32) * 2 -
-           (ek == 2 ? 7680 : 0);
+           (ek == 2 ? 7680 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
   }
 };
 
@@ -1499,6 +1558,10 @@ __global__ void __launch_bounds__(384, 1)
       ptx::mbar_init(&tempty[a], 32 * EW);
     }
     for (int a = 0; a < 2 * EW; ++a) ptx::mbar_init(&rbar[a], 1);
+    if constexpr (S::kTc) {
+      uint64_t* hmb = reinterpret_cast<uint64_t*>(smem + S::kTcOff + 8 * S::kTcA + 2 * S::kTcB + BN * 4);
+      for (int i = 0; i < 8; ++i) ptx::mbar_init(&hmb[i], 1);
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -1608,6 +1671,20 @@ __global__ void __launch_bounds__(384, 1)
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;
     const int et = ew * 32 + (int)lane;  // 0 .. 32*EW-1 over the epilogue warps
+    // tensor-core head (the row loop below): fp16 activations, all BN channels in one chunk
+    constexpr bool kTcHead = S::kTc && std::is_same<T, __half>::value && CH == BN;
+    uint8_t* tc_a = smem + S::kTcOff + half * 4 * S::kTcA;  // this half's A tiles: 2 rows x (hi, lo)
+    uint8_t* tc_b = smem + S::kTcOff + 8 * S::kTcA;         // B tiles: hi, lo
+    float* tc_b1 = reinterpret_cast<float*>(tc_b + 2 * S::kTcB);
+    uint64_t* tc_bar = reinterpret_cast<uint64_t*>(tc_b + 2 * S::kTcB + BN * 4);
+    uint32_t tc_phase = 0;
+    int tl[BN / 8 > 0 ? BN / 8 : 1];
+    int ns = 0;
+    bool tc = false;
+    (void)tc_a;
+    (void)tc_bar;
+    (void)tc_phase;
+    (void)tl;
     if constexpr (MODE == kHeadFused) {
       for (int i = et; i < kHead * CH; i += 32 * EW) {  // transposed: s_w[j * 8 + o]
         const int o = i / CH, j = i - o * CH;
@@ -1653,6 +1730,52 @@ __global__ void __launch_bounds__(384, 1)
           oy = min((int)((id >> 15) & 0x7FFF) * hargs.S, hargs.Hp / f - hargs.P);
           ox = min((int)(id & 0x7FFF) * hargs.S, hargs.Wp / f - hargs.P);
         }
+        if constexpr (kTcHead) {
+          // tensor-core head for this item: the window's tasks of its scale, at most BN / 8
+          ns = 0;
+          if (hargs.tiles && !hargs.out_F) {
+            for (int t = 0; t < hargs.ntasks; ++t)
+              if (hargs.tt.log2f[t] == lf) {
+#pragma unroll
+                for (int k = 0; k < BN / 8; ++k)
+                  if (k == ns) tl[k] = t;  // constant indices: tl stays in registers
+                ++ns;
+              }
+          }
+          tc = ns >= 1 && ns <= BN / 8 && !(OS_EXP && hargs.no_tc);
+          if (tc) {
+            // B = W1' (rows n = task * 8 + o, K = BN input channels of precls), fp16 hi / lo in
+            // the no-swizzle K-major layout: W1'[n][k] = sum_j W1_t[o][j] Wpre[j][k];
+            // b1'[n] = b1_t[o] + sum_j W1_t[o][j] bpre[j] (layer 1 folded through precls)
+            for (int i = et; i < BN * BN; i += 32 * EW) {
+              const int n = i / BN, k = i - n * BN, ti = n >> 3, o = n & 7;
+              float wv = 0.f;
+              if (ti < ns) {
+                const float* th = s_th + tl[ti] * 156;
+#pragma unroll
+                for (int j = 0; j < kHead; ++j) wv = fmaf(th[j * 8 + o], s_w[k * 8 + j], wv);
+              }
+              const __half hv = __float2half_rn(wv);
+              const __half lv = __float2half_rn(wv - __half2float(hv));
+              const int off = (k >> 3) * (BN * 16) + (n >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+              *reinterpret_cast<__half*>(tc_b + off) = hv;
+              *reinterpret_cast<__half*>(tc_b + S::kTcB + off) = lv;
+            }
+            if (et < BN) {
+              const int ti = et >> 3, o = et & 7;
+              float bv = 0.f;
+              if (ti < ns) {
+                const float* th = s_th + tl[ti] * 156;
+                bv = th[64 + o];
+#pragma unroll
+                for (int j = 0; j < kHead; ++j) bv = fmaf(th[j * 8 + o], s_b[j], bv);
+              }
+              tc_b1[et] = bv;
+            }
+            ptx::fence_proxy_async();
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+          }
+        }
       }
       constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
       constexpr int NC = BN / CH;
@@ -1663,7 +1786,106 @@ __global__ void __launch_bounds__(384, 1)
         epi_res_issue<CH>(es, 0, &tmR, &lo.R, nt * BN, args.Cout, args.split, xb, tyg * R + half, b + args.b_res, lane);
       ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
-      if constexpr (MODE == kHeadFused && NC == 1 && RM % 2 == 0) {
+      if (kTcHead && tc) {
+        // Tensor-core dynamic head. Phase 1, for each of the warp's RM rows: D0 = ReLU(acc + b +
+        // U0) -> fp16 hi + lo into the row's A tiles (pixel m = 32 q + lane: the 4 quadrant warps
+        // of the half fill the 128-pixel row) -> named barrier of the half -> the quadrant-0 warp
+        // issues D = A_hi B_hi + A_lo B_hi + A_hi B_lo (M = 128, N = BN: every task's layer-1
+        // pre-activation W1' D0) into the row's own TMEM columns past the accumulator buffers
+        // and commits to the row's mbarrier. Phase 2: wait, load the warp's 32 lanes, run
+        // W2 / W3 / sigmoid / stitch on the CUDA cores (head_tail). All RM rows' MMAs are in
+        // flight before the first wait.
+        static_assert(!kTcHead || RM * NH * BN <= 512 - 2 * R * BN, "TMEM columns for the head");
+#pragma unroll
+        for (int i = 0; i < RM; ++i) {
+          const int r = i * NH + half, slot = i & 1;
+          if (i + 1 < RM)
+            epi_res_issue<CH>(es, slot ^ 1, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + (i + 1) * NH + half,
+                              b + args.b_res, lane);
+          const uint32_t taddr =
+              tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (DYF ? (R - 1 - r) : r) * BN;
+          float v[CH];
+          epi_values<T, CH, kHeadFused>(es, slot, taddr, args.bias, 0, args.split, lane, v);
+          if (!args.split) {
+#pragma unroll
+            for (int j = 0; j < CH; ++j) v[j] = float(T(v[j]));
+          }
+          uint8_t* ta = tc_a + i * 2 * S::kTcA;
+          const int m = q * 32 + (int)lane;
+#pragma unroll
+          for (int g = 0; g < CH / 8; ++g) {
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __half2 h2 = __floats2half2_rn(v[8 * g + 2 * e], v[8 * g + 2 * e + 1]);
+              const float2 hf = __half22float2(h2);
+              const __half2 l2 = __floats2half2_rn(v[8 * g + 2 * e] - hf.x, v[8 * g + 2 * e + 1] - hf.y);
+              hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l2);
+            }
+            const int off = g * 2048 + (m >> 3) * 128 + (m & 7) * 16;
+            *reinterpret_cast<uint4*>(ta + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(ta + S::kTcA + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          ptx::fence_proxy_async();
+          ptx::tc_fence_before();
+          asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+          if (q == 0) {
+            ptx::tc_fence_after();
+            constexpr uint32_t id = ptx::idesc_f16(128, BN, false);
+            const uint32_t a_hi = ptx::smem_u32(ta), a_lo = a_hi + S::kTcA;
+            const uint32_t b_hi = ptx::smem_u32(tc_b), b_lo = b_hi + S::kTcB;
+            const uint32_t d = tmem_base + 2 * R * BN + (half * RM + i) * BN;
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk) {
+              const uint64_t dah = ptx::smem_desc_noswz(a_hi + kk * 4096, 2048, 128);
+              const uint64_t dal = ptx::smem_desc_noswz(a_lo + kk * 4096, 2048, 128);
+              const uint64_t dbh = ptx::smem_desc_noswz(b_hi + kk * BN * 32, BN * 16, 128);
+              const uint64_t dbl = ptx::smem_desc_noswz(b_lo + kk * BN * 32, BN * 16, 128);
+              ptx::mma_f16_w(d, dah, dbh, id, kk > 0 ? 1u : 0u);
+              ptx::mma_f16_w(d, dal, dbh, id, 1u);
+              ptx::mma_f16_w(d, dah, dbl, id, 1u);
+            }
+            ptx::mma_commit_w(&tc_bar[half * RM + i]);
+          }
+        }
+        // every accumulator row of this warp has been read: zero them (DYF) and hand the buffer
+        // back to the MMA warp before waiting for the head MMAs
+        if constexpr (DYF) {
+          for (int j = 0; j < RM; ++j) {
+            const int r = j * NH + half;
+            for (int c = 0; c < BN; c += 16)
+              ptx::tmem_st_zero16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (R - 1 - r) * BN + c);
+          }
+          ptx::tmem_st_wait();
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+#pragma unroll
+        for (int i = 0; i < RM; ++i) {
+          const int r = i * NH + half;
+          ptx::mbar_wait(&tc_bar[half * RM + i], tc_phase);
+          ptx::tc_fence_after();
+          uint32_t hr[CH];
+          const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + 2 * R * BN + (half * RM + i) * BN;
+          if constexpr (CH == 32)
+            ptx::tmem_ld_32x32b_x32(tq, *reinterpret_cast<uint32_t(*)[32]>(hr));
+          else
+            ptx::tmem_ld_32x32b_x16(tq, *reinterpret_cast<uint32_t(*)[16]>(hr));
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int ti = 0; ti < BN / 8; ++ti) {  // constant indices: hr / tl stay in registers
+            if (ti < ns) {
+              float h1[kHead];
+#pragma unroll
+              for (int o = 0; o < kHead; ++o) h1[o] = fmaxf(__uint_as_float(hr[ti * 8 + o]) + tc_b1[ti * 8 + o], 0.f);
+              head_tail(h1, s_th + tl[ti] * 156, hargs, tl[ti], xb + (int)lane, tyg * R + r, lf, oy, ox);
+            }
+          }
+        }
+        tc_phase ^= 1;
+        continue;  // accumulator already released
+      } else if constexpr (MODE == kHeadFused && NC == 1 && RM % 2 == 0) {
         // two rows (pixels (xb + lane, r0) and (xb + lane, r1)) per pass: both residual slots
         // are consumed by epi_values before the head math, so the next pair's residual loads
         // are issued right away and overlap it

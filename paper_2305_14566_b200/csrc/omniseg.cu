@@ -113,6 +113,7 @@ struct Arch {
   int vote = 0;             // fusion rule: 0 mean of p (R11), 1 hard majority vote
   int fgmin = 0;            // drop foreground components below fgmin level-8 pixels
   int maskfg = 0;           // AND the output masks with the foreground
+  int headtc = 0;           // 1: the fused head's layer 1 (+ precls) on tcgen05 (measured slower)
   std::vector<int> vthr;    // vote fusion: literal vote-count threshold per scale code; empty = majority
   int sp(int level) const { return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain; }
   // bytes per channel of a tensor stored with kind k
@@ -153,6 +154,7 @@ Arch parse_arch(const char* s) {
     else if (k == "xal") a.xal = toi(v);
     else if (k == "fgmin") a.fgmin = toi(v);
     else if (k == "maskfg") a.maskfg = toi(v);
+    else if (k == "headtc") a.headtc = toi(v);
     else if (k == "vthr") {
       a.vthr.clear();
       std::stringstream s2(v);
@@ -549,7 +551,8 @@ void ensure_workspace(omniseg* h, int P) {
   h->head_fusable = false;
   if (!exp_flag("OMNISEG_NO_HEAD_FUSION") && rc[0]) {
     LevelBufs& q = h->lv[0];
-    ConvPlan hp = plan(h->dec_b[0], q.Bt.p, q.P, q.A.p, q.E.p, kHeadFused, 0, rc[0], rc[0], 0);
+    ConvPlan hp = plan(h->dec_b[0], q.Bt.p, q.P, q.A.p, q.E.p, h->arch.headtc ? kHeadFusedTc : kHeadFused, 0, rc[0],
+                       rc[0], 0);
     if (hp.nz_R > 0 && hp.bn == h->Cp[0] && h->C[0] <= 32) {
       h->head_plan = hp;
       h->head_fusable = true;
@@ -672,6 +675,7 @@ void fill_head(HeadArgs& ha, omniseg* h, int ntasks, int P, int S, int Hp, int W
   ha.first = first;
   ha.out_p = out_p;
   ha.out_F = out_F;
+  ha.no_tc = exp_flag("OMNISEG_NO_TC_HEAD") ? 1 : 0;
   ha.tt = tt;
 }
 

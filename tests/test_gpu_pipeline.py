@@ -115,6 +115,18 @@ def check_votes(ref, p_gpu, m_gpu, pad, P, task=0, f=1, tag=""):
     return same, agree
 
 
+def test_cfg1_tensor_core_head_gated(gpu_lib):
+    """The optional tcgen05 dynamic head (arch headtc=1: precls folded into layer 1, W1' D0 as
+    fp16 hi/lo MMAs) under the same gates as the default head."""
+    w = workload(1)
+    w.arch["headtc"] = 1
+    slide, ref = _cfg1_ref()
+    h, prob, mask, area = run_gpu(w, slide)
+    H, W = slide.shape[:2]
+    dmax, agree = check_prob_mask(prob.reshape(H, W), mask.reshape(H, W), ref["prob"][0], ref["mask"][0], "headtc")
+    print(f"headtc: max |dp| {dmax:.4g}, mask agreement {agree:.5f}")
+
+
 def test_cfg1_vote_fusion(gpu_lib):
     """Hard majority-vote fusion (arch fusion=vote) against the oracle's vote mode:
     every window votes p >= 1/2; the canvas holds the vote fraction, the mask is 'at least
@@ -411,8 +423,9 @@ def test_shift_identity_network_bit_exact(gpu_lib, levels, base, P, dtype):
     assert (p == 0.5).all()
 
 
-@pytest.mark.parametrize("levels, base, P, S, pad", [(3, 8, 256, 128, 128), (5, 32, 512, 256, 256)])
-def test_shift_identity_network_slide_parity(gpu_lib, levels, base, P, S, pad):
+@pytest.mark.parametrize("levels, base, P, S, pad, headtc", [(3, 8, 256, 128, 128, 0), (5, 32, 512, 256, 256, 0),
+                                                             (3, 8, 256, 128, 128, 1), (5, 32, 512, 256, 256, 1)])
+def test_shift_identity_network_slide_parity(gpu_lib, levels, base, P, S, pad, headtc):
     """The identity network end to end through omniseg_segment_slide (fused gather + stem,
     trunk, fused head + stitch, finalize) on the cfg1 slide, with theta = bc chosen so that
     z = F_0 / 256 - 2 (W1 = W2 = I, W3 = e_0 / 256, b3 = -2): F is exact on both sides, so
@@ -428,6 +441,8 @@ def test_shift_identity_network_slide_parity(gpu_lib, levels, base, P, S, pad):
     theta[144] = 1.0 / 256
     theta[152] = -2.0
     a, net, blob = _shift_identity_net(levels, base, bc=theta)
+    if headtc:
+        a["headtc"] = 1   # the optional tcgen05 head (layer 1 + precls as MMAs): exact here too
     w = workload(1)
     slide, _ = _cfg1_ref()
     H, W = slide.shape[:2]
