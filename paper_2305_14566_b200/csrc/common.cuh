@@ -90,6 +90,7 @@ struct HeadArgs {
   const float* Wpre;    // [8][C0] precls weights (fp32)
   const float* bpre;    // [8]
   const float* theta;   // [B][ntasks][153] controller output
+  const float* theta_t; // [B][ntasks][156] the same with W1 / W2 transposed ([in * 8 + out]), 16-B rows
   int ntasks, C0, P, S, Hp, Wp, pad;
   const uint32_t* tiles;  // kept-tile ids (NULL: debug windows, every task applies)
   int first;              // index of batch tile 0 in `tiles`

@@ -1670,6 +1670,7 @@ __global__ void __launch_bounds__(384, 1)
     float* s_th = reinterpret_cast<float*>(smem + S::kHeadOff);
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;
+    const float* th_g = nullptr;         // this item's transposed theta rows (global, or s_th)
     const int et = ew * 32 + (int)lane;  // 0 .. 32*EW-1 over the epilogue warps
     // tensor-core head (the row loop below): fp16 activations, all BN channels in one chunk
     constexpr bool kTcHead = S::kTc && std::is_same<T, __half>::value && CH == BN;
@@ -1713,16 +1714,17 @@ __global__ void __launch_bounds__(384, 1)
       const int b = m / args.tiles_y;
       int lf = 0, oy = 0, ox = 0;
       if constexpr (MODE == kHeadFused) {
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // previous theta no longer read
-        const int nth = hargs.ntasks * kTheta;
-        for (int i = et; i < nth; i += 32 * EW) {
-          const int t = i / kTheta;
-          int k = i - t * kTheta;  // W1 [0, 64) and W2 [72, 136) stored transposed: [in * 8 + out]
-          if (k < 64) k = (k & 7) * 8 + (k >> 3);
-          else if (k >= 72 && k < 136) k = 72 + ((k - 72) & 7) * 8 + ((k - 72) >> 3);
-          s_th[t * 156 + k] = hargs.theta[(int64_t)(b + args.b_head) * nth + i];
+        // the window's theta (W1 / W2 transposed, rows of 156 floats, written by the controller)
+        // is read straight from global memory by the head (warp-uniform float4 loads, L1
+        // broadcast): no per-item staging and no epilogue-wide barrier. The tensor-core head
+        // stages it in shared memory for the B-operand build.
+        th_g = hargs.theta_t + (int64_t)(b + args.b_head) * hargs.ntasks * 156;
+        if constexpr (S::kTc) {
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // previous theta no longer read
+          for (int i = et; i < hargs.ntasks * 156; i += 32 * EW) s_th[i] = th_g[i];
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+          th_g = s_th;
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
         if (hargs.tiles) {
           const uint32_t id = hargs.tiles[hargs.first + b + args.b_head];
           lf = id >> 30;
@@ -1907,7 +1909,7 @@ __global__ void __launch_bounds__(384, 1)
               v1[j] = float(T(v1[j]));
             }
           }
-          epi_head2<T, CH>(v0, v1, xb + (int)lane, tyg * R + r0, tyg * R + r1, b + args.b_head, hargs, s_w, s_b, s_th,
+          epi_head2<T, CH>(v0, v1, xb + (int)lane, tyg * R + r0, tyg * R + r1, b + args.b_head, hargs, s_w, s_b, th_g,
                            lf, oy, ox);
         }
       } else
@@ -1931,7 +1933,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         } else if constexpr (MODE == kHeadFused) {
           epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs, s_w,
-                          s_b, s_th, lf, oy, ox);
+                          s_b, th_g, lf, oy, ox);
         } else {
           epi_chunk<T, CH, MODE>(es, slot, &tmO, &lo.O, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
                                  tyg * R + r, b + args.b_out, lane);

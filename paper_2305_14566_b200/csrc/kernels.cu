@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(256) gap_partial_kernel(const T* E, int hw, in
 __global__ void __launch_bounds__(256) controller_kernel(const float* part, int hw, int C, int Cb, const float* Wc,
                                                          const float* bc, int ncls, int nscl, const int* task_cls,
                                                          const int* task_scl, int ntasks, float* g_out,
-                                                         float* theta) {
+                                                         float* theta, float* theta_t) {
   extern __shared__ float sh[];  // g [Cb] | u [kTheta]
   float* g = sh;
   float* u = sh + Cb;
@@ -516,7 +516,14 @@ __global__ void __launch_bounds__(256) controller_kernel(const float* part, int 
   for (int idx = threadIdx.x; idx < ntasks * kTheta; idx += blockDim.x) {
     const int t = idx / kTheta, j = idx - t * kTheta;
     const float* w = Wc + (int64_t)j * nin;
-    theta[((int64_t)b * ntasks + t) * kTheta + j] = u[j] + w[Cb + task_cls[t]] + w[Cb + ncls + task_scl[t]];
+    const float v = u[j] + w[Cb + task_cls[t]] + w[Cb + ncls + task_scl[t]];
+    theta[((int64_t)b * ntasks + t) * kTheta + j] = v;
+    if (theta_t) {  // the fused head's layout: W1 [0, 64) and W2 [72, 136) transposed, rows of 156
+      int k = j;
+      if (k < 64) k = (k & 7) * 8 + (k >> 3);
+      else if (k >= 72 && k < 136) k = 72 + ((k - 72) & 7) * 8 + ((k - 72) >> 3);
+      theta_t[((int64_t)b * ntasks + t) * 156 + k] = v;
+    }
   }
 }
 
@@ -997,11 +1004,11 @@ void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s)
 template <typename T>
 void launch_gap_controller(const T* E, int n, int hw, int C, int split, int Cb, const float* Wc, const float* bc,
                            int ncls, int nscl, const int* task_cls, const int* task_scl, int ntasks, float* part,
-                           float* g, float* theta, cudaStream_t s) {
+                           float* g, float* theta, float* theta_t, cudaStream_t s) {
   OS_REQUIRE(C % 8 == 0 && Cb <= C, "gap: channel count must be a multiple of 8");
   gap_partial_kernel<T><<<dim3(kGapSlices, n), 256, 0, s>>>(E, hw, C, split, part);
   controller_kernel<<<n, 256, (Cb + kTheta) * sizeof(float), s>>>(part, hw, C, Cb, Wc, bc, ncls, nscl, task_cls,
-                                                                   task_scl, ntasks, g, theta);
+                                                                   task_scl, ntasks, g, theta, theta_t);
 }
 size_t gap_scratch_floats(int n, int C) { return (size_t)n * kGapSlices * C; }
 template <typename T>
@@ -1055,7 +1062,7 @@ void launch_t_to_f32(const T* in, float* out, int64_t rows, int cout, int cpad, 
                                  const uint32_t*, const uint32_t*, const uint32_t*, T*, cudaStream_t);             \
   template void launch_gather_raw<T>(const uint8_t*, int, int, T*, cudaStream_t);                                  \
   template void launch_gap_controller<T>(const T*, int, int, int, int, int, const float*, const float*, int, int,    \
-                                         const int*, const int*, int, float*, float*, float*, cudaStream_t);      \
+                                         const int*, const int*, int, float*, float*, float*, float*, cudaStream_t); \
   template void launch_head<T>(const T*, int, int, int, int, int, const float*, const float*, const float*, int,        \
                                const uint32_t*, int, const HeadTaskTable&, int, int, int, int, float*, float*,     \
                                cudaStream_t);                                                                     \

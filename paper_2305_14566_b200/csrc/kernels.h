@@ -37,7 +37,7 @@ void launch_gather_raw(const uint8_t* tiles, int n, int P, T* X, cudaStream_t s)
 template <typename T>
 void launch_gap_controller(const T* E, int n, int hw, int C, int split, int Cb, const float* Wc, const float* bc,
                            int ncls, int nscl, const int* task_cls, const int* task_scl, int ntasks, float* part,
-                           float* g, float* theta, cudaStream_t s);
+                           float* g, float* theta, float* theta_t, cudaStream_t s);
 size_t gap_scratch_floats(int n, int C);
 template <typename T>
 void launch_head(const T* D0, int n, int C0p, int C0, int split, int P, const float* Wpre, const float* bpre,

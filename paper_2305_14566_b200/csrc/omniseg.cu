@@ -233,7 +233,7 @@ struct omniseg {
   std::vector<LevelBufs> lv;
   std::vector<int> rc;   // per level: A_l / Bt_l stored row-chunked (see ensure_workspace)
   std::vector<int> erc;  // per level: E_l (encoder output / skip) stored row-chunked
-  DevBuf g, gpart, theta, task_cls, task_scl;
+  DevBuf g, gpart, theta, theta_t, task_cls, task_scl;
   // plans in launch order for one batch (rebuilt with the workspace)
   struct Step {
     int kind;  // 0 conv, 1 gap+controller marker
@@ -473,6 +473,7 @@ void ensure_workspace(omniseg* h, int P) {
   h->g.ensure((size_t)B * h->C[L - 1] * 4);
   h->gpart.ensure(gap_scratch_floats(B, h->Cp[L - 1]) * 4);
   h->theta.ensure((size_t)B * kMaxTasks * kTheta * 4);
+  h->theta_t.ensure((size_t)B * kMaxTasks * 156 * 4);
   const bool bf = ar.bf16;
   h->enc_plans.clear();
   h->dec_plans.clear();
@@ -664,6 +665,7 @@ void fill_head(HeadArgs& ha, omniseg* h, int ntasks, int P, int S, int Hp, int W
   ha.Wpre = h->Wpre.as<float>();
   ha.bpre = h->bpre.as<float>();
   ha.theta = h->theta.as<float>();
+  ha.theta_t = h->theta_t.as<float>();
   ha.ntasks = ntasks;
   ha.C0 = h->C[0];
   ha.P = P;
@@ -695,7 +697,7 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
   launch_gap_controller<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->arch.sp(L - 1), h->C[L - 1], h->Wc.as<float>(),
                            h->bc.as<float>(), h->arch.ncls, (int)h->arch.scale_codes.size(), h->task_cls.as<int>(),
                            h->task_scl.as<int>(), ntasks, h->gpart.as<float>(), h->g.as<float>(), h->theta.as<float>(),
-                           s);
+                           h->theta_t.as<float>(), s);
   h->launches += 2;
   if (out_g) OS_CUDA(cudaMemcpyAsync(out_g, h->g.p, (size_t)n * h->C[L - 1] * 4, cudaMemcpyDefault, s));
   // ---------------- decoder
