@@ -564,6 +564,38 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
   }
 }
 
+// A task of the item's window scale, compacted per epilogue warp (head_tasks): canvas pointer of
+// window pixel (0, 0), the window rows / columns that land on owned canvas pixels, row pitch.
+struct HeadTask {
+  uint32_t* base;
+  int t, Wt, ylo, yhi, xlo, xhi, pad_;
+};
+
+// Lanes t < ntasks describe task t if it runs at this window's level (lf); the valid ones are
+// compacted in task order into d[0..n) (warp-private shared memory; __syncwarp before use).
+__device__ __forceinline__ int head_tasks(const HeadArgs& ha, int lf, int oy, int ox, HeadTask* d, uint32_t lane) {
+  const int t = (int)lane;
+  const bool on = t < ha.ntasks && ha.tt.log2f[t] == lf;
+  const unsigned m = __ballot_sync(0xffffffffu, on);
+  if (on) {
+    const int f = 1 << lf;
+    const int cy0 = oy - ha.pad / f, cx0 = ox - ha.pad / f;  // canvas coords of window pixel (0, 0)
+    const int Wt = ha.tt.Wt[t];
+    HeadTask h;
+    h.t = t;
+    h.Wt = Wt;
+    h.ylo = max(0, max(ha.tt.row0[t], 0) - cy0);
+    h.yhi = min(ha.tt.Ht[t], ha.tt.row1[t]) - cy0;
+    h.xlo = max(0, -cx0);
+    h.xhi = Wt - cx0;
+    h.base = ha.tt.canvas[t] + ((int64_t)(cy0 - ha.tt.row0[t]) * Wt + cx0);
+    h.pad_ = 0;
+    d[__popc(m & ((1u << lane) - 1u))] = h;
+  }
+  __syncwarp();
+  return __popc(m);
+}
+
 // The fused head for TWO pixels per thread (rows r0, r1 of the warp's column): every shared
 // weight load feeds both, and the FMAs run as packed f32x2 (__ffma2_rn, sm_100) -- the same
 // fp32 arithmetic per pixel, half the FMA and load instructions of epi_head. v0 / v1: the D0
@@ -571,7 +603,7 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
 template <typename T, int CH>
 __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v1)[CH], int x, int y0, int y1, int b,
                                           const HeadArgs& ha, const float* s_w, const float* s_b, const float* s_th,
-                                          int lf, int oy, int ox) {
+                                          int lf, int oy, int ox, const HeadTask* ht = nullptr, int nht = 0) {
   // precls with transposed weights (s_w[j * 8 + o]): input-outer, 8 independent packed chains
   float2 F[kHead];
 #pragma unroll
@@ -598,8 +630,14 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
     }
   }
   const int f = 1 << lf;
-  for (int t = 0; t < ha.ntasks; ++t) {
-    if (ha.tiles && ha.tt.log2f[t] != lf) continue;
+  const int nloop = ht ? nht : ha.ntasks;
+  for (int k = 0; k < nloop; ++k) {
+    int t = k;
+    if (ht) {
+      t = ht[k].t;
+    } else if (ha.tiles && ha.tt.log2f[t] != lf) {
+      continue;
+    }
     const float* th = s_th + t * 156;  // W1 / W2 transposed: [i * 8 + o]
     float2 h1[kHead], h2[kHead];
 #pragma unroll
@@ -648,6 +686,17 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
     z = __ffma2_rn(make_float2(d4.y, d4.y), h2[5], z);
     z = __ffma2_rn(make_float2(d4.z, d4.z), h2[6], z);
     z = __ffma2_rn(make_float2(d4.w, d4.w), h2[7], z);
+    if (ht) {  // the stitch through the item's compacted task descriptor
+      const HeadTask d = ht[k];
+      const bool xin = x >= d.xlo && x < d.xhi;
+      // sigmoid with the fast exp / reciprocal (relative error ~1e-7, far inside the 2^-20
+      // fixed point the stitch rounds to; the vote decision uses z itself)
+      if (xin && y0 >= d.ylo && y0 < d.yhi)
+        atomicAdd(d.base + (int64_t)y0 * d.Wt + x, stitch_value(__frcp_rn(1.0f + __expf(-z.x)), z.x, ha.tt.vote));
+      if (xin && y1 >= d.ylo && y1 < d.yhi)
+        atomicAdd(d.base + (int64_t)y1 * d.Wt + x, stitch_value(__frcp_rn(1.0f + __expf(-z.y)), z.y, ha.tt.vote));
+      continue;
+    }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const float zz = k ? z.y : z.x;
@@ -1435,7 +1484,7 @@ struct NzSmem {
   static constexpr int kWarpEpi = (EK == 2 ? 4 : EK == 1 ? 6 : 3) * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
-  static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 : 0;
+  static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 + EW * 32 * 32 : 0;
   // tensor-core dynamic head (fp16 activations, see epi_head_tc): per epilogue half the D0 row
   // as UMMA A operands (128 px x BN channels, fp16 hi and lo, no-swizzle K-major), the item's B
   // operand W1' = W1 Wpre (BN x BN, hi and lo), b1' and one MMA-completion mbarrier per half
@@ -1469,7 +1518,7 @@ struct NzCfg {
   static constexpr int tc_bytes(int bn) { return 8 * 128 * bn * 2 + 2 * bn * bn * 2 + bn * 4 + 64; }
   static constexpr int budget(int bn, int ek, int r) {
     return 227 * 1024 - 3 * 1024 - 8 * (ek == 2 ? 4 : ek == 1 ? 6 : 3) * 32 * (bn < 32 ? bn : 32) * 2 -
-           (ek == 2 ? 7680 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
+           (ek == 2 ? 7680 + 8192 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
   }
 };
 
@@ -1671,6 +1720,10 @@ __global__ void __launch_bounds__(384, 1)
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;
     const float* th_g = nullptr;         // this item's transposed theta rows (global, or s_th)
+    HeadTask* s_ht = reinterpret_cast<HeadTask*>(s_b + kHead) + ew * 32;  // this warp's task descriptors
+    bool h_ok = false;
+    int h_n = 0;
+    (void)s_ht;
     const int et = ew * 32 + (int)lane;  // 0 .. 32*EW-1 over the epilogue warps
     // tensor-core head (the row loop below): fp16 activations, all BN channels in one chunk
     constexpr bool kTcHead = S::kTc && std::is_same<T, __half>::value && CH == BN;
@@ -1732,6 +1785,8 @@ __global__ void __launch_bounds__(384, 1)
           oy = min((int)((id >> 15) & 0x7FFF) * hargs.S, hargs.Hp / f - hargs.P);
           ox = min((int)(id & 0x7FFF) * hargs.S, hargs.Wp / f - hargs.P);
         }
+        h_ok = hargs.tiles != nullptr && hargs.out_p == nullptr && hargs.out_F == nullptr;
+        if (h_ok) h_n = head_tasks(hargs, lf, oy, ox, s_ht, lane);
         if constexpr (kTcHead) {
           // tensor-core head for this item: the window's tasks of its scale, at most BN / 8
           ns = 0;
@@ -1910,7 +1965,7 @@ __global__ void __launch_bounds__(384, 1)
             }
           }
           epi_head2<T, CH>(v0, v1, xb + (int)lane, tyg * R + r0, tyg * R + r1, b + args.b_head, hargs, s_w, s_b, th_g,
-                           lf, oy, ox);
+                           lf, oy, ox, h_ok ? s_ht : nullptr, h_n);
         }
       } else
 #pragma unroll 1
