@@ -53,6 +53,9 @@ struct StemPlan {
   ConvPlan conv;   // output maps, bias, weights, storage kind
   StemArgs args;
   int grid = 0;
+  StemInMaps inm{};                       // TMA maps of the RGBX levels (rebuilt when they change)
+  const void* inm_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+  int inm_Hp = 0, inm_Wp = 0;
 };
 bool stem_fusable(int P, int Cout);
 StemPlan make_stem_plan(const ConvPlan& stem_conv, const void* w, int P);

@@ -600,7 +600,21 @@ void launch_stem(const StemPlan& p, cudaStream_t s) {
   auto kern = stem_tc_kernel<T, BN, kStemR, kStemNA>;
   static std::once_flag once;
   std::call_once(once, [&] { OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal)); });
-  kern<<<p.grid, S::kThreads, S::kTotal, s>>>(p.conv.tmO, p.args, p.conv.lo);
+  kern<<<p.grid, S::kThreads, S::kTotal, s>>>(p.conv.tmO, p.args, p.conv.lo, p.inm.m[0], p.inm.m[1], p.inm.m[2],
+                                              p.inm.m[3]);
+}
+
+// TMA map of one RGBX level (u32 elements {Wp/f, Hp/f}), box {kStemBoxW, kStemR + 2}; reads past
+// the image edge return 0 (the converters zero everything outside the window anyway).
+void encode_level_map(CUtensorMap* m, const uint32_t* L, int Hl, int Wl) {
+  cuuint64_t dims[2] = {(cuuint64_t)Wl, (cuuint64_t)Hl};
+  cuuint64_t strides[1] = {(cuuint64_t)Wl * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kStemBoxW, (cuuint32_t)(kStemR + 2)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(L), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(stem level) failed: " + std::to_string((int)r));
 }
 
 void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32_t* const L[4], int S, int Hp, int Wp,
@@ -615,6 +629,15 @@ void run_stem(StemPlan& p, const uint32_t* tiles, int first, int n, const uint32
   a.num_work = n * a.tiles_x * a.tiles_y;
   if (a.num_work <= 0) return;
   p.grid = a.num_work < num_sms() ? a.num_work : num_sms();
+  if (Hp != p.inm_Hp || Wp != p.inm_Wp || L[0] != p.inm_ptr[0] || L[1] != p.inm_ptr[1] || L[2] != p.inm_ptr[2] ||
+      L[3] != p.inm_ptr[3]) {
+    for (int l = 0; l < 4; ++l) {
+      p.inm_ptr[l] = L[l];
+      if (L[l]) encode_level_map(&p.inm.m[l], L[l], Hp >> l, Wp >> l);
+    }
+    p.inm_Hp = Hp;
+    p.inm_Wp = Wp;
+  }
   static unsigned long long* sdbg = nullptr;
   const bool dbg = (exp_int("OMNISEG_DBG") & 8) != 0;
   if (dbg && !sdbg) OS_CUDA(cudaMalloc(&sdbg, 148 * 4 * 8));

@@ -2352,6 +2352,16 @@ struct StemArgs {
   unsigned long long* dbg_out;  // experiments (OMNISEG_DBG & 8): MMA-warp cycle counters
 };
 
+// TMA maps of the four RGBX levels (u32 elements, dims {Wp/f, Hp/f}, box {kStemBoxW, R + 2}):
+// the stem's input ring is filled by TMA (window halo included, image-edge OOB -> 0).
+struct StemInMaps {
+  CUtensorMap m[4];
+};
+// 136 pixels: the 128-pixel tile + the 3x3 halo, started 4 pixels early -- a tiled TMA box must
+// start 16-byte aligned in its innermost dimension (measured: a start at -1 faults with an
+// illegal instruction, scripts/micro/tma_u32_box.cu), so the box covers [x0 - 4, x0 + 132)
+constexpr int kStemBoxW = 136;
+
 template <int BN, int R, int NA>
 struct StemSmem {
   // K = 48: the 3x3 window's 9 pixels x RGBX (k = (dy*3 + dx)*4 + c, X and k >= 36 weighted 0),
@@ -2361,11 +2371,15 @@ struct StemSmem {
   static constexpr int kB = kKC * BN * 16;       // [kc][BN][16 B]
   static constexpr int kCH = BN < 32 ? BN : 32;  // output box width (make_stem_plan's maps)
   static constexpr int kBOff = NA * kA;
-  static constexpr int kBarOff = ((kBOff + kB + 1023) / 1024) * 1024;
+  // TMA input ring: kNI items of (R + 2) rows x kStemBoxW RGBX words
+  static constexpr int kNI = 6;
+  static constexpr int kIn = (((R + 2) * kStemBoxW * 4) + 127) / 128 * 128;
+  static constexpr int kInOff = ((kBOff + kB + 127) / 128) * 128;
+  static constexpr int kBarOff = ((kInOff + kNI * kIn + 1023) / 1024) * 1024;
   // epilogue warps: 16 for 32 channels (one output row each per 4-row item), else 8
   static constexpr int kEW = (BN == 32 && R == 4) ? 16 : 8;
   static constexpr int kThreads = 256 + 32 * kEW;
-  static constexpr int kBars = (2 * NA + 4 + 2 * kEW) * 8 + 16;
+  static constexpr int kBars = (2 * NA + 2 * kNI + 4 + 2 * kEW) * 8 + 16;
   static constexpr int kEpiOff = ((kBarOff + kBars + 1023) / 1024) * 1024;
   static constexpr int kTotal = kEpiOff + kEW * 3 * EpiTile<kCH>::kBuf + 1024;
   static constexpr uint32_t kTmemCols = (2 * R * BN <= 32) ? 32 : (2 * R * BN <= 64) ? 64 : (2 * R * BN <= 128) ? 128
@@ -2375,7 +2389,9 @@ struct StemSmem {
 template <typename T, int BN, int R, int NA>
 __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
     stem_tc_kernel(const __grid_constant__ CUtensorMap tmO, const __grid_constant__ StemArgs args,
-                   const __grid_constant__ LoMaps lo) {
+                   const __grid_constant__ LoMaps lo, const __grid_constant__ CUtensorMap in0,
+                   const __grid_constant__ CUtensorMap in1, const __grid_constant__ CUtensorMap in2,
+                   const __grid_constant__ CUtensorMap in3) {
   using S = StemSmem<BN, R, NA>;
   constexpr int CH = S::kCH;
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
@@ -2386,7 +2402,9 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
   uint64_t* tfull = aempty + NA;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;  // unused by the output-only epilogue (EpiState needs the slots)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * S::kEW);
+  uint64_t* infull = rbar + 2 * S::kEW;
+  uint64_t* inempty = infull + S::kNI;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inempty + S::kNI);
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   const int tid = threadIdx.x;
@@ -2400,6 +2418,10 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
       ptx::mbar_init(&tempty[a], 32 * S::kEW);
     }
     for (int a = 0; a < 2 * S::kEW; ++a) ptx::mbar_init(&rbar[a], 1);
+    for (int i = 0; i < S::kNI; ++i) {
+      ptx::mbar_init(&infull[i], 1);
+      ptx::mbar_init(&inempty[i], 4);  // one arrival per converter warp
+    }
     ptx::fence_barrier_init();
   }
   // weights -> smem B operand (no-swizzle K-major: [kc][n][8 x 16-bit])
@@ -2419,46 +2441,38 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
 
   if (warp < 4) {
     // ------------------------------------------ im2col converters: thread = output pixel
+    // The (R+2) x 130 RGBX neighbourhood of the item arrives in the TMA input ring (producer:
+    // warp 6, kNI items ahead); each thread reads its (R+2) x 3 words from shared memory,
+    // applies the window's zero padding and releases the slot.
     const int px = tid;
     int stage = 0;
     uint32_t phase = 0;
-    // the (R+2) x 3 RGBX neighbourhood of this pixel's R output rows; the NEXT work item's
-    // loads are issued before this item is converted (software pipelining: a load-use chain
-    // per item left the converters latency-bound)
-    auto fetch = [&](int w, uint32_t (&win)[R + 2][3]) {
+    int istage = 0;
+    uint32_t iphase = 0;
+    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
       const int tx = w % args.tiles_x;
-      int m = w / args.tiles_x;
-      const int tyg = m % args.tiles_y;
-      const int b = m / args.tiles_y;
-      const uint32_t id = __ldg(args.tiles + args.first + b);
-      const int lf = id >> 30, f = 1 << lf;
-      const int Ex = args.Wp / f, Ey = args.Hp / f;
-      const int oy = min((int)((id >> 15) & 0x7FFF) * args.S, Ey - args.P);
-      const int ox = min((int)(id & 0x7FFF) * args.S, Ex - args.P);
-      const uint32_t* L = args.L[lf];
+      const int tyg = (w / args.tiles_x) % args.tiles_y;
       const int x = tx * 128 + px;  // window column
       const int y0 = tyg * R;
+      uint32_t win[R + 2][3];
+      ptx::mbar_wait(&infull[istage], iphase);
+      const uint32_t* in = reinterpret_cast<const uint32_t*>(smem + S::kInOff + istage * S::kIn);
 #pragma unroll
       for (int i = 0; i < R + 2; ++i) {
         const int yy = y0 + i - 1;
 #pragma unroll
         for (int dx = 0; dx < 3; ++dx) {
           const int xx = x + dx - 1;
-          win[i][dx] = (yy >= 0 && yy < args.P && xx >= 0 && xx < args.P)
-                           ? __ldg(L + (int64_t)(oy + yy) * Ex + (ox + xx))
-                           : 0u;  // the window's zero padding
+          const uint32_t v = in[i * kStemBoxW + px + dx + 3];  // box column 0 = window column x0 - 4
+          win[i][dx] = (yy >= 0 && yy < args.P && xx >= 0 && xx < args.P) ? v : 0u;  // window zero padding
         }
       }
-    };
-    uint32_t nxt[R + 2][3];
-    if ((int)blockIdx.x < args.num_work) fetch(blockIdx.x, nxt);
-    for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
-      uint32_t win[R + 2][3];
-#pragma unroll
-      for (int i = 0; i < R + 2; ++i)
-#pragma unroll
-        for (int dx = 0; dx < 3; ++dx) win[i][dx] = nxt[i][dx];
-      if (w + (int)gridDim.x < args.num_work) fetch(w + gridDim.x, nxt);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&inempty[istage]);
+      if (++istage == S::kNI) {
+        istage = 0;
+        iphase ^= 1;
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         ptx::mbar_wait(&aempty[stage], phase ^ 1);
@@ -2490,6 +2504,33 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
         if (++stage == NA) {
           stage = 0;
           phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 6) {
+    // ------------------------------------------ TMA producer of the input ring
+    if (lane == 0) {
+      int istage = 0;
+      uint32_t iphase = 0;
+      constexpr uint32_t kTx = (R + 2) * kStemBoxW * 4;
+      for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
+        const int tx = w % args.tiles_x;
+        int m = w / args.tiles_x;
+        const int tyg = m % args.tiles_y;
+        const int b = m / args.tiles_y;
+        const uint32_t id = __ldg(args.tiles + args.first + b);
+        const int lf = id >> 30, f = 1 << lf;
+        const int oy = min((int)((id >> 15) & 0x7FFF) * args.S, args.Hp / f - args.P);
+        const int ox = min((int)(id & 0x7FFF) * args.S, args.Wp / f - args.P);
+        ptx::mbar_wait(&inempty[istage], iphase ^ 1);
+        ptx::mbar_arrive_expect_tx(&infull[istage], kTx);
+        // static addresses of the __grid_constant__ maps (a dynamic index would copy the
+        // parameter struct to local memory, where TMA cannot read a tensor map)
+        const CUtensorMap* mp = lf == 0 ? &in0 : lf == 1 ? &in1 : lf == 2 ? &in2 : &in3;
+        ptx::tma_load_2d(smem + S::kInOff + istage * S::kIn, mp, &infull[istage], ox + tx * 128 - 4, oy + tyg * R - 1);
+        if (++istage == S::kNI) {
+          istage = 0;
+          iphase ^= 1;
         }
       }
     }
