@@ -40,12 +40,12 @@ CUtensorMapSwizzle swz(int bytes) {
   return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
 }
 
-template <typename T, int BN, int BK, int MODE>
+template <typename T, int BN, int BK, int MODE, int CL = 1>
 struct Cfg {
-  static constexpr int kStageBytes = ConvSmem<BN, BK, 1, MODE>::kStage;
+  static constexpr int kStageBytes = ConvSmem<BN, BK, 1, MODE, CL>::kStage;
   static constexpr int kStages0 = (MODE == kUpAdd ? kStageBudgetTapUp : kStageBudgetTap) / kStageBytes;
   static constexpr int STAGES = kStages0 > 8 ? 8 : (kStages0 < 2 ? 2 : kStages0);
-  using Smem = ConvSmem<BN, BK, STAGES, MODE>;
+  using Smem = ConvSmem<BN, BK, STAGES, MODE, CL>;
 };
 
 template <typename T, int BN, int BK>
@@ -83,14 +83,17 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
     OS_CUDA(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo));
   };
   if constexpr (BN == 256) {
-    if (p.cl == 2) {
+    if (p.cl == 2) {  // CTA pair (cta_group::2): half the B rows per CTA -> a deeper ring
+      using P0 = Cfg<T, BN, BK, kReluBias, 2>;
+      using P1 = Cfg<T, BN, BK, kResidualRelu, 2>;
+      using P3 = Cfg<T, BN, BK, kBias, 2>;
       switch (p.mode) {
-        case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, C0::STAGES, kReluBias, 2>, C0::Smem::kTotal, 2); break;
+        case kReluBias: launch_mode(conv_tc_kernel<T, BN, BK, P0::STAGES, kReluBias, 2>, P0::Smem::kTotal, 2); break;
         case kResidualRelu:
-          launch_mode(conv_tc_kernel<T, BN, BK, C1::STAGES, kResidualRelu, 2>, C1::Smem::kTotal, 2);
+          launch_mode(conv_tc_kernel<T, BN, BK, P1::STAGES, kResidualRelu, 2>, P1::Smem::kTotal, 2);
           break;
-        case kUpAdd: launch_mode(conv_tc_kernel<T, BN, BK, CU::STAGES, kUpAdd, 2>, CU::Smem::kTotal, 2); break;
-        default: launch_mode(conv_tc_kernel<T, BN, BK, C3::STAGES, kBias, 2>, C3::Smem::kTotal, 2); break;
+        case kBias: launch_mode(conv_tc_kernel<T, BN, BK, P3::STAGES, kBias, 2>, P3::Smem::kTotal, 2); break;
+        default: throw Error(-1, "CTA-pair conv: unsupported mode");
       }
       return;
     }
@@ -273,6 +276,7 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   p.bk = Cin % 64 == 0 ? 64 : Cin % 32 == 0 ? 32 : 16;
   p.bn = 256;
   while (Cout % p.bn) p.bn >>= 1;
+  if (p.bn == 256 && p.bk == 64 && exp_flag("OMNISEG_TAP_BK32")) p.bk = 32;  // experiment: deeper ring
   const int Ho = (Hin - 1) / stride + 1, Wo = (Win - 1) / stride + 1;
   ConvArgs& a = p.args;
   a.B = B;
@@ -375,9 +379,10 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.res = res;
   a.out = out;
   a.split = split_out;
-  // per-tap 256-channel layers: CTA pairs sharing (multicasting) the weight tiles
-  if (p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bn == 256 && (a.tiles_x * a.tiles_y) % 2 == 0 &&
-      exp_flag("OMNISEG_CLUSTER"))  // opt-in: measured no faster (these layers are tensor-bound)
+  // per-tap 256-channel layers (levels 3-4): CTA pairs (cta_group::2, M = 256), each CTA holding
+  // half of the weight rows; pairs need an even M-tile count per N tile
+  if (p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bn == 256 && mode != kUpAdd &&
+      (a.tiles_x * a.tiles_y) % 2 == 0 && !exp_flag("OMNISEG_NO_PAIR"))
     p.cl = 2;
   // per-tap kernel: 128-channel lo chunks when the K chunk is 64 (one SW128 row like the hi chunks)
   a.lo2 = (f8in && p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bk == 64 && Cin % 128 == 0) ? 1 : 0;

@@ -768,11 +768,12 @@ __host__ __device__ constexpr int tap_epi_warps(int bn, int mode) {
   return (mode == kUpAdd || tap_split8(bn, mode)) ? 8 : 4;
 }
 
-template <int BN, int BK, int STAGES, int MODE = kReluBias>
+template <int BN, int BK, int STAGES, int MODE = kReluBias, int CL = 1>
 struct ConvSmem {
   static constexpr bool UP = MODE == kUpAdd;
   static constexpr int kA = 128 * BK * 2;
-  static constexpr int kB = ((BN * BK * 2 + 1023) / 1024) * 1024;
+  // CL = 2 (CTA pair, cta_group::2): each CTA holds half of the N rows of B
+  static constexpr int kB = ((BN / CL * BK * 2 + 1023) / 1024) * 1024;
   static constexpr int kStage = kA + kB;
   static constexpr int kBars = (2 * STAGES + 4 + 16) * 8 + 16;  // full/empty, tfull/tempty, 2 x 8 epilogue warps
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
@@ -793,17 +794,21 @@ struct ConvSmem {
   static constexpr uint32_t kSBOLo = 8 * BK;
 };
 
-// CL = 2: a cluster of two CTAs processes work items in pairs (two M tiles, the same N tile
-// and K sequence); each CTA loads half of every B (weight) tile and multicasts it to both, and
-// each MMA warp's stage release is multicast to both CTAs' empty barriers -- half the L2 ->
-// SM weight traffic, which bounds the 256-channel layers (measured: their MMA warp waited on
-// loads a third of the time).
+// CL = 2: a CTA pair (cluster of two, cta_group::2) processes work items in pairs (two M
+// tiles, the same N tile and K sequence) as ONE M = 256 MMA: each CTA loads its own 128-pixel
+// A tile and HALF of the B (weight) rows into its own shared memory, both CTAs' TMA bytes
+// complete on the leader's `full` barrier, the leader (rank 0) issues the pair MMAs and
+// multicasts its commits to both CTAs' `empty` / `tfull` barriers, and both epilogues release
+// the accumulators on the leader's `tempty`. Per SM that is 2/3 of the shared-memory fill of
+// the 1-CTA kernel (A + B/2 instead of A + B per K step), which is what bounds the 256-channel
+// layers (measured: their MMA warp waited on loads a third of the time; multicasting B, which
+// halves L2 reads but not the smem fill, did not help).
 template <typename T, int BN, int BK, int STAGES, int MODE, int CL = 1>
 __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
                    const ConvArgs args, const __grid_constant__ LoMaps lo) {
-  using S = ConvSmem<BN, BK, STAGES, MODE>;
+  using S = ConvSmem<BN, BK, STAGES, MODE, CL>;
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
@@ -837,19 +842,24 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
     ptx::tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], CL);  // CL = 2: released by both CTAs' MMA warps
+      ptx::mbar_init(&empty[s], 1);  // CL = 2: the leader's multicast commit arrives in both CTAs
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 32 * EW);
+      ptx::mbar_init(&tempty[a], CL == 2 ? 2 * EW : 32 * EW);  // CL = 2: one arrival per epilogue warp of the pair
     }
     for (int a = 0; a < 2 * EW; ++a) ptx::mbar_init(&rbar[a], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CL == 2)
+      ptx::tmem_alloc_cg2<S::kTmemCols>(tmem_slot);
+    else
+      ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  }
   ptx::tc_fence_before();
   if constexpr (CL == 2)
-    ptx::cluster_sync();  // both CTAs' barriers initialised before any multicast
+    ptx::cluster_sync();  // both CTAs' barriers initialised before any cross-CTA arrive
   else
     __syncthreads();
   ptx::tc_fence_after();
@@ -859,8 +869,9 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
   const int taps = args.ksize * args.ksize;
   const int kct = args.kchunks + args.kch_lo;  // hi chunks, then (F8 input) lo chunks
   const int kiters = taps * kct;
-  constexpr uint32_t kTx = S::kA + BN * BK * 2;
-  constexpr uint32_t kTxLo = 128 * BK + BN * BK;  // F8 lo chunk: BK bytes per row
+  // bytes landing on one K step's `full` barrier (CL = 2: the leader's, from both CTAs)
+  constexpr uint32_t kTx = CL * (S::kA + BN / CL * BK * 2);
+  constexpr uint32_t kTxLo = CL * (128 * BK + BN / CL * BK);  // F8 lo chunk: BK bytes per row
 
   if (warp == 0) {
     if (lane == 0) {
@@ -886,25 +897,31 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
             ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStage;
           uint8_t* sb = sa + S::kA;
-          if (kc < args.kchunks) {
+          if constexpr (CL == 2) {
+            // both CTAs: own A tile + own half of the B rows, completing on the LEADER's barrier;
+            // the leader expects both CTAs' bytes
+            const uint32_t fb = ptx::mapa(&full[stage], 0);
+            if (kc < args.kchunks) {
+              if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+              ptx::tma_load_4d_cg2(sa, &tmA, fb, kc * BK, x0 + dx, y0 + dy, b + args.b_in);
+              ptx::tma_load_2d_cg2(sb, &tmB, fb, tap * args.Cin + kc * BK, nt * BN + crank * (BN / 2));
+            } else {
+              const int kl = kc - args.kchunks, kw = args.lo2 ? 2 * BK : BK;
+              if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], args.lo2 ? 2 * kTxLo : kTxLo);
+              ptx::tma_load_4d_cg2(sa, &lo.A, fb, kl * kw, x0 + dx, y0 + dy, b + args.b_in);
+              ptx::tma_load_2d_cg2(sb, &lo.B, fb, tap * args.Cin + kl * kw, nt * BN + crank * (BN / 2));
+            }
+          } else if (kc < args.kchunks) {
             ptx::mbar_arrive_expect_tx(&full[stage], kTx);
             ptx::tma_load_4d(sa, &tmA, &full[stage], kc * BK, x0 + dx, y0 + dy, b + args.b_in);
-            if constexpr (CL == 2)
-              ptx::tma_load_2d_mc(sb + crank * (BN / 2) * BK * 2, &tmB, &full[stage], tap * args.Cin + kc * BK,
-                                  nt * BN + crank * (BN / 2), 0x3);
-            else
-              ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
+            ptx::tma_load_2d(sb, &tmB, &full[stage], tap * args.Cin + kc * BK, nt * BN);
           } else {
             // lo chunk: BK e4m3 channels (BK-byte rows), or 2 BK (lo2: 128-byte rows, as many TMA
             // rows as a hi chunk for twice the MMAs of a BK-wide lo chunk)
             const int kl = kc - args.kchunks, kw = args.lo2 ? 2 * BK : BK;
             ptx::mbar_arrive_expect_tx(&full[stage], args.lo2 ? 2 * kTxLo : kTxLo);
             ptx::tma_load_4d(sa, &lo.A, &full[stage], kl * kw, x0 + dx, y0 + dy, b + args.b_in);
-            if constexpr (CL == 2)
-              ptx::tma_load_2d_mc(sb + crank * (BN / 2) * kw, &lo.B, &full[stage], tap * args.Cin + kl * kw,
-                                  nt * BN + crank * (BN / 2), 0x3);
-            else
-              ptx::tma_load_2d(sb, &lo.B, &full[stage], tap * args.Cin + kl * kw, nt * BN);
+            ptx::tma_load_2d(sb, &lo.B, &full[stage], tap * args.Cin + kl * kw, nt * BN);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -914,10 +931,11 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
       }
     }
   } else if (warp == 1) {
-    {
-      // ------------------------------------------------------------ MMA issuer (warp-collective)
-      constexpr uint32_t idesc = ptx::idesc_f16(128, BN, std::is_same<T, __nv_bfloat16>::value);
-      constexpr uint32_t idesc8 = ptx::idesc_f8(128, BN);
+    if (CL == 1 || crank == 0) {
+      // ------------------------------------------------------------ MMA issuer (warp-collective;
+      // CL = 2: the leader issues M = 256 pair MMAs)
+      constexpr uint32_t idesc = ptx::idesc_f16(128 * CL, BN, std::is_same<T, __nv_bfloat16>::value);
+      constexpr uint32_t idesc8 = ptx::idesc_f8(128 * CL, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -942,7 +960,10 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBO, S::kLayout);
               const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBO, S::kLayout);
-              ptx::mma_f16_w(d_tmem, da, db, idesc, (it | k) != 0);
+              if constexpr (CL == 2)
+                ptx::mma_f16_cg2_w(d_tmem, da, db, idesc, (it | k) != 0);
+              else
+                ptx::mma_f16_w(d_tmem, da, db, idesc, (it | k) != 0);
             }
           } else if (BK == 64 && args.lo2) {
             // F8 lo chunk of 2 BK = 128 channels: 128-byte rows (SW128), 32 K per MMA
@@ -950,7 +971,10 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
             for (int k = 0; k < 4; ++k) {
               const uint64_t da = ptx::smem_desc(sa + k * 32, 1024, 2u);
               const uint64_t db = ptx::smem_desc(sb + k * 32, 1024, 2u);
-              ptx::mma_f8_w(d_tmem, da, db, idesc8, 1u);
+              if constexpr (CL == 2)
+                ptx::mma_f8_cg2_w(d_tmem, da, db, idesc8, 1u);
+              else
+                ptx::mma_f8_w(d_tmem, da, db, idesc8, 1u);
             }
           } else if constexpr (BK >= 32) {
             // F8 lo chunk: BK bytes per row (SW64 / SW32), 32 K per MMA
@@ -958,11 +982,14 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
             for (int k = 0; k < BK / 32; ++k) {
               const uint64_t da = ptx::smem_desc(sa + k * 32, S::kSBOLo, S::kLayoutLo);
               const uint64_t db = ptx::smem_desc(sb + k * 32, S::kSBOLo, S::kLayoutLo);
-              ptx::mma_f8_w(d_tmem, da, db, idesc8, 1u);
+              if constexpr (CL == 2)
+                ptx::mma_f8_cg2_w(d_tmem, da, db, idesc8, 1u);
+              else
+                ptx::mma_f8_w(d_tmem, da, db, idesc8, 1u);
             }
           }
           if constexpr (CL == 2)
-            ptx::mma_commit_mc_w(&empty[stage], 0x3);
+            ptx::mma_commit_cg2_mc_w(&empty[stage], 0x3);
           else
             ptx::mma_commit_w(&empty[stage]);
           if (++stage == STAGES) {
@@ -970,7 +997,10 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
             phase ^= 1;
           }
         }
-        ptx::mma_commit_w(&tfull[acc]);
+        if constexpr (CL == 2)
+          ptx::mma_commit_cg2_mc_w(&tfull[acc], 0x3);
+        else
+          ptx::mma_commit_w(&tfull[acc]);
       }
       if (OS_EXP && (args.dbg & 8) && lane == 0) {
         args.dbg_out[blockIdx.x * 4 + 0] = OS_CLK() - t_start;
@@ -1193,18 +1223,26 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
+      if constexpr (CL == 2) {  // one arrival per warp on the leader's barrier
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&tempty[acc], 0));
+      } else {
+        ptx::mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
   if constexpr (CL == 2)
-    ptx::cluster_sync();  // no CTA leaves while its peer may still multicast into it
+    ptx::cluster_sync();  // no CTA leaves while its peer may still signal or read it
   else
     __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
+    if constexpr (CL == 2)
+      ptx::tmem_dealloc_cg2<S::kTmemCols>(tmem_base);
+    else
+      ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
   }
 }
 
