@@ -82,7 +82,7 @@ void launch_tpl(const ConvPlan& p, cudaStream_t s) {
     cfg.numAttrs = 1;
     OS_CUDA(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.lo));
   };
-  if constexpr (BN == 256) {
+  if constexpr (BN == 256 || BN == 128) {
     if (p.cl == 2) {  // CTA pair (cta_group::2): half the B rows per CTA -> a deeper ring
       using P0 = Cfg<T, BN, BK, kReluBias, 2>;
       using P1 = Cfg<T, BN, BK, kResidualRelu, 2>;
@@ -379,9 +379,10 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   a.res = res;
   a.out = out;
   a.split = split_out;
-  // per-tap 256-channel layers (levels 3-4): CTA pairs (cta_group::2, M = 256), each CTA holding
-  // half of the weight rows; pairs need an even M-tile count per N tile
-  if (p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && p.bn == 256 && mode != kUpAdd &&
+  // per-tap layers with 256 / 128-wide N tiles (levels 3-4, the down convs): CTA pairs
+  // (cta_group::2, M = 256), each CTA holding half of the weight rows; pairs need an even M-tile
+  // count per N tile
+  if (p.nz_R == 0 && p.s2_R == 0 && p.rows_R == 0 && (p.bn == 256 || p.bn == 128) && mode != kUpAdd &&
       (a.tiles_x * a.tiles_y) % 2 == 0 && !exp_flag("OMNISEG_NO_PAIR"))
     p.cl = 2;
   // per-tap kernel: 128-channel lo chunks when the K chunk is 64 (one SW128 row like the hi chunks)
