@@ -156,6 +156,40 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
     }
     kern<<<p.grid, threads, smem, s>>>(p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head, p.lo);
   };
+  if constexpr (BN == 128 && !DYF) {
+    if (p.cl == 2) {  // CTA pair (cta_group::2), cluster (2, 1, 1)
+      constexpr int ST2 = NzCfg::STAGES_CL2(BN, 0), STR2 = NzCfg::STAGES_CL2(BN, 1);
+      auto go2 = [&](auto kern, int sm) {
+        static std::mutex mu;
+        static std::unordered_set<const void*> done;
+        {
+          std::lock_guard<std::mutex> g(mu);
+          if (done.insert(reinterpret_cast<const void*>(kern)).second)
+            OS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(p.grid);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        OS_CUDA(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head, p.lo));
+      };
+      if (p.mode == kReluBias)
+        go2(conv3_nz_kernel<T, BN, R, ST2, kReluBias, false, 2>, NzSmem<BN, R, ST2, false, 8, 0, 2>::kTotal);
+      else if (p.mode == kResidualRelu)
+        go2(conv3_nz_kernel<T, BN, R, STR2, kResidualRelu, false, 2>, NzSmem<BN, R, STR2, false, 8, 1, 2>::kTotal);
+      else
+        throw Error(-1, "nz CTA pair: unsupported mode");
+      return;
+    }
+  }
   switch (p.mode) {
     case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;
     case kResidualRelu: go(conv3_nz_kernel<T, BN, R, STR, kResidualRelu, DYF>); break;
@@ -357,6 +391,11 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
     a.kchunks = Cin / 16;
     a.kch_lo = f8in ? Cin / 32 : 0;
     a.tiles_y /= R;
+    // 128-channel layers (level 2): CTA pairs (cta_group::2) with half the weight image per CTA;
+    // the image is built in the pair layout and read through a 3-D map (build_conv_wimage)
+    if (p.bn == 128 && (mode == kReluBias || mode == kResidualRelu) && (a.tiles_x * a.tiles_y) % 2 == 0 &&
+        !exp_flag("OMNISEG_NO_PAIR"))
+      p.cl = 2;
   }
   // multi-row variant for 3x3 stride-1 convs with N <= 128 (see conv3_rows_kernel)
   if (p.nz_R == 0 && k == 3 && stride == 1 && mode != kUpAdd && p.bn <= 128 && (a.hb == 1 || a.hb == 2) &&
@@ -530,7 +569,7 @@ struct SlotMap {
 };
 // one thread per (n tile, K step, slot, row n, 16-B half j)
 __global__ void wimage_kernel(const uint8_t* w16, const uint8_t* wlo, uint8_t* dst, int ntn, int BN, int taps_cin,
-                              int Cin, int khi, int klo, SlotMap sm) {
+                              int Cin, int khi, int klo, SlotMap sm, int cl) {
   const int nks = khi + klo;
   const int64_t total = (int64_t)ntn * nks * 9 * BN * 2;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -546,7 +585,9 @@ __global__ void wimage_kernel(const uint8_t* w16, const uint8_t* wlo, uint8_t* d
   const int co = nt * BN + n, tap = sm.tap[slot];
   const uint8_t* src = ks < khi ? w16 + ((int64_t)co * taps_cin + (int64_t)tap * Cin + 16 * ks + 8 * j) * 2
                                 : wlo + (int64_t)co * taps_cin + (int64_t)tap * Cin + 32 * (ks - khi) + 16 * j;
-  uint8_t* d = dst + (((int64_t)nt * nks + ks) * 9 + slot) * BN * 32 + n * 32 + 16 * (j ^ ((n >> 2) & 1));
+  // cl = 2 (CTA pair): [nt][ks][half][slot][n % (BN/2)][32 B], each CTA's half of a K step contiguous
+  const int bnh = BN / cl, hf = n / bnh, nl = n - hf * bnh;
+  uint8_t* d = dst + ((((int64_t)nt * nks + ks) * cl + hf) * 9 + slot) * bnh * 32 + nl * 32 + 16 * (j ^ ((nl >> 2) & 1));
   *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(src);
 }
 }  // namespace
@@ -571,9 +612,22 @@ void build_conv_wimage(ConvPlan& p, const void* w, const void* w_lo, void* dst, 
   const int64_t total = (int64_t)bytes / 16;
   wimage_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
       static_cast<const uint8_t*>(w), static_cast<const uint8_t*>(w_lo), static_cast<uint8_t*>(dst),
-      p.args.n_tiles_n, p.bn, 9 * p.args.Cin, p.args.Cin, p.args.kchunks, p.args.kch_lo, sm);
+      p.args.n_tiles_n, p.bn, 9 * p.args.Cin, p.args.Cin, p.args.kchunks, p.args.kch_lo, sm, p.cl);
   OS_CUDA(cudaGetLastError());
   p.args.wimg = static_cast<const uint8_t*>(dst);
+  if (p.cl == 2 && p.nz_R > 0) {
+    // 3-D view {32 B, BN/2 rows, planes} of the pair-layout image; box = one CTA's 9 tap slots
+    const int bnh = p.bn / 2;
+    const uint64_t planes = (uint64_t)p.args.n_tiles_n * (p.args.kchunks + p.args.kch_lo) * 2 * 9;
+    cuuint64_t dims[3] = {32, (cuuint64_t)bnh, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {32, (cuuint64_t)bnh * 32};
+    cuuint32_t box[3] = {32, (cuuint32_t)bnh, 9};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, dst, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(weight image pair) failed: " + std::to_string((int)r));
+  }
 }
 
 constexpr int kStemR = 4, kStemNA = 8;

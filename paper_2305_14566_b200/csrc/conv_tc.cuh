@@ -1504,7 +1504,7 @@ __global__ void __launch_bounds__(256, 1)
 // output). Weights: 9 per-tap SW32 boxes per chunk, shared by the R blocks.
 // EK: epilogue kind -- 0 output only (two compact output slots, 3 kBuf per warp), 1 output +
 // residual (6 kBuf), 2 fused head (residual slots only, 4 kBuf).
-template <int BN, int R, int STAGES, bool DYF = false, int EW = 8, int EK = 0>
+template <int BN, int R, int STAGES, bool DYF = false, int EW = 8, int EK = 0, int CL = 1>
 struct NzSmem {
   static constexpr bool HEAD = EK == 2;
   static constexpr int kPx = 144;                                   // 18 units of 8 pixels
@@ -1514,7 +1514,8 @@ struct NzSmem {
   static constexpr int kA = ((kABytes + 1023) / 1024) * 1024;
   // one tap's BN x 16-channel weight tile (SW32); the dy-stacked variant packs the three dy
   // tiles of one dx back to back, so they must be exactly BN*32 bytes apart
-  static constexpr int kBt = BN * 32;  // tap slots back to back (one bulk copy per K step)
+  // tap slots back to back (one bulk copy per K step); CL = 2 (CTA pair): this CTA's half of N
+  static constexpr int kBt = BN / CL * 32;
   static constexpr int kStage = kA + ((9 * kBt + 1023) / 1024) * 1024;
   static constexpr int kBars = (2 * STAGES + 24) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
@@ -1545,8 +1546,12 @@ struct NzCfg {
   static constexpr int R(int bn) { return 256 / bn < 8 ? 256 / bn : 8; }
   static constexpr int RTC = 4;
   static constexpr bool tc(int bn, int ek, int r) { return ek == 2 && bn <= 32 && r == RTC; }
-  static constexpr int stage_bytes(int bn, int r) {
-    return (((r + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + ((9 * bn * 32 + 1023) / 1024) * 1024;
+  static constexpr int stage_bytes(int bn, int r, int cl = 1) {
+    return (((r + 2) * 2 * 144 * 16 + 1023) / 1024) * 1024 + ((9 * (bn / cl) * 32 + 1023) / 1024) * 1024;
+  }
+  // CTA pairs (CL = 2): half the weight image per stage
+  static constexpr int STAGES_CL2(int bn, int ek) {
+    return budget(bn, ek, R(bn)) / stage_bytes(bn, R(bn), 2) > 6 ? 6 : budget(bn, ek, R(bn)) / stage_bytes(bn, R(bn), 2);
   }
   // ring depth from what the 8 epilogue warps (kind ek, see NzSmem) leave of 227 KB
   static constexpr int STAGES(int bn, int ek, int r) {
@@ -1562,7 +1567,7 @@ struct NzCfg {
 
 // The MMAs of one 32-byte K chunk of conv3_nz_kernel (warp-collective issue). F8: the lo
 // chunk (e4m3 activations x e5m2 weights, kind::f8f6f4); otherwise 16-bit (kind::f16).
-template <int BN, int R, bool DYF, bool F8, bool BF, typename S>
+template <int BN, int R, bool DYF, bool F8, bool BF, typename S, int CL = 1>
 __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int kc) {
   if constexpr (DYF) {
 #pragma unroll
@@ -1592,10 +1597,16 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
       for (int r = 0; r < R; ++r) {
         const uint32_t a0 = sa + (uint32_t)((r + dy) * S::kRowStride + (7 + dx) * 16);
         const uint64_t da = ptx::smem_desc_noswz(a0, S::kChunkStride, 128);
-        if constexpr (F8)
+        if constexpr (CL == 2) {  // CTA pair: M = 256 over both CTAs' A tiles, N = BN over their B halves
+          if constexpr (F8)
+            ptx::mma_f8_cg2_w(d_base + r * BN, da, db, ptx::idesc_f8(256, BN), 1u);
+          else
+            ptx::mma_f16_cg2_w(d_base + r * BN, da, db, ptx::idesc_f16(256, BN, BF), (kc | tap) != 0);
+        } else if constexpr (F8) {
           ptx::mma_f8_w(d_base + r * BN, da, db, ptx::idesc_f8(128, BN), 1u);
-        else
+        } else {
           ptx::mma_f16_w(d_base + r * BN, da, db, ptx::idesc_f16(128, BN, BF), (kc | tap) != 0);
+        }
       }
     }
   }
@@ -1608,7 +1619,7 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
 // accumulators first-written by different MMAs, they are zeroed by the epilogue
 // (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
 // tensor-core operand traffic than one MMA per (tap, row).
-template <typename T, int BN, int R, int STAGES, int MODE, bool DYF>
+template <typename T, int BN, int R, int STAGES, int MODE, bool DYF, int CL = 1>
 __global__ void __launch_bounds__(384, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
@@ -1619,8 +1630,22 @@ __global__ void __launch_bounds__(384, 1)
   // sub-partition leaves the epilogue latency-bound (measured: it, not the loads or MMAs, set
   // the pace of the thin layers)
   constexpr int EW = 8;
-  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? 2 : MODE == kResidualRelu ? 1 : 0>;
+  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? 2 : MODE == kResidualRelu ? 1 : 0, CL>;
   static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
+  // CL = 2: CTA pair (cta_group::2, see conv_tc_kernel): items in pairs (two M items, one N tile),
+  // each CTA's A rows + its half of the weight image complete on the leader's `full` barrier
+  static_assert(CL == 1 || (!DYF && MODE != kHeadFused), "CTA pairs: plain multi-row layers only");
+  const uint32_t crank = CL == 2 ? ptx::cluster_ctarank() : 0;
+  auto decode = [&](int w, int& nt, int& m) {
+    if constexpr (CL == 2) {
+      const int pp = w >> 1;
+      nt = pp % args.n_tiles_n;
+      m = 2 * (pp / args.n_tiles_n) + (w & 1);
+    } else {
+      nt = w % args.n_tiles_n;
+      m = w / args.n_tiles_n;
+    }
+  };
   static_assert(S::kTotal <= 227 * 1024, "shared memory");
   static_assert(2 * R * BN <= 512, "TMEM");
   extern __shared__ uint8_t smem_raw[];
@@ -1642,7 +1667,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 32 * EW);
+      ptx::mbar_init(&tempty[a], CL == 2 ? 2 * EW : 32 * EW);
     }
     for (int a = 0; a < 2 * EW; ++a) ptx::mbar_init(&rbar[a], 1);
     if constexpr (S::kTc) {
@@ -1651,22 +1676,30 @@ __global__ void __launch_bounds__(384, 1)
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CL == 2)
+      ptx::tmem_alloc_cg2<S::kTmemCols>(tmem_slot);
+    else
+      ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // 32-byte K chunks: kchunks hi chunks (16 fp16 channels), then kch_lo F8 lo chunks (32 e4m3)
   const int kiters = args.kchunks + args.kch_lo;
-  constexpr uint32_t kTx = S::kABytes + 9 * BN * 32;
+  constexpr uint32_t kTx = CL * (S::kABytes + 9 * S::kBt);
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
-        const int nt = w % args.n_tiles_n;
-        int m = w / args.n_tiles_n;
+        int nt, m;
+        decode(w, nt, m);
         const int tx = m % args.tiles_x;
         m /= args.tiles_x;
         const int tyg = m % args.tiles_y;
@@ -1689,12 +1722,22 @@ __global__ void __launch_bounds__(384, 1)
             }
             continue;
           }
-          ptx::mbar_arrive_expect_tx(&full[stage], kTx);
-          // chunks 2kc, 2kc+1 of the RC input: hi chunks first, then (F8) the lo chunks
-          ptx::tma_load_5d(sa, &tmA, &full[stage], 0, u0, 2 * kc, y0, b + args.b_in);
           (void)hi;
           (void)kk;
-          ptx::bulk_load(sa + S::kA, args.wimg + ((size_t)nt * kiters + kc) * 9 * BN * 32, 9 * BN * 32, &full[stage]);
+          if constexpr (CL == 2) {
+            // own A rows + own half of the K step's weight image (3-D map {32 B, BN/2 rows, 9
+            // tap planes} over the pair-layout image, tmB) -> the leader's barrier
+            const uint32_t fb = ptx::mapa(&full[stage], 0);
+            if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+            ptx::tma_load_5d_cg2(sa, &tmA, fb, 0, u0, 2 * kc, y0, b + args.b_in);
+            ptx::tma_load_3d_cg2(sa + S::kA, &tmB, fb, 0, 0, (((nt * kiters + kc) * 2) + (int)crank) * 9);
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+            // chunks 2kc, 2kc+1 of the RC input: hi chunks first, then (F8) the lo chunks
+            ptx::tma_load_5d(sa, &tmA, &full[stage], 0, u0, 2 * kc, y0, b + args.b_in);
+            ptx::bulk_load(sa + S::kA, args.wimg + ((size_t)nt * kiters + kc) * 9 * BN * 32, 9 * BN * 32,
+                           &full[stage]);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1703,7 +1746,8 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    {  // MMA issuer (warp-collective; the hi/lo kind branch is per chunk, outside the MMA loops)
+    if (CL == 1 || crank == 0) {  // MMA issuer (warp-collective; the hi/lo kind branch is per
+                                  // chunk, outside the MMA loops; CL = 2: the leader only)
       constexpr bool kBf = std::is_same<T, __nv_bfloat16>::value;
       int stage = 0;
       uint32_t phase = 0;
@@ -1725,17 +1769,23 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t sa = ptx::smem_u32(smem + stage * S::kStage);
           if (OS_EXP && (args.dbg & 2)) {
           } else if (kc >= args.kchunks) {  // F8 lo chunk: same smem image, kind::f8f6f4
-            nz_mma_chunk<BN, R, DYF, true, kBf, S>(sa, d_base, kc);
+            nz_mma_chunk<BN, R, DYF, true, kBf, S, CL>(sa, d_base, kc);
           } else {
-            nz_mma_chunk<BN, R, DYF, false, kBf, S>(sa, d_base, kc);
+            nz_mma_chunk<BN, R, DYF, false, kBf, S, CL>(sa, d_base, kc);
           }
-          ptx::mma_commit_w(&empty[stage]);
+          if constexpr (CL == 2)
+            ptx::mma_commit_cg2_mc_w(&empty[stage], 0x3);
+          else
+            ptx::mma_commit_w(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit_w(&tfull[acc]);
+        if constexpr (CL == 2)
+          ptx::mma_commit_cg2_mc_w(&tfull[acc], 0x3);
+        else
+          ptx::mma_commit_w(&tfull[acc]);
       }
       c_all = OS_CLK() - t_start;
       if (OS_EXP && (args.dbg & 8) && lane == 0) {
@@ -1797,8 +1847,8 @@ __global__ void __launch_bounds__(384, 1)
     int local = 0;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
-      const int nt = w % args.n_tiles_n;
-      int m = w / args.n_tiles_n;
+      int nt, m;
+      decode(w, nt, m);
       const int tx = m % args.tiles_x;
       m /= args.tiles_x;
       const int tyg = m % args.tiles_y;
@@ -2041,15 +2091,26 @@ __global__ void __launch_bounds__(384, 1)
         ptx::tmem_st_wait();
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
+      if constexpr (CL == 2) {  // one arrival per warp on the leader's barrier
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&tempty[acc], 0));
+      } else {
+        ptx::mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
+    if constexpr (CL == 2)
+      ptx::tmem_dealloc_cg2<S::kTmemCols>(tmem_base);
+    else
+      ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
   }
 }
 
