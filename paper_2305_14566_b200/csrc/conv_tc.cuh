@@ -461,6 +461,40 @@ __device__ __forceinline__ void epi_store(EpiState& es, const CUtensorMap* tmO, 
   }
 }
 
+constexpr int kHeadDescs = 16;  // task descriptors per epilogue warp (tasks of one scale)
+// A task of the item's window scale, compacted per epilogue warp (head_tasks): canvas pointer of
+// window pixel (0, 0), the window rows / columns that land on owned canvas pixels, row pitch.
+struct HeadTask {
+  uint32_t* base;
+  int t, Wt, ylo, yhi, xlo, xhi, pad_;
+};
+
+// Lanes t < ntasks describe task t if it runs at this window's level (lf); the valid ones are
+// compacted in task order into d[0..n) (warp-private shared memory; __syncwarp before use).
+__device__ __forceinline__ int head_tasks(const HeadArgs& ha, int lf, int oy, int ox, HeadTask* d, uint32_t lane) {
+  const int t = (int)lane;
+  const bool on = t < ha.ntasks && ha.tt.log2f[t] == lf;
+  const unsigned m = __ballot_sync(0xffffffffu, on);
+  if (on) {
+    const int f = 1 << lf;
+    const int cy0 = oy - ha.pad / f, cx0 = ox - ha.pad / f;  // canvas coords of window pixel (0, 0)
+    const int Wt = ha.tt.Wt[t];
+    HeadTask h;
+    h.t = t;
+    h.Wt = Wt;
+    h.ylo = max(0, max(ha.tt.row0[t], 0) - cy0);
+    h.yhi = min(ha.tt.Ht[t], ha.tt.row1[t]) - cy0;
+    h.xlo = max(0, -cx0);
+    h.xhi = Wt - cx0;
+    h.base = ha.tt.canvas[t] + ((int64_t)(cy0 - ha.tt.row0[t]) * Wt + cx0);
+    h.pad_ = 0;
+    const int k = __popc(m & ((1u << lane) - 1u));
+    if (k < kHeadDescs) d[k] = h;
+  }
+  __syncwarp();
+  return __popc(m) <= kHeadDescs ? __popc(m) : -1;  // -1: more tasks than descriptors (generic path)
+}
+
 // Fused dynamic head + stitch (MODE kHeadFused, last decoder conv, CH = BN = all C0 channels):
 // D0 = ReLU(acc + b + U0) (the storage-rounded value in plain 16-bit modes, the exact fp32
 // value in x2 modes, i.e. hi + lo to 2^-22), F = precls(D0), then per task of the tile's
@@ -469,7 +503,8 @@ __device__ __forceinline__ void epi_store(EpiState& es, const CUtensorMap* tmO, 
 template <typename T, int CH>
 __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr, const float* bias, int split,
                                          int xb, int yb, int b, uint32_t lane, const HeadArgs& ha, const float* s_w,
-                                         const float* s_b, const float* s_th, int lf, int oy, int ox) {
+                                         const float* s_b, const float* s_th, int lf, int oy, int ox,
+                                         const HeadTask* ht = nullptr, int nht = 0) {
   float v[CH];
   epi_values<T, CH, kHeadFused>(es, slot, taddr, bias, 0, split, lane, v);
   if (!split) {
@@ -500,8 +535,14 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
     for (int o = 0; o < kHead; ++o) ha.out_F[(((int64_t)b * ha.P + y) * ha.P + x) * kHead + o] = F[o];
   }
   const int f = 1 << lf;
-  for (int t = 0; t < ha.ntasks; ++t) {
-    if (ha.tiles && ha.tt.log2f[t] != lf) continue;
+  const int nloop = ht ? nht : ha.ntasks;
+  for (int k = 0; k < nloop; ++k) {
+    int t = k;
+    if (ht) {
+      t = ht[k].t;
+    } else if (ha.tiles && ha.tt.log2f[t] != lf) {
+      continue;
+    }
     // theta in smem with W1 / W2 transposed: [i * 8 + o] (see the theta load)
     const float* th = s_th + t * 156;
     float h1[kHead], h2[kHead];
@@ -551,6 +592,12 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
     z = fmaf(d4.y, h2[5], z);
     z = fmaf(d4.z, h2[6], z);
     z = fmaf(d4.w, h2[7], z);
+    if (ht) {  // the stitch through the item's compacted task descriptor
+      const HeadTask d = ht[k];
+      if (x >= d.xlo && x < d.xhi && y >= d.ylo && y < d.yhi)
+        atomicAdd(d.base + (int64_t)y * d.Wt + x, stitch_value(__frcp_rn(1.0f + __expf(-z)), z, ha.tt.vote));
+      continue;
+    }
     const float p = 1.0f / (1.0f + expf(-z));
     if (ha.out_p) {
       ha.out_p[(((int64_t)b * ha.ntasks + t) * ha.P + y) * ha.P + x] = p;
@@ -562,38 +609,6 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
       }
     }
   }
-}
-
-// A task of the item's window scale, compacted per epilogue warp (head_tasks): canvas pointer of
-// window pixel (0, 0), the window rows / columns that land on owned canvas pixels, row pitch.
-struct HeadTask {
-  uint32_t* base;
-  int t, Wt, ylo, yhi, xlo, xhi, pad_;
-};
-
-// Lanes t < ntasks describe task t if it runs at this window's level (lf); the valid ones are
-// compacted in task order into d[0..n) (warp-private shared memory; __syncwarp before use).
-__device__ __forceinline__ int head_tasks(const HeadArgs& ha, int lf, int oy, int ox, HeadTask* d, uint32_t lane) {
-  const int t = (int)lane;
-  const bool on = t < ha.ntasks && ha.tt.log2f[t] == lf;
-  const unsigned m = __ballot_sync(0xffffffffu, on);
-  if (on) {
-    const int f = 1 << lf;
-    const int cy0 = oy - ha.pad / f, cx0 = ox - ha.pad / f;  // canvas coords of window pixel (0, 0)
-    const int Wt = ha.tt.Wt[t];
-    HeadTask h;
-    h.t = t;
-    h.Wt = Wt;
-    h.ylo = max(0, max(ha.tt.row0[t], 0) - cy0);
-    h.yhi = min(ha.tt.Ht[t], ha.tt.row1[t]) - cy0;
-    h.xlo = max(0, -cx0);
-    h.xhi = Wt - cx0;
-    h.base = ha.tt.canvas[t] + ((int64_t)(cy0 - ha.tt.row0[t]) * Wt + cx0);
-    h.pad_ = 0;
-    d[__popc(m & ((1u << lane) - 1u))] = h;
-  }
-  __syncwarp();
-  return __popc(m);
 }
 
 // The fused head for TWO pixels per thread (rows r0, r1 of the warp's column): every shared
@@ -1517,13 +1532,14 @@ struct NzSmem {
   // tap slots back to back (one bulk copy per K step); CL = 2 (CTA pair): this CTA's half of N
   static constexpr int kBt = BN / CL * 32;
   static constexpr int kStage = kA + ((9 * kBt + 1023) / 1024) * 1024;
-  static constexpr int kBars = (2 * STAGES + 24) * 8 + 16;
+  // full / empty per stage, tfull / tempty x 2, two residual barriers per epilogue warp, + TMEM slot
+  static constexpr int kBars = (2 * STAGES + 4 + 2 * EW) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
   static constexpr int kWarpEpi = (EK == 2 ? 4 : EK == 1 ? 6 : 3) * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
-  static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 + EW * 32 * 32 : 0;
+  static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 + EW * kHeadDescs * 32 : 0;
   // tensor-core dynamic head (fp16 activations, see epi_head_tc): per epilogue half the D0 row
   // as UMMA A operands (128 px x BN channels, fp16 hi and lo, no-swizzle K-major), the item's B
   // operand W1' = W1 Wpre (BN x BN, hi and lo), b1' and one MMA-completion mbarrier per half
@@ -1561,8 +1577,9 @@ struct NzCfg {
   static constexpr int tc_bytes(int bn) { return 8 * 128 * bn * 2 + 2 * bn * bn * 2 + bn * 4 + 64; }
   static constexpr int budget(int bn, int ek, int r) {
     return 227 * 1024 - 3 * 1024 - 8 * (ek == 2 ? 4 : ek == 1 ? 6 : 3) * 32 * (bn < 32 ? bn : 32) * 2 -
-           (ek == 2 ? 7680 + 8192 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
+           (ek == 2 ? 7680 + 8 * kHeadDescs * 32 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
   }
+
 };
 
 // The MMAs of one 32-byte K chunk of conv3_nz_kernel (warp-collective issue). F8: the lo
@@ -1808,7 +1825,7 @@ __global__ void __launch_bounds__(384, 1)
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;
     const float* th_g = nullptr;         // this item's transposed theta rows (global, or s_th)
-    HeadTask* s_ht = reinterpret_cast<HeadTask*>(s_b + kHead) + ew * 32;  // this warp's task descriptors
+    HeadTask* s_ht = reinterpret_cast<HeadTask*>(s_b + kHead) + ew * kHeadDescs;  // this warp's task descriptors
     bool h_ok = false;
     int h_n = 0;
     (void)s_ht;
@@ -2053,7 +2070,7 @@ __global__ void __launch_bounds__(384, 1)
             }
           }
           epi_head2<T, CH>(v0, v1, xb + (int)lane, tyg * R + r0, tyg * R + r1, b + args.b_head, hargs, s_w, s_b, th_g,
-                           lf, oy, ox, h_ok ? s_ht : nullptr, h_n);
+                           lf, oy, ox, h_ok && h_n >= 0 ? s_ht : nullptr, h_n);
         }
       } else
 #pragma unroll 1
@@ -2076,7 +2093,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         } else if constexpr (MODE == kHeadFused) {
           epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs, s_w,
-                          s_b, th_g, lf, oy, ox);
+                          s_b, th_g, lf, oy, ox, h_ok && h_n >= 0 ? s_ht : nullptr, h_n);
         } else {
           epi_chunk<T, CH, MODE>(es, slot, &tmO, &lo.O, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
                                  tyg * R + r, b + args.b_out, lane);
