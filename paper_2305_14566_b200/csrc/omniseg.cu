@@ -813,7 +813,9 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   if (h->inject) OS_CUDA(cudaMemcpyAsync(h->hist.p, h->inj_hist, 256 * 8, cudaMemcpyHostToDevice, s));
   OS_CUDA(cudaMemcpyAsync(h->last_hist, h->hist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
   launch_otsu(h->hist.as<unsigned long long>(), st, s);
-  const bool partial = row0 > 0 || row1 < Hp;
+  // a band call of a multi-rank communicator always takes the exchange path (even a rank whose
+  // band is the whole frame: the other ranks' empty bands join the same all-reduce)
+  const bool partial = row0 > 0 || row1 < Hp || (h->comm && h->world > 1);
   if (h->arch.fgmin > 0 && partial) {
     // Tiny-component removal needs whole components: a band computes the foreground
     // of its OWNED level-8 rows only, the bands' disjoint rows are summed over the ranks
