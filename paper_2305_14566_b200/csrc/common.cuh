@@ -38,6 +38,26 @@ struct Error : std::runtime_error {
 #else
 #define OS_CLK() 0ull
 #endif
+// Bounds-checked build (`scripts/build_variant.sh checks -DOMNISEG_CHECKS=1`; the stand-in for
+// compute-sanitizer, which this GPU pool does not allow): device-side checks of the global
+// writes the atomics / finalize / labelling make; a failure prints the site and traps.
+#ifndef OMNISEG_CHECKS
+#define OMNISEG_CHECKS 0
+#endif
+#if OMNISEG_CHECKS
+#define OS_DCHECK(cond, what)                                                                          \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("OMNISEG_CHECKS failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                       \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define OS_DCHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
 // true iff the experiment build runs with the environment variable `name` set
 bool exp_flag(const char* name);
 int exp_int(const char* name);

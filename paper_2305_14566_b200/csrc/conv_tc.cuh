@@ -495,6 +495,23 @@ __device__ __forceinline__ int head_tasks(const HeadArgs& ha, int lf, int oy, in
   return __popc(m) <= kHeadDescs ? __popc(m) : -1;  // -1: more tasks than descriptors (generic path)
 }
 
+// OMNISEG_CHECKS: the descriptor's bounds and address agree with the direct canvas formula.
+__device__ __forceinline__ void head_check(const HeadArgs& ha, const HeadTask& d, int lf, int oy, int ox, int x, int y,
+                                           bool in) {
+#if OMNISEG_CHECKS
+  const int t = d.t, f = 1 << lf;
+  const int cy = oy + y - ha.pad / f, cx = ox + x - ha.pad / f;
+  const bool ok = cy >= 0 && cy < ha.tt.Ht[t] && cx >= 0 && cx < ha.tt.Wt[t] && cy >= ha.tt.row0[t] &&
+                  cy < ha.tt.row1[t];
+  OS_DCHECK(ok == in, "head stitch: descriptor bounds differ from the canvas formula");
+  if (in)
+    OS_DCHECK(d.base + (int64_t)y * d.Wt + x == ha.tt.canvas[t] + (int64_t)(cy - ha.tt.row0[t]) * ha.tt.Wt[t] + cx,
+              "head stitch: descriptor address differs from the canvas formula");
+#else
+  (void)ha, (void)d, (void)lf, (void)oy, (void)ox, (void)x, (void)y, (void)in;
+#endif
+}
+
 // Fused dynamic head + stitch (MODE kHeadFused, last decoder conv, CH = BN = all C0 channels):
 // D0 = ReLU(acc + b + U0) (the storage-rounded value in plain 16-bit modes, the exact fp32
 // value in x2 modes, i.e. hi + lo to 2^-22), F = precls(D0), then per task of the tile's
@@ -594,8 +611,9 @@ __device__ __forceinline__ void epi_head(EpiState& es, int slot, uint32_t taddr,
     z = fmaf(d4.w, h2[7], z);
     if (ht) {  // the stitch through the item's compacted task descriptor
       const HeadTask d = ht[k];
-      if (x >= d.xlo && x < d.xhi && y >= d.ylo && y < d.yhi)
-        atomicAdd(d.base + (int64_t)y * d.Wt + x, stitch_value(__frcp_rn(1.0f + __expf(-z)), z, ha.tt.vote));
+      const bool in = x >= d.xlo && x < d.xhi && y >= d.ylo && y < d.yhi;
+      head_check(ha, d, lf, oy, ox, x, y, in);
+      if (in) atomicAdd(d.base + (int64_t)y * d.Wt + x, stitch_value(__frcp_rn(1.0f + __expf(-z)), z, ha.tt.vote));
       continue;
     }
     const float p = 1.0f / (1.0f + expf(-z));
@@ -704,6 +722,8 @@ __device__ __forceinline__ void epi_head2(const float (&v0)[CH], const float (&v
     if (ht) {  // the stitch through the item's compacted task descriptor
       const HeadTask d = ht[k];
       const bool xin = x >= d.xlo && x < d.xhi;
+      head_check(ha, d, lf, oy, ox, x, y0, xin && y0 >= d.ylo && y0 < d.yhi);
+      head_check(ha, d, lf, oy, ox, x, y1, xin && y1 >= d.ylo && y1 < d.yhi);
       // sigmoid with the fast exp / reciprocal (relative error ~1e-7, far inside the 2^-20
       // fixed point the stitch rounds to; the vote decision uses z itself)
       if (xin && y0 >= d.ylo && y0 < d.yhi)

@@ -876,6 +876,7 @@ __device__ __forceinline__ void uf_unite(int* l, int a, int b) {
       b = t;
     }
     // link the larger root a under b; retry if a stopped being a root meanwhile
+    OS_DCHECK(a >= 0 && b >= 0, "components: negative label");
     const int old = atomicMin(l + a, b);
     if (old == a) return;
     a = old;
@@ -901,6 +902,7 @@ __global__ void cc_count_kernel(const uint8_t* fg, int* lab, int* size, int64_t 
 }
 __global__ void cc_filter_kernel(uint8_t* fg, const int* lab, const int* size, int min_area, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && fg[i]) OS_DCHECK(lab[i] >= 0 && lab[i] < n, "components: label out of range");
   if (i < n && fg[i] && size[lab[i]] < min_area) fg[i] = 0;
 }
 

@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-op unless a tool (ncu --nvtx, nsys) attaches
+
 #include "../../include/omniseg.h"
 #include "../../include/omniseg_debug.h"
 #include "common.cuh"
@@ -29,6 +31,15 @@ using namespace osg;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX range of one pipeline stage on the calling (host) thread: the enqueue timeline of a
+// segment call (ncu --nvtx --nvtx-include "omniseg/..." selects a stage's kernels).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct DevBuf {
   void* p = nullptr;
@@ -744,9 +755,11 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   const int H8 = Hp / 8, W8 = Wp / 8;
   h->H8 = H8;
   h->W8 = W8;
+  NvtxRange nv_call("omniseg/segment");
   ensure_workspace(h, P);
   record(h, 0);
   // ---- upload (the band's slide rows [b0, b1))
+  nvtxRangePushA("omniseg/upload");
   const int64_t rows = b1 - b0;
   const size_t slide_bytes = (size_t)rows * W * 3;
   const uint8_t* dslide = rgb;
@@ -755,8 +768,10 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
     OS_CUDA(cudaMemcpyAsync(h->slide.p, rgb, slide_bytes, cudaMemcpyHostToDevice, s));
     dslide = h->slide.as<uint8_t>();
   }
+  nvtxRangePop();
   record(h, 1);
   // ---- front end
+  nvtxRangePushA("omniseg/front_end");
   h->state.ensure(sizeof(DevState));
   DevState* st = h->state.as<DevState>();
   if (b0 == 0) launch_pad_colour(dslide, W, st, s);
@@ -882,6 +897,7 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   h->n_tiles = counts[kMaxScales];
   h->otsu_t = hst.otsu_t;
   h->g_pad = hst.g_pad;
+  nvtxRangePop();
   record(h, 2);
   // ---- canvases (owned rows only)
   HeadTaskTable tt{};
@@ -989,7 +1005,9 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   const int B = h->arch.batch;
   const bool fused = h->stem_fused && !exp_flag("OMNISEG_NO_STEM_FUSION");
   const uint32_t* Lv[4] = {h->L1.as<uint32_t>(), h->L2.as<uint32_t>(), h->L4.as<uint32_t>(), h->L8.as<uint32_t>()};
+  nvtxRangePushA("omniseg/windows");
   for (int64_t first = 0; first < h->n_tiles; first += B) {
+    NvtxRange nv_batch("omniseg/batch");
     const int n = (int)std::min<int64_t>(B, h->n_tiles - first);
     if (fused) {
       // window gather + stem in one kernel (A5 + the first conv of A6)
@@ -1006,8 +1024,10 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
                           nullptr);
     if (host_out) progress(first + n);
   }
+  nvtxRangePop();
   record(h, 3);
   // ---- finalize the remaining rows
+  NvtxRange nv_fin("omniseg/finalize");
   for (int t = 0; t < tk.n; ++t) finalize_rows(t, done[t], r1[t]);
   if (h->comm)
     g_nccl.check(g_nccl.allReduce(h->area.p, h->area.p, tk.n, ncclUint64, ncclSum, h->comm, s), "ncclAllReduce(area)");
@@ -1265,6 +1285,7 @@ int omniseg_gather_bands(omniseg_t* h, int root, int64_t H, int64_t W, int pad, 
                  "gather_bands: the root needs device out_prob / out_mask for every band output given");
     }
     cudaStream_t s = h->stream;
+    NvtxRange nv("omniseg/gather_bands");
     // per task: offset of the task in the full output and in each rank's band output
     std::vector<int64_t> full_off(tk.n);
     int64_t acc = 0;
