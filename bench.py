@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--dtype", default=None,
                     help="fp16f8 (default: fp16 + e4m3 residual, parity-gated), fp16x2 (gated), fp16, bf16")
     ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--arch", action="append", default=[], metavar="KEY=VALUE",
+                    help="extra arch key (repeatable), e.g. --arch grp=1 --arch glev=2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="1 warmup + 1 step, for ncu")
@@ -317,6 +319,9 @@ def main():
         w.arch["dtype"] = a.dtype
     if a.batch:
         w.arch["batch"] = a.batch
+    for kv in a.arch:
+        k, v = kv.split("=", 1)
+        w.arch[k] = int(v) if v.lstrip("-").isdigit() else v
     H, W = w.H, w.W
     Hp = (H + 2 * w.pad + 127) // 128 * 128
     fmax = max(w.arch["slide_mag"] // s for s in w.scales)
@@ -484,6 +489,8 @@ def main():
                           "stride": w.stride if len(gsl) == 1 else {"x".join(map(str, g[1])): g[0] for g in gsl},
                           "pad": w.pad, "fusion": w.arch.get("fusion", "mean"),
                           "tasks": len(w.scales), "kept_tiles": n_tiles, "batch": w.arch["batch"],
+                          "schedule": (f"L2-resident groups of {w.arch['grp']} windows for levels < "
+                                       f"{w.arch.get('glev', 2)}" if w.arch.get("grp") else "batch-wide"),
                           "parallelism": (f"row-bands x{world} + NCCL band gather to rank 0" if world > 1
                                           else "single GPU"),
                           "l2": "inputs larger than L2 (slide %.1f GB, canvases %.1f GB)"

@@ -53,6 +53,10 @@ def arch_string(a: dict) -> str:
         s += ";headtc=%d" % a["headtc"]
     if a.get("vthr") is not None:
         s += ";vthr=" + ",".join(str(int(v)) for v in a["vthr"])
+    if a.get("grp") is not None:
+        s += ";grp=%d" % a["grp"]
+    if a.get("glev") is not None:
+        s += ";glev=%d" % a["glev"]
     return s
 
 

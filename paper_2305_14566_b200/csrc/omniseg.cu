@@ -125,6 +125,11 @@ struct Arch {
   int fgmin = 0;            // drop foreground components below fgmin level-8 pixels
   int maskfg = 0;           // AND the output masks with the foreground
   int headtc = 0;           // 1: the fused head's layer 1 (+ precls) on tcgen05 (measured slower)
+  // L2-resident schedule of the shallow levels: the U-Net levels < glev run per
+  // group of grp windows (their intermediates in a group-sized scratch slice that stays in L2,
+  // only the skips E_l per window), the deeper levels over the whole batch. grp = 0: every layer
+  // over the whole batch.
+  int grp = 0, glev = 2;
   std::vector<int> vthr;    // vote fusion: literal vote-count threshold per scale code; empty = majority
   int sp(int level) const { return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain; }
   // bytes per channel of a tensor stored with kind k
@@ -166,6 +171,8 @@ Arch parse_arch(const char* s) {
     else if (k == "fgmin") a.fgmin = toi(v);
     else if (k == "maskfg") a.maskfg = toi(v);
     else if (k == "headtc") a.headtc = toi(v);
+    else if (k == "grp") a.grp = toi(v);
+    else if (k == "glev") a.glev = toi(v);
     else if (k == "vthr") {
       a.vthr.clear();
       std::stringstream s2(v);
@@ -200,6 +207,8 @@ Arch parse_arch(const char* s) {
   OS_REQUIRE(a.ncls >= 1 && a.ncls <= 64, "arch: ncls out of range");
   OS_REQUIRE(!a.scale_codes.empty() && a.scale_codes.size() <= 8, "arch: 1..8 scale codes");
   OS_REQUIRE(a.batch >= 1 && a.batch <= 4096, "arch: batch out of range");
+  OS_REQUIRE(a.grp >= 0 && a.grp <= a.batch, "arch: grp must be in [0, batch]");
+  OS_REQUIRE(a.glev >= 1 && a.glev <= 8, "arch: glev must be in [1, 8]");
   OS_REQUIRE(a.slide_mag >= 1, "arch: slide_mag must be positive");
   OS_REQUIRE(a.vthr.empty() || a.vthr.size() == a.scale_codes.size(), "arch: vthr needs one entry per scale code");
   return a;
@@ -736,6 +745,101 @@ void run_trunk_and_head(omniseg* h, int n, int P, const uint32_t* tiles, int fir
   OS_CUDA(cudaGetLastError());
 }
 
+// Batch-index offsets of a plan's input / residual / output / head-tile tensors.
+void set_boffs(ConvPlan& p, int bin, int bres, int bout, int bhead = 0) {
+  p.args.b_in = bin;
+  p.args.b_res = bres;
+  p.args.b_out = bout;
+  p.args.b_head = bhead;
+}
+
+// The L2-resident schedule (arch grp / glev) of one batch of n windows whose
+// gather + stem is fused: per group of G windows, the levels < GL run back to back with their
+// stem / down / up outputs and conv_a outputs in the scratch slice [0, G) of the level buffers
+// (rewritten by every group, so it stays in L2) and only the skips E_l in the windows' own
+// slots; the levels >= GL and the GAP + controller run once over the batch; then per group the
+// decoder levels < GL down to the fused head. Same kernels, same arithmetic per window: the
+// outputs are bit-identical to the batch-wide schedule.
+template <typename T>
+void run_grouped(omniseg* h, int n, int P, const uint32_t* tiles, int first, const HeadTaskTable& tt, int ntasks, int S,
+                 int Hp, int Wp, int pad, const uint32_t* const Lv[4]) {
+  const int L = h->arch.levels, GL = std::min(h->arch.glev, L - 1), G = h->arch.grp;
+  cudaStream_t s = h->stream;
+  const size_t ne = h->enc_plans.size(), ndec = h->dec_plans.size();
+  auto enc_idx = [](int l, int j) { return 1 + 3 * l + j; };          // j: 0 conv_a, 1 conv_b, 2 down
+  auto dec_idx = [L](int l, int j) { return 3 * (L - 2 - l) + j; };  // j: 0 up, 1 conv_a, 2 conv_b
+  auto run = [&](ConvPlan& p, size_t layer_list_idx, bool dec, int nn) {
+    set_conv_batch(p, nn);
+    run_conv_prof(h, p, dec ? *h->dec_layers[layer_list_idx] : *h->enc_layers[layer_list_idx],
+                  (int)(dec ? ne + layer_list_idx : layer_list_idx), nn);
+    h->conv_launches++;
+  };
+  // ---- encoder, levels < GL, per group
+  for (int g0 = 0; g0 < n; g0 += G) {
+    const int gn = std::min(G, n - g0);
+    h->stem_plan.args.b_out = 0;
+    run_prof(h, h->enc_plans[0], *h->enc_layers[0], 0, gn,
+             [&] { run_stem(h->stem_plan, tiles, first + g0, gn, Lv, S, Hp, Wp, s); });
+    h->conv_launches++;
+    for (int l = 0; l < GL; ++l) {
+      ConvPlan& a = h->enc_plans[enc_idx(l, 0)];
+      ConvPlan& b = h->enc_plans[enc_idx(l, 1)];
+      ConvPlan& d = h->enc_plans[enc_idx(l, 2)];
+      set_boffs(a, 0, 0, 0);
+      run(a, enc_idx(l, 0), false, gn);
+      set_boffs(b, 0, 0, g0);  // E_l: the window's own slot (skip)
+      run(b, enc_idx(l, 1), false, gn);
+      set_boffs(d, g0, 0, l + 1 < GL ? 0 : g0);  // the batch phase reads A_GL per window
+      run(d, enc_idx(l, 2), false, gn);
+    }
+  }
+  // ---- levels >= GL over the batch
+  for (size_t i = enc_idx(GL, 0); i < ne; ++i) {
+    set_boffs(h->enc_plans[i], 0, 0, 0);
+    run(h->enc_plans[i], i, false, n);
+  }
+  const LevelBufs& bl = h->lv[L - 1];
+  launch_gap_controller<T>(bl.E.as<T>(), n, bl.P * bl.P, bl.C, h->arch.sp(L - 1), h->C[L - 1], h->Wc.as<float>(),
+                           h->bc.as<float>(), h->arch.ncls, (int)h->arch.scale_codes.size(), h->task_cls.as<int>(),
+                           h->task_scl.as<int>(), ntasks, h->gpart.as<float>(), h->g.as<float>(), h->theta.as<float>(),
+                           h->theta_t.as<float>(), s);
+  h->launches += 2;
+  for (int l = L - 2; l >= GL; --l)
+    for (int j = 0; j < 3; ++j) {
+      set_boffs(h->dec_plans[dec_idx(l, j)], 0, 0, 0);
+      run(h->dec_plans[dec_idx(l, j)], dec_idx(l, j), true, n);
+    }
+  // ---- decoder, levels < GL, per group, down to the fused head
+  for (int g0 = 0; g0 < n; g0 += G) {
+    const int gn = std::min(G, n - g0);
+    for (int l = GL - 1; l >= 0; --l) {
+      ConvPlan& u = h->dec_plans[dec_idx(l, 0)];
+      ConvPlan& a = h->dec_plans[dec_idx(l, 1)];
+      set_boffs(u, l + 1 >= GL ? g0 : 0, g0, 0);  // D_{l+1} (per window from the batch phase, else scratch), skip E_l
+      run(u, dec_idx(l, 0), true, gn);
+      set_boffs(a, 0, 0, 0);
+      run(a, dec_idx(l, 1), true, gn);
+      if (l > 0) {
+        ConvPlan& b = h->dec_plans[dec_idx(l, 2)];
+        set_boffs(b, 0, 0, 0);  // D_l into the scratch slice of E_l (its skips there are consumed)
+        run(b, dec_idx(l, 2), true, gn);
+      } else {
+        ConvPlan& hp = h->head_plan;
+        fill_head(hp.head, h, ntasks, P, S, Hp, Wp, pad, tiles, first, tt, nullptr, nullptr);
+        set_boffs(hp, 0, 0, 0, g0);
+        set_conv_batch(hp, gn);
+        run_conv_prof(h, hp, *h->dec_layers[ndec - 1], (int)(ne + ndec - 1), gn);
+        h->conv_launches++;
+      }
+    }
+  }
+  // back to the batch-wide offsets for the other entry points
+  for (auto& p : h->enc_plans) set_boffs(p, 0, 0, 0);
+  for (auto& p : h->dec_plans) set_boffs(p, 0, 0, 0);
+  set_boffs(h->head_plan, 0, 0, 0, 0);
+  OS_CUDA(cudaGetLastError());
+}
+
 void upload_tasks(omniseg* h, const Tasks& t) {
   h->task_cls.ensure(kMaxTasks * 4);
   h->task_scl.ensure(kMaxTasks * 4);
@@ -1009,6 +1113,11 @@ void segment(omniseg* h, const uint8_t* rgb, int64_t H, int64_t W, int64_t row0,
   for (int64_t first = 0; first < h->n_tiles; first += B) {
     NvtxRange nv_batch("omniseg/batch");
     const int n = (int)std::min<int64_t>(B, h->n_tiles - first);
+    if (fused && h->arch.grp > 0 && h->head_fusable && tk.n <= 8) {
+      run_grouped<T>(h, n, P, h->tiles.as<uint32_t>(), (int)first, tt, tk.n, S, Hp, Wp, pad, Lv);
+      if (host_out) progress(first + n);
+      continue;
+    }
     if (fused) {
       // window gather + stem in one kernel (A5 + the first conv of A6)
       run_prof(h, h->enc_plans[0], *h->enc_layers[0], 0, n, [&] {
