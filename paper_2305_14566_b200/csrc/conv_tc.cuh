@@ -326,7 +326,9 @@ __device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUte
 // Accumulator -> bias (+ residual from a TMA-loaded smem tile) -> ReLU (MODE != kBias), for
 // one CH-wide chunk of the warp's 32 rows. (xb, yb, b): box origin; n0: first channel.
 // The residual of this chunk was issued earlier into `slot` (epi_res_issue).
-template <typename T, int CH, int MODE>
+// SB: `bias` points to a shared-memory copy (16-B aligned): vector LDS instead of per-element
+// uniform global loads (the fused head's epilogue is issue-bound)
+template <typename T, int CH, int MODE, bool SB = false>
 __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t taddr, const float* bias, int n0,
                                            int split, uint32_t lane, float (&v)[CH]) {
   using E = EpiTile<CH>;
@@ -340,12 +342,26 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
     ptx::tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
   }
   ptx::tmem_ld_wait();
+  if constexpr (SB) {
 #pragma unroll
-  for (int j = 0; j < CH; j += 2) {  // + bias, packed
-    const float2 r = __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
-                                make_float2(__ldg(bias + n0 + j), __ldg(bias + n0 + j + 1)));
-    v[j] = r.x;
-    v[j + 1] = r.y;
+    for (int j = 0; j < CH; j += 4) {  // + bias, packed, from shared memory
+      const float4 b4 = *reinterpret_cast<const float4*>(bias + n0 + j);
+      const float2 r0 = __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])), make_float2(b4.x, b4.y));
+      const float2 r1 =
+          __fadd2_rn(make_float2(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])), make_float2(b4.z, b4.w));
+      v[j] = r0.x;
+      v[j + 1] = r0.y;
+      v[j + 2] = r1.x;
+      v[j + 3] = r1.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < CH; j += 2) {  // + bias, packed
+      const float2 r = __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
+                                  make_float2(__ldg(bias + n0 + j), __ldg(bias + n0 + j + 1)));
+      v[j] = r.x;
+      v[j + 1] = r.y;
+    }
   }
   if constexpr (kRes) {
     const int rc = es.res_rc;
@@ -1864,12 +1880,18 @@ __global__ void __launch_bounds__(384, 1)
     (void)tc_bar;
     (void)tc_phase;
     (void)tl;
+    // the fused head's conv bias (two-row path): in the theta staging area, which only the
+    // tensor-core head uses
+    float* s_bias = s_th;
+    (void)s_bias;
     if constexpr (MODE == kHeadFused) {
       for (int i = et; i < kHead * CH; i += 32 * EW) {  // transposed: s_w[j * 8 + o]
         const int o = i / CH, j = i - o * CH;
         s_w[j * 8 + o] = j < hargs.C0 ? hargs.Wpre[o * hargs.C0 + j] : 0.f;
       }
       if (et < kHead) s_b[et] = hargs.bpre[et];
+      if (!S::kTc && et < BN) s_bias[et] = args.bias[et];
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // s_w / s_b / s_bias complete
     }
     if constexpr (DYF) {
       // zero both accumulator buffers (this warp's lanes; the NH warps of a quadrant split the
@@ -2077,8 +2099,10 @@ __global__ void __launch_bounds__(384, 1)
           epi_res_issue<CH>(es, 1, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res, lane);
           const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN;
           float v0[CH], v1[CH];
-          epi_values<T, CH, kHeadFused>(es, 0, tq + (DYF ? (R - 1 - r0) : r0) * BN, args.bias, 0, args.split, lane, v0);
-          epi_values<T, CH, kHeadFused>(es, 1, tq + (DYF ? (R - 1 - r1) : r1) * BN, args.bias, 0, args.split, lane, v1);
+          constexpr bool kSB = !S::kTc;  // s_bias staged (the tensor-core build keeps theta there)
+          const float* bsrc = kSB ? s_bias : args.bias;
+          epi_values<T, CH, kHeadFused, kSB>(es, 0, tq + (DYF ? (R - 1 - r0) : r0) * BN, bsrc, 0, args.split, lane, v0);
+          epi_values<T, CH, kHeadFused, kSB>(es, 1, tq + (DYF ? (R - 1 - r1) : r1) * BN, bsrc, 0, args.split, lane, v1);
           if (i + 2 < RM)
             epi_res_issue<CH>(es, 0, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + (i + 2) * NH + half,
                               b + args.b_res, lane);

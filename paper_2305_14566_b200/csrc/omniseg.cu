@@ -120,7 +120,9 @@ struct Arch {
   int xlevels = -1;         // split storage only for tensors at U-Net levels < xlevels (-1: all levels)
   int xa = 1;               // 0: residual-block intermediates (conv_a outputs) stored plain 16-bit
   int xal = 64;             // with xa = 1: conv_a outputs keep the split kind only at levels < xal
-  int xa_level(int l) const { return xa && l < xal ? l : 1000; }  // level passed to sp() for conv_a outputs
+  int xap = 0;              // conv_a outputs stored plain 16-bit at levels < xap (precision budget)
+  int plainl = 0;           // bitmask of U-Net levels whose tensors are all stored plain 16-bit
+  int xa_level(int l) const { return xa && l < xal && l >= xap ? l : 1000; }  // level passed to sp() for conv_a outputs
   int vote = 0;             // fusion rule: 0 mean of p (R11), 1 hard majority vote
   int fgmin = 0;            // drop foreground components below fgmin level-8 pixels
   int maskfg = 0;           // AND the output masks with the foreground
@@ -131,7 +133,10 @@ struct Arch {
   // over the whole batch.
   int grp = 0, glev = 2;
   std::vector<int> vthr;    // vote fusion: literal vote-count threshold per scale code; empty = majority
-  int sp(int level) const { return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain; }
+  int sp(int level) const {
+    if (level < 31 && ((plainl >> level) & 1)) return kStorePlain;
+    return level < (xlevels < 0 ? 64 : xlevels) ? split : kStorePlain;
+  }
   // bytes per channel of a tensor stored with kind k
   static int bpc(int k) { return k == kStoreX2 ? 4 : k == kStoreF8 ? 3 : 2; }
   // channel padding: 16 (MMA K step), 32 in the f8 mode (an e4m3 MMA consumes 32 channels)
@@ -172,6 +177,8 @@ Arch parse_arch(const char* s) {
     else if (k == "maskfg") a.maskfg = toi(v);
     else if (k == "headtc") a.headtc = toi(v);
     else if (k == "grp") a.grp = toi(v);
+    else if (k == "xap") a.xap = toi(v);
+    else if (k == "plainl") a.plainl = toi(v);
     else if (k == "glev") a.glev = toi(v);
     else if (k == "vthr") {
       a.vthr.clear();

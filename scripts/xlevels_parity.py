@@ -27,8 +27,9 @@ def stitched(cfg, crop, xls):
     for xl in xls:
         a = dict(w.arch)
         if isinstance(xl, str):
-            k, v = xl.split("=")
-            a[k] = int(v) if v.lstrip("-").isdigit() else v
+            for kv in xl.split("+"):  # several keys: k1=v1+k2=v2
+                k, v = kv.split("=")
+                a[k] = int(v) if v.lstrip("-").isdigit() else v
         else:
             a["xlevels"] = xl
         h = Omniseg(arch_string(a), w.weights())
