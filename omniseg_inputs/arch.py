@@ -53,7 +53,7 @@ def arch_string(a: dict) -> str:
         s += ";headtc=%d" % a["headtc"]
     if a.get("vthr") is not None:
         s += ";vthr=" + ",".join(str(int(v)) for v in a["vthr"])
-    for k in ("xap", "plainl", "hrm"):
+    for k in ("xap", "plainl"):
         if a.get(k) is not None:
             s += ";%s=%d" % (k, a[k])
     if a.get("grp") is not None:

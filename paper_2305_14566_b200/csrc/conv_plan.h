@@ -20,7 +20,6 @@ struct ConvPlan {
   int hb = 1;
   bool bf16;
   bool head_tc = false;  // kHeadFused with the tensor-core head (R = NzCfg::RTC)
-  bool head_rm = false;  // kHeadFused with the residual through the tensor core (tmO: the residual-row map)
   HeadArgs head{};       // kHead mode (fused dynamic head + stitch), set by the caller per launch
   double flops;          // algorithmic FLOPs of one launch (2 * M * N * K)
 };

@@ -145,10 +145,6 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   const int threads = 384;
   if (p.mode == kResidualRelu) smem = NzSmem<BN, R, STR, DYF, 8, 1>::kTotal;
   else if (p.mode == kHeadFused) smem = p.head_tc ? NzSmem<BN, RT, STT, DYF, 8, 2>::kTotal : NzSmem<BN, R, STH, DYF, 8, 2>::kTotal;
-  constexpr bool kRmOk = std::is_same<T, __half>::value && BN == 32 && DYF;  // conv3_nz_kernel RMM
-  constexpr int STM = NzCfg::STAGES(BN, 3);
-  static_assert(!kRmOk || STM >= 2, "RMM head does not fit shared memory");
-  if (kRmOk && p.mode == kHeadFused && p.head_rm) smem = NzSmem<BN, R, STM, DYF, 8, 3>::kTotal;
   OS_REQUIRE(p.nz_R == (p.head_tc ? RT : R), "nz plan: rows per work item mismatch");
   auto go = [&](auto kern) {
     static std::mutex mu;
@@ -201,12 +197,6 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
       if constexpr (BN <= 32) {
         if (p.head_tc) {
           go(conv3_nz_kernel<T, BN, RT, STT, kHeadFused, DYF>);
-          break;
-        }
-      }
-      if constexpr (kRmOk) {
-        if (p.head_rm) {
-          go(conv3_nz_kernel<T, BN, R, STM, kHeadFused, DYF, 1, true>);
           break;
         }
       }
@@ -313,10 +303,6 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
   if (mode == kHeadFusedTc) {
     mode = kHeadFused;
     p.head_tc = !bf16 && Cout <= 32;
-  }
-  if (mode == kHeadFusedRm) {
-    mode = kHeadFused;
-    p.head_rm = !bf16 && Cout == 32 && split_out == kStoreF8 && res_rc && in_rc;
   }
   p.mode = mode;
   p.bf16 = bf16;
@@ -557,20 +543,6 @@ ConvPlan make_conv_plan(bool bf16, const void* in, int B, int Hin, int Win, int 
       } else {
         p.tmR = p.tmO;
       }
-    }
-    if (p.head_rm) {
-      // the RMM head (no output tensor): tmO = the residual's R rows of one 128-pixel tile,
-      // all chunks (fp16 hi, e4m3 lo) -> smem [row][chunk][128 px][16 B]
-      OS_REQUIRE(p.nz_R > 0 && res && f8o, "RMM head: row-chunked F8 residual and the nz kernel");
-      const uint64_t nch = opx / 16;
-      cuuint64_t d5[5] = {128, (cuuint64_t)Wo / 8, nch, (cuuint64_t)Ho, (cuuint64_t)B_res};
-      cuuint64_t s5[4] = {128, (cuuint64_t)Wo * 16, nch * Wo * 16, (cuuint64_t)Ho * nch * Wo * 16};
-      cuuint32_t b5[5] = {128, 16, (cuuint32_t)nch, (cuuint32_t)p.nz_R, 1};
-      cuuint32_t e5[5] = {1, 1, 1, 1, 1};
-      CUresult r = encode_fn()(&p.tmO, d8, 5, const_cast<void*>(res), d5, s5, b5, e5, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw Error(-2, "cuTensorMapEncodeTiled(RMM residual rows) failed: " + std::to_string((int)r));
     }
   }
   p.stages = (p.rows_R > 0 || p.nz_R > 0 || p.s2_R > 0) ? 0 : stages_for(p.bn, p.bk);

@@ -32,10 +32,6 @@ enum ConvMode : int { kReluBias = 0, kResidualRelu = 1, kUpAdd = 2, kBias = 3, k
 // plan-level request (make_conv_plan only): kHeadFused with the tensor-core head (arch headtc=1):
 // R = 4 rows per work item, the plan's mode is kHeadFused and ConvPlan::head_tc is set
 constexpr int kHeadFusedTc = 5;
-// plan-level request: kHeadFused with the residual added by identity MMAs (conv3_nz_kernel RMM)
-// where the configuration allows it (fp16 + e4m3 split storage, row-chunked residual, 32
-// channels); the plan's mode is kHeadFused and ConvPlan::head_rm is set
-constexpr int kHeadFusedRm = 6;
 
 // Storage of an activation tensor, per pixel (R9):
 //   kStorePlain  [C] 16-bit
@@ -1577,9 +1573,7 @@ __global__ void __launch_bounds__(256, 1)
 // residual (6 kBuf), 2 fused head (residual slots only, 4 kBuf).
 template <int BN, int R, int STAGES, bool DYF = false, int EW = 8, int EK = 0, int CL = 1>
 struct NzSmem {
-  // EK 3: the fused head with the residual added by the tensor core (RMM, see conv3_nz_kernel)
-  static constexpr bool HEAD = EK == 2 || EK == 3;
-  static constexpr bool kRm = EK == 3;
+  static constexpr bool HEAD = EK == 2;
   static constexpr int kPx = 144;                                   // 18 units of 8 pixels
   static constexpr int kChunkStride = kPx * 16;                      // LBO of the A operand
   static constexpr int kRowStride = 2 * kChunkStride;                // two chunks (K = 32 B) per row
@@ -1594,7 +1588,7 @@ struct NzSmem {
   static constexpr int kBars = (2 * STAGES + 4 + 2 * EW) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
-  static constexpr int kWarpEpi = (EK == 3 ? 0 : EK == 2 ? 4 : EK == 1 ? 6 : 3) * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
+  static constexpr int kWarpEpi = (EK == 2 ? 4 : EK == 1 ? 6 : 3) * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
   static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 + EW * kHeadDescs * 32 : 0;
@@ -1608,17 +1602,7 @@ struct NzSmem {
   static constexpr int kTcOff = ((kHeadOff + kHeadBytes + 1023) / 1024) * 1024;
   static constexpr bool kTc = EK == 2 && BN <= 32 && R == 4;  // = NzCfg::tc(BN, EK, R)
   static constexpr int kTcBytes = kTc ? 8 * kTcA + 2 * kTcB + BN * 4 + 64 : 0;
-  // RMM: the item's residual rows U0 (row-chunked [row][chunk][128 px][16 B], fp16 hi chunks then
-  // e4m3 lo chunks: 3 BN / 16 chunks) as UMMA A operands, the identity B tiles (fp16 I for the hi
-  // chunks, 2^-6 I in e5m2 for the lo chunk) and the ufull / uempty barriers
-  static constexpr int kUChunks = 3 * BN / 16;
-  static constexpr int kURow = kUChunks * 2048;
-  static constexpr int kUOff = kTcOff + kTcBytes;
-  static constexpr int kUBytes = kRm ? R * kURow : 0;
-  static constexpr int kIOff = kUOff + kUBytes;
-  static constexpr int kIBytes = kRm ? 3 * BN * BN : 0;
-  static constexpr int kUBar = kIOff + kIBytes;
-  static constexpr int kTotal = kUBar + (kRm ? 16 : 0) + 1024;
+  static constexpr int kTotal = kTcOff + kTcBytes + 1024;
   static constexpr uint32_t kTmemCols = kTc || 2 * R * BN > 256 ? 512 : 256;
 };
 
@@ -1644,9 +1628,8 @@ struct NzCfg {
   static constexpr int STAGES(int bn, int ek) { return STAGES(bn, ek, R(bn)); }
   static constexpr int tc_bytes(int bn) { return 8 * 128 * bn * 2 + 2 * bn * bn * 2 + bn * 4 + 64; }
   static constexpr int budget(int bn, int ek, int r) {
-    return 227 * 1024 - 3 * 1024 - 8 * (ek == 3 ? 0 : ek == 2 ? 4 : ek == 1 ? 6 : 3) * 32 * (bn < 32 ? bn : 32) * 2 -
-           (ek >= 2 ? 7680 + 8 * kHeadDescs * 32 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0) -
-           (ek == 3 ? r * 3 * bn * 128 + 3 * bn * bn + 1024 : 0);
+    return 227 * 1024 - 3 * 1024 - 8 * (ek == 2 ? 4 : ek == 1 ? 6 : 3) * 32 * (bn < 32 ? bn : 32) * 2 -
+           (ek == 2 ? 7680 + 8 * kHeadDescs * 32 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
   }
 
 };
@@ -1705,12 +1688,7 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
 // accumulators first-written by different MMAs, they are zeroed by the epilogue
 // (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
 // tensor-core operand traffic than one MMA per (tap, row).
-// RMM (fused head, F8 residual in the row-chunked layout, DYF): the producer TMA-loads the item's
-// R residual rows once, and the MMA warp adds them to the accumulators with identity MMAs (U0_hi I
-// + U0_lo 2^-6 I, exact products, fp32 accumulation) before the conv MMAs -- the epilogue reads
-// acc = conv + U0 and only adds the bias (no per-pixel residual loads and fp16 / e4m3 conversions
-// on the issue-bound head epilogue).
-template <typename T, int BN, int R, int STAGES, int MODE, bool DYF, int CL = 1, bool RMM = false>
+template <typename T, int BN, int R, int STAGES, int MODE, bool DYF, int CL = 1>
 __global__ void __launch_bounds__(384, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
@@ -1721,9 +1699,7 @@ __global__ void __launch_bounds__(384, 1)
   // sub-partition leaves the epilogue latency-bound (measured: it, not the loads or MMAs, set
   // the pace of the thin layers)
   constexpr int EW = 8;
-  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? (RMM ? 3 : 2) : MODE == kResidualRelu ? 1 : 0, CL>;
-  static_assert(!RMM || (MODE == kHeadFused && DYF && BN == 32 && CL == 1 && std::is_same<T, __half>::value),
-                "RMM: fused fp16 head, dy-fused, 32 channels");
+  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? 2 : MODE == kResidualRelu ? 1 : 0, CL>;
   static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
   // CL = 2: CTA pair (cta_group::2, see conv_tc_kernel): items in pairs (two M items, one N tile),
   // each CTA's A rows + its half of the weight image complete on the leader's `full` barrier
@@ -1762,11 +1738,6 @@ __global__ void __launch_bounds__(384, 1)
       ptx::mbar_init(&tempty[a], CL == 2 ? 2 * EW : 32 * EW);
     }
     for (int a = 0; a < 2 * EW; ++a) ptx::mbar_init(&rbar[a], 1);
-    if constexpr (RMM) {
-      uint64_t* ub = reinterpret_cast<uint64_t*>(smem + S::kUBar);
-      ptx::mbar_init(&ub[0], 1);  // ufull: the item's residual rows landed
-      ptx::mbar_init(&ub[1], 1);  // uempty: their identity MMAs completed
-    }
     if constexpr (S::kTc) {
       uint64_t* hmb = reinterpret_cast<uint64_t*>(smem + S::kTcOff + 8 * S::kTcA + 2 * S::kTcB + BN * 4);
       for (int i = 0; i < 8; ++i) ptx::mbar_init(&hmb[i], 1);
@@ -1779,19 +1750,6 @@ __global__ void __launch_bounds__(384, 1)
     else
       ptx::tmem_alloc<S::kTmemCols>(tmem_slot);
   }
-  if constexpr (RMM) {
-    // identity B operands (no-swizzle K-major, 8-row x 16-B core matrices): fp16 I[n][k] for the
-    // two K = 16 hi steps, e5m2 2^-6 I (0x24) for the K = 32 lo step
-    uint8_t* ih = smem + S::kIOff;
-    uint8_t* il = ih + 2 * BN * BN;
-    for (int i = threadIdx.x; i < BN * BN; i += blockDim.x) {
-      const int n = i / BN, k = i - n * BN;
-      *reinterpret_cast<__half*>(ih + (k >> 3) * (BN * 16) + (n >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) =
-          __float2half(n == k ? 1.f : 0.f);
-      il[(k >> 4) * (BN * 16) + (n >> 3) * 128 + (n & 7) * 16 + (k & 15)] = n == k ? 0x24 : 0;
-    }
-    ptx::fence_proxy_async();
-  }
   ptx::tc_fence_before();
   if constexpr (CL == 2)
     ptx::cluster_sync();
@@ -1799,8 +1757,6 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  uint64_t* ubar = reinterpret_cast<uint64_t*>(smem + S::kUBar);  // RMM: ufull, uempty
-  (void)ubar;
   // 32-byte K chunks: kchunks hi chunks (16 fp16 channels), then kch_lo F8 lo chunks (32 e4m3)
   const int kiters = args.kchunks + args.kch_lo;
   constexpr uint32_t kTx = CL * (S::kABytes + 9 * S::kBt);
@@ -1808,8 +1764,7 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0, uphase = 0;
-      (void)uphase;
+      uint32_t phase = 0;
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x) {
         int nt, m;
         decode(w, nt, m);
@@ -1819,12 +1774,6 @@ __global__ void __launch_bounds__(384, 1)
         const int b = m / args.tiles_y;
         const int u0 = tx * 16 - 1;  // first 8-pixel unit of the box (pixels [x0 - 8, x0 + 136))
         const int y0 = tyg * R - 1;
-        if constexpr (RMM) {  // the item's R residual rows (tmO: {128 B, 16 units, all chunks, R rows} box)
-          ptx::mbar_wait(&ubar[1], uphase ^ 1);
-          ptx::mbar_arrive_expect_tx(&ubar[0], S::kUBytes);
-          ptx::tma_load_5d(smem + S::kUOff, &tmO, &ubar[0], 0, tx * 16, 0, tyg * R, b + args.b_res);
-          uphase ^= 1;
-        }
         for (int kc = 0; kc < kiters; ++kc) {
           if constexpr (MODE == kHeadFused)  // epilogue-bound: leave the issue slots to the head math
             ptx::mbar_wait_backoff(&empty[stage], phase ^ 1);
@@ -1869,8 +1818,7 @@ __global__ void __launch_bounds__(384, 1)
                                   // chunk, outside the MMA loops; CL = 2: the leader only)
       constexpr bool kBf = std::is_same<T, __nv_bfloat16>::value;
       int stage = 0;
-      uint32_t phase = 0, uphase = 0;
-      (void)uphase;
+      uint32_t phase = 0;
       int local = 0;
       unsigned long long c_te = 0, c_full = 0, c_all = 0, t_start = OS_CLK();
       for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
@@ -1881,26 +1829,6 @@ __global__ void __launch_bounds__(384, 1)
         c_te += OS_CLK() - t0;
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + acc * R * BN;
-        if constexpr (RMM) {
-          // acc += U0: per output row, two K = 16 fp16 MMAs over the hi chunks and one K = 32
-          // e4m3 x e5m2 MMA over the lo chunks against identity B tiles (DYF: accumulators zeroed,
-          // every MMA accumulates; row r at column (R - 1 - r) BN); then release the buffer
-          ptx::mbar_wait(&ubar[0], uphase);
-          uphase ^= 1;
-          ptx::tc_fence_after();
-          const uint32_t ua = ptx::smem_u32(smem + S::kUOff), ib = ptx::smem_u32(smem + S::kIOff);
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const uint32_t d = d_base + (R - 1 - r) * BN, a = ua + r * S::kURow;
-#pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk)
-              ptx::mma_f16_w(d, ptx::smem_desc_noswz(a + kk * 4096, 2048, 128),
-                             ptx::smem_desc_noswz(ib + kk * BN * 32, BN * 16, 128), ptx::idesc_f16(128, BN, false), 1u);
-            ptx::mma_f8_w(d, ptx::smem_desc_noswz(a + (BN / 8) * 2048, 2048, 128),
-                          ptx::smem_desc_noswz(ib + 2 * BN * BN, BN * 16, 128), ptx::idesc_f8(128, BN), 1u);
-          }
-          ptx::mma_commit_w(&ubar[1]);
-        }
         for (int kc = 0; kc < kiters; ++kc) {
           t0 = OS_CLK();
           ptx::mbar_wait(&full[stage], phase);
@@ -2065,7 +1993,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
       }
-      constexpr bool kRes = MODE == kResidualRelu || (MODE == kHeadFused && !RMM);
+      constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
       constexpr int NC = BN / CH;
       const int xb = tx * 128 + q * 32;
       constexpr int RM = R / NH;  // rows of this warp: r = j * NH + half
@@ -2184,20 +2112,17 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
           for (int i = 0; i < RM; i += 2) {
             const int r0 = i * NH + half, r1 = (i + 1) * NH + half;
-            if constexpr (!RMM)
-              epi_res_issue<CH, F8RC>(es, 1, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res,
+            epi_res_issue<CH, F8RC>(es, 1, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res,
                                       lane);
             const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN;
             float v0[CH], v1[CH];
             constexpr bool kSB = !S::kTc;  // s_bias staged (the tensor-core build keeps theta there)
             const float* bsrc = kSB ? s_bias : args.bias;
-            // RMM: the accumulator already holds conv + U0 (bias, ReLU only)
-            constexpr int VM = RMM ? (int)kReluBias : (int)kHeadFused;
-            epi_values<T, CH, VM, kSB, F8RC>(es, 0, tq + (DYF ? (R - 1 - r0) : r0) * BN, bsrc, 0, args.split, lane,
+            epi_values<T, CH, kHeadFused, kSB, F8RC>(es, 0, tq + (DYF ? (R - 1 - r0) : r0) * BN, bsrc, 0, args.split, lane,
                                              v0);
-            epi_values<T, CH, VM, kSB, F8RC>(es, 1, tq + (DYF ? (R - 1 - r1) : r1) * BN, bsrc, 0, args.split, lane,
+            epi_values<T, CH, kHeadFused, kSB, F8RC>(es, 1, tq + (DYF ? (R - 1 - r1) : r1) * BN, bsrc, 0, args.split, lane,
                                              v1);
-            if (!RMM && i + 2 < RM)
+            if (i + 2 < RM)
               epi_res_issue<CH, F8RC>(es, 0, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + (i + 2) * NH + half,
                                       b + args.b_res, lane);
             if (!F8RC && !args.split) {

@@ -132,7 +132,6 @@ struct Arch {
   // only the skips E_l per window), the deeper levels over the whole batch. grp = 0: every layer
   // over the whole batch.
   int grp = 0, glev = 2;
-  int hrm = 1;              // fused head: the residual added by identity MMAs (where the storage allows)
   std::vector<int> vthr;    // vote fusion: literal vote-count threshold per scale code; empty = majority
   int sp(int level) const {
     if (level < 31 && ((plainl >> level) & 1)) return kStorePlain;
@@ -178,7 +177,6 @@ Arch parse_arch(const char* s) {
     else if (k == "maskfg") a.maskfg = toi(v);
     else if (k == "headtc") a.headtc = toi(v);
     else if (k == "grp") a.grp = toi(v);
-    else if (k == "hrm") a.hrm = toi(v);
     else if (k == "xap") a.xap = toi(v);
     else if (k == "plainl") a.plainl = toi(v);
     else if (k == "glev") a.glev = toi(v);
@@ -582,7 +580,7 @@ void ensure_workspace(omniseg* h, int P) {
   if (!exp_flag("OMNISEG_NO_HEAD_FUSION") && rc[0]) {
     LevelBufs& q = h->lv[0];
     ConvPlan hp = plan(h->dec_b[0], q.Bt.p, q.P, q.A.p, q.E.p,
-                       h->arch.headtc ? kHeadFusedTc : h->arch.hrm ? kHeadFusedRm : kHeadFused, 0, rc[0], rc[0], 0);
+                       h->arch.headtc ? kHeadFusedTc : kHeadFused, 0, rc[0], rc[0], 0);
     if (hp.nz_R > 0 && hp.bn == h->Cp[0] && h->C[0] <= 32) {
       h->head_plan = hp;
       h->head_fusable = true;
