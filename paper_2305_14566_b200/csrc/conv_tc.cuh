@@ -312,18 +312,18 @@ __device__ __forceinline__ uint32_t off8(int rc, int px, int j8) {
 // Issue the TMA loads of one residual chunk into buffer slot `slot` (lane 0). F8: the lo part
 // comes from the e4m3 map tmR2. RC: 5-D maps {128 B = 8 px, W/8, chunk, H, B}; the chunks of channels
 // [n0, n0 + CH) are n0/8.. (hi), C/8 + n0/8.. (x2 lo) and C/8 + n0/16.. (F8 lo).
-// F8RC: compile-time F8 split + row-chunked residual (the fused head's product configuration):
-// the runtime kind / layout branches fold away
-template <int CH, bool F8RC = false>
+// SK / RC >= 0: storage kind / row-chunked flag of the residual known at compile time (the
+// product configurations: the runtime kind / layout branches fold away); -1: runtime
+template <int CH, int SK = -1, int RC = -1>
 __device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUtensorMap* tmR, const CUtensorMap* tmR2,
                                               int n0, int Cout, int split_, int xb, int yb, int b, uint32_t lane) {
   using E = EpiTile<CH>;
-  const int split = F8RC ? (int)kStoreF8 : split_;
+  const int split = SK >= 0 ? SK : split_;
   if (lane == 0) {
     uint8_t* hi = es.buf + es.res_off[slot];
     const uint32_t tx = split == kStoreF8 ? E::kBuf + 32 * CH : (split ? 2 : 1) * E::kBuf;
     ptx::mbar_arrive_expect_tx(&es.rbar[slot], tx);
-    if (F8RC || es.res_rc) {
+    if (RC >= 0 ? RC != 0 : es.res_rc != 0) {
       ptx::tma_load_5d(hi, tmR, &es.rbar[slot], 0, xb / 8, n0 / 8, yb, b);
       if (split == kStoreF8)
         ptx::tma_load_5d(hi + E::kBuf, tmR2, &es.rbar[slot], 0, xb / 8, Cout / 8 + n0 / 16, yb, b);
@@ -344,11 +344,11 @@ __device__ __forceinline__ void epi_res_issue(EpiState& es, int slot, const CUte
 // The residual of this chunk was issued earlier into `slot` (epi_res_issue).
 // SB: `bias` points to a shared-memory copy (16-B aligned): vector LDS instead of per-element
 // uniform global loads (the fused head's epilogue is issue-bound)
-template <typename T, int CH, int MODE, bool SB = false, bool F8RC = false>
+template <typename T, int CH, int MODE, bool SB = false, int SK = -1, int RC = -1>
 __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t taddr, const float* bias, int n0,
                                            int split_, uint32_t lane, float (&v)[CH]) {
   using E = EpiTile<CH>;
-  const int split = F8RC ? (int)kStoreF8 : split_;
+  const int split = SK >= 0 ? SK : split_;
   uint8_t* res_hi = es.buf + es.res_off[slot];
   uint8_t* res_lo = res_hi + E::kBuf;
   constexpr bool kRes = MODE == kResidualRelu || MODE == kHeadFused;
@@ -373,15 +373,19 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < CH; j += 2) {  // + bias, packed
-      const float2 r = __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
-                                  make_float2(__ldg(bias + n0 + j), __ldg(bias + n0 + j + 1)));
-      v[j] = r.x;
-      v[j + 1] = r.y;
+    for (int j = 0; j < CH; j += 4) {  // + bias, packed (bias + n0 is 16-B aligned: n0 % 16 == 0)
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
+      const float2 r0 = __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])), make_float2(b4.x, b4.y));
+      const float2 r1 =
+          __fadd2_rn(make_float2(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])), make_float2(b4.z, b4.w));
+      v[j] = r0.x;
+      v[j + 1] = r0.y;
+      v[j + 2] = r1.x;
+      v[j + 3] = r1.y;
     }
   }
   if constexpr (kRes) {
-    const int rc = F8RC ? 1 : es.res_rc;
+    const int rc = RC >= 0 ? RC : es.res_rc;
     ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
     es.rphase[slot] ^= 1;
     if (split == kStoreF8) {
@@ -414,25 +418,27 @@ __device__ __forceinline__ void epi_values(EpiState& es, int slot, uint32_t tadd
 }
 
 // One CH-wide chunk: values -> 16-bit (hi, + lo in x2 / F8) -> STS -> TMA store.
-template <typename T, int CH>
+template <typename T, int CH, int SK = -1>
 __device__ __forceinline__ void epi_store(EpiState& es, const CUtensorMap* tmO, const CUtensorMap* tmO2,
                                           const float (&v)[CH], int n0, int Cout, int split, int xb, int yb, int b,
                                           uint32_t lane);
 
-template <typename T, int CH, int MODE>
+// SK >= 0: the residual / output storage kind known at compile time (see epi_res_issue)
+template <typename T, int CH, int MODE, int SK = -1>
 __device__ __forceinline__ void epi_chunk(EpiState& es, int slot, const CUtensorMap* tmO, const CUtensorMap* tmO2,
                                           uint32_t taddr, const float* bias, int n0, int Cout, int split, int xb,
                                           int yb, int b, uint32_t lane) {
   float v[CH];
-  epi_values<T, CH, MODE>(es, slot, taddr, bias, n0, split, lane, v);
-  epi_store<T, CH>(es, tmO, tmO2, v, n0, Cout, split, xb, yb, b, lane);
+  epi_values<T, CH, MODE, false, SK>(es, slot, taddr, bias, n0, split, lane, v);
+  epi_store<T, CH, SK>(es, tmO, tmO2, v, n0, Cout, split, xb, yb, b, lane);
 }
 
 // The store half of epi_chunk: v (final values) -> storage kind -> STS -> TMA store.
-template <typename T, int CH>
+template <typename T, int CH, int SK>
 __device__ __forceinline__ void epi_store(EpiState& es, const CUtensorMap* tmO, const CUtensorMap* tmO2,
-                                          const float (&v)[CH], int n0, int Cout, int split, int xb, int yb, int b,
+                                          const float (&v)[CH], int n0, int Cout, int split_, int xb, int yb, int b,
                                           uint32_t lane) {
+  const int split = SK >= 0 ? SK : split_;
   uint8_t* out_hi = es.buf + es.out_off[es.oslot];
   uint8_t* out_lo = out_hi + EpiTile<CH>::kBuf;
   const bool dbl = es.out_off[1] != es.out_off[0];
@@ -2112,18 +2118,18 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
           for (int i = 0; i < RM; i += 2) {
             const int r0 = i * NH + half, r1 = (i + 1) * NH + half;
-            epi_res_issue<CH, F8RC>(es, 1, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res,
+            epi_res_issue<CH, F8RC ? (int)kStoreF8 : -1, F8RC ? 1 : -1>(es, 1, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + r1, b + args.b_res,
                                       lane);
             const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN;
             float v0[CH], v1[CH];
             constexpr bool kSB = !S::kTc;  // s_bias staged (the tensor-core build keeps theta there)
             const float* bsrc = kSB ? s_bias : args.bias;
-            epi_values<T, CH, kHeadFused, kSB, F8RC>(es, 0, tq + (DYF ? (R - 1 - r0) : r0) * BN, bsrc, 0, args.split, lane,
+            epi_values<T, CH, kHeadFused, kSB, F8RC ? (int)kStoreF8 : -1, F8RC ? 1 : -1>(es, 0, tq + (DYF ? (R - 1 - r0) : r0) * BN, bsrc, 0, args.split, lane,
                                              v0);
-            epi_values<T, CH, kHeadFused, kSB, F8RC>(es, 1, tq + (DYF ? (R - 1 - r1) : r1) * BN, bsrc, 0, args.split, lane,
+            epi_values<T, CH, kHeadFused, kSB, F8RC ? (int)kStoreF8 : -1, F8RC ? 1 : -1>(es, 1, tq + (DYF ? (R - 1 - r1) : r1) * BN, bsrc, 0, args.split, lane,
                                              v1);
             if (i + 2 < RM)
-              epi_res_issue<CH, F8RC>(es, 0, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + (i + 2) * NH + half,
+              epi_res_issue<CH, F8RC ? (int)kStoreF8 : -1, F8RC ? 1 : -1>(es, 0, &tmR, &lo.R, 0, args.Cout, args.split, xb, tyg * R + (i + 2) * NH + half,
                                       b + args.b_res, lane);
             if (!F8RC && !args.split) {
 #pragma unroll
@@ -2140,32 +2146,42 @@ __global__ void __launch_bounds__(384, 1)
           passes(std::true_type{});
         else
           passes(std::false_type{});
-      } else
+      } else {
+        // F8 storage (the product dtype) runs a copy of the chunk loop with the kind known at
+        // compile time
+        auto chunks = [&](auto f8_tag) {
+          constexpr int SK = decltype(f8_tag)::value ? (int)kStoreF8 : -1;
 #pragma unroll 1
-      for (int i = 0; i < RM * NC; ++i) {
-        const int r = (i / NC) * NH + half, c = (i % NC) * CH;
-        const int slot = i & 1;
-        if constexpr (kRes) {
-          if (i + 1 < RM * NC) {
-            const int r1 = ((i + 1) / NC) * NH + half, c1 = ((i + 1) % NC) * CH;
-            epi_res_issue<CH>(es, slot ^ 1, &tmR, &lo.R, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1,
-                              b + args.b_res, lane);
+          for (int i = 0; i < RM * NC; ++i) {
+            const int r = (i / NC) * NH + half, c = (i % NC) * CH;
+            const int slot = i & 1;
+            if constexpr (kRes) {
+              if (i + 1 < RM * NC) {
+                const int r1 = ((i + 1) / NC) * NH + half, c1 = ((i + 1) % NC) * CH;
+                epi_res_issue<CH, SK>(es, slot ^ 1, &tmR, &lo.R, nt * BN + c1, args.Cout, args.split, xb, tyg * R + r1,
+                                      b + args.b_res, lane);
+              }
+            }
+            const uint32_t taddr =
+                tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (DYF ? (R - 1 - r) : r) * BN + c;
+            if (OS_EXP && (args.dbg & 1)) {
+              if constexpr (kRes) {
+                ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
+                es.rphase[slot] ^= 1;
+              }
+            } else if constexpr (MODE == kHeadFused) {
+              epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs,
+                              s_w, s_b, th_g, lf, oy, ox, h_ok && h_n >= 0 ? s_ht : nullptr, h_n);
+            } else {
+              epi_chunk<T, CH, MODE, SK>(es, slot, &tmO, &lo.O, taddr, args.bias, nt * BN + c, args.Cout, args.split,
+                                         xb, tyg * R + r, b + args.b_out, lane);
+            }
           }
-        }
-        const uint32_t taddr =
-            tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + (DYF ? (R - 1 - r) : r) * BN + c;
-        if (OS_EXP && (args.dbg & 1)) {
-          if constexpr (kRes) {
-            ptx::mbar_wait(&es.rbar[slot], es.rphase[slot]);
-            es.rphase[slot] ^= 1;
-          }
-        } else if constexpr (MODE == kHeadFused) {
-          epi_head<T, CH>(es, slot, taddr, args.bias, args.split, xb, tyg * R + r, b + args.b_head, lane, hargs, s_w,
-                          s_b, th_g, lf, oy, ox, h_ok && h_n >= 0 ? s_ht : nullptr, h_n);
-        } else {
-          epi_chunk<T, CH, MODE>(es, slot, &tmO, &lo.O, taddr, args.bias, nt * BN + c, args.Cout, args.split, xb,
-                                 tyg * R + r, b + args.b_out, lane);
-        }
+        };
+        if (MODE != kHeadFused && args.split == kStoreF8)
+          chunks(std::true_type{});
+        else
+          chunks(std::false_type{});
       }
       if constexpr (DYF) {
         for (int j = 0; j < RM; ++j) {
@@ -2772,12 +2788,14 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
       for (int j = 0; j < CH; ++j) bias_r[j] = __ldg(args.bias + j);
     }
     int local = 0;
+    // F8 storage (the product dtype) runs a copy of the item loop with the kind known at compile time
+    auto items = [&](auto f8_tag) {
+    constexpr int SK = decltype(f8_tag)::value ? (int)kStoreF8 : -1;
     for (int w = blockIdx.x; w < args.num_work; w += gridDim.x, ++local) {
       const int acc = local & 1;
-      const int tx = w % args.tiles_x;
-      int m = w / args.tiles_x;
-      const int tyg = m % args.tiles_y;
-      const int b = m / args.tiles_y;
+      int tx, m, tyg, b;
+      udivmod(w, args.tiles_x, m, tx);
+      udivmod(m, args.tiles_y, b, tyg);
       ptx::mbar_wait_backoff(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
       const int xb = tx * 128 + q * 32;
@@ -2801,7 +2819,7 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
           v[j + 2] = fmaxf(t1.x, 0.f);
           v[j + 3] = fmaxf(t1.y, 0.f);
         }
-        epi_store<T, CH>(es, &tmO, &lo.O, v, 0, args.Cout, args.split, xb, tyg * R + half, b + args.b_out, lane);
+        epi_store<T, CH, SK>(es, &tmO, &lo.O, v, 0, args.Cout, args.split, xb, tyg * R + half, b + args.b_out, lane);
         continue;
       } else if constexpr (BN == CH && CH == 32) {
         // one 32-channel chunk per row: bias held in registers, the next row's accumulator
@@ -2822,8 +2840,8 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
             v[j] = fmaxf(t2.x, 0.f);
             v[j + 1] = fmaxf(t2.y, 0.f);
           }
-          epi_store<T, CH>(es, &tmO, &lo.O, v, 0, args.Cout, args.split, xb, tyg * R + i * 2 + half, b + args.b_out,
-                           lane);
+          epi_store<T, CH, SK>(es, &tmO, &lo.O, v, 0, args.Cout, args.split, xb, tyg * R + i * 2 + half,
+                               b + args.b_out, lane);
           ptx::tmem_ld_wait();
         }
       } else {
@@ -2831,13 +2849,18 @@ __global__ void __launch_bounds__(StemSmem<BN, R, NA>::kThreads, 1)
         for (int i = 0; i < (R / 2) * (BN / CH); ++i) {
           const int r = (i / (BN / CH)) * 2 + half, c = (i % (BN / CH)) * CH;
           const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * R * BN + r * BN + c;
-          epi_chunk<T, CH, kReluBias>(es, 0, &tmO, &lo.O, taddr, args.bias, c, args.Cout, args.split, xb,
-                                      tyg * R + r, b + args.b_out, lane);
+          epi_chunk<T, CH, kReluBias, SK>(es, 0, &tmO, &lo.O, taddr, args.bias, c, args.Cout, args.split, xb,
+                                          tyg * R + r, b + args.b_out, lane);
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
     }
+    };
+    if (args.split == kStoreF8)
+      items(std::true_type{});
+    else
+      items(std::false_type{});
     if (lane == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
