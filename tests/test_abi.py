@@ -72,6 +72,9 @@ def test_no_oracle_import_in_product():
     ("levels=5;base=1024;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=64", "base must"),
     ("levels=5;base=32;head=4;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=64", "head must be 8"),
     ("levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;color=1", "unknown key"),
+    ("levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;batch=8;grp=9", "grp must"),
+    ("levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;grp=2;glev=0", "glev must"),
+    ("levels=5;base=32;head=8;ncls=6;scale_codes=5,10,20,40;slide_mag=40;dtype=fp16f8;hrm=1", "unknown key"),
 ])
 def test_create_rejects_bad_arch_strings_before_touching_the_device(arch, msg):
     """omniseg_create parses and validates the arch string first: a bad one returns NULL with
