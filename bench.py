@@ -286,15 +286,21 @@ def path_roofline(w, gsl, kept_ids, prof, steps, rank_windows, ms, pk, pk_kind):
     return out
 
 
+# committed ncu launch-list summaries of the cfg4 command, newest first
+NCU_SUMMARIES = ("r02z_cfg4_ncu_summary.json", "r02_cfg4_ncu_summary.json")
+
+
 def hbm_kernels():
     """Per-kernel DRAM throughput of the HBM-bound kernels from the committed ncu capture of the
-    cfg4 command (profiles/r02_cfg4_ncu_summary.json, scripts/summarize_ncu_r02.py)."""
-    p = os.path.join(ROOT, "profiles", "r02_cfg4_ncu_summary.json")
-    try:
-        with open(p) as f:
-            return json.load(f).get("hbm_kernels")
-    except (OSError, ValueError):
-        return None
+    cfg4 command (the newest profiles/r02*_cfg4_ncu_summary.json, scripts/summarize_ncu_r02.py)."""
+    for name in NCU_SUMMARIES:
+        p = os.path.join(ROOT, "profiles", name)
+        try:
+            with open(p) as f:
+                return json.load(f).get("hbm_kernels")
+        except (OSError, ValueError):
+            continue
+    return None
 
 
 def main():
@@ -446,7 +452,7 @@ def main():
     # DRAM traffic per conv launch from the committed ncu capture of the same launch shapes
     # (batch-64 launches of the cfg2 profile run: dram__bytes_read.sum + dram__bytes_write.sum)
     traffic, traffic_src = None, None
-    for tname in ("r02_cfg4_ncu_summary.json", "r01o_cfg2_summary.json"):
+    for tname in NCU_SUMMARIES + ("r01o_cfg2_summary.json",):
         tpath = os.path.join(ROOT, "profiles", tname)
         if os.path.exists(tpath):
             tj = json.load(open(tpath))

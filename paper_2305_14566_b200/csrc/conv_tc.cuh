@@ -1167,7 +1167,17 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
           ptx::tmem_ld_wait();
           float v[CH];
 #pragma unroll
-          for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(args.bias + n0 + j);
+          for (int j = 0; j < CH; j += 4) {  // + bias (float4 loads, packed adds; n0 % 16 == 0)
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n0 + j));
+            const float2 r0 =
+                __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])), make_float2(b4.x, b4.y));
+            const float2 r1 =
+                __fadd2_rn(make_float2(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])), make_float2(b4.z, b4.w));
+            v[j] = r0.x;
+            v[j + 1] = r0.y;
+            v[j + 2] = r1.x;
+            v[j + 3] = r1.y;
+          }
           if (args.wb >= 32) {
             // TMA path: the warp's 32 low-res pixels (one row) -> two output rows of 64 pixels
             using E = EpiTile<CH>;
@@ -1224,15 +1234,25 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
 #pragma unroll
                 for (int j = 0; j < CH / 8; ++j) {
                   const uint4 h4 = *reinterpret_cast<const uint4*>(sk_hi + so16(rr, j));
-                  uint4 l4 = make_uint4(0, 0, 0, 0);
-                  if (args.split == kStoreX2) l4 = *reinterpret_cast<const uint4*>(sk_lo + so16(rr, j));
-                  const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+                  const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+                  if (args.split == kStoreX2) {  // (hi + lo) + v
+                    const uint4 l4 = *reinterpret_cast<const uint4*>(sk_lo + so16(rr, j));
+                    const uint32_t ll[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const float2 fh = StoreT<T>::unpack(hh[e]);
-                    const float2 fl = StoreT<T>::unpack(ll[e]);
-                    x[q2][8 * j + 2 * e] = fh.x + fl.x + v[8 * j + 2 * e];
-                    x[q2][8 * j + 2 * e + 1] = fh.y + fl.y + v[8 * j + 2 * e + 1];
+                    for (int e = 0; e < 4; ++e) {
+                      const float2 t = __fadd2_rn(__fadd2_rn(StoreT<T>::unpack(hh[e]), StoreT<T>::unpack(ll[e])),
+                                                  make_float2(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]));
+                      x[q2][8 * j + 2 * e] = t.x;
+                      x[q2][8 * j + 2 * e + 1] = t.y;
+                    }
+                  } else {  // hi + v (F8: the lo part is added below; plain: none)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                      const float2 t =
+                          __fadd2_rn(StoreT<T>::unpack(hh[e]), make_float2(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]));
+                      x[q2][8 * j + 2 * e] = t.x;
+                      x[q2][8 * j + 2 * e + 1] = t.y;
+                    }
                   }
                 }
                 if (f8) {
