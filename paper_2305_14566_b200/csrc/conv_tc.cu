@@ -143,7 +143,10 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   constexpr int STT = NzCfg::STAGES(BN, 2, RT);  // tensor-core head
   int smem = NzSmem<BN, R, ST, DYF, 8, 0>::kTotal;
   const int threads = 384;
-  if (p.mode == kResidualRelu) smem = NzSmem<BN, R, STR, DYF, 8, 1>::kTotal;
+  // residual convs in F8 / plain storage: the lean epilogue layout buys another ring stage
+  constexpr int STL = NzCfg::STAGES(BN, 3);
+  const bool lean = p.mode == kResidualRelu && p.args.split != kStoreX2 && STL > STR;
+  if (p.mode == kResidualRelu) smem = lean ? NzSmem<BN, R, STL, DYF, 8, 3>::kTotal : NzSmem<BN, R, STR, DYF, 8, 1>::kTotal;
   else if (p.mode == kHeadFused) smem = p.head_tc ? NzSmem<BN, RT, STT, DYF, 8, 2>::kTotal : NzSmem<BN, R, STH, DYF, 8, 2>::kTotal;
   OS_REQUIRE(p.nz_R == (p.head_tc ? RT : R), "nz plan: rows per work item mismatch");
   auto go = [&](auto kern) {
@@ -158,7 +161,7 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   };
   if constexpr (BN == 128 && !DYF) {
     if (p.cl == 2) {  // CTA pair (cta_group::2), cluster (2, 1, 1)
-      constexpr int ST2 = NzCfg::STAGES_CL2(BN, 0), STR2 = NzCfg::STAGES_CL2(BN, 1);
+      constexpr int ST2 = NzCfg::STAGES_CL2(BN, 0), STR2 = NzCfg::STAGES_CL2(BN, 1), STL2 = NzCfg::STAGES_CL2(BN, 3);
       auto go2 = [&](auto kern, int sm) {
         static std::mutex mu;
         static std::unordered_set<const void*> done;
@@ -183,6 +186,8 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
       };
       if (p.mode == kReluBias)
         go2(conv3_nz_kernel<T, BN, R, ST2, kReluBias, false, 2>, NzSmem<BN, R, ST2, false, 8, 0, 2>::kTotal);
+      else if (p.mode == kResidualRelu && p.args.split != kStoreX2 && STL2 > STR2)
+        go2(conv3_nz_kernel<T, BN, R, STL2, kResidualRelu, false, 2, true>, NzSmem<BN, R, STL2, false, 8, 3, 2>::kTotal);
       else if (p.mode == kResidualRelu)
         go2(conv3_nz_kernel<T, BN, R, STR2, kResidualRelu, false, 2>, NzSmem<BN, R, STR2, false, 8, 1, 2>::kTotal);
       else
@@ -192,7 +197,15 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   }
   switch (p.mode) {
     case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;
-    case kResidualRelu: go(conv3_nz_kernel<T, BN, R, STR, kResidualRelu, DYF>); break;
+    case kResidualRelu:
+      if constexpr (STL > STR) {
+        if (lean) {
+          go(conv3_nz_kernel<T, BN, R, STL, kResidualRelu, DYF, 1, true>);
+          break;
+        }
+      }
+      go(conv3_nz_kernel<T, BN, R, STR, kResidualRelu, DYF>);
+      break;
     case kHeadFused:
       if constexpr (BN <= 32) {
         if (p.head_tc) {

@@ -281,10 +281,16 @@ struct EpiState {
 // none). Plain / F8 slots take 1.5 kBuf, so there is room for TWO output slots (double-
 // buffered TMA stores: the next chunk's STS does not wait for the previous store) beside the
 // two residual slots; x2 keeps one output slot.
+// lean (residual epilogues, F8 / plain storage): ONE output slot + the two residual slots (4.5
+// kBuf per warp instead of 6), so the nz kernel's operand ring gets another stage
 template <int CH>
-__device__ __forceinline__ void epi_layout(EpiState& es, int split) {
+__device__ __forceinline__ void epi_layout(EpiState& es, int split, bool lean = false) {
   constexpr int kB = EpiTile<CH>::kBuf;
-  if (split == kStoreX2) {
+  if (lean && split != kStoreX2) {
+    es.out_off[0] = es.out_off[1] = 0;
+    es.res_off[0] = kB + kB / 2;
+    es.res_off[1] = 3 * kB;
+  } else if (split == kStoreX2) {
     es.out_off[0] = es.out_off[1] = 0;
     es.res_off[0] = es.res_base * kB;
     es.res_off[1] = (es.res_base + 2) * kB;
@@ -1167,17 +1173,7 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
           ptx::tmem_ld_wait();
           float v[CH];
 #pragma unroll
-          for (int j = 0; j < CH; j += 4) {  // + bias (float4 loads, packed adds; n0 % 16 == 0)
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + n0 + j));
-            const float2 r0 =
-                __fadd2_rn(make_float2(__uint_as_float(u[j]), __uint_as_float(u[j + 1])), make_float2(b4.x, b4.y));
-            const float2 r1 =
-                __fadd2_rn(make_float2(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])), make_float2(b4.z, b4.w));
-            v[j] = r0.x;
-            v[j + 1] = r0.y;
-            v[j + 2] = r1.x;
-            v[j + 3] = r1.y;
-          }
+          for (int j = 0; j < CH; ++j) v[j] = __uint_as_float(u[j]) + __ldg(args.bias + n0 + j);
           if (args.wb >= 32) {
             // TMA path: the warp's 32 low-res pixels (one row) -> two output rows of 64 pixels
             using E = EpiTile<CH>;
@@ -1234,25 +1230,15 @@ __global__ void __launch_bounds__(tap_epi_warps(BN, MODE) == 8 ? 384 : 256, 1)
 #pragma unroll
                 for (int j = 0; j < CH / 8; ++j) {
                   const uint4 h4 = *reinterpret_cast<const uint4*>(sk_hi + so16(rr, j));
-                  const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
-                  if (args.split == kStoreX2) {  // (hi + lo) + v
-                    const uint4 l4 = *reinterpret_cast<const uint4*>(sk_lo + so16(rr, j));
-                    const uint32_t ll[4] = {l4.x, l4.y, l4.z, l4.w};
+                  uint4 l4 = make_uint4(0, 0, 0, 0);
+                  if (args.split == kStoreX2) l4 = *reinterpret_cast<const uint4*>(sk_lo + so16(rr, j));
+                  const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                      const float2 t = __fadd2_rn(__fadd2_rn(StoreT<T>::unpack(hh[e]), StoreT<T>::unpack(ll[e])),
-                                                  make_float2(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]));
-                      x[q2][8 * j + 2 * e] = t.x;
-                      x[q2][8 * j + 2 * e + 1] = t.y;
-                    }
-                  } else {  // hi + v (F8: the lo part is added below; plain: none)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                      const float2 t =
-                          __fadd2_rn(StoreT<T>::unpack(hh[e]), make_float2(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]));
-                      x[q2][8 * j + 2 * e] = t.x;
-                      x[q2][8 * j + 2 * e + 1] = t.y;
-                    }
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 fh = StoreT<T>::unpack(hh[e]);
+                    const float2 fl = StoreT<T>::unpack(ll[e]);
+                    x[q2][8 * j + 2 * e] = fh.x + fl.x + v[8 * j + 2 * e];
+                    x[q2][8 * j + 2 * e + 1] = fh.y + fl.y + v[8 * j + 2 * e + 1];
                   }
                 }
                 if (f8) {
@@ -1614,7 +1600,8 @@ struct NzSmem {
   static constexpr int kBars = (2 * STAGES + 4 + 2 * EW) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
-  static constexpr int kWarpEpi = (EK == 2 ? 4 : EK == 1 ? 6 : 3) * EpiTile<(BN < 32 ? BN : 32)>::kBuf;
+  // EK 3: lean residual epilogue (one output slot, epi_layout lean): 4.5 kBuf
+  static constexpr int kWarpEpi = (EK == 3 ? 9 : EK == 2 ? 8 : EK == 1 ? 12 : 6) * EpiTile<(BN < 32 ? BN : 32)>::kBuf / 2;
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
   static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 + EW * kHeadDescs * 32 : 0;
@@ -1654,7 +1641,7 @@ struct NzCfg {
   static constexpr int STAGES(int bn, int ek) { return STAGES(bn, ek, R(bn)); }
   static constexpr int tc_bytes(int bn) { return 8 * 128 * bn * 2 + 2 * bn * bn * 2 + bn * 4 + 64; }
   static constexpr int budget(int bn, int ek, int r) {
-    return 227 * 1024 - 3 * 1024 - 8 * (ek == 2 ? 4 : ek == 1 ? 6 : 3) * 32 * (bn < 32 ? bn : 32) * 2 -
+    return 227 * 1024 - 3 * 1024 - 8 * (ek == 3 ? 9 : ek == 2 ? 8 : ek == 1 ? 12 : 6) * 32 * (bn < 32 ? bn : 32) -
            (ek == 2 ? 7680 + 8 * kHeadDescs * 32 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
   }
 
@@ -1714,7 +1701,8 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
 // accumulators first-written by different MMAs, they are zeroed by the epilogue
 // (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
 // tensor-core operand traffic than one MMA per (tap, row).
-template <typename T, int BN, int R, int STAGES, int MODE, bool DYF, int CL = 1>
+// LEAN (kResidualRelu, F8 / plain storage): the lean epilogue layout (EK 3), one more ring stage
+template <typename T, int BN, int R, int STAGES, int MODE, bool DYF, int CL = 1, bool LEAN = false>
 __global__ void __launch_bounds__(384, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR,
@@ -1725,7 +1713,8 @@ __global__ void __launch_bounds__(384, 1)
   // sub-partition leaves the epilogue latency-bound (measured: it, not the loads or MMAs, set
   // the pace of the thin layers)
   constexpr int EW = 8;
-  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? 2 : MODE == kResidualRelu ? 1 : 0, CL>;
+  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? 2 : MODE == kResidualRelu ? (LEAN ? 3 : 1) : 0, CL>;
+  static_assert(!LEAN || MODE == kResidualRelu, "lean epilogue: residual mode");
   static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
   // CL = 2: CTA pair (cta_group::2, see conv_tc_kernel): items in pairs (two M items, one N tile),
   // each CTA's A rows + its half of the weight image complete on the leader's `full` barrier
@@ -1897,7 +1886,7 @@ __global__ void __launch_bounds__(384, 1)
     constexpr int CH = BN < 32 ? BN : 32;
     EpiState es{smem + S::kEpiOff + ew * S::kWarpEpi, &rbar[2 * ew], {0, 0}, MODE == kHeadFused ? 0 : 2, args.res_rc,
                 args.out_rc};
-    epi_layout<CH>(es, args.split);
+    epi_layout<CH>(es, args.split, LEAN);
     float* s_th = reinterpret_cast<float*>(smem + S::kHeadOff);
     float* s_w = s_th + S::kHeadTasks * 156;
     float* s_b = s_w + kHead * 64;
