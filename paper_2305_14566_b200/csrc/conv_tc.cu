@@ -141,7 +141,9 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   static_assert(ST >= 2 && STR >= 2 && STH >= 2, "no-swizzle tile does not fit shared memory");
   constexpr int RT = NzCfg::RTC;
   constexpr int STT = NzCfg::STAGES(BN, 2, RT);  // tensor-core head
-  int smem = NzSmem<BN, R, ST, DYF, 8, 0>::kTotal;
+  constexpr int STL0 = NzCfg::STAGES(BN, 4);  // lean output-only epilogue
+  const bool lean0 = p.mode == kReluBias && p.args.split != kStoreX2 && STL0 > ST;
+  int smem = lean0 ? NzSmem<BN, R, STL0, DYF, 8, 4>::kTotal : NzSmem<BN, R, ST, DYF, 8, 0>::kTotal;
   const int threads = 384;
   // residual convs in F8 / plain storage: the lean epilogue layout buys another ring stage
   constexpr int STL = NzCfg::STAGES(BN, 3);
@@ -161,7 +163,8 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
   };
   if constexpr (BN == 128 && !DYF) {
     if (p.cl == 2) {  // CTA pair (cta_group::2), cluster (2, 1, 1)
-      constexpr int ST2 = NzCfg::STAGES_CL2(BN, 0), STR2 = NzCfg::STAGES_CL2(BN, 1), STL2 = NzCfg::STAGES_CL2(BN, 3);
+      constexpr int ST2 = NzCfg::STAGES_CL2(BN, 0), STR2 = NzCfg::STAGES_CL2(BN, 1), STL2 = NzCfg::STAGES_CL2(BN, 3),
+                    STL20 = NzCfg::STAGES_CL2(BN, 4);
       auto go2 = [&](auto kern, int sm) {
         static std::mutex mu;
         static std::unordered_set<const void*> done;
@@ -184,7 +187,9 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
         cfg.numAttrs = 1;
         OS_CUDA(cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.tmO, p.tmR, p.args, p.head, p.lo));
       };
-      if (p.mode == kReluBias)
+      if (p.mode == kReluBias && p.args.split != kStoreX2 && STL20 > ST2)
+        go2(conv3_nz_kernel<T, BN, R, STL20, kReluBias, false, 2, true>, NzSmem<BN, R, STL20, false, 8, 4, 2>::kTotal);
+      else if (p.mode == kReluBias)
         go2(conv3_nz_kernel<T, BN, R, ST2, kReluBias, false, 2>, NzSmem<BN, R, ST2, false, 8, 0, 2>::kTotal);
       else if (p.mode == kResidualRelu && p.args.split != kStoreX2 && STL2 > STR2)
         go2(conv3_nz_kernel<T, BN, R, STL2, kResidualRelu, false, 2, true>, NzSmem<BN, R, STL2, false, 8, 3, 2>::kTotal);
@@ -196,7 +201,15 @@ void launch_nz(const ConvPlan& p, cudaStream_t s) {
     }
   }
   switch (p.mode) {
-    case kReluBias: go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>); break;
+    case kReluBias:
+      if constexpr (STL0 > ST) {
+        if (lean0) {
+          go(conv3_nz_kernel<T, BN, R, STL0, kReluBias, DYF, 1, true>);
+          break;
+        }
+      }
+      go(conv3_nz_kernel<T, BN, R, ST, kReluBias, DYF>);
+      break;
     case kResidualRelu:
       if constexpr (STL > STR) {
         if (lean) {

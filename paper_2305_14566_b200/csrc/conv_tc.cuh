@@ -1600,8 +1600,9 @@ struct NzSmem {
   static constexpr int kBars = (2 * STAGES + 4 + 2 * EW) * 8 + 16;
   static constexpr int kEpiOff = ((STAGES * kStage + kBars + 1023) / 1024) * 1024;
   // EW epilogue warps; with 8 (fused head: no output tiles) each warp keeps residual slots only
-  // EK 3: lean residual epilogue (one output slot, epi_layout lean): 4.5 kBuf
-  static constexpr int kWarpEpi = (EK == 3 ? 9 : EK == 2 ? 8 : EK == 1 ? 12 : 6) * EpiTile<(BN < 32 ? BN : 32)>::kBuf / 2;
+  // EK 3 / 4: lean residual / output-only epilogue (one output slot, epi_layout lean): 4.5 / 1.5 kBuf
+  static constexpr int kWarpEpi =
+      (EK == 4 ? 3 : EK == 3 ? 9 : EK == 2 ? 8 : EK == 1 ? 12 : 6) * EpiTile<(BN < 32 ? BN : 32)>::kBuf / 2;
   static constexpr int kHeadOff = kEpiOff + EW * kWarpEpi;
   static constexpr int kHeadTasks = 8;  // fused head supports up to 8 tasks per batch
   static constexpr int kHeadBytes = HEAD ? (kHeadTasks * 156 + kHead * 64 + kHead) * 4 + EW * kHeadDescs * 32 : 0;
@@ -1641,7 +1642,7 @@ struct NzCfg {
   static constexpr int STAGES(int bn, int ek) { return STAGES(bn, ek, R(bn)); }
   static constexpr int tc_bytes(int bn) { return 8 * 128 * bn * 2 + 2 * bn * bn * 2 + bn * 4 + 64; }
   static constexpr int budget(int bn, int ek, int r) {
-    return 227 * 1024 - 3 * 1024 - 8 * (ek == 3 ? 9 : ek == 2 ? 8 : ek == 1 ? 12 : 6) * 32 * (bn < 32 ? bn : 32) -
+    return 227 * 1024 - 3 * 1024 - 8 * (ek == 4 ? 3 : ek == 3 ? 9 : ek == 2 ? 8 : ek == 1 ? 12 : 6) * 32 * (bn < 32 ? bn : 32) -
            (ek == 2 ? 7680 + 8 * kHeadDescs * 32 : 0) - (tc(bn, ek, r) ? 1024 + tc_bytes(bn) : 0);
   }
 
@@ -1701,7 +1702,7 @@ __device__ __forceinline__ void nz_mma_chunk(uint32_t sa, uint32_t d_base, int k
 // accumulators first-written by different MMAs, they are zeroed by the epilogue
 // (tcgen05.st) after each use and every MMA accumulates. ~1.9x (BN=32) / 1.5x (BN=64) less
 // tensor-core operand traffic than one MMA per (tap, row).
-// LEAN (kResidualRelu, F8 / plain storage): the lean epilogue layout (EK 3), one more ring stage
+// LEAN (kResidualRelu / kReluBias, F8 / plain storage): the lean epilogue layout (EK 3 / 4), more ring stages
 template <typename T, int BN, int R, int STAGES, int MODE, bool DYF, int CL = 1, bool LEAN = false>
 __global__ void __launch_bounds__(384, 1)
     conv3_nz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -1713,8 +1714,9 @@ __global__ void __launch_bounds__(384, 1)
   // sub-partition leaves the epilogue latency-bound (measured: it, not the loads or MMAs, set
   // the pace of the thin layers)
   constexpr int EW = 8;
-  using S = NzSmem<BN, R, STAGES, DYF, EW, MODE == kHeadFused ? 2 : MODE == kResidualRelu ? (LEAN ? 3 : 1) : 0, CL>;
-  static_assert(!LEAN || MODE == kResidualRelu, "lean epilogue: residual mode");
+  using S = NzSmem<BN, R, STAGES, DYF, EW,
+                   MODE == kHeadFused ? 2 : MODE == kResidualRelu ? (LEAN ? 3 : 1) : (LEAN ? 4 : 0), CL>;
+  static_assert(!LEAN || MODE == kResidualRelu || MODE == kReluBias, "lean epilogue: residual / output-only modes");
   static_assert(!DYF || 3 * BN <= 256, "dy-fused N");
   // CL = 2: CTA pair (cta_group::2, see conv_tc_kernel): items in pairs (two M items, one N tile),
   // each CTA's A rows + its half of the weight image complete on the leader's `full` barrier
