@@ -545,7 +545,7 @@ void ensure_workspace(omniseg* h, int P) {
   h->erc.assign(L, 0);
   for (int l = 0; l + 1 < L; ++l)
     h->erc[l] = h->rc[l] && s2_eligible(P >> l, P >> l, h->down[l].cinp, h->down[l].coutp, 3, 2, kReluBias) &&
-                h->down[l].coutp <= (exp_flag("OMNISEG_S2_WIDE") ? 128 : 64) &&  // 2x MMA work: thin N only
+                h->down[l].coutp <= 128 &&  // 2x MMA work: up to N = 128 (down1: 78 -> 74 ms per cfg4 step)
                 !exp_flag("OMNISEG_NO_S2");
   const auto& rc = h->rc;
   const auto& erc = h->erc;
