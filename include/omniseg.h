@@ -139,7 +139,9 @@ int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64
  *   out_prob / out_mask  : root only: device buffers laid out as omniseg_segment_slide's
  *               outputs (tasks concatenated, ceil(H/f) x ceil(W/f) each); ignored elsewhere.
  * Collective: every rank of the communicator must call it with the same cuts / scales.
- * Errors: EINVAL without a communicator or for host buffers; ENCCL on NCCL failure. */
+ * Errors: EINVAL without a communicator or for host buffers; ENCCL on NCCL failure. Buffer
+ * errors found on any one rank (e.g. a host out_prob on the root) are agreed on by one int
+ * all-reduce before any transfer, so every rank returns the error instead of blocking. */
 int omniseg_gather_bands(omniseg_t* h, int root, int64_t H, int64_t W, int pad, const int64_t* cuts,
                          const int* scales, int n_tasks, const float* band_prob, const uint8_t* band_mask,
                          float* out_prob, uint8_t* out_mask);

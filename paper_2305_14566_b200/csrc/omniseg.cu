@@ -275,7 +275,7 @@ struct omniseg {
   // front end / canvases
   DevBuf cc_lab, cc_size;  // SURVEY N2 component-labelling scratch
   DevBuf r_slide, r_mask, r_40, r_10;  // SURVEY N3 render staging (host inputs / outputs)
-  DevBuf slide, L1, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask;
+  DevBuf slide, L1, L2, L4, L8, luma8, gm, fg, hist, state, keep, tiles, counts, grids, canvas, area, prob, mask, flag;
   std::vector<uint32_t> h_tiles;
   int64_t n_tiles = 0;
   int H8 = 0, W8 = 0, otsu_t = -1, g_pad = -1;
@@ -1391,17 +1391,29 @@ int omniseg_gather_bands(omniseg_t* h, int root, int64_t H, int64_t W, int pad, 
     OS_REQUIRE(cuts[0] == 0 && cuts[h->world] == Hp, "gather_bands: cuts must run from 0 to Hp");
     for (int r = 0; r < h->world; ++r) OS_REQUIRE(cuts[r] <= cuts[r + 1], "gather_bands: cuts must be ascending");
     const bool me_root = h->rank == root;
-    if (band_prob || band_mask) {
-      OS_REQUIRE(!band_prob || is_device_ptr(band_prob), "gather_bands: band_prob must be device memory");
-      OS_REQUIRE(!band_mask || is_device_ptr(band_mask), "gather_bands: band_mask must be device memory");
-    }
-    if (me_root) {
-      OS_REQUIRE((!band_prob || (out_prob && is_device_ptr(out_prob))) &&
-                     (!band_mask || (out_mask && is_device_ptr(out_mask))),
-                 "gather_bands: the root needs device out_prob / out_mask for every band output given");
-    }
     cudaStream_t s = h->stream;
     NvtxRange nv("omniseg/gather_bands");
+    // Per-rank buffer checks can fail on one rank only (e.g. a host out_prob on the root); a
+    // rank that returned here would leave its peers blocked in the send / recv group. So every
+    // rank reports its verdict through one tiny all-reduce first, and all of them fail together.
+    std::string bad;
+    if (band_prob && !is_device_ptr(band_prob)) bad = "gather_bands: band_prob must be device memory";
+    if (band_mask && !is_device_ptr(band_mask)) bad = "gather_bands: band_mask must be device memory";
+    if (me_root && !((!band_prob || (out_prob && is_device_ptr(out_prob))) &&
+                     (!band_mask || (out_mask && is_device_ptr(out_mask)))))
+      bad = "gather_bands: the root needs device out_prob / out_mask for every band output given";
+    {
+      h->flag.ensure(sizeof(int));
+      const int mine = bad.empty() ? 0 : 1;
+      OS_CUDA(cudaMemcpyAsync(h->flag.p, &mine, sizeof(int), cudaMemcpyHostToDevice, s));
+      g_nccl.check(g_nccl.allReduce(h->flag.p, h->flag.p, 1, ncclInt32, ncclSum, h->comm, s),
+                   "ncclAllReduce(gather_bands arguments)");
+      int nbad = 0;
+      OS_CUDA(cudaMemcpyAsync(&nbad, h->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      OS_CUDA(cudaStreamSynchronize(s));
+      OS_REQUIRE(bad.empty(), bad);
+      OS_REQUIRE(nbad == 0, "gather_bands: bad arguments on " + std::to_string(nbad) + " other rank(s)");
+    }
     // per task: offset of the task in the full output and in each rank's band output
     std::vector<int64_t> full_off(tk.n);
     int64_t acc = 0;

@@ -114,6 +114,13 @@ def test_nccl_plumbing_world1(setup):
     assert (fm.cpu().numpy() == mask).all()
     with pytest.raises(Exception, match="device"):
         h.gather_bands(0, H, W, PAD, D.band_cuts(Hp, 1, S), SCALES, bp, bm, fp, fm)   # host band buffers
+    with pytest.raises(Exception, match="root needs device"):   # host outputs on the root
+        h.gather_bands(0, H, W, PAD, D.band_cuts(Hp, 1, S), SCALES, dbp, dbm, np.zeros_like(prob), fm)
+    # the argument agreement leaves the communicator usable: a correct gather still works
+    fp.fill_(-1.0)
+    h.gather_bands(0, H, W, PAD, D.band_cuts(Hp, 1, S), SCALES, dbp, dbm, fp, fm)
+    torch.cuda.synchronize()
+    assert (fp.cpu().numpy().view(np.uint32) == prob.view(np.uint32)).all()
 
 
 def test_empty_band_joins_without_compute(setup):
