@@ -1342,28 +1342,62 @@ int omniseg_comm_init(omniseg_t* h, const void* id, int world, int rank) {
   }
 }
 
+// Argument agreement of the band entry points: a check that fails on one rank only (a bad band,
+// a host buffer on the root) would otherwise return on that rank and leave its peers blocked in
+// the next collective. Every rank reports its verdict through one int all-reduce before any
+// other collective, and all of them fail together (the failing rank with its own message).
+static void agree_args(omniseg_t* h, const std::string& bad, const char* what) {
+  if (!h->comm) {
+    OS_REQUIRE(bad.empty(), bad);
+    return;
+  }
+  cudaStream_t s = h->stream;
+  h->flag.ensure(sizeof(int));
+  const int mine = bad.empty() ? 0 : 1;
+  OS_CUDA(cudaMemcpyAsync(h->flag.p, &mine, sizeof(int), cudaMemcpyHostToDevice, s));
+  g_nccl.check(g_nccl.allReduce(h->flag.p, h->flag.p, 1, ncclInt32, ncclSum, h->comm, s),
+               (std::string("ncclAllReduce(") + what + " arguments)").c_str());
+  int nbad = 0;
+  OS_CUDA(cudaMemcpyAsync(&nbad, h->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  OS_CUDA(cudaStreamSynchronize(s));
+  OS_REQUIRE(bad.empty(), bad);
+  OS_REQUIRE(nbad == 0, std::string(what) + ": bad arguments on " + std::to_string(nbad) + " other rank(s)");
+}
+
 int omniseg_segment_band(omniseg_t* h, const uint8_t* rgb_band, int64_t H, int64_t W, int64_t row0, int64_t row1,
                          int pad, int patch, int stride, const int* scales, const int* classes, int n_tasks,
                          float* out_prob, uint8_t* out_mask, uint64_t* out_area) {
   try {
     OS_REQUIRE(h != nullptr, "handle is NULL");
     OS_CUDA(cudaSetDevice(h->device));
-    validate_common(H, W, pad, patch, stride, h->arch.vote != 0);
-    Tasks tk = make_tasks(h, scales, classes, n_tasks, H, W);
-    const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
-    OS_REQUIRE(row0 >= 0 && row0 <= row1 && row1 <= Hp, "band: need 0 <= row0 <= row1 <= Hp");
+    Tasks tk;
+    int64_t b0 = 0, b1 = 0;
+    std::string bad;
+    try {
+      validate_common(H, W, pad, patch, stride, h->arch.vote != 0);
+      tk = make_tasks(h, scales, classes, n_tasks, H, W);
+      const int64_t Hp = (H + 2 * pad + 127) / 128 * 128;
+      OS_REQUIRE(row0 >= 0 && row0 <= row1 && row1 <= Hp, "band: need 0 <= row0 <= row1 <= Hp");
+      if (row0 == row1) {
+        OS_REQUIRE(row0 > 0, "band 0 must not be empty (it holds the pad colour, the broadcast root)");
+      } else {
+        OS_REQUIRE(row0 % (8 * stride) == 0 && (row1 == Hp || row1 % (8 * stride) == 0),
+                   "band: row0/row1 must be multiples of 8*stride (row1 may be Hp)");
+        const int64_t halo = (int64_t)patch * tk.fmax + 64;
+        b0 = std::max<int64_t>(0, std::min<int64_t>(H, row0 - pad - halo));
+        b1 = std::max<int64_t>(0, std::min<int64_t>(H, row1 - pad + halo));
+        OS_REQUIRE(b1 > b0 || rgb_band != nullptr, "band: empty");
+        if (row0 == 0) OS_REQUIRE(b0 == 0, "band 0 must start at slide row 0");
+      }
+    } catch (const Error& e) {
+      if (e.code != -1) throw;  // CUDA / allocation errors are not argument errors
+      bad = e.what();
+    }
+    agree_args(h, bad, "segment_band");
     if (row0 == row1) {  // an empty band: collectives only
-      OS_REQUIRE(row0 > 0, "band 0 must not be empty (it holds the pad colour, the broadcast root)");
       segment_empty(h, H, W, pad, tk, out_area);
       return 0;
     }
-    OS_REQUIRE(row0 % (8 * stride) == 0 && (row1 == Hp || row1 % (8 * stride) == 0),
-               "band: row0/row1 must be multiples of 8*stride (row1 may be Hp)");
-    const int64_t halo = (int64_t)patch * tk.fmax + 64;
-    const int64_t b0 = std::max<int64_t>(0, std::min<int64_t>(H, row0 - pad - halo));
-    const int64_t b1 = std::max<int64_t>(0, std::min<int64_t>(H, row1 - pad + halo));
-    OS_REQUIRE(b1 > b0 || rgb_band != nullptr, "band: empty");
-    if (row0 == 0) OS_REQUIRE(b0 == 0, "band 0 must start at slide row 0");
     if (h->arch.bf16)
       segment<__nv_bfloat16>(h, rgb_band, H, W, row0, row1, b0, b1, pad, patch, stride, tk, out_prob, out_mask,
                              out_area);
@@ -1402,18 +1436,7 @@ int omniseg_gather_bands(omniseg_t* h, int root, int64_t H, int64_t W, int pad, 
     if (me_root && !((!band_prob || (out_prob && is_device_ptr(out_prob))) &&
                      (!band_mask || (out_mask && is_device_ptr(out_mask)))))
       bad = "gather_bands: the root needs device out_prob / out_mask for every band output given";
-    {
-      h->flag.ensure(sizeof(int));
-      const int mine = bad.empty() ? 0 : 1;
-      OS_CUDA(cudaMemcpyAsync(h->flag.p, &mine, sizeof(int), cudaMemcpyHostToDevice, s));
-      g_nccl.check(g_nccl.allReduce(h->flag.p, h->flag.p, 1, ncclInt32, ncclSum, h->comm, s),
-                   "ncclAllReduce(gather_bands arguments)");
-      int nbad = 0;
-      OS_CUDA(cudaMemcpyAsync(&nbad, h->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-      OS_CUDA(cudaStreamSynchronize(s));
-      OS_REQUIRE(bad.empty(), bad);
-      OS_REQUIRE(nbad == 0, "gather_bands: bad arguments on " + std::to_string(nbad) + " other rank(s)");
-    }
+    agree_args(h, bad, "gather_bands");
     // per task: offset of the task in the full output and in each rank's band output
     std::vector<int64_t> full_off(tk.n);
     int64_t acc = 0;

@@ -100,6 +100,8 @@ def test_nccl_plumbing_world1(setup):
     bp = np.zeros_like(prob)
     bm = np.zeros_like(mask)
     ba = np.zeros_like(area)
+    with pytest.raises(Exception, match="multiples of 8"):   # argument error agreed on, then raised
+        h.segment_band(slide, H, W, S, Hp, PAD, P, S, SCALES, CLASSES, bp, bm, ba)
     h.segment_band(slide, H, W, 0, Hp, PAD, P, S, SCALES, CLASSES, bp, bm, ba)
     assert (bp.view(np.uint32) == prob.view(np.uint32)).all() and (bm == mask).all() and (ba == area).all()
     # device-resident band outputs -> gather to rank 0
